@@ -1,0 +1,279 @@
+"""SAGA-NN layer oracle: GCN and G-GCN forward/backward (test infrastructure only).
+
+Two restatements of the same math:
+
+* ``ref_*`` -- the literal reference composition: the SAGA-NN stages written
+  with the ``tensor.py`` primitives over the whole CSC-ordered edge list, in
+  tape order (Scatter = take_rows tensor.py:424, ApplyEdge = mul/add/sigmoid
+  tensor.py:204-303, Gather = segment_sum tensor.py:439, ApplyVertex =
+  matmul + relu tensor.py:306/207, loss tensor.py:487, backward = the reverse
+  sweep of tensor.py:91-121).  Checked bit-for-bit against golden fixtures
+  produced by the real reference (tests/golden/make_golden.py).
+* chunked -- the SPEC's engine semantics: Locality order over the 2D grid
+  (for each destination interval j, all source intervals i in
+  ascending order accumulate into A_j), per-destination accumulation in CSC
+  order and large groups split into consecutive subgroups of
+  ``T`` edges combined in fixed order.  With
+  P = 1 and no split this is the reference composition exactly.
+"""
+
+import numpy as np
+
+from . import primitives as prim
+
+
+# ------------------------------------------------------------------ gather core
+def seq_sum_rows(ptr, t, A=None, T=None, F=None, dtype=None):
+    """Sum per-edge terms ``t`` (CSC/CSR order) into rows, deterministic order.
+
+    Row u with ``n_u <= T`` edges continues the chain ``acc = A[u]; acc += t_e``
+    in edge order; a row with ``n_u > T`` edges is split into consecutive
+    subgroups of ``T`` edges, each summed from 0, and the partials are added
+    onto ``A[u]`` in subgroup order.  ``T=None`` never splits.
+    """
+    ptr = np.asarray(ptr, np.int64)
+    n = len(ptr) - 1
+    if A is None:
+        A = np.zeros((n, t.shape[1] if F is None else F), dtype=t.dtype if dtype is None else dtype)
+    out = A.copy()
+    nnz = int(ptr[-1])
+    if nnz == 0:
+        return out
+    deg = np.diff(ptr)
+    rows = np.repeat(np.arange(n, dtype=np.int64), deg)
+    if T is None:
+        np.add.at(out, rows, t)
+        return out
+    esplit = (deg > T)[rows]
+    keep = ~esplit
+    np.add.at(out, rows[keep], t[keep])
+    if esplit.any():
+        pos = np.arange(nnz, dtype=np.int64) - ptr[rows]
+        r_s, sub = rows[esplit], pos[esplit] // T
+        change = np.ones(r_s.shape[0], dtype=bool)
+        change[1:] = (r_s[1:] != r_s[:-1]) | (sub[1:] != sub[:-1])
+        gid = np.cumsum(change) - 1
+        partial = np.zeros((int(gid[-1]) + 1, t.shape[1]), dtype=t.dtype)
+        np.add.at(partial, gid, t[esplit])
+        np.add.at(out, r_s[change], partial)
+    return out
+
+
+def local_rows(ptr):
+    ptr = np.asarray(ptr, np.int64)
+    return np.repeat(np.arange(len(ptr) - 1, dtype=np.int64), np.diff(ptr))
+
+
+def _rows(part, X, k):
+    b = part.begin(k)
+    return X[b: b + int(part.sizes[k])]
+
+
+# ------------------------------------------------------------------ GCN propagation
+def gcn_propagate_fwd(part, H, w_edge, T=None):
+    """fused_gather_chunk for GCN over all columns, Locality order.
+
+    ``A[u] = sum_{e in in(u)} w_e * H[src_e]`` with ``t_e = H[src] * w_e``
+    exactly as ``mul(take_rows(H, src), w)`` (tensor.py:249)."""
+    A = np.zeros((part.V, H.shape[1]), dtype=H.dtype)
+    for j in range(part.P):
+        Aj = np.zeros((int(part.sizes[j]), H.shape[1]), dtype=H.dtype)
+        for i in range(part.P):
+            ch = part.chunk(i, j)
+            if ch["nnz"] == 0:
+                continue  # SPEC.md:427 empty chunk -> A_j unchanged
+            t = _rows(part, H, i)[ch["csc_idx"]]
+            if w_edge is not None:
+                t = t * w_edge[ch["csc_eid"]][:, None]
+            Aj = seq_sum_rows(ch["csc_ptr"], t, Aj, T)
+        A[part.begin(j): part.begin(j) + int(part.sizes[j])] = Aj
+    return A
+
+
+def gcn_propagate_bwd(part, G, w_edge, T=None):
+    """backward Gather+ApplyEdge+Scatter for GCN over the transposed (CSR) index.
+
+    ``dH[v] = sum_{e in out(v)} G[dst_e] * w_e`` (tensor.py:447-448, :263, :431-434);
+    per source interval i, destination intervals j ascending."""
+    out = np.zeros((part.V, G.shape[1]), dtype=G.dtype)
+    for i in range(part.P):
+        Oi = np.zeros((int(part.sizes[i]), G.shape[1]), dtype=G.dtype)
+        for j in range(part.P):
+            ch = part.chunk(i, j)
+            if ch["nnz"] == 0:
+                continue
+            t = _rows(part, G, j)[ch["csr_idx"]]
+            if w_edge is not None:
+                t = t * w_edge[ch["csr_eid"]][:, None]
+            Oi = seq_sum_rows(ch["csr_ptr"], t, Oi, T)
+        out[part.begin(i): part.begin(i) + int(part.sizes[i])] = Oi
+    return out
+
+
+# ------------------------------------------------------------------ G-GCN propagation
+def ggcn_propagate_fwd(part, h, P_, Q_, T=None):
+    """Fused gated gather (post-hoist G-GCN):
+    ``A[u] = sum sigmoid(P[v] + Q[u]) * h[v]`` -- add(Ps, Qd) -> sigmoid -> mul(eta, hs)."""
+    A = np.zeros((part.V, h.shape[1]), dtype=h.dtype)
+    for j in range(part.P):
+        Aj = np.zeros((int(part.sizes[j]), h.shape[1]), dtype=h.dtype)
+        Qj = _rows(part, Q_, j)
+        for i in range(part.P):
+            ch = part.chunk(i, j)
+            if ch["nnz"] == 0:
+                continue
+            src = ch["csc_idx"]
+            u = local_rows(ch["csc_ptr"])
+            eta = prim.sigmoid(_rows(part, P_, i)[src] + Qj[u])
+            t = eta * _rows(part, h, i)[src]
+            Aj = seq_sum_rows(ch["csc_ptr"], t, Aj, T)
+        A[part.begin(j): part.begin(j) + int(part.sizes[j])] = Aj
+    return A
+
+
+def ggcn_propagate_bwd(part, h, P_, Q_, Ga, T=None):
+    """G-GCN backward duals with eta recomputed.
+
+    Pass A (CSC): dQ[u] = sum_in(u) t_e.  Pass B (CSR): dP[v] = sum_out(v) t_e and
+    dh_take[v] = sum_out(v) Ga[u] * eta_e, where g_eta = Ga[u] * h[v] (mul bwd,
+    tensor.py:263) and t_e = g_eta * eta * (1 - eta) (sigmoid bwd, tensor.py:232)."""
+    F = h.shape[1]
+    dQ = np.zeros((part.V, F), dtype=h.dtype)
+    dP = np.zeros((part.V, F), dtype=h.dtype)
+    dH = np.zeros((part.V, F), dtype=h.dtype)
+    for j in range(part.P):  # pass A
+        Gj, Qj = _rows(part, Ga, j), _rows(part, Q_, j)
+        acc = np.zeros((int(part.sizes[j]), F), dtype=h.dtype)
+        for i in range(part.P):
+            ch = part.chunk(i, j)
+            if ch["nnz"] == 0:
+                continue
+            v = ch["csc_idx"]
+            u = local_rows(ch["csc_ptr"])
+            eta = prim.sigmoid(_rows(part, P_, i)[v] + Qj[u])
+            t = prim.sigmoid_bwd(Gj[u] * _rows(part, h, i)[v], eta)
+            acc = seq_sum_rows(ch["csc_ptr"], t, acc, T)
+        dQ[part.begin(j): part.begin(j) + int(part.sizes[j])] = acc
+    for i in range(part.P):  # pass B
+        Pi, hi = _rows(part, P_, i), _rows(part, h, i)
+        accP = np.zeros((int(part.sizes[i]), F), dtype=h.dtype)
+        accH = np.zeros((int(part.sizes[i]), F), dtype=h.dtype)
+        for j in range(part.P):
+            ch = part.chunk(i, j)
+            if ch["nnz"] == 0:
+                continue
+            u = ch["csr_idx"]
+            v = local_rows(ch["csr_ptr"])
+            Gu = _rows(part, Ga, j)[u]
+            eta = prim.sigmoid(Pi[v] + _rows(part, Q_, j)[u])
+            t = prim.sigmoid_bwd(Gu * hi[v], eta)
+            accP = seq_sum_rows(ch["csr_ptr"], t, accP, T)
+            accH = seq_sum_rows(ch["csr_ptr"], Gu * eta, accH, T)
+        dP[part.begin(i): part.begin(i) + int(part.sizes[i])] = accP
+        dH[part.begin(i): part.begin(i) + int(part.sizes[i])] = accH
+    return dQ, dP, dH
+
+
+# ------------------------------------------------------------------ models (chunked)
+def gcn_epoch(part, X, Ws, labels, w_edge, T=None):
+    """2-layer (or L-layer) GCN forward + backward.
+
+    Returns dict(loss, a=[...], z=[...], out=[...], grads=[dW...])."""
+    hs, As, Zs = [X], [], []
+    for W in Ws:
+        a = gcn_propagate_fwd(part, hs[-1], w_edge, T)
+        z = prim.matmul(a, W)
+        As.append(a)
+        Zs.append(z)
+        hs.append(prim.relu(z))
+    loss, p = prim.softmax_cross_entropy(hs[-1], labels)
+    g = prim.softmax_cross_entropy_bwd(np.asarray(1.0, dtype=X.dtype), p, labels)
+    grads = [None] * len(Ws)
+    for l in range(len(Ws) - 1, -1, -1):
+        gz = prim.relu_bwd(g, Zs[l])
+        ga, grads[l] = prim.matmul_bwd(gz, As[l], Ws[l])
+        if l > 0:
+            g = gcn_propagate_bwd(part, ga, w_edge, T)
+    return dict(loss=loss, p=p, a=As, z=Zs, out=hs[1:], grads=grads)
+
+
+def ggcn_epoch(part, X, layers, labels, T=None):
+    """2-layer G-GCN, hoisted (P = h W_H, Q = h W_C), forward + backward.
+
+    ``layers`` = [(W_H, W_C, W), ...]; grads returned in the same structure."""
+    hs, cache = [X], []
+    for (WH, WC, W) in layers:
+        h = hs[-1]
+        P_ = prim.matmul(h, WH)
+        Q_ = prim.matmul(h, WC)
+        a = ggcn_propagate_fwd(part, h, P_, Q_, T)
+        z = prim.matmul(a, W)
+        cache.append((h, P_, Q_, a, z))
+        hs.append(prim.relu(z))
+    loss, p = prim.softmax_cross_entropy(hs[-1], labels)
+    g = prim.softmax_cross_entropy_bwd(np.asarray(1.0, dtype=X.dtype), p, labels)
+    grads = [None] * len(layers)
+    for l in range(len(layers) - 1, -1, -1):
+        WH, WC, W = layers[l]
+        h, P_, Q_, a, z = cache[l]
+        gz = prim.relu_bwd(g, z)
+        ga, gW = prim.matmul_bwd(gz, a, W)
+        dQ, dP, dH = ggcn_propagate_bwd(part, h, P_, Q_, ga, T)
+        gh_q, gWC = prim.matmul_bwd(dQ, h, WC)
+        gh_p, gWH = prim.matmul_bwd(dP, h, WH)
+        grads[l] = (gWH, gWC, gW)
+        g = (dH + gh_q) + gh_p  # tape order: take_rows(h) part, then Q-, then P-matmul
+    return dict(loss=loss, p=p, out=hs[1:], cache=cache, grads=grads)
+
+
+def sgd(params, grads, lr):
+    """W <- W - lr * dW."""
+    return [W - lr * g for W, g in zip(params, grads)]
+
+
+# ------------------------------------------------------------------ literal reference composition
+def ref_gcn_layer(h, W, src, dst, w_col, V):
+    """GCN layer as PAPER.md:552-564 on the primitives; edges in CSC order."""
+    es = prim.take_rows(h, src)              # Scatter
+    acc = prim.mul(es, w_col)                # ApplyEdge: edge.src x edge.data
+    accum = prim.segment_sum(acc, dst, V)    # Gather(sum)
+    z = prim.matmul(accum, W)                # ApplyVertex
+    return es, accum, z, prim.relu(z)
+
+
+def ref_gcn_epoch(X, Ws, labels, src, dst, w, V):
+    w_col = w.reshape(-1, 1)
+    hs, cache = [X], []
+    for W in Ws:
+        es, a, z, out = ref_gcn_layer(hs[-1], W, src, dst, w_col, V)
+        cache.append((a, z))
+        hs.append(out)
+    loss, p = prim.softmax_cross_entropy(hs[-1], labels)
+    g = prim.softmax_cross_entropy_bwd(np.asarray(1.0, dtype=X.dtype), p, labels)
+    grads = [None] * len(Ws)
+    for l in range(len(Ws) - 1, -1, -1):
+        a, z = cache[l]
+        gz = prim.relu_bwd(g, z)
+        ga, grads[l] = prim.matmul_bwd(gz, a, Ws[l])
+        gacc = prim.segment_sum_bwd(ga, dst)
+        ges = gacc * w_col                      # mul bwd, ga = g * w (tensor.py:263)
+        g = prim.take_rows_bwd(ges, src, V)     # backward-Scatter (tensor.py:431-434)
+    return dict(loss=loss, a=[c[0] for c in cache], z=[c[1] for c in cache],
+                out=hs[1:], grads=grads)
+
+
+def ref_ggcn_layer(h, WH, WC, W, src, dst, V, hoisted=True):
+    """G-GCN layer per the listing PAPER.md:172-173 / SPEC.md:193 (W_H on src)."""
+    if hoisted:
+        P_ = prim.matmul(h, WH)
+        Q_ = prim.matmul(h, WC)
+        pre = prim.add(prim.take_rows(P_, src), prim.take_rows(Q_, dst))
+    else:
+        hs_ = prim.take_rows(h, src)
+        hd_ = prim.take_rows(h, dst)
+        pre = prim.add(prim.matmul(hs_, WH), prim.matmul(hd_, WC))
+    eta = prim.sigmoid(pre)
+    acc = prim.mul(eta, prim.take_rows(h, src))
+    accum = prim.segment_sum(acc, dst, V)
+    z = prim.matmul(accum, W)
+    return accum, z, prim.relu(z)

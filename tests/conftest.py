@@ -1,0 +1,54 @@
+import os
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+GOLDEN = os.path.join(ROOT, "tests", "golden")
+GOLDEN_CASES = ["uniform_v40_e160", "rmat_v64_e600", "isolated_v30_e20"]
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA GPU (B200) and the built libsagann.so")
+    config.addinivalue_line("markers", "slow: long-running")
+
+
+def pytest_collection_modifyitems(config, items):
+    try:
+        import torch
+        has_gpu = torch.cuda.is_available()
+    except Exception:  # pragma: no cover
+        has_gpu = False
+    if has_gpu:
+        return
+    skip = pytest.mark.skip(reason="no CUDA device in this container")
+    for item in items:
+        if "gpu" in item.keywords:
+            item.add_marker(skip)
+
+
+def load_golden(name):
+    with np.load(os.path.join(GOLDEN, name + ".npz")) as z:
+        return {k: z[k] for k in z.files}
+
+
+def assert_close(got, ref, rel=1e-4, what=""):
+    """SURVEY §8(c) parity criterion: normwise rel <= rel AND
+    elementwise |d| <= rel*|ref| + 1e-2*rel*max|ref|."""
+    got = np.asarray(got, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    assert got.shape == ref.shape, (what, got.shape, ref.shape)
+    d = np.abs(got - ref)
+    nref = np.linalg.norm(ref)
+    scale = float(np.abs(ref).max()) if ref.size else 0.0
+    if nref > 0:
+        nrm = np.linalg.norm(got - ref) / nref
+        assert nrm <= rel, f"{what}: normwise rel err {nrm:.3e} > {rel:.1e}"
+    bad = d > rel * np.abs(ref) + 1e-2 * rel * scale + 1e-30
+    assert not bad.any(), (
+        f"{what}: {int(bad.sum())} elements out of tolerance; max abs err {d.max():.3e}, "
+        f"max |ref| {scale:.3e}")
