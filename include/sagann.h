@@ -1,0 +1,187 @@
+/*
+ * sagann.h -- C-ABI of the B200-native SAGA-NN layer hot path (libsagann.so).
+ *
+ * The reference (/root/reference/pkg/src/sagastream) is pure Python/numpy and
+ * has no FFI; each entry point below replaces the reference interface named in
+ * its comment (file:line).  Conventions:
+ *   - plain pointers and sizes only; every buffer is caller-owned (device memory
+ *     for sg_* kernels, host memory for sg_host_*); no hidden allocations;
+ *   - row-major matrices with an explicit leading dimension (elements);
+ *   - kernels are asynchronous on the given stream (a cudaStream_t, passed as
+ *     void*; NULL = legacy default stream) and deterministic run to run (no
+ *     float atomics);
+ *   - every call returns a status code (SG_OK = 0) and never throws; the message
+ *     of the last failure on the calling thread is sg_last_error().  Status codes
+ *     mirror the reference's exceptions (errors.py:4-29): SG_ESHAPE -> ShapeError,
+ *     SG_ENUMERIC -> NumericError, SG_EBUDGET -> BudgetError.
+ */
+#ifndef SAGANN_H
+#define SAGANN_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum sg_status {
+  SG_OK = 0,
+  SG_ESHAPE = 1,   /* ShapeError   (errors.py:8)  */
+  SG_ENUMERIC = 2, /* NumericError (errors.py:12) */
+  SG_EBUDGET = 3,  /* BudgetError  (errors.py:24) */
+  SG_ECUDA = 4,
+  SG_ENCCL = 5,
+  SG_EINVAL = 6
+};
+
+enum sg_dtype { SG_F32 = 0, SG_BF16 = 1 };
+
+/* Propagation modes of sg_propagate (one fused Scatter-ApplyEdge-Gather pass). */
+enum sg_prop_mode {
+  SG_PROP_PASS = 0,         /* t_e = G[idx_e]                 (passthrough / segment_sum)   */
+  SG_PROP_GCN = 1,          /* t_e = G[idx_e] * w_e           (GCN fwd on CSC, bwd on CSR)  */
+  SG_PROP_GGCN_FWD = 2,     /* G=[h|P], R=Q:  t = sig(P[v]+Q[u]) * h[v]                     */
+  SG_PROP_GGCN_BWD_DST = 3, /* CSC. G=[h|P], R=[dA|Q]: dQ[u] = sum ((dA[u]*h[v])*eta)*(1-eta) */
+  SG_PROP_GGCN_BWD_SRC = 4  /* CSR. G=[dA|Q], R=[h|P]: dP[v] = sum t_e, dH[v] = sum dA[u]*eta */
+};
+
+enum sg_epilogue { SG_EPI_NONE = 0, SG_EPI_RELU_DUAL = 1 };
+enum sg_gemm_prec { SG_GEMM_F32 = 0, SG_GEMM_TF32X3 = 1, SG_GEMM_BF16 = 2 };
+
+/* Work item of a propagation pass (32 bytes).  A non-split item covers the whole
+ * rows [row_begin, row_end); a split item covers edges [e_begin, e_end) of one
+ * row (row_end = row_begin + 1), subgroup `sub` of split record `split`. */
+typedef struct sg_item {
+  int32_t row_begin, row_end;
+  int64_t e_begin, e_end;
+  int32_t split, sub;
+} sg_item;
+
+/* A row whose edge count exceeds the split threshold T. */
+typedef struct sg_split {
+  int32_t row, n_sub;
+  int64_t slot0; /* partial rows slot0 .. slot0 + n_sub - 1 in the workspace */
+} sg_split;
+
+const char* sg_last_error(void);
+int sg_version(void);
+int sg_device_sm_count(int device, int* sm_count);
+/* Number of device kernels this library has launched in this process (bench evidence). */
+int64_t sg_launch_count(void);
+
+/* ---------------------------------------------------------------- host: graph store
+ * Synthetic generators (counter-based, identical to oracle/rng.py). */
+int sg_host_gen_rmat(int64_t V, int64_t E, uint64_t seed, double t1, double t2, double t3,
+                     int64_t edge_begin, int32_t* src, int32_t* dst);
+int sg_host_gen_uniform(int64_t V, int64_t E, uint64_t seed, int64_t edge_begin,
+                        int32_t* src, int32_t* dst);
+int sg_host_gen_features(int64_t V, int64_t F, uint64_t seed, int64_t row_begin,
+                         float* x, int64_t ldx);
+/* degrees: deg_out / deg_in (int64 [V]). */
+int sg_host_degrees(const int32_t* src, const int32_t* dst, int64_t E, int64_t V,
+                    int64_t* dout, int64_t* din);
+/* reencode_balance: perm[old] = new. */
+int sg_host_reencode_balance(const int32_t* src, const int32_t* dst, int64_t E, int64_t V,
+                             int64_t num_intervals, int64_t* perm);
+/* partition_2d.  sg_host_partition_layout gives P and the length
+ * of each pointer array (= P * (V + P)); sg_host_partition_2d fills the layout of
+ * oracle/graph.py:Partition (chunk id c = i * P + j). */
+int sg_host_partition_layout(int64_t V, int64_t interval_size, int64_t* P, int64_t* ptr_len);
+int sg_host_partition_2d(const int32_t* src, const int32_t* dst, int64_t E, int64_t V,
+                         int64_t interval_size, int64_t* edge_off, int64_t* cptr_off,
+                         int64_t* rptr_off, int64_t* csc_ptr, int32_t* csc_idx, int64_t* csc_eid,
+                         int64_t* csr_ptr, int32_t* csr_idx, int64_t* csr_eid);
+/* GCN static edge weight w = 1/sqrt(deg_out(src) * deg_in(dst)),
+ * evaluated in fp64 and rounded to fp32, for edges eid[0..n). */
+int sg_host_gcn_weights(const int32_t* src, const int32_t* dst, const int64_t* dout,
+                        const int64_t* din, const int64_t* eid, int64_t n, float* w);
+/* Work plan of a CSC/CSR pass: rows with > split_edges edges become split rows
+ * (subgroups of split_edges edges); other rows are packed in order
+ * into items of <= pack_edges edges and <= max_rows rows.  Call with items ==
+ * NULL to count. */
+int sg_host_plan(const int64_t* ptr, int64_t n_rows, int64_t pack_edges, int64_t max_rows,
+                 int64_t split_edges, sg_item* items, sg_split* splits, int64_t* n_items,
+                 int64_t* n_splits, int64_t* n_slots);
+
+/* ---------------------------------------------------------------- device: propagation
+ * One fused Scatter-ApplyEdge-Gather pass over a CSC (forward) or CSR (backward)
+ * index: for each row r, out[r] (+)= sum over e in [ptr[r], ptr[r+1]) of t_e in
+ * edge order (split rows: subgroup partials combined in fixed order).
+ * Replaces take_rows -> mul/add/sigmoid -> segment_sum (tensor.py:424-450,
+ * :204-303) and SPEC stage ops fused_gather_chunk / backward_* (SPEC.md:419-436).
+ *   G, ldg, g_off : gathered rows (second operand segment at column g_off)
+ *   R, ldr, r_off : row-side rows (may be NULL for PASS / GCN)
+ *   out0/out1     : outputs (out1 only for GGCN_BWD_SRC)
+ *   mask, ldm     : optional ReLU-backward mask: out0 = acc * (mask > 0) (tensor.py:236)
+ *   workspace     : >= sg_propagate_workspace_bytes(...) bytes of device memory
+ */
+int64_t sg_propagate_workspace_bytes(int64_t n_items, int64_t n_splits, int64_t n_slots,
+                                     int64_t F, int mode);
+int sg_propagate(int mode, int dtype, const int64_t* ptr, const int32_t* idx, const float* w,
+                 int64_t n_rows, const sg_item* items, int64_t n_items, const sg_split* splits,
+                 int64_t n_splits, int64_t n_slots, const void* G, int64_t ldg, int64_t g_off,
+                 const void* R, int64_t ldr, int64_t r_off, void* out0, int64_t ld0, void* out1,
+                 int64_t ld1, const void* mask, int64_t ldm, int64_t F, int accumulate,
+                 void* workspace, int64_t workspace_bytes, void* stream);
+
+/* Gather(max) with argmax (segment_max, tensor.py:453-484):
+ * out[r] = max over rows X[idx_e] (strict >, lowest edge position wins), -inf
+ * init, empty rows get empty_fill and argmax -1; argmax holds idx_e (int64). */
+int sg_segment_max(int dtype, const int64_t* ptr, const int32_t* idx, int64_t n_rows,
+                   const void* X, int64_t ldx, void* out, int64_t ldo, int64_t* argmax,
+                   int64_t lda, int64_t F, float empty_fill, void* stream);
+/* backward of segment_max: gx[argmax[r,f], f] = g[r, f] (gx pre-zeroed by caller). */
+int sg_segment_max_bwd(int dtype, const void* g, int64_t ldg, const int64_t* argmax, int64_t lda,
+                       int64_t n_rows, void* gx, int64_t ldx, int64_t F, void* stream);
+/* Scatter (take_rows, tensor.py:424-436): out[k] = X[idx[k]] (int64 idx, bounds
+ * checked on device: *err_flag set to 1 if any index is out of [0, n_src)). */
+int sg_take_rows(int dtype, const void* X, int64_t ldx, int64_t n_src, const int64_t* idx,
+                 int64_t n, void* out, int64_t ldo, int64_t F, int32_t* err_flag, void* stream);
+/* Stable counting sort of segment ids (int64 [n], values in [0, n_seg)) into a
+ * CSC-like (ptr [n_seg+1], perm int32 [n]); perm is stable (row order within a
+ * segment), so sg_propagate(PASS) over it equals np.add.at (tensor.py:445).
+ * Sets *err_flag if an id is out of range.  workspace >= sg_sort_workspace_bytes. */
+int64_t sg_sort_workspace_bytes(int64_t n, int64_t n_seg);
+int sg_segment_sort(const int64_t* seg, int64_t n, int64_t n_seg, int64_t* ptr, int32_t* perm,
+                    int32_t* err_flag, void* workspace, int64_t workspace_bytes, void* stream);
+
+/* ---------------------------------------------------------------- device: dense
+ * ApplyVertex GEMM (matmul, tensor.py:306-319): C[M,N] = op(A)[M,K] . op(B)[K,N],
+ * row-major; trans_a: A is stored [K,M]; trans_b: B is stored [N,K].  Epilogue
+ * RELU_DUAL also writes D = relu(C) (tensor.py:207).  Split-K reductions are
+ * deterministic (fixed order).  prec: SG_GEMM_F32 (SIMT fp32), SG_GEMM_TF32X3 /
+ * SG_GEMM_BF16 (tcgen05 tensor cores, TMEM accumulators). */
+int64_t sg_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K, int prec);
+int sg_gemm(int prec, int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, const float* A,
+            int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc, int epilogue,
+            float* D, int64_t ldd, void* workspace, int64_t workspace_bytes, void* stream);
+
+/* Softmax cross-entropy head (tensor.py:487-506) on logits = relu(Z) when
+ * relu_input (the last layer's ReLU) else Z: writes the mean
+ * loss to *loss (device fp32 scalar) and dZ = seed * (p - onehot) / n, times the
+ * ReLU mask when relu_input.  labels int64 [n]; *err_flag <- 1 on a bad label. */
+int64_t sg_xent_workspace_bytes(int64_t n);
+int sg_softmax_xent(const float* Z, int64_t ldz, int relu_input, const int64_t* labels, int64_t n,
+                    int64_t C, float* loss, float* dZ, int64_t lddz, int32_t* err_flag,
+                    void* workspace, int64_t workspace_bytes, void* stream);
+
+/* Plain gradient descent W <- W - lr * dW. */
+int sg_sgd(float* W, const float* dW, int64_t n, float lr, void* stream);
+/* Strict mode (tensor.py:18-19, :161-163): *flag |= 1 if any non-finite element. */
+int sg_check_finite(int dtype, const void* X, int64_t rows, int64_t cols, int64_t ld,
+                    int32_t* flag, void* stream);
+/* Elementwise ops used by unfused ApplyEdge programs (tensor.py:204-303):
+ * op 0 add, 1 sub, 2 mul, 3 div, 4 max, 5 sigmoid, 6 tanh, 7 relu, 8 relu-backward
+ * (a * (b > 0), tensor.py:236); b is broadcast
+ * per row when b_cols == 1 (the "b_row" kind, tensor.py:184-185), along the
+ * leading axis when b_rows == 1 ("b_lead"). */
+int sg_ewise(int op, int64_t rows, int64_t cols, const float* a, int64_t lda, const float* b,
+             int64_t b_rows, int64_t b_cols, int64_t ldb, float* out, int64_t ldo, void* stream);
+/* fp32 <-> bf16 row copy with padding (feature staging). */
+int sg_convert(int src_dtype, int dst_dtype, const void* X, int64_t ldx, void* Y, int64_t ldy,
+               int64_t rows, int64_t cols, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SAGANN_H */

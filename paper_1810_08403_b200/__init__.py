@@ -1,0 +1,36 @@
+"""B200-native SAGA-NN layer hot path (NGra, arXiv 1810.08403).
+
+Drop-in for the reference's SAGA-NN path: the ``tensor.py`` primitive names
+(``ops``), the SAGA-NN front end and model zoo (``program``), the graph store
+(``graph``) and the chunk-dataflow executor (``engine``), all running on the
+hand-written sm_100a kernels of ``libsagann.so`` (C-ABI: include/sagann.h).
+"""
+
+from . import errors
+from ._lib import lib as _native  # noqa: F401  (fails loudly if libsagann.so is missing)
+from .errors import (BudgetError, ConfigError, EngineError, GraphFormatError, NumericError,
+                     ProgramError, ShapeError)
+from .graph import (ChunkGrid, Graph, Partition, partition_2d, reencode_balance, rmat_graph,
+                    synthetic_features, uniform_graph)
+from .program import (FusedGather, LayerProgram, PassReport, build_commnet, build_gcn, build_ggcn,
+                      evaluate_expr, fuse_sag, hoist_vertex_computation, make_program, matmul_rows,
+                      optimize, trace_udf, validate_program)
+
+__all__ = [
+    "errors", "BudgetError", "ConfigError", "EngineError", "GraphFormatError", "NumericError",
+    "ProgramError", "ShapeError", "ChunkGrid", "Graph", "Partition", "partition_2d",
+    "reencode_balance", "rmat_graph", "synthetic_features", "uniform_graph", "FusedGather",
+    "LayerProgram", "PassReport", "build_commnet", "build_gcn", "build_ggcn", "evaluate_expr",
+    "fuse_sag", "hoist_vertex_computation", "make_program", "matmul_rows", "optimize", "trace_udf",
+    "validate_program", "SAGAModel", "gcn_model", "ggcn_model", "run_train",
+]
+
+
+def __getattr__(name):
+    # the executor needs torch + CUDA; import it lazily so the host-side graph store
+    # and front end stay importable on a CPU-only machine
+    if name in ("SAGAModel", "gcn_model", "ggcn_model", "run_train"):
+        from . import engine
+
+        return getattr(engine, name)
+    raise AttributeError(name)

@@ -1,0 +1,225 @@
+// Loss head, optimizer step, strict-mode check, elementwise ApplyEdge ops, dtype staging.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "common.h"
+
+namespace {
+
+int grid_for(int64_t work, int per_block) {
+  int64_t g = (work + per_block - 1) / per_block;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(g, 148 * 32));
+}
+
+// softmax_cross_entropy (tensor.py:487-506): one warp per row.
+__global__ void xent_rows_kernel(const float* Z, int64_t ldz, int relu_input, const int64_t* lab,
+                                 int64_t n, int64_t C, float* dZ, int64_t lddz, float* logp_out,
+                                 int32_t* err) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const float inv_n = 1.0f / (float)n;
+  for (int64_t r = warp; r < n; r += nwarps) {
+    const float* z = Z + r * ldz;
+    int64_t l = lab[r];
+    if (l < 0 || l >= C) {
+      if (lane == 0) atomicOr(err, 1);
+      l = 0;
+    }
+    float zmax = -INFINITY;
+    for (int64_t c = lane; c < C; c += 32) {
+      float v = z[c];
+      if (relu_input) v = fmaxf(v, 0.f);
+      zmax = fmaxf(zmax, v);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) zmax = fmaxf(zmax, __shfl_xor_sync(0xffffffffu, zmax, o));
+    float denom = 0.f;
+    for (int64_t c = lane; c < C; c += 32) {
+      float v = z[c];
+      if (relu_input) v = fmaxf(v, 0.f);
+      denom += expf(v - zmax);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) denom += __shfl_xor_sync(0xffffffffu, denom, o);
+    const float logd = logf(denom);
+    for (int64_t c = lane; c < C; c += 32) {
+      const float zc = z[c];
+      const float v = relu_input ? fmaxf(zc, 0.f) : zc;
+      const float p = expf(v - zmax) / denom;
+      float g = (p - (c == l ? 1.f : 0.f)) * inv_n;     // g * (p - onehot) / n, g = 1
+      if (relu_input) g = g * (zc > 0.f ? 1.f : 0.f);   // relu bwd (tensor.py:236)
+      dZ[r * lddz + c] = g;
+      if (c == l) logp_out[r] = (v - zmax) - logd;
+    }
+  }
+}
+
+// Deterministic mean: one block, fixed per-thread strided order, fixed tree.
+__global__ void xent_mean_kernel(const float* logp, int64_t n, float* loss) {
+  __shared__ double s[1024];
+  double acc = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) acc += (double)logp[i];
+  s[threadIdx.x] = acc;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) s[threadIdx.x] += s[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *loss = (float)(-s[0] / (double)n);
+}
+
+__global__ void sgd_kernel(float* W, const float* dW, int64_t n, float lr) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    W[i] = __fsub_rn(W[i], __fmul_rn(lr, dW[i]));  // W - lr * g
+}
+
+template <typename T>
+__device__ __forceinline__ float to_f(T v);
+template <>
+__device__ __forceinline__ float to_f<float>(float v) { return v; }
+template <>
+__device__ __forceinline__ float to_f<__nv_bfloat16>(__nv_bfloat16 v) { return __bfloat162float(v); }
+
+template <typename T>
+__global__ void finite_kernel(const T* X, int64_t rows, int64_t cols, int64_t ld, int32_t* flag) {
+  const int64_t total = rows * cols;
+  int bad = 0;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const float v = to_f<T>(X[(t / cols) * ld + t % cols]);
+    bad |= !isfinite(v);
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
+__global__ void ewise_kernel(int op, int64_t rows, int64_t cols, const float* a, int64_t lda,
+                             const float* b, int64_t b_rows, int64_t b_cols, int64_t ldb, float* out,
+                             int64_t ldo) {
+  const int64_t total = rows * cols;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = t / cols, c = t % cols;
+    const float x = a[r * lda + c];
+    float y = 0.f, w = 0.f;
+    if (op <= 4 || op == 8) w = b[(b_rows == 1 ? 0 : r) * ldb + (b_cols == 1 ? 0 : c)];
+    switch (op) {  // tensor.py:204-303
+      case 0: y = __fadd_rn(x, w); break;
+      case 1: y = __fsub_rn(x, w); break;
+      case 2: y = __fmul_rn(x, w); break;
+      case 3: y = __fdiv_rn(x, w); break;
+      case 4: y = x >= w ? x : w; break;
+      case 5: y = __fdiv_rn(1.0f, __fadd_rn(1.0f, expf(-x))); break;
+      case 6: y = tanhf(x); break;
+      case 7: y = fmaxf(x, 0.f); break;
+      default: y = __fmul_rn(x, w > 0.f ? 1.f : 0.f); break;  // relu bwd: g * (z > 0)
+    }
+    out[r * ldo + c] = y;
+  }
+}
+
+template <typename S, typename D>
+__device__ __forceinline__ D cvt(S v);
+template <>
+__device__ __forceinline__ float cvt<float, float>(float v) { return v; }
+template <>
+__device__ __forceinline__ __nv_bfloat16 cvt<float, __nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
+template <>
+__device__ __forceinline__ float cvt<__nv_bfloat16, float>(__nv_bfloat16 v) { return __bfloat162float(v); }
+template <>
+__device__ __forceinline__ __nv_bfloat16 cvt<__nv_bfloat16, __nv_bfloat16>(__nv_bfloat16 v) { return v; }
+
+template <typename S, typename D>
+__global__ void convert_kernel(const S* X, int64_t ldx, D* Y, int64_t ldy, int64_t rows, int64_t cols) {
+  const int64_t total = rows * cols;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = t / cols, c = t % cols;
+    Y[r * ldy + c] = cvt<S, D>(X[r * ldx + c]);
+  }
+}
+
+#define SG_LAUNCH_CHECK(what)                                                  \
+  do {                                                                         \
+    cudaError_t e_ = cudaGetLastError();                                       \
+    if (e_ != cudaSuccess) SG_FAIL(SG_ECUDA, "%s: %s", what, cudaGetErrorString(e_)); \
+  } while (0)
+
+}  // namespace
+
+extern "C" {
+
+int64_t sg_xent_workspace_bytes(int64_t n) { return std::max<int64_t>(n, 1) * 4; }
+
+int sg_softmax_xent(const float* Z, int64_t ldz, int relu_input, const int64_t* labels, int64_t n,
+                    int64_t C, float* loss, float* dZ, int64_t lddz, int32_t* err_flag,
+                    void* workspace, int64_t workspace_bytes, void* stream) {
+  SG_REQUIRE(n >= 1 && C >= 1, SG_ESHAPE, "logits must be [n, classes] with n, classes >= 1");
+  SG_REQUIRE(workspace_bytes >= sg_xent_workspace_bytes(n), SG_EBUDGET, "xent workspace too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  float* logp = (float*)workspace;
+  xent_rows_kernel<<<grid_for(n * 32, 256), 256, 0, st>>>(Z, ldz, relu_input, labels, n, C, dZ,
+                                                         lddz, logp, err_flag);
+  SG_LAUNCH_CHECK("xent rows");
+  xent_mean_kernel<<<1, 1024, 0, st>>>(logp, n, loss);
+  SG_LAUNCH_CHECK("xent mean");
+  sg::count_launch(2);
+  return SG_OK;
+}
+
+int sg_sgd(float* W, const float* dW, int64_t n, float lr, void* stream) {
+  if (n == 0) return SG_OK;
+  sgd_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(W, dW, n, lr);
+  SG_LAUNCH_CHECK("sgd");
+  sg::count_launch(1);
+  return SG_OK;
+}
+
+int sg_check_finite(int dtype, const void* X, int64_t rows, int64_t cols, int64_t ld, int32_t* flag,
+                    void* stream) {
+  if (rows == 0 || cols == 0) return SG_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int g = grid_for(rows * cols, 256);
+  if (dtype == SG_F32)
+    finite_kernel<float><<<g, 256, 0, st>>>((const float*)X, rows, cols, ld, flag);
+  else
+    finite_kernel<__nv_bfloat16><<<g, 256, 0, st>>>((const __nv_bfloat16*)X, rows, cols, ld, flag);
+  SG_LAUNCH_CHECK("check_finite");
+  sg::count_launch(1);
+  return SG_OK;
+}
+
+int sg_ewise(int op, int64_t rows, int64_t cols, const float* a, int64_t lda, const float* b,
+             int64_t b_rows, int64_t b_cols, int64_t ldb, float* out, int64_t ldo, void* stream) {
+  SG_REQUIRE(op >= 0 && op <= 8, SG_EINVAL, "ewise: unknown op %d", op);
+  SG_REQUIRE((op > 4 && op != 8) || b, SG_EINVAL, "ewise: binary op needs b");
+  if (rows == 0 || cols == 0) return SG_OK;
+  ewise_kernel<<<grid_for(rows * cols, 256), 256, 0, (cudaStream_t)stream>>>(
+      op, rows, cols, a, lda, b, b_rows, b_cols, ldb, out, ldo);
+  SG_LAUNCH_CHECK("ewise");
+  sg::count_launch(1);
+  return SG_OK;
+}
+
+int sg_convert(int sdt, int ddt, const void* X, int64_t ldx, void* Y, int64_t ldy, int64_t rows,
+               int64_t cols, void* stream) {
+  if (rows == 0 || cols == 0) return SG_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int g = grid_for(rows * cols, 256);
+  if (sdt == SG_F32 && ddt == SG_BF16)
+    convert_kernel<float, __nv_bfloat16><<<g, 256, 0, st>>>((const float*)X, ldx, (__nv_bfloat16*)Y, ldy, rows, cols);
+  else if (sdt == SG_BF16 && ddt == SG_F32)
+    convert_kernel<__nv_bfloat16, float><<<g, 256, 0, st>>>((const __nv_bfloat16*)X, ldx, (float*)Y, ldy, rows, cols);
+  else if (sdt == SG_F32)
+    convert_kernel<float, float><<<g, 256, 0, st>>>((const float*)X, ldx, (float*)Y, ldy, rows, cols);
+  else
+    convert_kernel<__nv_bfloat16, __nv_bfloat16><<<g, 256, 0, st>>>((const __nv_bfloat16*)X, ldx, (__nv_bfloat16*)Y, ldy, rows, cols);
+  SG_LAUNCH_CHECK("convert");
+  sg::count_launch(1);
+  return SG_OK;
+}
+
+}  // extern "C"

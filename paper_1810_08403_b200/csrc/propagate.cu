@@ -1,0 +1,519 @@
+// Fused Scatter-ApplyEdge-Gather propagation kernels for sm_100a (K1-K7).
+//
+// One persistent-warp kernel template covers every SAGA-NN propagation pass on
+// the hot path: GCN forward over CSC, GCN backward dual
+// over the transposed (CSR) index with a fused ReLU-mask epilogue, passthrough
+// segment_sum, and the three G-GCN gated passes.  Edge tensors never touch HBM:
+// each warp walks the edges of its rows, loads source-feature rows with 128-bit
+// loads (feature dimension across lanes -> coalesced), evaluates the ApplyEdge
+// function in registers and accumulates in fp32 registers.
+//
+// Determinism / parity: per destination row the edge terms are added one by one
+// in CSC (or CSR) order with IEEE round-to-nearest mul/add (this file is built
+// with -fmad=false and uses explicit __f*_rn intrinsics), which is exactly the
+// sequential np.add.at of segment_sum (tensor.py:445) and take_rows' backward
+// (tensor.py:433).  Rows with more than T edges are split into consecutive
+// subgroups: each subgroup's partial is summed from
+// 0 into a workspace slot, and the last subgroup to finish (atomic ticket)
+// combines the partials in subgroup order -- a fixed order, so results are
+// identical run to run and to oracle/saga.py:seq_sum_rows.  No float atomics.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cub/cub.cuh>
+
+#include "common.h"
+#include "vecio.cuh"
+
+namespace {
+using sg::VecIO;
+
+constexpr int kWarpsPerBlock = 8;
+
+// ------------------------------------------------------------------ modes
+template <int MODE>
+struct ModeT;
+
+template <>
+struct ModeT<SG_PROP_PASS> {
+  static constexpr int NG = 1, NR = 0, NOUT = 1;
+  static constexpr bool USE_W = false;
+  static __device__ __forceinline__ void term(const float* g0, const float*, const float*,
+                                              const float*, float, float* t0, float*) {
+    t0[0] = g0[0];
+  }
+};
+
+template <>
+struct ModeT<SG_PROP_GCN> {
+  static constexpr int NG = 1, NR = 0, NOUT = 1;
+  static constexpr bool USE_W = true;
+  // mul(take_rows(H, src), w): x * w (tensor.py:249); mul bwd g * w (tensor.py:263)
+  static __device__ __forceinline__ void term(const float* g0, const float*, const float*,
+                                              const float*, float w, float* t0, float*) {
+    t0[0] = __fmul_rn(g0[0], w);
+  }
+};
+
+__device__ __forceinline__ float sigmoid_ref(float x) {
+  // 1.0 / (1.0 + np.exp(-x))  (tensor.py:205)
+  return __fdiv_rn(1.0f, __fadd_rn(1.0f, expf(-x)));
+}
+
+template <>
+struct ModeT<SG_PROP_GGCN_FWD> {
+  static constexpr int NG = 2, NR = 1, NOUT = 1;
+  static constexpr bool USE_W = false;
+  // G = [h | P] row of v, R = Q row of u: eta = sigmoid(P[v] + Q[u]); t = eta * h[v]
+  static __device__ __forceinline__ void term(const float* g0, const float* g1, const float* r0,
+                                              const float*, float, float* t0, float*) {
+    float eta = sigmoid_ref(__fadd_rn(g1[0], r0[0]));
+    t0[0] = __fmul_rn(eta, g0[0]);
+  }
+};
+
+template <>
+struct ModeT<SG_PROP_GGCN_BWD_DST> {
+  static constexpr int NG = 2, NR = 2, NOUT = 1;
+  static constexpr bool USE_W = false;
+  // CSC row u.  G = [h | P] of v, R = [dA | Q] of u.
+  // g_eta = dA[u] * h[v] (mul bwd, tensor.py:263); t = (g_eta * eta) * (1 - eta) (tensor.py:232)
+  static __device__ __forceinline__ void term(const float* g0, const float* g1, const float* r0,
+                                              const float* r1, float, float* t0, float*) {
+    float eta = sigmoid_ref(__fadd_rn(g1[0], r1[0]));
+    float ge = __fmul_rn(r0[0], g0[0]);
+    t0[0] = __fmul_rn(__fmul_rn(ge, eta), __fsub_rn(1.0f, eta));
+  }
+};
+
+template <>
+struct ModeT<SG_PROP_GGCN_BWD_SRC> {
+  static constexpr int NG = 2, NR = 2, NOUT = 2;
+  static constexpr bool USE_W = false;
+  // CSR row v.  G = [dA | Q] of u, R = [h | P] of v.
+  // dP[v] += (dA[u]*h[v]*eta)*(1-eta);  dH[v] += dA[u] * eta  (g_hs = g * eta)
+  static __device__ __forceinline__ void term(const float* g0, const float* g1, const float* r0,
+                                              const float* r1, float, float* t0, float* t1) {
+    float eta = sigmoid_ref(__fadd_rn(r1[0], g1[0]));
+    float ge = __fmul_rn(g0[0], r0[0]);
+    t0[0] = __fmul_rn(__fmul_rn(ge, eta), __fsub_rn(1.0f, eta));
+    t1[0] = __fmul_rn(g0[0], eta);
+  }
+};
+
+struct PropArgs {
+  const int64_t* ptr;
+  const int32_t* idx;
+  const float* w;
+  const sg_item* items;
+  const sg_split* splits;
+  float* partial;       // [NOUT][n_slots][pld] fp32
+  int64_t pld, n_slots;
+  int32_t* counters;    // [n_splits]
+  int32_t* queue;       // work-queue ticket
+  const void* G;
+  int64_t ldg, g_off;
+  const void* R;
+  int64_t ldr, r_off;
+  void* out0;
+  int64_t ld0;
+  void* out1;
+  int64_t ld1;
+  const void* mask;
+  int64_t ldm;
+  int32_t n_items;
+  int32_t Fv;        // vectors per row in this column slice
+  int32_t Fcols;     // valid columns in this column slice
+  int32_t accumulate;
+};
+
+template <int MODE, int DT, int W, int VPL, int LPR, int DEPTH>
+struct Prop {
+  using M = ModeT<MODE>;
+  using IO = VecIO<DT, W>;
+  static constexpr int NG = M::NG, NR = M::NR, NOUT = M::NOUT;
+
+  // Load the lane's slice of DEPTH gathered rows, then add their terms in edge order.
+  static __device__ __forceinline__ void step(const PropArgs& a, const int (&s)[DEPTH],
+                                              const float (&wv)[DEPTH], int n,
+                                              const float (&rs)[NR > 0 ? NR : 1][VPL][W],
+                                              float (&acc)[NOUT][VPL][W], int tl) {
+    float g[DEPTH][NG][VPL][W];
+#pragma unroll
+    for (int d = 0; d < DEPTH; ++d) {
+      if (d < n) {
+        const int64_t rowoff = (int64_t)s[d] * a.ldg;
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) {
+          const int cv = v * LPR + tl;
+          if (cv < a.Fv) {
+#pragma unroll
+            for (int q = 0; q < NG; ++q)
+              IO::ld_nc(a.G, rowoff + (q ? a.g_off : 0) + (int64_t)cv * W, g[d][q][v]);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int d = 0; d < DEPTH; ++d) {
+      if (d < n) {
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) {
+#pragma unroll
+          for (int k = 0; k < W; ++k) {
+            float t0, t1 = 0.f;
+            M::term(&g[d][0][v][k], &g[d][NG - 1][v][k], &rs[0][v][k], &rs[NR > 1 ? 1 : 0][v][k],
+                    wv[d], &t0, &t1);
+            acc[0][v][k] = __fadd_rn(acc[0][v][k], t0);
+            if (NOUT > 1) acc[NOUT - 1][v][k] = __fadd_rn(acc[NOUT - 1][v][k], t1);
+          }
+        }
+      }
+    }
+  }
+
+  // Sequentially accumulate edges [e0, e1) of one row into acc (team-cooperative).
+  static __device__ __forceinline__ void run_edges(const PropArgs& a, int64_t e0, int64_t e1,
+                                                   const float (&rs)[NR > 0 ? NR : 1][VPL][W],
+                                                   float (&acc)[NOUT][VPL][W], unsigned tmask,
+                                                   int tl) {
+    if constexpr (LPR == 32) {
+      // warp-wide index window: 32 (src, w) pairs loaded coalesced, broadcast by shuffle
+      for (int64_t eb = e0; eb < e1; eb += 32) {
+        const int n = (int)min((int64_t)32, e1 - eb);
+        int my_src = 0;
+        float my_w = 0.f;
+        if (tl < n) {
+          my_src = __ldcs(a.idx + eb + tl);
+          if (M::USE_W) my_w = __ldcs(a.w + eb + tl);
+        }
+        for (int d0 = 0; d0 < n; d0 += DEPTH) {
+          int s[DEPTH];
+          float wv[DEPTH];
+#pragma unroll
+          for (int d = 0; d < DEPTH; ++d) {
+            s[d] = __shfl_sync(tmask, my_src, (d0 + d) & 31);
+            wv[d] = M::USE_W ? __shfl_sync(tmask, my_w, (d0 + d) & 31) : 0.f;
+          }
+          step(a, s, wv, n - d0, rs, acc, tl);
+        }
+      }
+    } else {
+      // narrow rows: every team lane reads the (broadcast) index directly
+      for (int64_t e = e0; e < e1; e += DEPTH) {
+        const int n = (int)min((int64_t)DEPTH, e1 - e);
+        int s[DEPTH];
+        float wv[DEPTH];
+#pragma unroll
+        for (int d = 0; d < DEPTH; ++d) {
+          s[d] = d < n ? __ldcs(a.idx + e + d) : 0;
+          wv[d] = (M::USE_W && d < n) ? __ldcs(a.w + e + d) : 0.f;
+        }
+        step(a, s, wv, n, rs, acc, tl);
+      }
+    }
+    (void)tmask;
+  }
+
+  static __device__ __forceinline__ void load_row_state(const PropArgs& a, int64_t r, int tl,
+                                                        float (&rs)[NR > 0 ? NR : 1][VPL][W]) {
+    if (NR == 0) return;
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) {
+      const int cv = v * LPR + tl;
+      if (cv < a.Fv) {
+#pragma unroll
+        for (int q = 0; q < NR; ++q)
+          IO::ld_cs(a.R, r * a.ldr + (q ? a.r_off : 0) + (int64_t)cv * W, rs[q][v]);
+      }
+    }
+  }
+
+  static __device__ __forceinline__ void init_acc(const PropArgs& a, int64_t r, int tl,
+                                                  float (&acc)[NOUT][VPL][W], bool from_out) {
+#pragma unroll
+    for (int o = 0; o < NOUT; ++o)
+#pragma unroll
+      for (int v = 0; v < VPL; ++v)
+#pragma unroll
+        for (int k = 0; k < W; ++k) acc[o][v][k] = 0.f;
+    if (!from_out) return;
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) {
+      const int cv = v * LPR + tl;
+      if (cv < a.Fv) {
+        IO::ld_cs(a.out0, r * a.ld0 + (int64_t)cv * W, acc[0][v]);
+        if (NOUT > 1) IO::ld_cs(a.out1, r * a.ld1 + (int64_t)cv * W, acc[NOUT - 1][v]);
+      }
+    }
+  }
+
+  static __device__ __forceinline__ void store_row(const PropArgs& a, int64_t r, int tl,
+                                                   float (&acc)[NOUT][VPL][W]) {
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) {
+      const int cv = v * LPR + tl;
+      if (cv < a.Fv) {
+        const int nvalid = min(W, a.Fcols - cv * W);
+        if (a.mask) {
+          float m[W];
+          IO::ld_cs(a.mask, r * a.ldm + (int64_t)cv * W, m);
+#pragma unroll
+          for (int k = 0; k < W; ++k)  // relu bwd: g * (x > 0.0)  (tensor.py:236)
+            acc[0][v][k] = __fmul_rn(acc[0][v][k], m[k] > 0.f ? 1.f : 0.f);
+        }
+        IO::st(a.out0, r * a.ld0 + (int64_t)cv * W, acc[0][v], nvalid);
+        if (NOUT > 1) IO::st(a.out1, r * a.ld1 + (int64_t)cv * W, acc[NOUT - 1][v], nvalid);
+      }
+    }
+  }
+};
+
+template <int MODE, int DT, int W, int VPL, int LPR, int DEPTH>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+    prop_kernel(const PropArgs a) {
+  using K = Prop<MODE, DT, W, VPL, LPR, DEPTH>;
+  constexpr int NOUT = K::NOUT;
+  constexpr int NRr = K::NR > 0 ? K::NR : 1;
+  constexpr int NT = 32 / LPR;
+  const int lane = threadIdx.x & 31;
+  const int team = lane / LPR, tl = lane % LPR;
+  const unsigned tmask = LPR == 32 ? 0xffffffffu : (((1u << LPR) - 1u) << (team * LPR));
+
+  for (;;) {
+    int it = 0;
+    if (lane == 0) it = atomicAdd(a.queue, 1);
+    it = __shfl_sync(0xffffffffu, it, 0);
+    if (it >= a.n_items) break;
+    const sg_item item = a.items[it];
+    if (item.split < 0) {
+      for (int r = item.row_begin + team; r < item.row_end; r += NT) {
+        float rs[NRr][VPL][W];
+        float acc[NOUT][VPL][W];
+        K::load_row_state(a, r, tl, rs);
+        K::init_acc(a, r, tl, acc, a.accumulate != 0);
+        K::run_edges(a, __ldg(a.ptr + r), __ldg(a.ptr + r + 1), rs, acc, tmask, tl);
+        K::store_row(a, r, tl, acc);
+      }
+    } else {
+      const sg_split sp = a.splits[item.split];
+      const int64_t r = item.row_begin;
+      if (team == 0) {
+        float rs[NRr][VPL][W];
+        float acc[NOUT][VPL][W];
+        K::load_row_state(a, r, tl, rs);
+        K::init_acc(a, r, tl, acc, false);
+        K::run_edges(a, item.e_begin, item.e_end, rs, acc, tmask, tl);
+        const int64_t slot = sp.slot0 + item.sub;
+#pragma unroll
+        for (int o = 0; o < NOUT; ++o)
+#pragma unroll
+          for (int v = 0; v < VPL; ++v) {
+            const int cv = v * LPR + tl;
+            if (cv < a.Fv) {
+              float* p = a.partial + ((int64_t)o * a.n_slots + slot) * a.pld + (int64_t)cv * W;
+#pragma unroll
+              for (int k = 0; k < W; ++k) __stcg(p + k, acc[o][v][k]);
+            }
+          }
+      }
+      __threadfence();
+      __syncwarp();
+      int ticket = 0;
+      if (lane == 0) ticket = atomicAdd(a.counters + item.split, 1);
+      ticket = __shfl_sync(0xffffffffu, ticket, 0);
+      if (ticket == sp.n_sub - 1) {
+        __threadfence();
+        if (team == 0) {
+          float acc[NOUT][VPL][W];
+          K::init_acc(a, r, tl, acc, a.accumulate != 0);
+          for (int s = 0; s < sp.n_sub; ++s) {
+#pragma unroll
+            for (int o = 0; o < NOUT; ++o)
+#pragma unroll
+              for (int v = 0; v < VPL; ++v) {
+                const int cv = v * LPR + tl;
+                if (cv < a.Fv) {
+                  const float* p =
+                      a.partial + ((int64_t)o * a.n_slots + sp.slot0 + s) * a.pld + (int64_t)cv * W;
+#pragma unroll
+                  for (int k = 0; k < W; ++k) acc[o][v][k] = __fadd_rn(acc[o][v][k], __ldcg(p + k));
+                }
+              }
+          }
+          K::store_row(a, r, tl, acc);
+        }
+        if (lane == 0) a.counters[item.split] = 0;
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ dispatch
+struct LaunchCfg {
+  int W, VPL, LPR;
+};
+
+int mode_nout(int mode) { return mode == SG_PROP_GGCN_BWD_SRC ? 2 : 1; }
+int mode_ng(int mode) { return mode >= SG_PROP_GGCN_FWD ? 2 : 1; }
+
+int g_sm_count = 0;
+
+int sm_count() {
+  if (!g_sm_count) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_sm_count, cudaDevAttrMultiProcessorCount, dev);
+    if (g_sm_count <= 0) g_sm_count = 148;
+  }
+  return g_sm_count;
+}
+
+template <int MODE, int DT, int W, int VPL, int LPR>
+cudaError_t launch_one(const PropArgs& a, cudaStream_t st) {
+  constexpr int NG = ModeT<MODE>::NG;
+  constexpr int DEPTH = (VPL * NG) <= 4 ? 8 / (VPL * NG) : 2;
+  auto kern = prop_kernel<MODE, DT, W, VPL, LPR, DEPTH>;
+  static int blocks_per_sm = 0;
+  if (!blocks_per_sm) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, kWarpsPerBlock * 32, 0);
+    if (blocks_per_sm <= 0) blocks_per_sm = 1;
+  }
+  int64_t want = ((int64_t)a.n_items + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  int64_t cap = (int64_t)blocks_per_sm * sm_count();
+  int grid = (int)std::max<int64_t>(1, std::min(want, cap));
+  kern<<<grid, kWarpsPerBlock * 32, 0, st>>>(a);
+  sg::count_launch();
+  return cudaGetLastError();
+}
+
+// Widest vectors-per-lane instantiated: register pressure grows as VPL * W * (NG + NOUT);
+// wider rows are processed in column slices.
+constexpr int vpl_max(int mode, int dt) {
+  return (dt == SG_F32 && (mode == SG_PROP_PASS || mode == SG_PROP_GCN)) ? 8 : 4;
+}
+
+template <int MODE, int DT, int W>
+cudaError_t dispatch_vpl(const PropArgs& a, int LPR, int VPL, cudaStream_t st) {
+  constexpr int VMAX = vpl_max(MODE, DT);
+  if (LPR < 32) {
+    switch (LPR) {
+      case 2: return launch_one<MODE, DT, W, 1, 2>(a, st);
+      case 4: return launch_one<MODE, DT, W, 1, 4>(a, st);
+      case 8: return launch_one<MODE, DT, W, 1, 8>(a, st);
+      default: return launch_one<MODE, DT, W, 1, 16>(a, st);
+    }
+  }
+  switch (VPL) {
+    case 1: return launch_one<MODE, DT, W, 1, 32>(a, st);
+    case 2: return launch_one<MODE, DT, W, 2, 32>(a, st);
+    case 3: return launch_one<MODE, DT, W, 3, 32>(a, st);
+    case 4: return launch_one<MODE, DT, W, 4, 32>(a, st);
+    case 5: return launch_one<MODE, DT, W, (VMAX >= 5 ? 5 : 4), 32>(a, st);
+    case 6: return launch_one<MODE, DT, W, (VMAX >= 6 ? 6 : 4), 32>(a, st);
+    case 7: return launch_one<MODE, DT, W, (VMAX >= 7 ? 7 : 4), 32>(a, st);
+    default: return launch_one<MODE, DT, W, (VMAX >= 8 ? 8 : 4), 32>(a, st);
+  }
+}
+
+template <int MODE>
+cudaError_t dispatch_mode(int dtype, bool vec, const PropArgs& a, int LPR, int VPL, cudaStream_t st) {
+  if (dtype == SG_F32)
+    return vec ? dispatch_vpl<MODE, SG_F32, 4>(a, LPR, VPL, st)
+               : dispatch_vpl<MODE, SG_F32, 1>(a, LPR, VPL, st);
+  return vec ? dispatch_vpl<MODE, SG_BF16, 8>(a, LPR, VPL, st)
+             : dispatch_vpl<MODE, SG_BF16, 1>(a, LPR, VPL, st);
+}
+
+inline bool aligned(const void* p, int bytes) { return p == nullptr || ((uintptr_t)p % bytes) == 0; }
+
+inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+}  // namespace
+
+extern "C" {
+
+int sg_device_sm_count(int device, int* out) {
+  cudaError_t e = cudaDeviceGetAttribute(out, cudaDevAttrMultiProcessorCount, device);
+  if (e != cudaSuccess) SG_FAIL(SG_ECUDA, "cudaDeviceGetAttribute: %s", cudaGetErrorString(e));
+  return SG_OK;
+}
+
+int64_t sg_propagate_workspace_bytes(int64_t n_items, int64_t n_splits, int64_t n_slots, int64_t F,
+                                     int mode) {
+  (void)n_items;
+  return 256 + align_up(4 * std::max<int64_t>(n_splits, 1), 256) +
+         (int64_t)mode_nout(mode) * n_slots * align_up(std::max<int64_t>(F, 1), 8) * 4;
+}
+
+int sg_propagate(int mode, int dtype, const int64_t* ptr, const int32_t* idx, const float* w,
+                 int64_t n_rows, const sg_item* items, int64_t n_items, const sg_split* splits,
+                 int64_t n_splits, int64_t n_slots, const void* G, int64_t ldg, int64_t g_off,
+                 const void* R, int64_t ldr, int64_t r_off, void* out0, int64_t ld0, void* out1,
+                 int64_t ld1, const void* mask, int64_t ldm, int64_t F, int accumulate,
+                 void* workspace, int64_t workspace_bytes, void* stream) {
+  SG_REQUIRE(mode >= SG_PROP_PASS && mode <= SG_PROP_GGCN_BWD_SRC, SG_EINVAL, "bad mode %d", mode);
+  SG_REQUIRE(dtype == SG_F32 || dtype == SG_BF16, SG_EINVAL, "bad dtype %d", dtype);
+  SG_REQUIRE(n_items >= 0 && n_items <= INT32_MAX, SG_EINVAL, "bad n_items");
+  if (n_rows == 0 || F == 0 || n_items == 0) return SG_OK;
+  SG_REQUIRE(ptr && idx && items && G && out0, SG_EINVAL, "null required pointer");
+  SG_REQUIRE(mode != SG_PROP_GCN || w, SG_EINVAL, "GCN mode needs edge weights");
+  SG_REQUIRE(mode < SG_PROP_GGCN_FWD || R, SG_EINVAL, "gated modes need row-side operand R");
+  SG_REQUIRE(mode != SG_PROP_GGCN_BWD_SRC || out1, SG_EINVAL, "GGCN_BWD_SRC needs out1");
+  SG_REQUIRE(n_splits == 0 || splits, SG_EINVAL, "split records missing");
+  const int64_t need = sg_propagate_workspace_bytes(n_items, n_splits, n_slots, F, mode);
+  SG_REQUIRE(workspace && workspace_bytes >= need, SG_EBUDGET,
+             "propagate workspace too small: %lld < %lld bytes", (long long)workspace_bytes,
+             (long long)need);
+  const int VW = dtype == SG_F32 ? 4 : 8;
+  const int esz = dtype == SG_F32 ? 4 : 2;
+  bool vec = (ldg % VW == 0) && (g_off % VW == 0) && (ld0 % VW == 0) && aligned(G, 16) &&
+             aligned(out0, 16);
+  if (R) vec = vec && (ldr % VW == 0) && (r_off % VW == 0) && aligned(R, 16);
+  if (out1) vec = vec && (ld1 % VW == 0) && aligned(out1, 16);
+  if (mask) vec = vec && (ldm % VW == 0) && aligned(mask, 16);
+  const int W = vec ? VW : 1;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+
+  char* ws = static_cast<char*>(workspace);
+  int32_t* queue = reinterpret_cast<int32_t*>(ws);
+  int32_t* counters = reinterpret_cast<int32_t*>(ws + 256);
+  float* partial = reinterpret_cast<float*>(ws + 256 + align_up(4 * std::max<int64_t>(n_splits, 1), 256));
+  const int64_t pld = align_up(F, 8);
+
+  // column slices of at most 32 lanes x vpl_max vectors
+  const int64_t slice_cols = (int64_t)32 * vpl_max(mode, dtype) * W;
+  for (int64_t c0 = 0; c0 < F; c0 += slice_cols) {
+    const int64_t cols = std::min(slice_cols, F - c0);
+    const int Fv = (int)((cols + W - 1) / W);
+    int LPR = 32, VPL = (Fv + 31) / 32;
+    if (Fv <= 16) {
+      LPR = 2;
+      while (LPR < Fv) LPR *= 2;
+      VPL = 1;
+    }
+    PropArgs a;
+    a.ptr = ptr; a.idx = idx; a.w = w; a.items = items; a.splits = splits;
+    a.partial = partial + c0; a.pld = pld; a.n_slots = n_slots;
+    a.counters = counters; a.queue = queue;
+    a.G = static_cast<const char*>(G) + c0 * esz; a.ldg = ldg; a.g_off = g_off;
+    a.R = R ? static_cast<const char*>(R) + c0 * esz : nullptr; a.ldr = ldr; a.r_off = r_off;
+    a.out0 = static_cast<char*>(out0) + c0 * esz; a.ld0 = ld0;
+    a.out1 = out1 ? static_cast<char*>(out1) + c0 * esz : nullptr; a.ld1 = ld1;
+    a.mask = mask ? static_cast<const char*>(mask) + c0 * esz : nullptr; a.ldm = ldm;
+    a.n_items = (int32_t)n_items; a.Fv = Fv; a.Fcols = (int32_t)cols; a.accumulate = accumulate;
+    cudaError_t e = cudaMemsetAsync(ws, 0, 256 + align_up(4 * std::max<int64_t>(n_splits, 1), 256), st);
+    if (e != cudaSuccess) SG_FAIL(SG_ECUDA, "memset: %s", cudaGetErrorString(e));
+    switch (mode) {
+      case SG_PROP_PASS: e = dispatch_mode<SG_PROP_PASS>(dtype, vec, a, LPR, VPL, st); break;
+      case SG_PROP_GCN: e = dispatch_mode<SG_PROP_GCN>(dtype, vec, a, LPR, VPL, st); break;
+      case SG_PROP_GGCN_FWD: e = dispatch_mode<SG_PROP_GGCN_FWD>(dtype, vec, a, LPR, VPL, st); break;
+      case SG_PROP_GGCN_BWD_DST: e = dispatch_mode<SG_PROP_GGCN_BWD_DST>(dtype, vec, a, LPR, VPL, st); break;
+      default: e = dispatch_mode<SG_PROP_GGCN_BWD_SRC>(dtype, vec, a, LPR, VPL, st); break;
+    }
+    if (e != cudaSuccess) SG_FAIL(SG_ECUDA, "propagate launch: %s", cudaGetErrorString(e));
+  }
+  return SG_OK;
+}
+
+}  // extern "C"

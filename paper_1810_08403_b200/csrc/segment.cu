@@ -1,0 +1,243 @@
+// Unfused Scatter / Gather(max) primitives and the device segment sort (K1, K2, K7).
+//
+//  * sg_take_rows      -- Scatter, take_rows (tensor.py:424-436)
+//  * sg_segment_max    -- Gather(max) + argmax (tensor.py:453-484)
+//  * sg_segment_sort   -- stable segment index (ptr, perm) so that segment_sum /
+//                         take_rows backward (np.add.at, tensor.py:433, :445) run
+//                         as an ordered sg_propagate(PASS) pass.
+#include <cuda_runtime.h>
+
+#include <cub/cub.cuh>
+
+#include "common.h"
+#include "vecio.cuh"
+
+namespace {
+using sg::VecIO;
+
+template <int DT, int W>
+__global__ void take_rows_kernel(const void* X, int64_t ldx, int64_t n_src, const int64_t* idx,
+                                 int64_t n, void* out, int64_t ldo, int F, int32_t* err) {
+  using IO = VecIO<DT, W>;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int Fv = (F + W - 1) / W;
+  for (int64_t k = warp; k < n; k += nwarps) {
+    int64_t s = idx[k];
+    if (s < 0 || s >= n_src) {
+      if (lane == 0) atomicOr(err, 1);
+      continue;
+    }
+    for (int cv = lane; cv < Fv; cv += 32) {
+      float v[W];
+      IO::ld_nc(X, s * ldx + (int64_t)cv * W, v);
+      IO::st(out, k * ldo + (int64_t)cv * W, v, min(W, F - cv * W));
+    }
+  }
+}
+
+// One warp per segment; lanes over columns; strict '>' so the first (lowest
+// position) maximum wins; -inf init; empty segment -> empty_fill, argmax -1.
+template <int DT, int W>
+__global__ void segmax_kernel(const int64_t* ptr, const int32_t* idx, int64_t n_rows,
+                              const void* X, int64_t ldx, void* out, int64_t ldo, int64_t* arg,
+                              int64_t lda, int F, float fill) {
+  using IO = VecIO<DT, W>;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int Fv = (F + W - 1) / W;
+  for (int64_t r = warp; r < n_rows; r += nwarps) {
+    const int64_t e0 = ptr[r], e1 = ptr[r + 1];
+    for (int cv = lane; cv < Fv; cv += 32) {
+      float best[W];
+      int64_t barg[W];
+#pragma unroll
+      for (int k = 0; k < W; ++k) {
+        best[k] = -INFINITY;
+        barg[k] = -1;
+      }
+      for (int64_t e = e0; e < e1; ++e) {
+        const int64_t s = idx[e];
+        float v[W];
+        IO::ld_nc(X, s * ldx + (int64_t)cv * W, v);
+#pragma unroll
+        for (int k = 0; k < W; ++k)
+          if (v[k] > best[k]) {
+            best[k] = v[k];
+            barg[k] = s;
+          }
+      }
+      const int nvalid = min(W, F - cv * W);
+#pragma unroll
+      for (int k = 0; k < W; ++k) {
+        if (barg[k] < 0) best[k] = fill;
+        if (k < nvalid) arg[r * lda + (int64_t)cv * W + k] = barg[k];
+      }
+      IO::st(out, r * ldo + (int64_t)cv * W, best, nvalid);
+    }
+  }
+}
+
+template <int DT>
+__global__ void segmax_bwd_kernel(const void* g, int64_t ldg, const int64_t* arg, int64_t lda,
+                                  int64_t n_rows, void* gx, int64_t ldx, int F) {
+  using IO = VecIO<DT, 1>;
+  const int64_t total = n_rows * (int64_t)F;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = t / F, f = t % F;
+    const int64_t a = arg[r * lda + f];
+    if (a < 0) continue;
+    float v;
+    IO::ld_nc(g, r * ldg + f, &v);
+    IO::st(gx, a * ldx + f, &v, 1);  // each (row, col) has at most one argmax owner
+  }
+}
+
+__global__ void seg_keys_kernel(const int64_t* seg, int64_t n, int64_t n_seg, int32_t* keys,
+                                int32_t* vals, int32_t* err) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    int64_t s = seg[k];
+    if (s < 0 || s >= n_seg) {
+      atomicOr(err, 1);
+      s = 0;
+    }
+    keys[k] = (int32_t)s;
+    vals[k] = (int32_t)k;
+  }
+}
+
+// ptr[s] = number of sorted keys < s (lower bound), ptr[n_seg] = n.
+__global__ void seg_ptr_kernel(const int32_t* sorted, int64_t n, int64_t n_seg, int64_t* ptr) {
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s <= n_seg;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+      int64_t mid = (lo + hi) >> 1;
+      if (sorted[mid] < s) lo = mid + 1;
+      else hi = mid;
+    }
+    ptr[s] = (s == n_seg) ? n : lo;
+  }
+}
+
+inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+inline bool aligned(const void* p, int b) { return ((uintptr_t)p % b) == 0; }
+
+int end_bit_for(int64_t n_seg) {
+  int b = 1;
+  while ((int64_t(1) << b) < n_seg) ++b;
+  return b;
+}
+
+size_t cub_temp_bytes(int64_t n, int64_t n_seg) {
+  size_t bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const int32_t*)nullptr, (int32_t*)nullptr,
+                                  (const int32_t*)nullptr, (int32_t*)nullptr, (int)n, 0,
+                                  end_bit_for(n_seg));
+  return bytes;
+}
+
+int grid_for(int64_t work, int per_block) {
+  int64_t g = (work + per_block - 1) / per_block;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(g, 148 * 32));
+}
+
+}  // namespace
+
+extern "C" {
+
+int sg_take_rows(int dtype, const void* X, int64_t ldx, int64_t n_src, const int64_t* idx,
+                 int64_t n, void* out, int64_t ldo, int64_t F, int32_t* err_flag, void* stream) {
+  if (n == 0 || F == 0) return SG_OK;
+  SG_REQUIRE(X && idx && out && err_flag, SG_EINVAL, "take_rows: null pointer");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int g = grid_for(n * 32, 256);
+  if (dtype == SG_F32) {
+    if (ldx % 4 == 0 && ldo % 4 == 0 && aligned(X, 16) && aligned(out, 16))
+      take_rows_kernel<SG_F32, 4><<<g, 256, 0, st>>>(X, ldx, n_src, idx, n, out, ldo, (int)F, err_flag);
+    else
+      take_rows_kernel<SG_F32, 1><<<g, 256, 0, st>>>(X, ldx, n_src, idx, n, out, ldo, (int)F, err_flag);
+  } else {
+    if (ldx % 8 == 0 && ldo % 8 == 0 && aligned(X, 16) && aligned(out, 16))
+      take_rows_kernel<SG_BF16, 8><<<g, 256, 0, st>>>(X, ldx, n_src, idx, n, out, ldo, (int)F, err_flag);
+    else
+      take_rows_kernel<SG_BF16, 1><<<g, 256, 0, st>>>(X, ldx, n_src, idx, n, out, ldo, (int)F, err_flag);
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) SG_FAIL(SG_ECUDA, "take_rows launch: %s", cudaGetErrorString(e));
+  sg::count_launch(1);
+  return SG_OK;
+}
+
+int sg_segment_max(int dtype, const int64_t* ptr, const int32_t* idx, int64_t n_rows,
+                   const void* X, int64_t ldx, void* out, int64_t ldo, int64_t* argmax,
+                   int64_t lda, int64_t F, float empty_fill, void* stream) {
+  if (n_rows == 0 || F == 0) return SG_OK;
+  SG_REQUIRE(ptr && idx && X && out && argmax, SG_EINVAL, "segment_max: null pointer");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int g = grid_for(n_rows * 32, 256);
+  if (dtype == SG_F32) {
+    if (ldx % 4 == 0 && ldo % 4 == 0 && aligned(X, 16) && aligned(out, 16))
+      segmax_kernel<SG_F32, 4><<<g, 256, 0, st>>>(ptr, idx, n_rows, X, ldx, out, ldo, argmax, lda, (int)F, empty_fill);
+    else
+      segmax_kernel<SG_F32, 1><<<g, 256, 0, st>>>(ptr, idx, n_rows, X, ldx, out, ldo, argmax, lda, (int)F, empty_fill);
+  } else {
+    segmax_kernel<SG_BF16, 1><<<g, 256, 0, st>>>(ptr, idx, n_rows, X, ldx, out, ldo, argmax, lda, (int)F, empty_fill);
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) SG_FAIL(SG_ECUDA, "segment_max launch: %s", cudaGetErrorString(e));
+  sg::count_launch(1);
+  return SG_OK;
+}
+
+int sg_segment_max_bwd(int dtype, const void* g, int64_t ldg, const int64_t* argmax, int64_t lda,
+                       int64_t n_rows, void* gx, int64_t ldx, int64_t F, void* stream) {
+  if (n_rows == 0 || F == 0) return SG_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int grid = grid_for(n_rows * F, 256);
+  if (dtype == SG_F32)
+    segmax_bwd_kernel<SG_F32><<<grid, 256, 0, st>>>(g, ldg, argmax, lda, n_rows, gx, ldx, (int)F);
+  else
+    segmax_bwd_kernel<SG_BF16><<<grid, 256, 0, st>>>(g, ldg, argmax, lda, n_rows, gx, ldx, (int)F);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) SG_FAIL(SG_ECUDA, "segment_max_bwd launch: %s", cudaGetErrorString(e));
+  sg::count_launch(1);
+  return SG_OK;
+}
+
+int64_t sg_sort_workspace_bytes(int64_t n, int64_t n_seg) {
+  return 3 * align_up(4 * std::max<int64_t>(n, 1), 256) + align_up((int64_t)cub_temp_bytes(n, n_seg), 256) + 256;
+}
+
+int sg_segment_sort(const int64_t* seg, int64_t n, int64_t n_seg, int64_t* ptr, int32_t* perm,
+                    int32_t* err_flag, void* workspace, int64_t workspace_bytes, void* stream) {
+  SG_REQUIRE(n >= 0 && n <= INT32_MAX && n_seg >= 0 && n_seg <= INT32_MAX, SG_EINVAL,
+             "segment_sort: sizes exceed int32");
+  SG_REQUIRE(workspace_bytes >= sg_sort_workspace_bytes(n, n_seg), SG_EBUDGET,
+             "segment_sort workspace too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  char* ws = (char*)workspace;
+  const int64_t a = align_up(4 * std::max<int64_t>(n, 1), 256);
+  int32_t* keys_in = (int32_t*)ws;
+  int32_t* keys_out = (int32_t*)(ws + a);
+  int32_t* vals_in = (int32_t*)(ws + 2 * a);
+  void* temp = ws + 3 * a;
+  size_t temp_bytes = cub_temp_bytes(n, n_seg);
+  if (n > 0) {
+    seg_keys_kernel<<<grid_for(n, 256), 256, 0, st>>>(seg, n, n_seg, keys_in, vals_in, err_flag);
+    cudaError_t e = cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys_in, keys_out, vals_in,
+                                                    perm, (int)n, 0, end_bit_for(n_seg), st);
+    if (e != cudaSuccess) SG_FAIL(SG_ECUDA, "radix sort: %s", cudaGetErrorString(e));
+  }
+  seg_ptr_kernel<<<grid_for(n_seg + 1, 256), 256, 0, st>>>(keys_out, n, n_seg, ptr);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) SG_FAIL(SG_ECUDA, "segment_sort: %s", cudaGetErrorString(e));
+  sg::count_launch(2);
+  return SG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,93 @@
+// 128-bit vector loads/stores with fp32 compute for fp32 / bf16 storage.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "../../include/sagann.h"
+
+namespace sg {
+
+template <int DT, int W>
+struct VecIO;
+
+template <>
+struct VecIO<SG_F32, 4> {
+  static __device__ __forceinline__ void ld_nc(const void* base, int64_t off, float* v) {
+    float4 r = __ldg(reinterpret_cast<const float4*>(static_cast<const float*>(base) + off));
+    v[0] = r.x; v[1] = r.y; v[2] = r.z; v[3] = r.w;
+  }
+  static __device__ __forceinline__ void ld_cs(const void* base, int64_t off, float* v) {
+    float4 r = __ldcs(reinterpret_cast<const float4*>(static_cast<const float*>(base) + off));
+    v[0] = r.x; v[1] = r.y; v[2] = r.z; v[3] = r.w;
+  }
+  static __device__ __forceinline__ void st(void* base, int64_t off, const float* v, int nvalid) {
+    float* p = static_cast<float*>(base) + off;
+    if (nvalid >= 4) {
+      __stcs(reinterpret_cast<float4*>(p), make_float4(v[0], v[1], v[2], v[3]));
+    } else {
+      for (int k = 0; k < nvalid; ++k) p[k] = v[k];
+    }
+  }
+};
+
+template <>
+struct VecIO<SG_F32, 1> {
+  static __device__ __forceinline__ void ld_nc(const void* base, int64_t off, float* v) {
+    v[0] = __ldg(static_cast<const float*>(base) + off);
+  }
+  static __device__ __forceinline__ void ld_cs(const void* base, int64_t off, float* v) {
+    v[0] = __ldcs(static_cast<const float*>(base) + off);
+  }
+  static __device__ __forceinline__ void st(void* base, int64_t off, const float* v, int nvalid) {
+    if (nvalid >= 1) static_cast<float*>(base)[off] = v[0];
+  }
+};
+
+template <>
+struct VecIO<SG_BF16, 8> {
+  static __device__ __forceinline__ void unpack(uint4 r, float* v) {
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&r);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      float2 f = __bfloat1622float2(h[k]);
+      v[2 * k] = f.x;
+      v[2 * k + 1] = f.y;
+    }
+  }
+  static __device__ __forceinline__ void ld_nc(const void* base, int64_t off, float* v) {
+    unpack(__ldg(reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(base) + off)), v);
+  }
+  static __device__ __forceinline__ void ld_cs(const void* base, int64_t off, float* v) {
+    unpack(__ldcs(reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(base) + off)), v);
+  }
+  static __device__ __forceinline__ void st(void* base, int64_t off, const float* v, int nvalid) {
+    __nv_bfloat16* p = static_cast<__nv_bfloat16*>(base) + off;
+    if (nvalid >= 8) {
+      uint4 r;
+      __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&r);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) h[k] = __floats2bfloat162_rn(v[2 * k], v[2 * k + 1]);
+      __stcs(reinterpret_cast<uint4*>(p), r);
+    } else {
+      for (int k = 0; k < nvalid; ++k) p[k] = __float2bfloat16_rn(v[k]);
+    }
+  }
+};
+
+template <>
+struct VecIO<SG_BF16, 1> {
+  static __device__ __forceinline__ void ld_nc(const void* base, int64_t off, float* v) {
+    v[0] = __bfloat162float(static_cast<const __nv_bfloat16*>(base)[off]);
+  }
+  static __device__ __forceinline__ void ld_cs(const void* base, int64_t off, float* v) {
+    v[0] = __bfloat162float(static_cast<const __nv_bfloat16*>(base)[off]);
+  }
+  static __device__ __forceinline__ void st(void* base, int64_t off, const float* v, int nvalid) {
+    if (nvalid >= 1) static_cast<__nv_bfloat16*>(base)[off] = __float2bfloat16_rn(v[0]);
+  }
+};
+
+
+}  // namespace sg

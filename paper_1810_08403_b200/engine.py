@@ -1,0 +1,398 @@
+"""Chunk-dataflow executor for SAGA-NN models (forward, backward, SGD) on one GPU.
+
+Lowers each optimized LayerProgram (program.optimize) onto the fused sm_100a
+kernels, following the reference's dataflow-builder / scheduler contracts:
+
+* forward, Locality order: for every destination interval
+  j, all source intervals i in ascending order run ``fused_gather_chunk`` into
+  the resident accumulator A_j, then ApplyVertex;
+* backward, stages in reverse: backward
+  ApplyVertex (GEMMs) -> backward Gather/ApplyEdge/Scatter fused into one pass
+  over the transposed (CSR) index, with the ReLU mask of the layer below fused
+  into its epilogue;
+* loss: softmax cross-entropy on ReLU(z_L) (tensor.py:487-506),
+  update W <- W - lr dW.
+
+All device buffers are allocated once; ``capture()`` records a whole training
+step into a CUDA graph, so an epoch is one graph launch.
+"""
+
+import numpy as np
+import torch
+
+from . import _lib
+from . import kernels as K
+from . import program as prog
+from .errors import ConfigError, NumericError, ProgramError, ShapeError
+
+
+def _ld(n, align=4):
+    return (n + align - 1) // align * align
+
+
+def _mat(V, n, device, align=4):
+    """[V, n] fp32 view of a zero-padded [V, ld] buffer (16-byte aligned rows)."""
+    return torch.zeros((V, _ld(n, align)), dtype=torch.float32, device=device)[:, :n]
+
+
+class _Layer:
+    pass
+
+
+class SAGAModel:
+    """An L-layer SAGA-NN model bound to a ChunkGrid and executed by libsagann kernels.
+
+    ``programs`` are LayerPrograms (e.g. ``build_gcn``/``build_ggcn``); each is run
+    through ``hoist_vertex_computation`` + ``fuse_sag`` and must lower to a fused
+    gather (gcn / pass / ggcn) followed by ApplyVertex = ReLU(W accum)."""
+
+    def __init__(self, programs, grid, weights=None, *, seed=2, gemm_prec=_lib.GEMM_F32,
+                 device="cuda", strict=True):
+        if not torch.cuda.is_available():
+            raise RuntimeError("SAGAModel needs a CUDA device (no CPU fallback)")
+        self.grid, self.device, self.strict = grid, torch.device(device), strict
+        self.V = grid.V
+        self.gemm_prec = gemm_prec
+        self.ws = K.Workspace(self.device)
+        self.layers = []
+        dims = []
+        for p in programs:
+            q, reports = prog.optimize(p)
+            diags = prog.validate_program(q)
+            if diags:
+                raise ProgramError("; ".join(diags))
+            if q.fused is None or q.fused.kind not in ("gcn", "pass", "ggcn"):
+                raise ProgramError(f"layer ApplyEdge {p.apply_edge!r} has no fused kernel "
+                                   f"({reports[-1].blocker or (q.fused and q.fused.kind)})")
+            wname = prog.vertex_kind(q)
+            if wname is None:
+                raise ProgramError("ApplyVertex must be ReLU(W accum) for the fused executor")
+            L = _Layer()
+            L.prog, L.kind, L.wname, L.F, L.O = q, q.fused.kind, wname, q.f_in, q.f_out
+            L.gate = q.fused.params
+            self.layers.append(L)
+            dims.append((q.f_in, q.f_out))
+        for a, b in zip(dims, dims[1:]):
+            if a[1] != b[0]:
+                raise ShapeError(f"layer widths do not chain: {a} -> {b}")
+        self._alloc()
+        self.set_weights(weights if weights is not None else self.init_weights(seed))
+        self.graph = None
+        self.prof = None
+
+    # ------------------------------------------------------------------ parameters
+    def param_shapes(self):
+        out = []
+        for L in self.layers:
+            if L.kind == "ggcn":
+                out += [(L.F, L.F), (L.F, L.F), (L.F, L.O)]
+            else:
+                out += [(L.F, L.O)]
+        return out
+
+    def init_weights(self, seed=2):
+        """Glorot-uniform from default_rng(seed) in parameter order."""
+        rng = np.random.default_rng(seed)
+        out = []
+        for fin, fout in self.param_shapes():
+            lim = np.sqrt(6.0 / (fin + fout))
+            out.append(rng.uniform(-lim, lim, (fin, fout)).astype(np.float32))
+        return out
+
+    def set_weights(self, weights):
+        flat = list(weights)
+        if len(flat) != len(self.param_shapes()):
+            raise ShapeError("wrong number of weight matrices")
+        k = 0
+        for L in self.layers:
+            for t in L.params:
+                w = torch.as_tensor(np.asarray(flat[k], np.float32))
+                if tuple(w.shape) != tuple(t.shape):
+                    raise ShapeError(f"weight {k} has shape {tuple(w.shape)}, want {tuple(t.shape)}")
+                t.copy_(w)
+                k += 1
+
+    def weights(self):
+        return [t.detach().cpu().numpy().copy() for L in self.layers for t in L.params]
+
+    def grads(self):
+        return [t.detach().cpu().numpy().copy() for L in self.layers for t in L.dparams]
+
+    # ------------------------------------------------------------------ buffers
+    def _alloc(self):
+        V, dev = self.V, self.device
+        for n, L in enumerate(self.layers):
+            F, O = L.F, L.O
+            L.W = torch.zeros((F, O), dtype=torch.float32, device=dev)
+            L.dW = torch.zeros_like(L.W)
+            if L.kind == "ggcn":
+                L.goff = _ld(F)
+                L.HP = torch.zeros((V, 2 * L.goff), dtype=torch.float32, device=dev)
+                L.GQ = torch.zeros((V, 2 * L.goff), dtype=torch.float32, device=dev)
+                L.hin = L.HP[:, :F]
+                L.Pv = L.HP[:, L.goff:L.goff + F]
+                L.Qv = L.GQ[:, L.goff:L.goff + F]
+                L.dAv = L.GQ[:, :F]
+                L.WH = torch.zeros((F, F), dtype=torch.float32, device=dev)
+                L.WC = torch.zeros((F, F), dtype=torch.float32, device=dev)
+                L.dWH, L.dWC = torch.zeros_like(L.WH), torch.zeros_like(L.WC)
+                L.dQ, L.dP, L.dHt = _mat(V, F, dev), _mat(V, F, dev), _mat(V, F, dev)
+                L.params = [L.WH, L.WC, L.W]
+                L.dparams = [L.dWH, L.dWC, L.dW]
+            else:
+                L.hin = None  # set below (previous layer's ReLU output or X)
+                L.da = _mat(V, F, dev)
+                L.params = [L.W]
+                L.dparams = [L.dW]
+            L.a = _mat(V, F, dev)
+            L.z = _mat(V, O, dev)
+            L.dz = _mat(V, O, dev)
+        for n, L in enumerate(self.layers):
+            if L.hin is None:
+                L.hin = _mat(V, L.F, dev) if n == 0 else None
+        for n, L in enumerate(self.layers[:-1]):
+            nxt = self.layers[n + 1]
+            if nxt.hin is None:
+                nxt.hin = _mat(V, nxt.F, dev)
+            L.hout = nxt.hin
+        self.layers[-1].hout = None
+        self.X = self.layers[0].hin
+        self.labels = torch.zeros(V, dtype=torch.int64, device=dev)
+        self.loss = torch.zeros(1, dtype=torch.float32, device=dev)
+        self.err = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.nonfinite = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.tmp1 = _mat(V, max(L.F for L in self.layers), dev)
+        self.tmp2 = _mat(V, max(L.F for L in self.layers), dev)
+
+    def load_features(self, X):
+        X = torch.as_tensor(X)
+        if tuple(X.shape[:1]) != (self.V,) or X.shape[1] < self.layers[0].F:
+            raise ShapeError(f"features must be [V={self.V}, {self.layers[0].F}]")
+        self.X.copy_(X[:, : self.layers[0].F], non_blocking=True)
+
+    def load_labels(self, labels):
+        self.labels.copy_(torch.as_tensor(np.asarray(labels, np.int64)), non_blocking=True)
+
+    # ------------------------------------------------------------------ passes
+    def _rows(self, t, k):
+        b = self.grid.begin(k)
+        return t[b: b + self.grid.size(k)]
+
+    def _fwd_propagate(self, L, stream=None):
+        g, P = self.grid, self.grid.P
+        for j in range(P):
+            chain = [i for i in range(P) if (i, j) in g.csc]
+            if not chain:
+                self._rows(L.a, j).zero_()
+                continue
+            for k, i in enumerate(chain):
+                pi = g.csc[(i, j)]
+                if L.kind == "ggcn":
+                    K.propagate(pi, _lib.PROP_GGCN_FWD, self._rows(L.HP, i), self._rows(L.a, j), L.F,
+                                g_off=L.goff, R=self._rows(L.Qv, j), accumulate=k > 0, ws=self.ws,
+                                stream=stream)
+                else:
+                    mode = _lib.PROP_GCN if L.kind == "gcn" else _lib.PROP_PASS
+                    K.propagate(pi, mode, self._rows(L.hin, i), self._rows(L.a, j), L.F,
+                                accumulate=k > 0, ws=self.ws, stream=stream)
+
+    def _bwd_propagate_gcn(self, L, out, mask, stream=None):
+        """dH[v] = sum_{out(v)} w_e dA[u] over CSR chunks, j ascending; ReLU mask on the last."""
+        g, P = self.grid, self.grid.P
+        mode = _lib.PROP_GCN if L.kind == "gcn" else _lib.PROP_PASS
+        for i in range(P):
+            chain = [j for j in range(P) if (i, j) in g.csr]
+            if not chain:
+                self._rows(out, i).zero_()
+                continue
+            for k, j in enumerate(chain):
+                K.propagate(g.csr[(i, j)], mode, self._rows(L.da, j), self._rows(out, i), L.F,
+                            mask=self._rows(mask, i) if k == len(chain) - 1 else None,
+                            accumulate=k > 0, ws=self.ws, stream=stream)
+
+    def _bwd_propagate_ggcn(self, L, stream=None):
+        g, P = self.grid, self.grid.P
+        for j in range(P):  # pass A over CSC: dQ[u]
+            chain = [i for i in range(P) if (i, j) in g.csc]
+            if not chain:
+                self._rows(L.dQ, j).zero_()
+            for k, i in enumerate(chain):
+                K.propagate(g.csc[(i, j)], _lib.PROP_GGCN_BWD_DST, self._rows(L.HP, i),
+                            self._rows(L.dQ, j), L.F, g_off=L.goff, R=self._rows(L.GQ, j),
+                            r_off=L.goff, accumulate=k > 0, ws=self.ws, stream=stream)
+        for i in range(P):  # pass B over CSR: dP[v], dH_take[v]
+            chain = [j for j in range(P) if (i, j) in g.csr]
+            if not chain:
+                self._rows(L.dP, i).zero_()
+                self._rows(L.dHt, i).zero_()
+            for k, j in enumerate(chain):
+                K.propagate(g.csr[(i, j)], _lib.PROP_GGCN_BWD_SRC, self._rows(L.GQ, j),
+                            self._rows(L.dP, i), L.F, g_off=L.goff, R=self._rows(L.HP, i),
+                            r_off=L.goff, out1=self._rows(L.dHt, i), accumulate=k > 0, ws=self.ws,
+                            stream=stream)
+
+    def _gemm(self, A, B, C, **kw):
+        K.gemm(A, B, C, prec=self.gemm_prec, ws=self.ws, **kw)
+
+    def _ewise(self, op, a, b, out, stream=None):
+        _lib.check(_lib.lib.sg_ewise(op, a.shape[0], a.shape[1], a.data_ptr(), a.stride(0),
+                                     b.data_ptr(), b.shape[0], b.shape[1], b.stride(0),
+                                     out.data_ptr(), out.stride(0), _lib.stream_handle(stream)))
+
+    # ------------------------------------------------------------------ step
+    def _mark(self, name):
+        """Stage boundary event (enabled by setting ``self.prof = []``)."""
+        if self.prof is not None:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()
+            self.prof.append((name, e))
+
+    def forward(self, stream=None):
+        """All layers forward; returns z_L (pre-ReLU logits)."""
+        self._mark("start")
+        for n, L in enumerate(self.layers):
+            if L.kind == "ggcn":
+                self._gemm(L.hin, L.WH, L.Pv)   # hoisted P = h W_H
+                self._gemm(L.hin, L.WC, L.Qv)   # hoisted Q = h W_C
+                self._mark(f"L{n}.fwd.hoist_gemm")
+            self._fwd_propagate(L, stream)
+            self._mark(f"L{n}.fwd.propagate")
+            self._gemm(L.a, L.W, L.z, relu_out=L.hout)  # ApplyVertex: z = a W, h' = relu(z)
+            self._mark(f"L{n}.fwd.apply_vertex")
+        return self.layers[-1].z
+
+    def backward(self, stream=None):
+        """Loss + all parameter gradients (reverse stage order)."""
+        last = self.layers[-1]
+        K.softmax_xent(last.z, self.labels, self.loss, last.dz, self.err, relu_input=True,
+                       ws=self.ws, stream=stream)
+        self._mark("loss")
+        for n in range(len(self.layers) - 1, -1, -1):
+            L = self.layers[n]
+            self._gemm(L.a, L.dz, L.dW, trans_a=True)           # dW = a^T dz
+            below = self.layers[n - 1] if n > 0 else None
+            if L.kind == "ggcn":
+                self._gemm(L.dz, L.W, L.dAv, trans_b=True)      # dA = dz W^T
+                self._mark(f"L{n}.bwd.apply_vertex")
+                self._bwd_propagate_ggcn(L, stream)
+                self._mark(f"L{n}.bwd.propagate")
+                self._gemm(L.hin, L.dQ, L.dWC, trans_a=True)    # dW_C = h^T dQ
+                self._gemm(L.hin, L.dP, L.dWH, trans_a=True)    # dW_H = h^T dP
+                if below is not None:
+                    t1, t2 = self.tmp1[:, : L.F], self.tmp2[:, : L.F]
+                    self._gemm(L.dQ, L.WC, t1, trans_b=True)
+                    self._ewise(0, L.dHt, t1, t1, stream)       # take_rows part + Q part
+                    self._gemm(L.dP, L.WH, t2, trans_b=True)
+                    self._ewise(0, t1, t2, t1, stream)          # + P part (tape order)
+                    self._ewise(8, t1, below.z, below.dz, stream)  # relu bwd of the layer below
+                self._mark(f"L{n}.bwd.hoist_gemm")
+            else:
+                if below is not None:
+                    self._gemm(L.dz, L.W, L.da, trans_b=True)   # dA = dz W^T
+                    self._mark(f"L{n}.bwd.apply_vertex")
+                    self._bwd_propagate_gcn(L, below.dz, below.z, stream)
+                    self._mark(f"L{n}.bwd.propagate")
+                else:
+                    self._mark(f"L{n}.bwd.apply_vertex")
+        if self.strict:
+            self.nonfinite.zero_()
+            K.check_finite(self.loss, self.nonfinite, stream)
+            for L in self.layers:
+                for d in L.dparams:
+                    K.check_finite(d, self.nonfinite, stream)
+        return self.loss
+
+    def sgd(self, lr, stream=None):
+        for L in self.layers:
+            for W, dW in zip(L.params, L.dparams):
+                K.sgd(W, dW, lr, stream)
+        self._mark("sgd")
+
+    def stage_times(self):
+        """{stage: ms} from the recorded marks (call after synchronize)."""
+        out = {}
+        for (_, a), (name, b) in zip(self.prof, self.prof[1:]):
+            if name != "start":
+                out[name] = out.get(name, 0.0) + a.elapsed_time(b)
+        return out
+
+    def train_step(self, lr=0.01):
+        self.forward()
+        self.backward()
+        self.sgd(lr)
+        return self.loss
+
+    # ------------------------------------------------------------------ CUDA graph
+    def capture(self, lr=0.01, warmup=1):
+        """Record one full training step (forward, backward, SGD) as a CUDA graph."""
+        s = torch.cuda.Stream(device=self.device)
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            snapshot = [t.clone() for L in self.layers for t in L.params]
+            for _ in range(warmup):  # sizes the workspace before capture
+                self.train_step(lr)
+            k = 0
+            for L in self.layers:
+                for t in L.params:
+                    t.copy_(snapshot[k])
+                    k += 1
+        torch.cuda.current_stream().wait_stream(s)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self.train_step(lr)
+        return self.graph
+
+    def replay(self):
+        self.graph.replay()
+        return self.loss
+
+    def check_status(self):
+        """Read the device flags (syncs): raise like the reference's strict mode."""
+        if int(self.err.item()):
+            raise ShapeError("label out of range [0, classes)")
+        if self.strict and int(self.nonfinite.item()):
+            raise NumericError("non-finite value produced in the training step")
+
+
+def gcn_model(grid, dims, **kw):
+    """2-layer (or L-layer) GCN: dims = [F, H, ..., C]."""
+    return SAGAModel([prog.build_gcn(a, b) for a, b in zip(dims, dims[1:])], grid, **kw)
+
+
+def ggcn_model(grid, dims, **kw):
+    return SAGAModel([prog.build_ggcn(a, b) for a, b in zip(dims, dims[1:])], grid, **kw)
+
+
+def run_train(config):
+    """SPEC.md:595-603 run_train on a synthetic graph; returns a metrics dict.
+
+    config keys (SPEC.md:622 subset + synthetic graph): model ('gcn'|'ggcn'),
+    graph ('rmat'|'uniform'), V, E, features F, hidden, classes, layers, epochs,
+    lr, seed, interval_size."""
+    from . import graph as G
+
+    known = {"model", "graph", "V", "E", "features", "hidden", "classes", "layers", "epochs", "lr",
+             "seed", "interval_size", "split_edges"}
+    bad = set(config) - known
+    if bad:
+        raise ConfigError(f"unknown config keys {sorted(bad)}")
+    model = config.get("model", "gcn")
+    if model not in ("gcn", "ggcn"):
+        raise ConfigError(f"unknown model '{model}'; valid: gcn, ggcn")
+    V, E = int(config["V"]), int(config["E"])
+    gen = G.rmat_graph if config.get("graph", "uniform") == "rmat" else G.uniform_graph
+    g = gen(V, E, seed=int(config.get("seed", 0)))
+    grid = G.ChunkGrid(g, config.get("interval_size") or V,
+                       split_edges=int(config.get("split_edges", G.DEFAULT_SPLIT_EDGES)))
+    F, H, C = int(config["features"]), int(config.get("hidden", 16)), int(config["classes"])
+    nl = int(config.get("layers", 2))
+    dims = [F] + [H] * (nl - 1) + [C]
+    m = (gcn_model if model == "gcn" else ggcn_model)(grid, dims)
+    m.load_features(torch.from_numpy(G.synthetic_features(V, F, seed=1)))
+    m.load_labels(np.random.default_rng(3).integers(0, C, V))
+    losses = []
+    for _ in range(int(config.get("epochs", 10))):
+        m.train_step(float(config.get("lr", 0.01)))
+        m.check_status()
+        losses.append(float(m.loss.item()))
+    return {"model": model, "V": V, "E": E, "epochs": len(losses), "loss": losses}

@@ -1,0 +1,237 @@
+"""Graph store: synthetic graphs, reencode_balance, partition_2d and the device ChunkGrid.
+
+Mirrors the graph-store module of the reference SPEC (``SPEC.md:96-165``):
+``Graph`` (:101-106), ``VertexChunk``/``EdgeChunk`` (:107-118),
+``reencode_balance`` (:130-138) and ``partition_2d`` (:139-147).  All index
+construction runs in native C++ (libsagann ``sg_host_*``); the resulting CSC
+(destination-sorted, forward) and CSR (source-sorted, the "transposed chunk
+index" used by backward) layouts are uploaded once per graph into a
+``ChunkGrid`` together with the per-pass work plans the propagation kernels
+consume.
+"""
+
+import numpy as np
+
+from . import _lib
+from ._lib import check, lib, nptr
+from .errors import GraphFormatError, ShapeError
+
+RMAT_ABC = (0.57, 0.19, 0.19)
+DEFAULT_SPLIT_EDGES = 4096     # subgroup size T for heavy rows
+
+
+class Graph:
+    """Edge list over vertices [0, V); self-loops and multi-edges kept (:124)."""
+
+    def __init__(self, V, src, dst):
+        src = np.ascontiguousarray(src, dtype=np.int32)
+        dst = np.ascontiguousarray(dst, dtype=np.int32)
+        if src.shape != dst.shape or src.ndim != 1:
+            raise GraphFormatError("src and dst must be 1-D arrays of equal length")
+        if V < 0 or V > np.iinfo(np.int32).max:
+            raise GraphFormatError(f"vertex count {V} out of range")
+        if src.size and (min(src.min(), dst.min()) < 0 or max(src.max(), dst.max()) >= V):
+            raise GraphFormatError(f"edge endpoint out of range [0, {V})")
+        self.V, self.src, self.dst = int(V), src, dst
+
+    @property
+    def E(self):
+        return int(self.src.shape[0])
+
+    def degrees(self):
+        dout = np.empty(self.V, np.int64)
+        din = np.empty(self.V, np.int64)
+        check(lib.sg_host_degrees(nptr(self.src), nptr(self.dst), self.E, self.V, nptr(dout), nptr(din)))
+        return dout, din
+
+    def gcn_weights(self, eid=None, degrees=None):
+        """w_e = 1/sqrt(deg_out(src) deg_in(dst)) in fp32, for edges ``eid``."""
+        dout, din = degrees if degrees is not None else self.degrees()
+        n = self.E if eid is None else eid.shape[0]
+        w = np.empty(n, np.float32)
+        check(lib.sg_host_gcn_weights(nptr(self.src), nptr(self.dst), nptr(dout), nptr(din),
+                                      nptr(eid) if eid is not None else None, n, nptr(w)))
+        return w
+
+    def permute(self, perm):
+        perm = np.asarray(perm, np.int64)
+        return Graph(self.V, perm[self.src], perm[self.dst])
+
+
+def rmat_graph(V, E, seed=0, abc=RMAT_ABC):
+    """R-MAT(a, b, c, 1-a-b-c) graph, ids folded into [0, V)."""
+    a, b, c = abc
+    t1, t2 = a, a + b
+    t3 = t2 + c
+    src = np.empty(E, np.int32)
+    dst = np.empty(E, np.int32)
+    check(lib.sg_host_gen_rmat(V, E, seed, t1, t2, t3, 0, nptr(src), nptr(dst)))
+    return Graph(V, src, dst)
+
+
+def uniform_graph(V, E, seed=0):
+    src = np.empty(E, np.int32)
+    dst = np.empty(E, np.int32)
+    check(lib.sg_host_gen_uniform(V, E, seed, 0, nptr(src), nptr(dst)))
+    return Graph(V, src, dst)
+
+
+def synthetic_features(V, F, seed=1, ld=None):
+    """U[-1, 1) features, fp32 [V, ld] with zeroed padding columns."""
+    ld = F if ld is None else ld
+    x = np.zeros((V, ld), np.float32)
+    check(lib.sg_host_gen_features(V, F, seed, 0, nptr(x), ld))
+    return x
+
+
+def reencode_balance(g, num_intervals):
+    """SPEC.md:130-138.  Returns (re-encoded Graph, perm) with perm[old] = new."""
+    perm = np.empty(g.V, np.int64)
+    check(lib.sg_host_reencode_balance(nptr(g.src), nptr(g.dst), g.E, g.V, num_intervals, nptr(perm)))
+    return g.permute(perm), perm
+
+
+class Partition:
+    """P x P grid of EdgeChunks; chunk id c = i * P + j.
+
+    Same flattened layout as the oracle's ``Partition``: chunk-local CSC
+    pointers by local destination (stable by input order) and chunk-local CSR
+    pointers by local source (stable by CSC position)."""
+
+    def __init__(self, g, interval_size):
+        if interval_size < 1:
+            raise ShapeError("interval_size must be >= 1")
+        P = np.zeros(1, np.int64)
+        plen = np.zeros(1, np.int64)
+        check(lib.sg_host_partition_layout(g.V, interval_size, nptr(P), nptr(plen)))
+        P, plen = int(P[0]), int(plen[0])
+        E = g.E
+        self.V, self.E, self.P, self.interval_size = g.V, E, P, int(interval_size)
+        self.sizes = np.full(P, interval_size, np.int64)
+        self.sizes[-1] = g.V - (P - 1) * interval_size
+        self.edge_off = np.zeros(P * P + 1, np.int64)
+        self.cptr_off = np.zeros(P * P + 1, np.int64)
+        self.rptr_off = np.zeros(P * P + 1, np.int64)
+        self.csc_ptr = np.zeros(plen, np.int64)
+        self.csr_ptr = np.zeros(plen, np.int64)
+        self.csc_idx = np.empty(E, np.int32)
+        self.csr_idx = np.empty(E, np.int32)
+        self.csc_eid = np.empty(E, np.int64)
+        self.csr_eid = np.empty(E, np.int64)
+        check(lib.sg_host_partition_2d(
+            nptr(g.src), nptr(g.dst), E, g.V, interval_size, nptr(self.edge_off),
+            nptr(self.cptr_off), nptr(self.rptr_off), nptr(self.csc_ptr), nptr(self.csc_idx),
+            nptr(self.csc_eid), nptr(self.csr_ptr), nptr(self.csr_idx), nptr(self.csr_eid)))
+
+    def begin(self, i):
+        return i * self.interval_size
+
+    def chunk(self, i, j):
+        c = i * self.P + j
+        e0, e1 = int(self.edge_off[c]), int(self.edge_off[c + 1])
+        nj, ni = int(self.sizes[j]), int(self.sizes[i])
+        return dict(i=i, j=j, nnz=e1 - e0, e0=e0,
+                    csc_ptr=self.csc_ptr[self.cptr_off[c]: self.cptr_off[c] + nj + 1],
+                    csc_idx=self.csc_idx[e0:e1], csc_eid=self.csc_eid[e0:e1],
+                    csr_ptr=self.csr_ptr[self.rptr_off[c]: self.rptr_off[c] + ni + 1],
+                    csr_idx=self.csr_idx[e0:e1], csr_eid=self.csr_eid[e0:e1])
+
+
+def partition_2d(g, interval_size):
+    """P = ceil(V / interval_size), explicit empty chunks."""
+    return Partition(g, interval_size)
+
+
+def plan(ptr, split_edges=DEFAULT_SPLIT_EDGES, pack_edges=None, max_rows=256):
+    """Work plan of one propagation pass over a CSC/CSR pointer array (native)."""
+    ptr = np.ascontiguousarray(ptr, np.int64)
+    n_rows = ptr.shape[0] - 1
+    nnz = int(ptr[-1]) if n_rows >= 0 else 0
+    if pack_edges is None:
+        pack_edges = int(min(max(32, nnz // (148 * 64)), split_edges))
+    cnt = np.zeros(3, np.int64)
+    check(lib.sg_host_plan(nptr(ptr), n_rows, pack_edges, max_rows, split_edges, None, None,
+                           nptr(cnt[0:1]), nptr(cnt[1:2]), nptr(cnt[2:3])))
+    items = np.zeros(int(cnt[0]), _lib.ITEM_DTYPE)
+    splits = np.zeros(max(int(cnt[1]), 1), _lib.SPLIT_DTYPE)
+    check(lib.sg_host_plan(nptr(ptr), n_rows, pack_edges, max_rows, split_edges, nptr(items),
+                           nptr(splits), nptr(cnt[0:1]), nptr(cnt[1:2]), nptr(cnt[2:3])))
+    return items, splits[: int(cnt[1])], int(cnt[2])
+
+
+class PassIndex:
+    """Device-resident index of one propagation pass over one chunk (CSC or CSR)."""
+
+    def __init__(self, ptr, idx, w, n_rows, split_edges, device):
+        import torch
+
+        items, splits, n_slots = plan(ptr, split_edges)
+        self.n_rows = int(n_rows)
+        self.nnz = int(ptr[-1])
+        self.n_items, self.n_splits, self.n_slots = len(items), len(splits), n_slots
+        self.ptr = torch.from_numpy(np.ascontiguousarray(ptr, np.int64)).to(device)
+        self.idx = torch.from_numpy(np.ascontiguousarray(idx, np.int32)).to(device)
+        self.w = None if w is None else torch.from_numpy(np.ascontiguousarray(w, np.float32)).to(device)
+        self.items = torch.from_numpy(items.view(np.uint8)).to(device)
+        self.splits = torch.from_numpy(splits.view(np.uint8)).to(device) if len(splits) else None
+        self.max_degree = int(np.diff(ptr).max()) if n_rows > 0 else 0
+
+    @classmethod
+    def from_device(cls, ptr, idx, split_edges=DEFAULT_SPLIT_EDGES):
+        """Index over device (ptr int64, idx int32) tensors; only the plan is built on the host."""
+        import torch
+
+        self = cls.__new__(cls)
+        ptr_h = ptr.cpu().numpy()
+        items, splits, n_slots = plan(ptr_h, split_edges)
+        self.n_rows = ptr_h.shape[0] - 1
+        self.nnz = int(ptr_h[-1])
+        self.n_items, self.n_splits, self.n_slots = len(items), len(splits), n_slots
+        self.ptr, self.idx, self.w = ptr, idx, None
+        self.items = torch.from_numpy(items.view(np.uint8)).to(ptr.device)
+        self.splits = torch.from_numpy(splits.view(np.uint8)).to(ptr.device) if len(splits) else None
+        self.max_degree = int(np.diff(ptr_h).max()) if self.n_rows > 0 else 0
+        return self
+
+    def workspace_bytes(self, F, mode):
+        return int(lib.sg_propagate_workspace_bytes(self.n_items, self.n_splits, self.n_slots, F, mode))
+
+
+class ChunkGrid:
+    """Device chunk grid: per non-empty chunk C_ij a CSC pass index (forward,
+    SPEC.md:142 "CSC sorted by local dest id") and a CSR pass index (backward),
+    each with its static GCN edge weights in that edge order."""
+
+    def __init__(self, g, interval_size=None, device="cuda", split_edges=DEFAULT_SPLIT_EDGES,
+                 gcn_weights=True, partition=None):
+        self.graph = g
+        self.part = partition if partition is not None else partition_2d(g, interval_size or max(g.V, 1))
+        self.V, self.E, self.P = g.V, g.E, self.part.P
+        self.split_edges = split_edges
+        self.device = device
+        degs = g.degrees() if gcn_weights else None
+        self.csc, self.csr = {}, {}
+        for i in range(self.P):
+            for j in range(self.P):
+                ch = self.part.chunk(i, j)
+                if ch["nnz"] == 0:
+                    continue
+                wc = g.gcn_weights(ch["csc_eid"], degs) if gcn_weights else None
+                wr = g.gcn_weights(ch["csr_eid"], degs) if gcn_weights else None
+                self.csc[(i, j)] = PassIndex(ch["csc_ptr"], ch["csc_idx"], wc, self.part.sizes[j],
+                                             split_edges, device)
+                self.csr[(i, j)] = PassIndex(ch["csr_ptr"], ch["csr_idx"], wr, self.part.sizes[i],
+                                             split_edges, device)
+
+    def begin(self, k):
+        return self.part.begin(k)
+
+    def size(self, k):
+        return int(self.part.sizes[k])
+
+    def workspace_bytes(self, F, mode):
+        m = 0
+        for d in (self.csc, self.csr):
+            for pi in d.values():
+                m = max(m, pi.workspace_bytes(F, mode))
+        return max(m, 256)

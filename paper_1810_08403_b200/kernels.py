@@ -1,0 +1,100 @@
+"""Typed torch-tensor wrappers over the libsagann device entry points.
+
+Every function here launches one of the repo's own sm_100a kernels on the
+current torch stream (or the given one) and raises the mirrored reference
+exception on a bad status.  torch is used only for device memory and streams.
+"""
+
+import torch
+
+from . import _lib
+from ._lib import check, lib, stream_handle, tptr
+
+_DT = {torch.float32: _lib.SG_F32, torch.bfloat16: _lib.SG_BF16}
+
+
+def dtype_code(t):
+    try:
+        return _DT[t.dtype]
+    except KeyError:
+        raise TypeError(f"unsupported dtype {t.dtype}; expected float32 or bfloat16") from None
+
+
+def ld(t):
+    """Leading dimension (row stride, elements) of a row-major 2-D view."""
+    if t.dim() != 2 or t.stride(1) != 1:
+        raise ValueError("expected a 2-D tensor with unit column stride")
+    return t.stride(0)
+
+
+class Workspace:
+    """Grow-only device scratch buffer (caller-owned workspace of the C-ABI)."""
+
+    def __init__(self, device):
+        self.device = device
+        self.buf = torch.empty(0, dtype=torch.uint8, device=device)
+
+    def get(self, nbytes):
+        nbytes = max(int(nbytes), 256)
+        if self.buf.numel() < nbytes:
+            self.buf = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        return self.buf
+
+
+def propagate(pi, mode, G, out0, F, *, g_off=0, R=None, r_off=0, out1=None, mask=None,
+              accumulate=False, ws=None, stream=None):
+    """One fused Scatter-ApplyEdge-Gather pass over PassIndex ``pi`` (sg_propagate)."""
+    dt = dtype_code(G)
+    wsb = pi.workspace_bytes(F, mode)
+    buf = ws.get(wsb) if ws is not None else torch.empty(wsb, dtype=torch.uint8, device=G.device)
+    check(lib.sg_propagate(
+        mode, dt, tptr(pi.ptr), tptr(pi.idx), tptr(pi.w), pi.n_rows, tptr(pi.items), pi.n_items,
+        tptr(pi.splits), pi.n_splits, pi.n_slots, tptr(G), ld(G), g_off,
+        tptr(R), ld(R) if R is not None else 0, r_off, tptr(out0), ld(out0),
+        tptr(out1), ld(out1) if out1 is not None else 0, tptr(mask),
+        ld(mask) if mask is not None else 0, F, int(bool(accumulate)), tptr(buf), buf.numel(),
+        stream_handle(stream)))
+
+
+def gemm(A, B, C, *, trans_a=False, trans_b=False, relu_out=None, prec=_lib.GEMM_F32, ws=None,
+         stream=None):
+    """C = op(A) @ op(B) (+ relu_out = relu(C)); fp32 storage."""
+    M = A.shape[1] if trans_a else A.shape[0]
+    K = A.shape[0] if trans_a else A.shape[1]
+    N = B.shape[0] if trans_b else B.shape[1]
+    Kb = B.shape[1] if trans_b else B.shape[0]
+    if K != Kb:
+        from .errors import ShapeError
+
+        raise ShapeError(f"matmul inner extents differ: {K} vs {Kb}")
+    wsb = int(lib.sg_gemm_workspace_bytes(M, N, K, prec))
+    buf = (ws.get(wsb) if ws is not None else torch.empty(max(wsb, 256), dtype=torch.uint8,
+                                                            device=A.device))
+    check(lib.sg_gemm(prec, int(trans_a), int(trans_b), M, N, K, tptr(A), ld(A), tptr(B), ld(B),
+                      tptr(C), ld(C), _lib.EPI_RELU_DUAL if relu_out is not None else _lib.EPI_NONE,
+                      tptr(relu_out), ld(relu_out) if relu_out is not None else 0, tptr(buf),
+                      buf.numel(), stream_handle(stream)))
+
+
+def softmax_xent(Z, labels, loss, dZ, err, *, relu_input=True, ws=None, stream=None):
+    n, C = Z.shape
+    wsb = int(lib.sg_xent_workspace_bytes(n))
+    buf = ws.get(wsb) if ws is not None else torch.empty(wsb, dtype=torch.uint8, device=Z.device)
+    check(lib.sg_softmax_xent(tptr(Z), ld(Z), int(relu_input), tptr(labels), n, C, tptr(loss),
+                              tptr(dZ), ld(dZ), tptr(err), tptr(buf), buf.numel(),
+                              stream_handle(stream)))
+
+
+def sgd(W, dW, lr, stream=None):
+    check(lib.sg_sgd(tptr(W), tptr(dW), W.numel(), float(lr), stream_handle(stream)))
+
+
+def check_finite(X, flag, stream=None):
+    X2 = X if X.dim() == 2 else X.reshape(1, -1)
+    check(lib.sg_check_finite(dtype_code(X2), tptr(X2), X2.shape[0], X2.shape[1], ld(X2),
+                              tptr(flag), stream_handle(stream)))
+
+
+def convert(X, Y, stream=None):
+    check(lib.sg_convert(dtype_code(X), dtype_code(Y), tptr(X), ld(X), tptr(Y), ld(Y), X.shape[0],
+                         X.shape[1], stream_handle(stream)))

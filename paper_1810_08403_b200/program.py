@@ -1,0 +1,395 @@
+"""SAGA-NN front end: UDF tracing, layer programs, optimizer passes, model zoo.
+
+The SAGA-NN API of the reference SPEC: ``trace_udf`` / ``validate_program`` /
+``evaluate_expr`` and ``LayerProgram`` (saga-frontend), the
+two optimizer passes ``hoist_vertex_computation`` and ``fuse_sag``
+ and the ``build_gcn`` / ``build_ggcn`` builders (model-zoo,
+SPEC.md:521-550).  Users write the ApplyEdge UDF as ``apply_edge(edge, p)``
+over ``edge.src / edge.dest / edge.data`` and the ApplyVertex UDF as
+``apply_vertex(vertex, accum, p)``; Scatter and Gather are
+not user-programmable, the accumulator is an enum.
+
+``fuse_sag`` is where the kernel is chosen: a post-hoist ApplyEdge made only of
+element-wise ops becomes a FusedGather descriptor naming the fused sm_100a
+propagation mode that implements it.
+"""
+
+from dataclasses import dataclass, field
+
+from .errors import ProgramError
+
+ELEMENTWISE = {"add", "sub", "mul", "div", "max", "sigmoid", "tanh", "relu"}
+EDGE_INPUTS = {"edge.src", "edge.dest", "edge.data"}
+VERTEX_INPUTS = {"vertex", "accum"}
+
+
+class Expr:
+    """A node of a traced ExprGraph."""
+
+    __slots__ = ("op", "args", "name", "width")
+
+    def __init__(self, op, args=(), name=None, width=None):
+        self.op, self.args, self.name, self.width = op, tuple(args), name, width
+
+    # operator sugar -> traced nodes
+    def __add__(self, o):
+        return _bin("add", self, o)
+
+    def __sub__(self, o):
+        return _bin("sub", self, o)
+
+    def __mul__(self, o):
+        return _bin("mul", self, o)
+
+    __rmul__ = __mul__
+
+    def __truediv__(self, o):
+        return _bin("div", self, o)
+
+    def __matmul__(self, o):
+        return matmul(self, o)
+
+    def __repr__(self):
+        if self.op in ("input", "param", "pre"):
+            return self.name
+        return f"{self.op}({', '.join(map(repr, self.args))})"
+
+    def key(self):
+        """Structural key (graph isomorphism for idempotence checks)."""
+        if self.op in ("input", "param", "pre"):
+            return (self.op, self.name)
+        return (self.op,) + tuple(a.key() for a in self.args)
+
+
+def _bin(op, a, b):
+    if not isinstance(a, Expr) or not isinstance(b, Expr):
+        raise ProgramError(f"'{op}' operands must be traced tensors")
+    return Expr(op, (a, b), width=_bw(a, b, op))
+
+
+def _bw(a, b, op):
+    wa, wb = a.width, b.width
+    if wa is None or wb is None:
+        return wa if wb is None else wb
+    if wa == wb or wb == 1:
+        return wa
+    if wa == 1:
+        return wb
+    raise ProgramError(f"'{op}' width mismatch {wa} vs {wb}")
+
+
+def sigmoid(x):
+    return Expr("sigmoid", (x,), width=x.width)
+
+
+def tanh(x):
+    return Expr("tanh", (x,), width=x.width)
+
+
+def relu(x):
+    return Expr("relu", (x,), width=x.width)
+
+
+def maximum(a, b):
+    return _bin("max", a, b)
+
+
+def matmul(a, b):
+    """Row convention x @ W (tensor.py:313).  ``W @ x`` (the paper's W (x) x) means the same."""
+    if a.op == "param" and b.op != "param":
+        a, b = b, a
+    if b.op != "param" or b.width is None:
+        raise ProgramError("matmul needs one per-row operand and one parameter matrix")
+    rows, cols = b.width
+    if a.width is not None and a.width != rows:
+        raise ProgramError(f"matmul inner extents differ: {a.width} vs {rows}")
+    return Expr("matmul", (a, b), width=cols)
+
+
+class _Edge:
+    def __init__(self, f_src, f_dest):
+        self.src = Expr("input", name="edge.src", width=f_src)
+        self.dest = Expr("input", name="edge.dest", width=f_dest)
+        self.data = Expr("input", name="edge.data", width=1)
+
+
+class _Params:
+    def __init__(self, shapes):
+        self._shapes = dict(shapes)
+
+    def __getattr__(self, k):
+        if k.startswith("_"):
+            raise AttributeError(k)
+        if k not in self._shapes:
+            raise ProgramError(f"unknown parameter '{k}'")
+        return Expr("param", name=k, width=tuple(self._shapes[k]))
+
+
+def trace_udf(udf, kind, params, f_in):
+    """Trace an ApplyEdge (kind='edge') or ApplyVertex (kind='vertex') UDF."""
+    p = _Params(params)
+    if kind == "edge":
+        out = udf(_Edge(f_in, f_in), p)
+        allowed = EDGE_INPUTS
+    elif kind == "vertex":
+        acc_w = params.get("__accum_width__", f_in)
+        out = udf(Expr("input", name="vertex", width=f_in),
+                  Expr("input", name="accum", width=acc_w), p)
+        allowed = VERTEX_INPUTS
+    else:
+        raise ProgramError(f"unknown UDF kind '{kind}'")
+    if not isinstance(out, Expr):
+        raise ProgramError("a UDF must return a traced tensor")
+    for n in inputs_of(out):
+        if n not in allowed and not n.startswith("pre_"):
+            raise ProgramError(f"placeholder '{n}' is out of scope in {kind} UDF")
+    return out
+
+
+def nodes(e):
+    seen, out = set(), []
+
+    def walk(x):
+        if id(x) in seen:
+            return
+        seen.add(id(x))
+        for a in x.args:
+            walk(a)
+        out.append(x)
+
+    walk(e)
+    return out
+
+
+def inputs_of(e):
+    return {n.name for n in nodes(e) if n.op in ("input", "pre")}
+
+
+@dataclass
+class FusedGather:
+    """Fused-gather descriptor: which sm_100a propagation mode runs the SAG phase."""
+
+    kind: str               # 'gcn' | 'pass' | 'ggcn' | 'generic'
+    params: tuple = ()      # parameter names the fused kernel needs (ggcn: (W_H, W_C))
+
+
+@dataclass
+class PassReport:
+    """SPEC.md:236-240."""
+
+    name: str
+    moved: list = field(default_factory=list)
+    matmul_rows_before: str = ""
+    matmul_rows_after: str = ""
+    blocker: str = ""
+
+
+@dataclass
+class LayerProgram:
+    """apply_edge / apply_vertex ExprGraphs, accumulator, named params."""
+
+    apply_edge: Expr
+    apply_vertex: Expr
+    accumulator: str
+    params: dict
+    f_in: int
+    f_out: int
+    precompute: dict = field(default_factory=dict)  # name -> (side, Expr) hoisted per-vertex work
+    fused: FusedGather = None
+
+
+def make_program(apply_edge, apply_vertex, accumulator, params, f_in, f_out, acc_width=None):
+    if accumulator not in ("sum", "max", "concat"):
+        raise ProgramError(f"accumulator must be sum, max or concat (got '{accumulator}')")
+    ae = trace_udf(apply_edge, "edge", params, f_in)
+    av = trace_udf(apply_vertex, "vertex", dict(params, __accum_width__=acc_width or ae.width), f_in)
+    return LayerProgram(ae, av, accumulator, dict(params), f_in, f_out)
+
+
+def validate_program(p):
+    """every violated rule as a diagnostic; [] means ok."""
+    diags = []
+    for n in inputs_of(p.apply_edge):
+        if n not in EDGE_INPUTS and not n.startswith("pre_"):
+            diags.append(f"apply_edge references out-of-scope placeholder '{n}'")
+    for n in inputs_of(p.apply_vertex):
+        if n not in VERTEX_INPUTS:
+            diags.append(f"apply_vertex references out-of-scope placeholder '{n}'")
+    if p.accumulator not in ("sum", "max", "concat"):
+        diags.append(f"unknown accumulator '{p.accumulator}'")
+    if p.accumulator == "concat":
+        diags.append("concat accumulator requires deterministic order mode")
+    acc_uses = [n for n in nodes(p.apply_vertex) if n.op == "input" and n.name == "accum"]
+    ew = p.apply_edge.width
+    for n in acc_uses:
+        if n.width is not None and ew is not None and n.width != ew:
+            diags.append(f"gather width {ew} feeds ApplyVertex expecting {n.width}")
+    if p.apply_vertex.width not in (None, p.f_out):
+        diags.append(f"apply_vertex output width {p.apply_vertex.width} != f_out {p.f_out}")
+    return diags
+
+
+def matmul_rows(e, n_edges, n_vertices, precompute=None):
+    """Matmul row applications of one layer's ApplyEdge (tensor.py:133-158 counting)."""
+    per_edge = sum(1 for n in nodes(e) if n.op == "matmul")
+    per_vertex = sum(sum(1 for n in nodes(x) if n.op == "matmul") for _, x in (precompute or {}).values())
+    return per_edge * n_edges + per_vertex * n_vertices
+
+
+def hoist_vertex_computation(p):
+    """move maximal {src,params}- / {dest,params}-only subtrees
+    containing a matmul out of ApplyEdge into per-vertex precompute."""
+    pre = dict(p.precompute)
+    moved = []
+
+    def side_of(x):
+        ins = inputs_of(x)
+        if ins and ins <= {"edge.src"}:
+            return "src"
+        if ins and ins <= {"edge.dest"}:
+            return "dest"
+        return None
+
+    def has_mm(x):
+        return any(n.op == "matmul" for n in nodes(x))
+
+    def rewrite(x):
+        s = side_of(x)
+        if s is not None and has_mm(x):
+            name = f"pre_{s}{len(pre)}"
+            vx = _to_vertex(x)
+            pre[name] = (s, vx)
+            moved.append(f"{x!r} -> per-vertex {name}")
+            return Expr("pre", name=name, width=x.width)
+        if not x.args:
+            return x
+        return Expr(x.op, tuple(rewrite(a) for a in x.args), x.name, x.width)
+
+    new_edge = rewrite(p.apply_edge)
+    q = LayerProgram(new_edge, p.apply_vertex, p.accumulator, p.params, p.f_in, p.f_out, pre, p.fused)
+    rep = PassReport("hoist_vertex_computation", moved,
+                     f"{sum(1 for n in nodes(p.apply_edge) if n.op == 'matmul')}*|E|",
+                     f"{sum(1 for n in nodes(new_edge) if n.op == 'matmul')}*|E| + "
+                     f"{sum(sum(1 for n in nodes(v) if n.op == 'matmul') for _, v in pre.values())}*|V|")
+    return q, rep
+
+
+def _to_vertex(x):
+    if x.op == "input" and x.name in ("edge.src", "edge.dest"):
+        return Expr("input", name="vertex", width=x.width)
+    if not x.args:
+        return x
+    return Expr(x.op, tuple(_to_vertex(a) for a in x.args), x.name, x.width)
+
+
+def _is(x, op, *names):
+    return x.op == op and (not names or x.name in names)
+
+
+def fuse_sag(p):
+    """an element-wise-only (post-hoist) ApplyEdge becomes a FusedGather."""
+    e = p.apply_edge
+    mm = [n for n in nodes(e) if n.op == "matmul"]
+    if mm:
+        rep = PassReport("fuse_sag", blocker="matmul")
+        return LayerProgram(e, p.apply_vertex, p.accumulator, p.params, p.f_in, p.f_out,
+                            p.precompute, None), rep
+    kind, params = "generic", ()
+    if p.accumulator == "sum":
+        if _is(e, "input", "edge.src"):
+            kind = "pass"
+        elif e.op == "mul" and {a.name for a in e.args if a.op == "input"} == {"edge.src", "edge.data"}:
+            kind = "gcn"
+        elif e.op == "mul":
+            a, b = e.args
+            gate, other = (a, b) if a.op == "sigmoid" else (b, a)
+            if gate.op == "sigmoid" and _is(other, "input", "edge.src") and gate.args[0].op == "add":
+                x, y = gate.args[0].args
+                sides = {}
+                for t in (x, y):
+                    if t.op == "pre":
+                        sides[p.precompute[t.name][0]] = p.precompute[t.name][1]
+                src_e, dst_e = sides.get("src"), sides.get("dest")
+                if src_e is not None and dst_e is not None and _is(src_e, "matmul") and \
+                        _is(dst_e, "matmul") and x.op == "pre" and y.op == "pre" and \
+                        p.precompute[x.name][0] == "src":
+                    kind = "ggcn"
+                    params = (src_e.args[1].name, dst_e.args[1].name)
+    fg = FusedGather(kind, params)
+    rep = PassReport("fuse_sag", [f"SAG -> FusedGather({kind})"])
+    return LayerProgram(e, p.apply_vertex, p.accumulator, p.params, p.f_in, p.f_out,
+                        p.precompute, fg), rep
+
+
+def evaluate_expr(e, bindings):
+    """evaluate a traced graph on CUDA tensors with the libsagann ops.
+
+    ``bindings`` maps input/param/pre names ('edge.src', 'edge.data', 'W', ...) to tensors;
+    row-wise semantics follow the reference primitives (tensor.py:204-319)."""
+    from . import ops
+
+    memo = {}
+
+    def ev(x):
+        if id(x) in memo:
+            return memo[id(x)]
+        if x.op in ("input", "param", "pre"):
+            if x.name not in bindings:
+                raise ProgramError(f"missing binding for '{x.name}'")
+            v = bindings[x.name]
+        elif x.op == "matmul":
+            v = ops.matmul(ev(x.args[0]), ev(x.args[1]))
+        elif x.op in ("sigmoid", "tanh", "relu"):
+            v = getattr(ops, x.op)(ev(x.args[0]))
+        else:
+            v = ops.elementwise(x.op, ev(x.args[0]), ev(x.args[1]))
+        memo[id(x)] = v
+        return v
+
+    return ev(e)
+
+
+def optimize(p):
+    """hoist then fuse (the paper's pipeline)."""
+    q, r1 = hoist_vertex_computation(p)
+    q, r2 = fuse_sag(q)
+    return q, [r1, r2]
+
+
+def vertex_kind(p):
+    """Recognise ApplyVertex = ReLU(W (x) accum); returns the W param name."""
+    v = p.apply_vertex
+    if v.op == "relu" and v.args[0].op == "matmul":
+        x, W = v.args[0].args
+        if _is(x, "input", "accum") and W.op == "param":
+            return W.name
+    return None
+
+
+# ------------------------------------------------------------------ model zoo
+def build_gcn(f_in, f_out):
+    """GCN: ApplyEdge = src x edge.data, sum, ReLU(W accum)."""
+    if f_in < 1 or f_out < 1:
+        raise ProgramError("invalid dimensions")
+    return make_program(lambda e, p: e.src * e.data,
+                        lambda v, acc, p: relu(matmul(acc, p.W)),
+                        "sum", {"W": (f_in, f_out)}, f_in, f_out)
+
+
+def build_ggcn(f_in, f_out):
+    """G-GCN (listing :172-173 -- W_H on src, W_C on dest, Appendix B.1)."""
+    if f_in < 1 or f_out < 1:
+        raise ProgramError("invalid dimensions")
+    return make_program(
+        lambda e, p: sigmoid(matmul(e.src, p.W_H) + matmul(e.dest, p.W_C)) * e.src,
+        lambda v, acc, p: relu(matmul(acc, p.W)),
+        "sum", {"W_H": (f_in, f_in), "W_C": (f_in, f_in), "W": (f_in, f_out)}, f_in, f_out)
+
+
+def build_commnet(f_in, f_out):
+    """CommNet-style passthrough edge with ReLU(W accum) vertex."""
+    return make_program(lambda e, p: e.src, lambda v, acc, p: relu(matmul(acc, p.W)), "sum",
+                        {"W": (f_in, f_out)}, f_in, f_out)
+
+
+MODELS = {"gcn": build_gcn, "ggcn": build_ggcn, "commnet": build_commnet}

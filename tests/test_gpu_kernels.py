@@ -1,0 +1,337 @@
+"""GPU parity: libsagann sm_100a kernels vs the CPU oracle (run on a B200: -m gpu)."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from conftest import GOLDEN_CASES, assert_close, load_golden  # noqa: E402
+from oracle import graph as og  # noqa: E402
+from oracle import primitives as prim  # noqa: E402
+from oracle import rng  # noqa: E402
+from oracle import saga  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def sg():
+    import paper_1810_08403_b200 as m
+
+    return m
+
+
+def _dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def _padded(x, align=4):
+    V, F = x.shape
+    ld = (F + align - 1) // align * align
+    t = torch.zeros((V, ld), dtype=torch.float32, device="cuda")
+    t[:, :F] = torch.from_numpy(np.ascontiguousarray(x, np.float32))
+    return t[:, :F]
+
+
+def _graph(kind, V, E, seed):
+    return (rng.rmat_edges if kind == "rmat" else rng.uniform_edges)(V, E, seed=seed)
+
+
+def _gpu_prop_fwd(sg, grid, H, F, mode, w=True):
+    from paper_1810_08403_b200 import kernels as K
+
+    out = _padded(np.zeros((grid.V, F), np.float32))
+    for j in range(grid.P):
+        chain = [i for i in range(grid.P) if (i, j) in grid.csc]
+        if not chain:
+            out[grid.begin(j): grid.begin(j) + grid.size(j)].zero_()
+        for k, i in enumerate(chain):
+            K.propagate(grid.csc[(i, j)], mode, H[grid.begin(i): grid.begin(i) + grid.size(i)],
+                        out[grid.begin(j): grid.begin(j) + grid.size(j)], F, accumulate=k > 0)
+    return out
+
+
+def _gpu_prop_bwd(sg, grid, G, F, mask=None):
+    from paper_1810_08403_b200 import _lib
+    from paper_1810_08403_b200 import kernels as K
+
+    out = _padded(np.zeros((grid.V, F), np.float32))
+    for i in range(grid.P):
+        chain = [j for j in range(grid.P) if (i, j) in grid.csr]
+        if not chain:
+            out[grid.begin(i): grid.begin(i) + grid.size(i)].zero_()
+        for k, j in enumerate(chain):
+            rows = slice(grid.begin(i), grid.begin(i) + grid.size(i))
+            K.propagate(grid.csr[(i, j)], _lib.PROP_GCN, G[grid.begin(j): grid.begin(j) + grid.size(j)],
+                        out[rows], F, accumulate=k > 0,
+                        mask=None if mask is None or k < len(chain) - 1 else mask[rows])
+    return out
+
+
+CASES = [  # kind, V, E, F, P, T
+    ("uniform", 19717 // 8, 88648 // 8, 500, 1, 4096),   # Pubmed-like (scaled), F=500 -> VPL 4
+    ("rmat", 4000, 120000, 602, 1, 4096),                 # Reddit F, hubs split
+    ("rmat", 3000, 60000, 128, 3, 256),                   # 2D grid, many splits
+    ("uniform", 500, 4000, 16, 1, 4096),                  # narrow rows: 4-lane teams
+    ("rmat", 800, 20000, 7, 2, 64),                       # scalar path (F % 4 != 0), split
+    ("rmat", 300, 5000, 1100, 1, 128),                    # column slicing (> 1024 cols)
+    ("uniform", 50, 0, 32, 1, 4096),                      # empty graph
+]
+
+
+@pytest.mark.parametrize("kind,V,E,F,P,T", CASES)
+def test_gcn_propagate_fwd_bitwise(sg, kind, V, E, F, P, T):
+    from paper_1810_08403_b200 import _lib
+
+    s, d = _graph(kind, V, E, 5)
+    g = sg.Graph(V, s, d)
+    grid = sg.ChunkGrid(g, -(-V // P), split_edges=T)
+    X = rng.features(V, F, seed=1)
+    out = _gpu_prop_fwd(sg, grid, _padded(X), F, _lib.PROP_GCN)
+    part = og.partition_2d(s, d, V, -(-V // P))
+    w = og.gcn_edge_weights(s, d, V, np.float32)
+    ref = saga.gcn_propagate_fwd(part, X, w, T=T)
+    assert np.array_equal(out.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("kind,V,E,F,P,T", CASES[:5])
+def test_gcn_propagate_bwd_masked_bitwise(sg, kind, V, E, F, P, T):
+    s, d = _graph(kind, V, E, 6)
+    g = sg.Graph(V, s, d)
+    grid = sg.ChunkGrid(g, -(-V // P), split_edges=T)
+    Gr = rng.features(V, F, seed=4)
+    Z = rng.features(V, F, seed=8)
+    out = _gpu_prop_bwd(sg, grid, _padded(Gr), F, mask=_padded(Z))
+    part = og.partition_2d(s, d, V, -(-V // P))
+    w = og.gcn_edge_weights(s, d, V, np.float32)
+    ref = prim.relu_bwd(saga.gcn_propagate_bwd(part, Gr, w, T=T), Z)
+    assert np.array_equal(out.cpu().numpy(), ref)
+
+
+def test_passthrough_segment_sum_bitwise(sg):
+    from paper_1810_08403_b200 import _lib
+
+    s, d = _graph("rmat", 2000, 50000, 9)
+    g = sg.Graph(2000, s, d)
+    grid = sg.ChunkGrid(g, 2000, split_edges=100, gcn_weights=False)
+    X = rng.features(2000, 64, seed=2)
+    out = _gpu_prop_fwd(sg, grid, _padded(X), 64, _lib.PROP_PASS)
+    part = og.partition_2d(s, d, 2000, 2000)
+    assert np.array_equal(out.cpu().numpy(), saga.gcn_propagate_fwd(part, X, None, T=100))
+
+
+@pytest.mark.parametrize("P,T", [(1, 4096), (2, 50)])
+def test_ggcn_propagate_fwd_bwd(sg, P, T):
+    """G-GCN gated passes vs oracle (tolerance: device expf vs numpy exp)."""
+    from paper_1810_08403_b200 import _lib
+    from paper_1810_08403_b200 import kernels as K
+
+    V, E, F = 1500, 40000, 128
+    s, d = _graph("rmat", V, E, 3)
+    g = sg.Graph(V, s, d)
+    size = -(-V // P)
+    grid = sg.ChunkGrid(g, size, split_edges=T, gcn_weights=False)
+    part = og.partition_2d(s, d, V, size)
+    h = rng.features(V, F, seed=1)
+    Pm = rng.features(V, F, seed=2)
+    Qm = rng.features(V, F, seed=3)
+    Ga = rng.features(V, F, seed=4) * np.float32(0.1)
+    HP = torch.from_numpy(np.concatenate([h, Pm], 1)).cuda()
+    GQ = torch.from_numpy(np.concatenate([Ga, Qm], 1)).cuda()
+    A = torch.zeros((V, F), device="cuda")
+    dQ, dP, dH = (torch.zeros((V, F), device="cuda") for _ in range(3))
+    rows = lambda t, k: t[grid.begin(k): grid.begin(k) + grid.size(k)]  # noqa: E731
+    for j in range(P):
+        for k, i in enumerate([i for i in range(P) if (i, j) in grid.csc]):
+            K.propagate(grid.csc[(i, j)], _lib.PROP_GGCN_FWD, rows(HP, i), rows(A, j), F, g_off=F,
+                        R=rows(GQ, j)[:, F:], accumulate=k > 0)
+            K.propagate(grid.csc[(i, j)], _lib.PROP_GGCN_BWD_DST, rows(HP, i), rows(dQ, j), F,
+                        g_off=F, R=rows(GQ, j), r_off=F, accumulate=k > 0)
+    for i in range(P):
+        for k, j in enumerate([j for j in range(P) if (i, j) in grid.csr]):
+            K.propagate(grid.csr[(i, j)], _lib.PROP_GGCN_BWD_SRC, rows(GQ, j), rows(dP, i), F,
+                        g_off=F, R=rows(HP, i), r_off=F, out1=rows(dH, i), accumulate=k > 0)
+    refA = saga.ggcn_propagate_fwd(part, h, Pm, Qm, T)
+    rQ, rP, rH = saga.ggcn_propagate_bwd(part, h, Pm, Qm, Ga, T)
+    assert_close(A.cpu().numpy(), refA, 1e-5, "A")
+    assert_close(dQ.cpu().numpy(), rQ, 1e-5, "dQ")
+    assert_close(dP.cpu().numpy(), rP, 1e-5, "dP")
+    assert_close(dH.cpu().numpy(), rH, 1e-5, "dH")
+
+
+@pytest.mark.parametrize("M,N,K,ta,tb", [(1000, 128, 602, 0, 0), (602, 128, 20000, 1, 0),
+                                         (3000, 41, 128, 0, 1), (7, 5, 3, 0, 0), (130, 3, 1, 1, 1),
+                                         (50, 70, 0, 0, 0)])
+def test_gemm_f32(sg, M, N, K, ta, tb):
+    from paper_1810_08403_b200 import kernels as Kn
+
+    r = np.random.default_rng(M + N + K)
+    A = r.uniform(-1, 1, (K, M) if ta else (M, K)).astype(np.float32)
+    B = r.uniform(-1, 1, (N, K) if tb else (K, N)).astype(np.float32)
+    C = torch.empty((M, N), device="cuda")
+    D = torch.empty((M, N), device="cuda")
+    Kn.gemm(_dev(A), _dev(B), C, trans_a=bool(ta), trans_b=bool(tb), relu_out=D)
+    ref = (A.T if ta else A).astype(np.float64) @ (B.T if tb else B).astype(np.float64)
+    assert_close(C.cpu().numpy(), ref, 1e-5, "C")
+    assert np.array_equal(D.cpu().numpy(), np.maximum(C.cpu().numpy(), 0))
+
+
+def test_primitives_vs_oracle(sg):
+    from paper_1810_08403_b200 import ops
+
+    r = np.random.default_rng(1)
+    x = r.uniform(-1, 1, (50, 6)).astype(np.float32)
+    idx = r.integers(0, 50, 200)
+    seg = r.integers(0, 30, 200)
+    xt = _dev(x).requires_grad_(True)
+    y = ops.take_rows(xt, idx)
+    assert np.array_equal(y.detach().cpu().numpy(), prim.take_rows(x, idx))
+    s = ops.segment_sum(y, seg, 30)
+    assert np.array_equal(s.detach().cpu().numpy(), prim.segment_sum(x[idx], seg, 30))
+    m = ops.segment_max(y, seg, 30)
+    ref_m, ref_arg = prim.segment_max(x[idx], seg, 30)
+    assert np.array_equal(m.detach().cpu().numpy(), ref_m)
+    (s.sum() + m.sum()).backward()
+    g_rows = prim.segment_sum_bwd(np.ones((30, 6), np.float32), seg) + \
+        prim.segment_max_bwd(np.ones((30, 6), np.float32), ref_arg, 200)
+    assert np.array_equal(xt.grad.cpu().numpy(), prim.take_rows_bwd(g_rows, idx, 50))
+    # reference unit-test vectors (test_tensor.py:198-218)
+    t = _dev(np.array([[1.0, 2.0], [3.0, 4.0], [5.0, 6.0]], np.float32)).requires_grad_(True)
+    yy = ops.take_rows(t, [2, 0, 2])
+    yy.backward(torch.ones_like(yy))
+    assert np.array_equal(t.grad.cpu().numpy(), [[1, 1], [0, 0], [2, 2]])
+    mm = ops.segment_max(_dev(np.array([[1.0, 5.0], [3.0, 4.0]], np.float32)), [0, 0], 2)
+    assert np.array_equal(mm.cpu().numpy(), [[3, 5], [0, 0]])
+    with pytest.raises(sg.ShapeError):
+        ops.take_rows(t, [3])
+    with pytest.raises(sg.NumericError):
+        ops.mul(_dev(np.array([1e30], np.float32)), _dev(np.array([1e30], np.float32)))
+    assert ops.sigmoid(_dev(np.zeros(1, np.float32))).item() == 0.5
+
+
+def test_softmax_xent_vs_oracle(sg):
+    from paper_1810_08403_b200 import ops
+
+    r = np.random.default_rng(5)
+    z0 = r.uniform(-1, 1, (400, 41)).astype(np.float32)
+    lab = r.integers(0, 41, 400)
+    zt = _dev(z0).requires_grad_(True)
+    loss = ops.softmax_cross_entropy(zt, lab)
+    loss.backward()
+    rl, p = prim.softmax_cross_entropy(z0.astype(np.float64), lab)
+    assert abs(loss.item() - float(rl)) <= 1e-5 * abs(float(rl))
+    assert_close(zt.grad.cpu().numpy(), prim.softmax_cross_entropy_bwd(1.0, p, lab), 1e-4, "dz")
+
+
+# ---------------------------------------------------------------- full models
+@pytest.mark.parametrize("case", GOLDEN_CASES)
+def test_gcn_model_vs_reference_golden(sg, case):
+    """The whole 2-layer GCN step on GPU vs the REAL reference's fp32/fp64 outputs."""
+    g = load_golden(case)
+    V = int(g["V"])
+    graph = sg.Graph(V, g["src_in"], g["dst_in"])
+    grid = sg.ChunkGrid(graph, V)
+    m = sg.gcn_model(grid, [int(g["F"]), int(g["H"]), int(g["C"])],
+                     weights=[g["gcn_f32_W0"], g["gcn_f32_W1"]])
+    m.load_features(torch.from_numpy(g["gcn_f32_X"]))
+    m.load_labels(g["labels"])
+    m.forward()
+    m.backward()
+    torch.cuda.synchronize()
+    m.check_status()
+    # the propagation is bit-exact with the reference's fp32 segment_sum
+    assert np.array_equal(m.layers[0].a.cpu().numpy(), g["gcn_f32_a0"])
+    loss = m.loss.item()
+    assert abs(loss - float(np.ravel(g["gcn_f64_loss"])[0])) <= 1e-4 * float(np.ravel(g["gcn_f64_loss"])[0])
+    for l in range(2):
+        assert_close(m.layers[l].z.cpu().numpy(), g[f"gcn_f64_z{l}"], 1e-4, f"z{l}")
+        assert_close(m.layers[l].dW.cpu().numpy(), g[f"gcn_f64_dW{l}"], 1e-4, f"dW{l}")
+
+
+@pytest.mark.parametrize("case", GOLDEN_CASES)
+def test_ggcn_model_vs_reference_golden(sg, case):
+    g = load_golden(case)
+    V = int(g["V"])
+    graph = sg.Graph(V, g["src_in"], g["dst_in"])
+    grid = sg.ChunkGrid(graph, V, gcn_weights=False)
+    weights = [g[f"ggcn_f32_L{l}_{k}"] for l in range(2) for k in range(3)]
+    m = sg.ggcn_model(grid, [int(g["F"]), int(g["H"]), int(g["C"])], weights=weights)
+    m.load_features(torch.from_numpy(g["gcn_f32_X"]))
+    m.load_labels(g["labels"])
+    m.forward()
+    m.backward()
+    m.check_status()
+    ref_loss = float(np.ravel(g["ggcnh_f64_loss"])[0])
+    assert abs(m.loss.item() - ref_loss) <= 1e-4 * ref_loss
+    got = m.grads()
+    for l in range(2):
+        for k in range(3):
+            assert_close(got[3 * l + k], g[f"ggcnh_f64_dL{l}_{k}"], 1e-4, f"L{l}.{k}")
+
+
+@pytest.mark.parametrize("model,P,T", [("gcn", 1, 4096), ("gcn", 4, 64), ("ggcn", 1, 4096), ("ggcn", 3, 100)])
+def test_model_epoch_vs_oracle_pubmed_like(sg, model, P, T):
+    """2-layer epoch at Pubmed-like shape (scaled V/E, F=500, H=16, C=3) vs the fp64 oracle."""
+    V, E, F, H, C = 4000, 18000, 500, 16, 3
+    if model == "ggcn":
+        F = 64
+    s, d = _graph("rmat", V, E, 0)
+    graph = sg.Graph(V, s, d)
+    size = -(-V // P)
+    grid = sg.ChunkGrid(graph, size, split_edges=T, gcn_weights=(model == "gcn"))
+    build = sg.gcn_model if model == "gcn" else sg.ggcn_model
+    m = build(grid, [F, H, C])
+    X = rng.features(V, F, seed=1)
+    lab = rng.labels(V, C)
+    m.load_features(torch.from_numpy(X))
+    m.load_labels(lab)
+    W = m.weights()
+    m.forward()
+    m.backward()
+    m.check_status()
+    part = og.partition_2d(s, d, V, size)
+    X64 = X.astype(np.float64)
+    if model == "gcn":
+        w = og.gcn_edge_weights(s, d, V, np.float64)
+        ref = saga.gcn_epoch(part, X64, [x.astype(np.float64) for x in W], lab, w, T=T)
+        refg = ref["grads"]
+    else:
+        layers = [tuple(x.astype(np.float64) for x in W[3 * l: 3 * l + 3]) for l in range(2)]
+        ref = saga.ggcn_epoch(part, X64, layers, lab, T=T)
+        refg = [x for L in ref["grads"] for x in L]
+    rl = float(np.ravel(ref["loss"])[0])
+    assert abs(m.loss.item() - rl) <= 1e-4 * rl
+    for k, (a, b) in enumerate(zip(m.grads(), refg)):
+        assert_close(a, b, 1e-4, f"grad {k}")
+
+
+def test_training_decreases_and_graph_replay_deterministic(sg):
+    V, E = 3000, 30000
+    g = sg.rmat_graph(V, E, seed=1)
+    grid = sg.ChunkGrid(g, V)
+    m = sg.gcn_model(grid, [64, 32, 8])
+    m.load_features(torch.from_numpy(sg.synthetic_features(V, 64)))
+    m.load_labels(rng.labels(V, 8))
+    W0 = m.weights()
+    losses = []
+    for _ in range(10):
+        m.train_step(0.01)
+        losses.append(m.loss.item())
+    assert all(b < a for a, b in zip(losses, losses[1:])), losses
+    # CUDA-graph replay reproduces eager steps bit for bit
+    m.set_weights(W0)
+    m.capture(0.01)
+    m.set_weights(W0)
+    replayed = []
+    for _ in range(10):
+        m.replay()
+        replayed.append(m.loss.item())
+    assert replayed == losses
+
+
+def test_run_train_entry_point(sg):
+    out = sg.run_train({"model": "gcn", "graph": "uniform", "V": 20, "E": 80, "features": 6,
+                        "hidden": 8, "classes": 3, "epochs": 10, "lr": 0.01})
+    assert out["epochs"] == 10 and all(b < a for a, b in zip(out["loss"], out["loss"][1:]))
+    with pytest.raises(sg.ConfigError):
+        sg.run_train({"model": "nope", "V": 2, "E": 1, "features": 1, "classes": 1})
