@@ -133,37 +133,45 @@ struct Prop {
   using IO = VecIO<DT, W>;
   static constexpr int NG = M::NG, NR = M::NR, NOUT = M::NOUT;
 
-  // Load the lane's slice of DEPTH gathered rows, then add their terms in edge order.
-  static __device__ __forceinline__ void step(const PropArgs& a, const int (&s)[DEPTH],
-                                              const float (&wv)[DEPTH], int n,
-                                              const float (&rs)[NR > 0 ? NR : 1][VPL][W],
-                                              float (&acc)[NOUT][VPL][W], int tl) {
-    float g[DEPTH][NG][VPL][W];
+  using Elem = typename IO::Elem;
+  using Raw = typename IO::Raw;
+
+  // Load the lane's slice of DEPTH gathered rows (raw 16-byte vectors in flight), then add
+  // their terms in edge order.  FULL: all DEPTH edges valid (no per-edge predicates).
+  // `gl` is G advanced to this lane's first column; only the last vector needs a bound check.
+  template <bool FULL>
+  static __device__ __forceinline__ void step(const PropArgs& a, const Elem* gl, bool last_ok,
+                                              const int (&s)[DEPTH], const float (&wv)[DEPTH],
+                                              int n, const float (&rs)[NR > 0 ? NR : 1][VPL][W],
+                                              float (&acc)[NOUT][VPL][W]) {
+    Raw g[DEPTH][NG][VPL];
 #pragma unroll
     for (int d = 0; d < DEPTH; ++d) {
-      if (d < n) {
-        const int64_t rowoff = (int64_t)s[d] * a.ldg;
+      if (FULL || d < n) {
+        // 32x32->64 IMAD.WIDE row address; column offsets are immediates
+        const Elem* row = gl + (uint64_t)(uint32_t)s[d] * (uint32_t)a.ldg;
 #pragma unroll
         for (int v = 0; v < VPL; ++v) {
-          const int cv = v * LPR + tl;
-          if (cv < a.Fv) {
+          if (v < VPL - 1 || last_ok) {
 #pragma unroll
             for (int q = 0; q < NG; ++q)
-              IO::ld_nc(a.G, rowoff + (q ? a.g_off : 0) + (int64_t)cv * W, g[d][q][v]);
+              g[d][q][v] = IO::ld_raw(row + (q ? a.g_off : 0) + v * LPR * W);
           }
         }
       }
     }
 #pragma unroll
     for (int d = 0; d < DEPTH; ++d) {
-      if (d < n) {
+      if (FULL || d < n) {
 #pragma unroll
         for (int v = 0; v < VPL; ++v) {
+          float x0[W], x1[W];
+          IO::unpack(g[d][0][v], x0);
+          IO::unpack(g[d][NG - 1][v], x1);
 #pragma unroll
           for (int k = 0; k < W; ++k) {
             float t0, t1 = 0.f;
-            M::term(&g[d][0][v][k], &g[d][NG - 1][v][k], &rs[0][v][k], &rs[NR > 1 ? 1 : 0][v][k],
-                    wv[d], &t0, &t1);
+            M::term(&x0[k], &x1[k], &rs[0][v][k], &rs[NR > 1 ? 1 : 0][v][k], wv[d], &t0, &t1);
             acc[0][v][k] = __fadd_rn(acc[0][v][k], t0);
             if (NOUT > 1) acc[NOUT - 1][v][k] = __fadd_rn(acc[NOUT - 1][v][k], t1);
           }
@@ -177,31 +185,67 @@ struct Prop {
                                                    const float (&rs)[NR > 0 ? NR : 1][VPL][W],
                                                    float (&acc)[NOUT][VPL][W], unsigned tmask,
                                                    int tl) {
+    const Elem* gl = static_cast<const Elem*>(a.G) + tl * W;
+    const bool last_ok = (VPL - 1) * LPR + tl < a.Fv;
     if constexpr (LPR == 32) {
-      // warp-wide index window: 32 (src, w) pairs loaded coalesced, broadcast by shuffle
+      // warp-wide index window: 32 (src, w) pairs loaded coalesced, broadcast by shuffle;
+      // the next window is prefetched while this one is consumed.
+      int n_next = (int)min((int64_t)32, e1 - e0);
+      int src_next = 0;
+      float w_next = 0.f;
+      if (tl < n_next) {
+        src_next = __ldcs(a.idx + e0 + tl);
+        if (M::USE_W) w_next = __ldcs(a.w + e0 + tl);
+      }
+      #pragma unroll 1
       for (int64_t eb = e0; eb < e1; eb += 32) {
-        const int n = (int)min((int64_t)32, e1 - eb);
-        int my_src = 0;
-        float my_w = 0.f;
-        if (tl < n) {
-          my_src = __ldcs(a.idx + eb + tl);
-          if (M::USE_W) my_w = __ldcs(a.w + eb + tl);
+        const int n = n_next;
+        const int my_src = src_next;
+        const float my_w = w_next;
+        n_next = (int)min((int64_t)32, e1 - (eb + 32));
+        if (tl < n_next) {
+          src_next = __ldcs(a.idx + eb + 32 + tl);
+          if (M::USE_W) w_next = __ldcs(a.w + eb + 32 + tl);
         }
-        for (int d0 = 0; d0 < n; d0 += DEPTH) {
+        int d0 = 0;
+        #pragma unroll 1
+        for (; d0 + DEPTH <= n; d0 += DEPTH) {
           int s[DEPTH];
           float wv[DEPTH];
 #pragma unroll
           for (int d = 0; d < DEPTH; ++d) {
-            s[d] = __shfl_sync(tmask, my_src, (d0 + d) & 31);
-            wv[d] = M::USE_W ? __shfl_sync(tmask, my_w, (d0 + d) & 31) : 0.f;
+            s[d] = __shfl_sync(0xffffffffu, my_src, d0 + d);
+            wv[d] = M::USE_W ? __shfl_sync(0xffffffffu, my_w, d0 + d) : 0.f;
           }
-          step(a, s, wv, n - d0, rs, acc, tl);
+          step<true>(a, gl, last_ok, s, wv, DEPTH, rs, acc);
+        }
+        if (d0 < n) {
+          int s[DEPTH];
+          float wv[DEPTH];
+#pragma unroll
+          for (int d = 0; d < DEPTH; ++d) {
+            s[d] = __shfl_sync(0xffffffffu, my_src, (d0 + d) & 31);
+            wv[d] = M::USE_W ? __shfl_sync(0xffffffffu, my_w, (d0 + d) & 31) : 0.f;
+          }
+          step<false>(a, gl, last_ok, s, wv, n - d0, rs, acc);
         }
       }
     } else {
       // narrow rows: every team lane reads the (broadcast) index directly
-      for (int64_t e = e0; e < e1; e += DEPTH) {
-        const int n = (int)min((int64_t)DEPTH, e1 - e);
+      int64_t e = e0;
+      #pragma unroll 1
+      for (; e + DEPTH <= e1; e += DEPTH) {
+        int s[DEPTH];
+        float wv[DEPTH];
+#pragma unroll
+        for (int d = 0; d < DEPTH; ++d) {
+          s[d] = __ldcs(a.idx + e + d);
+          wv[d] = M::USE_W ? __ldcs(a.w + e + d) : 0.f;
+        }
+        step<true>(a, gl, last_ok, s, wv, DEPTH, rs, acc);
+      }
+      if (e < e1) {
+        const int n = (int)(e1 - e);
         int s[DEPTH];
         float wv[DEPTH];
 #pragma unroll
@@ -209,7 +253,7 @@ struct Prop {
           s[d] = d < n ? __ldcs(a.idx + e + d) : 0;
           wv[d] = (M::USE_W && d < n) ? __ldcs(a.w + e + d) : 0.f;
         }
-        step(a, s, wv, n, rs, acc, tl);
+        step<false>(a, gl, last_ok, s, wv, n, rs, acc);
       }
     }
     (void)tmask;
@@ -269,8 +313,18 @@ struct Prop {
   }
 };
 
+// Resident blocks per SM to ask ptxas for: in-flight raw vectors (4 regs each) plus
+// fp32 accumulators and row state decide the register budget (64 / 80 / 128 regs).
+template <int MODE, int W, int VPL, int DEPTH>
+constexpr int prop_min_blocks() {
+  // per in-flight edge: raw vectors + 64-bit row pointer + shuffled (src, w)
+  constexpr int regs = DEPTH * (ModeT<MODE>::NG * VPL * 4 + 4) +
+                       (ModeT<MODE>::NOUT + ModeT<MODE>::NR) * VPL * W + 40;
+  return regs <= 80 ? 3 : 2;
+}
+
 template <int MODE, int DT, int W, int VPL, int LPR, int DEPTH>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, (prop_min_blocks<MODE, W, VPL, DEPTH>()))
     prop_kernel(const PropArgs a) {
   using K = Prop<MODE, DT, W, VPL, LPR, DEPTH>;
   constexpr int NOUT = K::NOUT;
@@ -286,25 +340,23 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
     it = __shfl_sync(0xffffffffu, it, 0);
     if (it >= a.n_items) break;
     const sg_item item = a.items[it];
-    if (item.split < 0) {
-      for (int r = item.row_begin + team; r < item.row_end; r += NT) {
-        float rs[NRr][VPL][W];
-        float acc[NOUT][VPL][W];
-        K::load_row_state(a, r, tl, rs);
-        K::init_acc(a, r, tl, acc, a.accumulate != 0);
-        K::run_edges(a, __ldg(a.ptr + r), __ldg(a.ptr + r + 1), rs, acc, tmask, tl);
+    const bool split = item.split >= 0;
+    // One inlined copy of the edge loop serves whole rows and split subgroups alike
+    // (a single call site keeps ptxas register allocation spill-free).
+    const int r_end = (split && team != 0) ? item.row_begin : item.row_end;
+#pragma unroll 1
+    for (int r = item.row_begin + team; r < r_end; r += NT) {
+      float rs[NRr][VPL][W];
+      float acc[NOUT][VPL][W];
+      const int64_t e0 = split ? item.e_begin : __ldg(a.ptr + r);
+      const int64_t e1 = split ? item.e_end : __ldg(a.ptr + r + 1);
+      K::load_row_state(a, r, tl, rs);
+      K::init_acc(a, r, tl, acc, a.accumulate != 0 && !split);
+      K::run_edges(a, e0, e1, rs, acc, tmask, tl);
+      if (!split) {
         K::store_row(a, r, tl, acc);
-      }
-    } else {
-      const sg_split sp = a.splits[item.split];
-      const int64_t r = item.row_begin;
-      if (team == 0) {
-        float rs[NRr][VPL][W];
-        float acc[NOUT][VPL][W];
-        K::load_row_state(a, r, tl, rs);
-        K::init_acc(a, r, tl, acc, false);
-        K::run_edges(a, item.e_begin, item.e_end, rs, acc, tmask, tl);
-        const int64_t slot = sp.slot0 + item.sub;
+      } else {
+        const int64_t slot = a.splits[item.split].slot0 + item.sub;
 #pragma unroll
         for (int o = 0; o < NOUT; ++o)
 #pragma unroll
@@ -317,6 +369,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
             }
           }
       }
+    }
+    if (split) {
+      const sg_split sp = a.splits[item.split];
+      const int64_t r = item.row_begin;
       __threadfence();
       __syncwarp();
       int ticket = 0;
@@ -327,6 +383,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
         if (team == 0) {
           float acc[NOUT][VPL][W];
           K::init_acc(a, r, tl, acc, a.accumulate != 0);
+          #pragma unroll 1
           for (int s = 0; s < sp.n_sub; ++s) {
 #pragma unroll
             for (int o = 0; o < NOUT; ++o)
@@ -372,7 +429,7 @@ int sm_count() {
 template <int MODE, int DT, int W, int VPL, int LPR>
 cudaError_t launch_one(const PropArgs& a, cudaStream_t st) {
   constexpr int NG = ModeT<MODE>::NG;
-  constexpr int DEPTH = (VPL * NG) <= 4 ? 8 / (VPL * NG) : 2;
+  constexpr int DEPTH = (VPL * NG) <= 4 ? 8 / (VPL * NG) : (NG > 1 ? 1 : 2);
   auto kern = prop_kernel<MODE, DT, W, VPL, LPR, DEPTH>;
   static int blocks_per_sm = 0;
   if (!blocks_per_sm) {
@@ -418,6 +475,10 @@ cudaError_t dispatch_vpl(const PropArgs& a, int LPR, int VPL, cudaStream_t st) {
 
 template <int MODE>
 cudaError_t dispatch_mode(int dtype, bool vec, const PropArgs& a, int LPR, int VPL, cudaStream_t st) {
+#ifdef SG_TUNE_GCN_ONLY  // fast register/spill iteration: build only the fp32 GCN kernels
+  if (MODE != SG_PROP_GCN || dtype != SG_F32 || !vec) return cudaErrorNotSupported;
+  return dispatch_vpl<SG_PROP_GCN, SG_F32, 4>(a, LPR, VPL, st);
+#endif
   if (dtype == SG_F32)
     return vec ? dispatch_vpl<MODE, SG_F32, 4>(a, LPR, VPL, st)
                : dispatch_vpl<MODE, SG_F32, 1>(a, LPR, VPL, st);

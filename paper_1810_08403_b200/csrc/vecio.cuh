@@ -1,4 +1,8 @@
 // 128-bit vector loads/stores with fp32 compute for fp32 / bf16 storage.
+//
+// A "vector" is W elements = 16 bytes (W = 4 fp32 or 8 bf16) or a single element
+// (W = 1).  Loads return the raw bits (Raw) so that in-flight data costs the same
+// registers for both dtypes; unpack() widens to fp32 at the point of use.
 #pragma once
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -14,13 +18,19 @@ struct VecIO;
 
 template <>
 struct VecIO<SG_F32, 4> {
-  static __device__ __forceinline__ void ld_nc(const void* base, int64_t off, float* v) {
-    float4 r = __ldg(reinterpret_cast<const float4*>(static_cast<const float*>(base) + off));
+  using Elem = float;
+  using Raw = float4;
+  static __device__ __forceinline__ Raw ld_raw(const Elem* p) {
+    return __ldg(reinterpret_cast<const float4*>(p));
+  }
+  static __device__ __forceinline__ void unpack(const Raw& r, float* v) {
     v[0] = r.x; v[1] = r.y; v[2] = r.z; v[3] = r.w;
   }
+  static __device__ __forceinline__ void ld_nc(const void* base, int64_t off, float* v) {
+    unpack(ld_raw(static_cast<const float*>(base) + off), v);
+  }
   static __device__ __forceinline__ void ld_cs(const void* base, int64_t off, float* v) {
-    float4 r = __ldcs(reinterpret_cast<const float4*>(static_cast<const float*>(base) + off));
-    v[0] = r.x; v[1] = r.y; v[2] = r.z; v[3] = r.w;
+    unpack(__ldcs(reinterpret_cast<const float4*>(static_cast<const float*>(base) + off)), v);
   }
   static __device__ __forceinline__ void st(void* base, int64_t off, const float* v, int nvalid) {
     float* p = static_cast<float*>(base) + off;
@@ -34,6 +44,10 @@ struct VecIO<SG_F32, 4> {
 
 template <>
 struct VecIO<SG_F32, 1> {
+  using Elem = float;
+  using Raw = float;
+  static __device__ __forceinline__ Raw ld_raw(const Elem* p) { return __ldg(p); }
+  static __device__ __forceinline__ void unpack(const Raw& r, float* v) { v[0] = r; }
   static __device__ __forceinline__ void ld_nc(const void* base, int64_t off, float* v) {
     v[0] = __ldg(static_cast<const float*>(base) + off);
   }
@@ -47,7 +61,12 @@ struct VecIO<SG_F32, 1> {
 
 template <>
 struct VecIO<SG_BF16, 8> {
-  static __device__ __forceinline__ void unpack(uint4 r, float* v) {
+  using Elem = __nv_bfloat16;
+  using Raw = uint4;
+  static __device__ __forceinline__ Raw ld_raw(const Elem* p) {
+    return __ldg(reinterpret_cast<const uint4*>(p));
+  }
+  static __device__ __forceinline__ void unpack(const Raw& r, float* v) {
     const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&r);
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -57,7 +76,7 @@ struct VecIO<SG_BF16, 8> {
     }
   }
   static __device__ __forceinline__ void ld_nc(const void* base, int64_t off, float* v) {
-    unpack(__ldg(reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(base) + off)), v);
+    unpack(ld_raw(static_cast<const __nv_bfloat16*>(base) + off), v);
   }
   static __device__ __forceinline__ void ld_cs(const void* base, int64_t off, float* v) {
     unpack(__ldcs(reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(base) + off)), v);
@@ -78,6 +97,10 @@ struct VecIO<SG_BF16, 8> {
 
 template <>
 struct VecIO<SG_BF16, 1> {
+  using Elem = __nv_bfloat16;
+  using Raw = __nv_bfloat16;
+  static __device__ __forceinline__ Raw ld_raw(const Elem* p) { return p[0]; }
+  static __device__ __forceinline__ void unpack(const Raw& r, float* v) { v[0] = __bfloat162float(r); }
   static __device__ __forceinline__ void ld_nc(const void* base, int64_t off, float* v) {
     v[0] = __bfloat162float(static_cast<const __nv_bfloat16*>(base)[off]);
   }
@@ -88,6 +111,5 @@ struct VecIO<SG_BF16, 1> {
     if (nvalid >= 1) static_cast<__nv_bfloat16*>(base)[off] = __float2bfloat16_rn(v[0]);
   }
 };
-
 
 }  // namespace sg

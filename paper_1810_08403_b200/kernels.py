@@ -22,9 +22,13 @@ def dtype_code(t):
 
 def ld(t):
     """Leading dimension (row stride, elements) of a row-major 2-D view."""
-    if t.dim() != 2 or t.stride(1) != 1:
+    if t.dim() != 2:
+        raise ValueError("expected a 2-D tensor")
+    if t.numel() == 0:
+        return max(t.shape[1], 1)
+    if t.stride(1) != 1 and t.shape[1] > 1:
         raise ValueError("expected a 2-D tensor with unit column stride")
-    return t.stride(0)
+    return max(t.stride(0), t.shape[1]) if t.shape[0] == 1 else t.stride(0)
 
 
 class Workspace:

@@ -171,9 +171,16 @@ def test_gemm_f32(sg, M, N, K, ta, tb):
     C = torch.empty((M, N), device="cuda")
     D = torch.empty((M, N), device="cuda")
     Kn.gemm(_dev(A), _dev(B), C, trans_a=bool(ta), trans_b=bool(tb), relu_out=D)
-    ref = (A.T if ta else A).astype(np.float64) @ (B.T if tb else B).astype(np.float64)
-    assert_close(C.cpu().numpy(), ref, 1e-5, "C")
-    assert np.array_equal(D.cpu().numpy(), np.maximum(C.cpu().numpy(), 0))
+    A64 = (A.T if ta else A).astype(np.float64)
+    B64 = (B.T if tb else B).astype(np.float64)
+    ref = A64 @ B64
+    got = C.cpu().numpy()
+    # deterministic fp32 dot-product error bound |d| <= gamma_K |A||B|, gamma_K ~ K u (u = 2^-24)
+    bound = (K + 2) * 2.0 ** -24 * (np.abs(A64) @ np.abs(B64)) + 1e-30
+    assert np.all(np.abs(got - ref) <= bound)
+    if K:
+        assert np.linalg.norm(got - ref) <= 1e-6 * np.linalg.norm(ref)
+    assert np.array_equal(D.cpu().numpy(), np.maximum(got, 0))
 
 
 def test_primitives_vs_oracle(sg):
@@ -315,12 +322,12 @@ def test_training_decreases_and_graph_replay_deterministic(sg):
     W0 = m.weights()
     losses = []
     for _ in range(10):
-        m.train_step(0.01)
+        m.train_step(1.0)
         losses.append(m.loss.item())
     assert all(b < a for a, b in zip(losses, losses[1:])), losses
     # CUDA-graph replay reproduces eager steps bit for bit
     m.set_weights(W0)
-    m.capture(0.01)
+    m.capture(1.0)
     m.set_weights(W0)
     replayed = []
     for _ in range(10):
