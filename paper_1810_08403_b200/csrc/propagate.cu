@@ -55,6 +55,19 @@ struct ModeT<SG_PROP_GCN> {
   }
 };
 
+// (a0, a1) += (t0, t1) with one packed FADD2 (add.rn.f32x2): per-lane IEEE
+// round-to-nearest, i.e. bitwise the same as two scalar adds.  (ptxas contracts a
+// packed mul.rn.f32x2 feeding this into FFMA2, so products stay scalar __fmul_rn.)
+__device__ __forceinline__ void add2_rn(float& a0, float& a1, float t0, float t1) {
+  asm("{\n\t.reg .b64 a, t;\n\t"
+      "mov.b64 a, {%0, %1};\n\t"
+      "mov.b64 t, {%2, %3};\n\t"
+      "add.rn.f32x2 a, a, t;\n\t"
+      "mov.b64 {%0, %1}, a;\n\t}"
+      : "+f"(a0), "+f"(a1)
+      : "f"(t0), "f"(t1));
+}
+
 __device__ __forceinline__ float sigmoid_ref(float x) {
   // 1.0 / (1.0 + np.exp(-x))  (tensor.py:205)
   return __fdiv_rn(1.0f, __fadd_rn(1.0f, expf(-x)));
@@ -168,12 +181,24 @@ struct Prop {
           float x0[W], x1[W];
           IO::unpack(g[d][0][v], x0);
           IO::unpack(g[d][NG - 1][v], x1);
+          if constexpr (W % 2 == 0) {
 #pragma unroll
-          for (int k = 0; k < W; ++k) {
-            float t0, t1 = 0.f;
-            M::term(&x0[k], &x1[k], &rs[0][v][k], &rs[NR > 1 ? 1 : 0][v][k], wv[d], &t0, &t1);
-            acc[0][v][k] = __fadd_rn(acc[0][v][k], t0);
-            if (NOUT > 1) acc[NOUT - 1][v][k] = __fadd_rn(acc[NOUT - 1][v][k], t1);
+            for (int k = 0; k < W; k += 2) {
+              float t0a, t1a = 0.f, t0b, t1b = 0.f;
+              M::term(&x0[k], &x1[k], &rs[0][v][k], &rs[NR > 1 ? 1 : 0][v][k], wv[d], &t0a, &t1a);
+              M::term(&x0[k + 1], &x1[k + 1], &rs[0][v][k + 1], &rs[NR > 1 ? 1 : 0][v][k + 1], wv[d],
+                      &t0b, &t1b);
+              add2_rn(acc[0][v][k], acc[0][v][k + 1], t0a, t0b);
+              if (NOUT > 1) add2_rn(acc[NOUT - 1][v][k], acc[NOUT - 1][v][k + 1], t1a, t1b);
+            }
+          } else {
+#pragma unroll
+            for (int k = 0; k < W; ++k) {
+              float t0, t1 = 0.f;
+              M::term(&x0[k], &x1[k], &rs[0][v][k], &rs[NR > 1 ? 1 : 0][v][k], wv[d], &t0, &t1);
+              acc[0][v][k] = __fadd_rn(acc[0][v][k], t0);
+              if (NOUT > 1) acc[NOUT - 1][v][k] = __fadd_rn(acc[NOUT - 1][v][k], t1);
+            }
           }
         }
       }
@@ -426,10 +451,51 @@ int sm_count() {
   return g_sm_count;
 }
 
+#include "propagate_tma.cuh"
+
+// TMA ring path for wide single-operand rows (opt-in with SG_PROP_TMA=1; see propagate_tma.cuh).
+bool tma_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("SG_PROP_TMA");
+    on = (e && e[0] == '1') ? 1 : 0;  // opt-in until it beats the register path
+  }
+  return on == 1;
+}
+
+template <int MODE, int DT, int VPL>
+cudaError_t launch_tma(const PropArgs& a, cudaStream_t st) {
+  constexpr int W = DT == SG_F32 ? 4 : 8;
+  (void)W;
+  const uint32_t slot_bytes = (uint32_t)a.Fv * 16u;
+  const int budget = 110 * 1024;  // per block; two 8-warp blocks per SM
+  int S = (int)((budget - 1024) / ((int64_t)kTmaWarps * slot_bytes));
+  S = std::max(2, std::min(S, 16));
+  const size_t smem = (size_t)((kTmaWarps * S * 8 + 127) / 128 * 128) + (size_t)kTmaWarps * S * slot_bytes;
+  auto kern = prop_tma_kernel<MODE, DT, VPL>;
+  static int configured = 0;
+  if (!configured) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    configured = 1;
+  }
+  int blocks_per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, kTmaWarps * 32, smem);
+  if (blocks_per_sm <= 0) blocks_per_sm = 1;
+  int64_t want = ((int64_t)a.n_items + kTmaWarps - 1) / kTmaWarps;
+  int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)blocks_per_sm * sm_count()));
+  kern<<<grid, kTmaWarps * 32, smem, st>>>(a, S, slot_bytes);
+  sg::count_launch();
+  return cudaGetLastError();
+}
+
 template <int MODE, int DT, int W, int VPL, int LPR>
 cudaError_t launch_one(const PropArgs& a, cudaStream_t st) {
   constexpr int NG = ModeT<MODE>::NG;
+  // rows in flight per warp: ~8 vectors per lane (DEPTH 3 at VPL 5 spills and runs 50% slower)
   constexpr int DEPTH = (VPL * NG) <= 4 ? 8 / (VPL * NG) : (NG > 1 ? 1 : 2);
+  if constexpr (LPR == 32 && VPL >= 2 && NG == 1 && W > 1) {
+    if (tma_enabled()) return launch_tma<MODE, DT, VPL>(a, st);
+  }
   auto kern = prop_kernel<MODE, DT, W, VPL, LPR, DEPTH>;
   static int blocks_per_sm = 0;
   if (!blocks_per_sm) {
