@@ -1,15 +1,352 @@
-// tcgen05 / TMEM tensor-core GEMM paths (SG_GEMM_TF32X3, SG_GEMM_BF16) -- see below.
+// ApplyVertex GEMM on the 5th-generation tensor cores (tcgen05 + TMEM), fp32 in/out.
+//
+// C[M,N] = op(A)[M,K] . op(B)[K,N] (matmul, tensor.py:306-319), every operand
+// fp32 in HBM.  Precision SG_GEMM_TF32X3 ("3xTF32"): each fp32 tile is split on
+// the fly into hi = tf32(x) (mantissa truncated to 10 bits) and lo = x - hi, and
+// the tensor core accumulates hi*hi + hi*lo + lo*hi in fp32 TMEM -- ~1e-6
+// relative error, inside the 1e-4 fp32 parity bar that a single TF32 pass misses
+// (SURVEY.md §7 "fp32 parity of the GEMM").
+//
+// CTA = 128 x BN output tile, K in blocks of 32, STAGES-deep shared-memory ring:
+//   warps 0-3  load A/B tiles with coalesced 128-bit LDG, split hi/lo and store them
+//              in the UMMA canonical K-major SWIZZLE_128B layout (operands stored
+//              MN-contiguous in HBM, e.g. a^T in dW = a^T dz, are transposed 4x4 in
+//              registers on the way, never in memory); after the K loop they drain
+//              the TMEM accumulator with tcgen05.ld (epilogue).
+//   warp 4     allocates TMEM and is the single-thread tcgen05.mma issuer; each
+//              stage is released back to the loaders by tcgen05.commit -> mbarrier.
+// Long-K products (dW = a^T dz, K = |V|) are split over K; fp32 partials are
+// reduced in a fixed order, so results are deterministic.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "common.h"
+#include "sm100.cuh"
+
+namespace {
+
+constexpr int BM = 128, BK = 32;
+constexpr int kLoadThreads = 128;
+constexpr int kThreads = kLoadThreads + 32;
+
+template <int BN>
+struct Cfg {
+  static constexpr int STAGES = BN >= 128 ? 3 : 4;
+  static constexpr int A_TILE = BM * BK * 4;  // bytes, fp32
+  static constexpr int B_TILE = BN * BK * 4;
+  static constexpr int STAGE = 2 * A_TILE + 2 * B_TILE;  // hi + lo planes
+  static constexpr int SMEM = STAGES * STAGE + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int TMEM_COLS = BN < 32 ? 32 : BN;
+};
+
+struct TcArgs {
+  const float* A;
+  const float* B;
+  float* C;
+  float* D;
+  float* partial;
+  int64_t lda, ldb, ldc, ldd;
+  int64_t M, N, K;
+  int kb_per_split, n_kb;
+  int epilogue;
+  int vec_a, vec_b;
+};
+
+__device__ __forceinline__ void split_tf32(float4 x, float4& hi, float4& lo) {
+  const uint32_t m = 0xFFFFE000u;
+  hi.x = __uint_as_float(__float_as_uint(x.x) & m);
+  hi.y = __uint_as_float(__float_as_uint(x.y) & m);
+  hi.z = __uint_as_float(__float_as_uint(x.z) & m);
+  hi.w = __uint_as_float(__float_as_uint(x.w) & m);
+  lo.x = __fsub_rn(x.x, hi.x);
+  lo.y = __fsub_rn(x.y, hi.y);
+  lo.z = __fsub_rn(x.z, hi.z);
+  lo.w = __fsub_rn(x.w, hi.w);
+}
+
+__device__ __forceinline__ float4 ld4(const float* base, int64_t ld, int64_t r, int64_t c, int64_t R,
+                                      int64_t Cn, bool vec) {
+  // element (r, c..c+3) of a row-major [R, Cn] matrix, zero outside
+  if (r >= R) return make_float4(0.f, 0.f, 0.f, 0.f);
+  const float* p = base + r * ld + c;
+  if (vec && c + 3 < Cn) return __ldg(reinterpret_cast<const float4*>(p));
+  float4 v;
+  v.x = c + 0 < Cn ? __ldg(p + 0) : 0.f;
+  v.y = c + 1 < Cn ? __ldg(p + 1) : 0.f;
+  v.z = c + 2 < Cn ? __ldg(p + 2) : 0.f;
+  v.w = c + 3 < Cn ? __ldg(p + 3) : 0.f;
+  return v;
+}
+
+__device__ __forceinline__ void sts128(uint32_t addr, float4 v) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(v.x), "f"(v.y), "f"(v.z),
+               "f"(v.w)
+               : "memory");
+}
+
+// Load + split one operand tile (R rows of the operand x 32 k) into hi/lo planes, stored
+// in the K-major SWIZZLE_128B canonical layout: atom = 8 rows x 128 B, the 16-B chunk c
+// of row r at chunk c ^ (r & 7), row-group stride (SBO) 1024 B.
+// byte offset of the 16-B chunk holding (row, k..k+3) in a K-major SWIZZLE_128B tile
+__device__ __forceinline__ uint32_t kmajor_off(int row, int kc) {
+  return (row >> 3) * 1024 + (row & 7) * 128 + ((kc ^ (row & 7)) << 4);
+}
+
+__device__ __forceinline__ void store_split(uint32_t hi_base, uint32_t lo_base, uint32_t off, float4 v) {
+  float4 hi, lo;
+  split_tf32(v, hi, lo);
+  sts128(hi_base + off, hi);
+  sts128(lo_base + off, lo);
+}
+
+template <bool MN_MAJOR, int R>
+__device__ __forceinline__ void load_tile(const float* X, int64_t ld, int64_t mn0, int64_t k0,
+                                          int64_t MNmax, int64_t Kmax, bool vec, uint32_t hi_base,
+                                          uint32_t lo_base, int t) {
+  if constexpr (!MN_MAJOR) {
+    // rows contiguous along k: one 16-B chunk per LDG.128 / STS.128
+    constexpr int PER = R * BK / 4 / kLoadThreads;
+    float4 v[PER];
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const int idx = t + kLoadThreads * i;
+      v[i] = ld4(X, ld, mn0 + idx / 8, k0 + (idx % 8) * 4, MNmax, Kmax, vec);
+    }
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const int idx = t + kLoadThreads * i;
+      store_split(hi_base, lo_base, kmajor_off(idx / 8, idx % 8), v[i]);
+    }
+  } else {
+    // memory contiguous along the operand rows (X[k, m]): load 4x4 blocks (4 k-rows of
+    // 4 consecutive m), transpose in registers and store K-major -- the shared-memory
+    // operand is always K-major, so no operand is ever transposed in HBM.
+    constexpr int BLOCKS = (R / 4) * (BK / 4);
+    constexpr int PER = BLOCKS / kLoadThreads;
+    float4 v[PER][4];
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const int idx = t + kLoadThreads * i;
+      const int mb = idx % (R / 4), kb = idx / (R / 4);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int64_t k = k0 + kb * 4 + q;
+        v[i][q] = k < Kmax ? ld4(X, ld, k, mn0 + mb * 4, Kmax, MNmax, vec)
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const int idx = t + kLoadThreads * i;
+      const int mb = idx % (R / 4), kb = idx / (R / 4);
+      store_split(hi_base, lo_base, kmajor_off(mb * 4 + 0, kb), make_float4(v[i][0].x, v[i][1].x, v[i][2].x, v[i][3].x));
+      store_split(hi_base, lo_base, kmajor_off(mb * 4 + 1, kb), make_float4(v[i][0].y, v[i][1].y, v[i][2].y, v[i][3].y));
+      store_split(hi_base, lo_base, kmajor_off(mb * 4 + 2, kb), make_float4(v[i][0].z, v[i][1].z, v[i][2].z, v[i][3].z));
+      store_split(hi_base, lo_base, kmajor_off(mb * 4 + 3, kb), make_float4(v[i][0].w, v[i][1].w, v[i][2].w, v[i][3].w));
+    }
+  }
+}
+
+// one tf32 UMMA consumes K = 8 = 32 B of each K-major row: advance the start address
+__device__ __forceinline__ uint64_t tile_desc(uint32_t base, int kk) {
+  return sm100::smem_desc(base + kk * 32, 16, 1024, sm100::kLayoutSW128);
+}
+
+template <bool A_MN, bool B_MN, int BN>
+__global__ void __launch_bounds__(kThreads, 1) gemm_tf32x3_kernel(const TcArgs p) {
+  using C = Cfg<BN>;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // 1024-byte alignment for the SWIZZLE_128B atoms
+  const uint32_t raw = sm100::smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  unsigned char* base_ptr = smem_raw + (base - raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(base_ptr + C::STAGES * C::STAGE);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* done = empty + C::STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
+  const int kb0 = blockIdx.z * p.kb_per_split;
+  const int kb1 = min(p.n_kb, kb0 + p.kb_per_split);
+  const int nkb = kb1 - kb0;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      sm100::mbar_init(full + s, kLoadThreads);
+      sm100::mbar_init(empty + s, 1);
+    }
+    sm100::mbar_init(done, 1);
+    sm100::fence_mbar_init();
+  }
+  if (warp == 4) sm100::tmem_alloc<C::TMEM_COLS>(tmem_slot);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp < 4) {
+    // ---------------- loaders: LDG -> split hi/lo -> swizzled STS
+    const int t = threadIdx.x;
+    for (int i = 0; i < nkb; ++i) {
+      const int s = i % C::STAGES;
+      const uint32_t use = i / C::STAGES;
+      sm100::mbar_wait(empty + s, (use & 1) ^ 1);
+      const uint32_t st = base + s * C::STAGE;
+      const int64_t k0 = (int64_t)(kb0 + i) * BK;
+      load_tile<A_MN, BM>(p.A, p.lda, m0, k0, p.M, p.K, p.vec_a, st, st + C::A_TILE, t);
+      load_tile<B_MN, BN>(p.B, p.ldb, n0, k0, p.N, p.K, p.vec_b, st + 2 * C::A_TILE,
+                          st + 2 * C::A_TILE + C::B_TILE, t);
+      sm100::fence_proxy_async_smem();
+      sm100::mbar_arrive(full + s);
+    }
+    // ---------------- epilogue: TMEM -> registers -> global
+    sm100::mbar_wait(done, 0);
+    sm100::tc_fence_after();
+    const int64_t row = m0 + warp * 32 + lane;
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 16) {
+      float v[16];
+      sm100::tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + c0, v);
+      if (row < p.M) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int64_t col = n0 + c0 + j;
+          if (col < p.N) {
+            if (p.partial) {
+              p.partial[((int64_t)blockIdx.z * p.M + row) * p.N + col] = v[j];
+            } else {
+              p.C[row * p.ldc + col] = v[j];
+              if (p.epilogue == SG_EPI_RELU_DUAL) p.D[row * p.ldd + col] = fmaxf(v[j], 0.f);
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 4) {
+    // ---------------- single-thread UMMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = sm100::idesc_tf32(BM, BN, false, false);  // smem always K-major
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % C::STAGES;
+        const uint32_t use = i / C::STAGES;
+        sm100::mbar_wait(full + s, use & 1);
+        sm100::tc_fence_after();
+        const uint32_t st = base + s * C::STAGE;
+        const uint32_t a_hi = st, a_lo = st + C::A_TILE;
+        const uint32_t b_hi = st + 2 * C::A_TILE, b_lo = b_hi + C::B_TILE;
+#pragma unroll
+        for (int kk = 0; kk < BK / 8; ++kk) {
+          const uint64_t ah = tile_desc(a_hi, kk), al = tile_desc(a_lo, kk);
+          const uint64_t bh = tile_desc(b_hi, kk), bl = tile_desc(b_lo, kk);
+          sm100::umma_tf32(tmem, ah, bh, idesc, (i > 0 || kk > 0) ? 1u : 0u);
+          sm100::umma_tf32(tmem, ah, bl, idesc, 1u);
+          sm100::umma_tf32(tmem, al, bh, idesc, 1u);
+        }
+        sm100::umma_commit(empty + s);  // frees the stage when these MMAs are done
+      }
+      sm100::umma_commit(done);
+    }
+    __syncwarp();
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  if (warp == 4) sm100::tmem_dealloc<C::TMEM_COLS>(tmem);
+}
+
+__global__ void tc_splitk_reduce(const float* partial, int splits, int64_t M, int64_t N, float* C,
+                                 int64_t ldc, float* D, int64_t ldd, int epilogue) {
+  const int64_t total = M * N;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    float s = 0.f;
+    for (int z = 0; z < splits; ++z) s += partial[(int64_t)z * total + t];  // fixed order
+    const int64_t m = t / N, n = t % N;
+    C[m * ldc + n] = s;
+    if (epilogue == SG_EPI_RELU_DUAL) D[m * ldd + n] = fmaxf(s, 0.f);
+  }
+}
+
+int pick_bn(int64_t N) { return N <= 64 ? 64 : 128; }
+
+int tc_splits(int64_t M, int64_t N, int64_t K) {
+  const int64_t tiles = ((M + BM - 1) / BM) * ((N + pick_bn(N) - 1) / pick_bn(N));
+  const int64_t nkb = (K + BK - 1) / BK;
+  if (tiles >= 148 || nkb < 16) return 1;
+  int64_t s = std::min<int64_t>((2 * 148 + tiles - 1) / tiles, nkb / 8);
+  return (int)std::max<int64_t>(1, std::min<int64_t>(s, 64));
+}
+
+template <bool A_MN, bool B_MN, int BN>
+cudaError_t launch_tc(const TcArgs& p, dim3 grid, cudaStream_t st) {
+  auto k = gemm_tf32x3_kernel<A_MN, B_MN, BN>;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM);
+    configured = true;
+  }
+  k<<<grid, kThreads, Cfg<BN>::SMEM, st>>>(p);
+  sg::count_launch();
+  return cudaGetLastError();
+}
+
+template <int BN>
+cudaError_t dispatch_major(bool a_mn, bool b_mn, const TcArgs& p, dim3 grid, cudaStream_t st) {
+  if (!a_mn && !b_mn) return launch_tc<false, false, BN>(p, grid, st);
+  if (!a_mn && b_mn) return launch_tc<false, true, BN>(p, grid, st);
+  if (a_mn && !b_mn) return launch_tc<true, false, BN>(p, grid, st);
+  return launch_tc<true, true, BN>(p, grid, st);
+}
+
+}  // namespace
 
 int64_t sg_gemm_tc_workspace_bytes(int64_t M, int64_t N, int64_t K, int prec) {
-  (void)M; (void)N; (void)K; (void)prec;
-  return 0;
+  (void)prec;
+  const int s = tc_splits(M, N, K);
+  return s > 1 ? (int64_t)s * M * N * 4 : 0;
 }
 
 int sg_gemm_tc(int prec, int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, const float* A,
                int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc, int epilogue,
                float* D, int64_t ldd, void* workspace, int64_t workspace_bytes, cudaStream_t st) {
-  SG_FAIL(SG_EINVAL, "tensor-core GEMM precision %d not built yet", prec);
+  SG_REQUIRE(prec == SG_GEMM_TF32X3, SG_EINVAL, "tensor-core GEMM precision %d not supported", prec);
+  if (K == 0) {
+    cudaMemset2DAsync(C, ldc * 4, 0, N * 4, M, st);
+    if (epilogue == SG_EPI_RELU_DUAL) cudaMemset2DAsync(D, ldd * 4, 0, N * 4, M, st);
+    return SG_OK;
+  }
+  // K-major when the reduction dim is contiguous: A stored [M,K] (!trans_a), B stored [N,K] (trans_b)
+  const bool a_mn = trans_a != 0, b_mn = trans_b == 0;
+  TcArgs p;
+  p.A = A; p.B = B; p.C = C; p.D = D;
+  p.lda = lda; p.ldb = ldb; p.ldc = ldc; p.ldd = ldd;
+  p.M = M; p.N = N; p.K = K;
+  p.epilogue = epilogue;
+  p.vec_a = (lda % 4 == 0) && ((uintptr_t)A % 16 == 0);
+  p.vec_b = (ldb % 4 == 0) && ((uintptr_t)B % 16 == 0);
+  p.n_kb = (int)((K + BK - 1) / BK);
+  const int splits = tc_splits(M, N, K);
+  p.kb_per_split = (p.n_kb + splits - 1) / splits;
+  const int gz = (p.n_kb + p.kb_per_split - 1) / p.kb_per_split;
+  p.partial = nullptr;
+  if (gz > 1) {
+    SG_REQUIRE(workspace && workspace_bytes >= (int64_t)gz * M * N * 4, SG_EBUDGET,
+               "tensor-core GEMM split-K workspace too small");
+    p.partial = (float*)workspace;
+  }
+  const int BN = pick_bn(N);
+  dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM), (unsigned)gz);
+  cudaError_t e = BN == 64 ? dispatch_major<64>(a_mn, b_mn, p, grid, st)
+                           : dispatch_major<128>(a_mn, b_mn, p, grid, st);
+  if (e != cudaSuccess) SG_FAIL(SG_ECUDA, "tcgen05 gemm launch: %s", cudaGetErrorString(e));
+  if (gz > 1) {
+    const int64_t total = M * N;
+    int g = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+    tc_splitk_reduce<<<g, 256, 0, st>>>(p.partial, gz, M, N, C, ldc, D, ldd, epilogue);
+    sg::count_launch();
+    e = cudaGetLastError();
+    if (e != cudaSuccess) SG_FAIL(SG_ECUDA, "split-k reduce: %s", cudaGetErrorString(e));
+  }
+  return SG_OK;
 }

@@ -46,7 +46,7 @@ class SAGAModel:
     through ``hoist_vertex_computation`` + ``fuse_sag`` and must lower to a fused
     gather (gcn / pass / ggcn) followed by ApplyVertex = ReLU(W accum)."""
 
-    def __init__(self, programs, grid, weights=None, *, seed=2, gemm_prec=_lib.GEMM_F32,
+    def __init__(self, programs, grid, weights=None, *, seed=2, gemm_prec=_lib.GEMM_TF32X3,
                  device="cuda", strict=True):
         if not torch.cuda.is_available():
             raise RuntimeError("SAGAModel needs a CUDA device (no CPU fallback)")

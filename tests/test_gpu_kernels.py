@@ -183,6 +183,33 @@ def test_gemm_f32(sg, M, N, K, ta, tb):
     assert np.array_equal(D.cpu().numpy(), np.maximum(got, 0))
 
 
+@pytest.mark.parametrize("M,N,K,ta,tb", [(1000, 128, 602, 0, 0), (602, 128, 20000, 1, 0),
+                                         (3000, 41, 128, 0, 1), (7, 5, 3, 0, 0), (130, 3, 1, 1, 1),
+                                         (300, 200, 77, 1, 1), (4096, 64, 604, 0, 0),
+                                         (128, 41, 40000, 1, 0)])
+def test_gemm_tcgen05_tf32x3(sg, M, N, K, ta, tb):
+    """tcgen05/TMEM 3xTF32 GEMM (all four operand majors, split-K) vs fp64."""
+    from paper_1810_08403_b200 import _lib
+    from paper_1810_08403_b200 import kernels as Kn
+
+    r = np.random.default_rng(M * 7 + N + K)
+    A = r.uniform(-1, 1, (K, M) if ta else (M, K)).astype(np.float32)
+    B = r.uniform(-1, 1, (N, K) if tb else (K, N)).astype(np.float32)
+    C = torch.empty((M, N), device="cuda")
+    D = torch.empty((M, N), device="cuda")
+    Kn.gemm(_dev(A), _dev(B), C, trans_a=bool(ta), trans_b=bool(tb), relu_out=D,
+            prec=_lib.GEMM_TF32X3)
+    A64 = (A.T if ta else A).astype(np.float64)
+    B64 = (B.T if tb else B).astype(np.float64)
+    ref = A64 @ B64
+    got = C.cpu().numpy()
+    # 3xTF32: operand split error ~2^-21 per product term plus fp32 accumulation
+    bound = (2.0 ** -19 + (K + 2) * 2.0 ** -24) * (np.abs(A64) @ np.abs(B64)) + 1e-30
+    assert np.all(np.abs(got - ref) <= bound), float(np.max(np.abs(got - ref) / bound))
+    assert np.linalg.norm(got - ref) <= 1e-5 * max(np.linalg.norm(ref), 1e-30)
+    assert np.array_equal(D.cpu().numpy(), np.maximum(got, 0))
+
+
 def test_primitives_vs_oracle(sg):
     from paper_1810_08403_b200 import ops
 
