@@ -157,13 +157,15 @@ int sg_gemm(int prec, int trans_a, int trans_b, int64_t M, int64_t N, int64_t K,
             float* D, int64_t ldd, void* workspace, int64_t workspace_bytes, void* stream);
 
 /* Softmax cross-entropy head (tensor.py:487-506) on logits = relu(Z) when
- * relu_input (the last layer's ReLU) else Z: writes the mean
- * loss to *loss (device fp32 scalar) and dZ = seed * (p - onehot) / n, times the
- * ReLU mask when relu_input.  labels int64 [n]; *err_flag <- 1 on a bad label. */
+ * relu_input (the last layer's ReLU) else Z, over n local rows:
+ * writes -sum(log p[label]) / n_total to *loss (device fp32 scalar) and
+ * dZ = (p - onehot) / n_total, times the ReLU mask when relu_input.  n_total is the
+ * global row count when rows are sharded across ranks (<= 0 means n).  labels int64
+ * [n]; *err_flag <- 1 on a bad label. */
 int64_t sg_xent_workspace_bytes(int64_t n);
 int sg_softmax_xent(const float* Z, int64_t ldz, int relu_input, const int64_t* labels, int64_t n,
-                    int64_t C, float* loss, float* dZ, int64_t lddz, int32_t* err_flag,
-                    void* workspace, int64_t workspace_bytes, void* stream);
+                    int64_t C, int64_t n_total, float* loss, float* dZ, int64_t lddz,
+                    int32_t* err_flag, void* workspace, int64_t workspace_bytes, void* stream);
 
 /* Plain gradient descent W <- W - lr * dW. */
 int sg_sgd(float* W, const float* dW, int64_t n, float lr, void* stream);

@@ -61,7 +61,7 @@ _SIGS = {
     "sg_gemm": (_i32, [_i32, _i32, _i32, _i64, _i64, _i64, _p, _i64, _p, _i64, _p, _i64, _i32,
                        _p, _i64, _p, _i64, _p]),
     "sg_xent_workspace_bytes": (_i64, [_i64]),
-    "sg_softmax_xent": (_i32, [_p, _i64, _i32, _p, _i64, _i64, _p, _p, _i64, _p, _p, _i64, _p]),
+    "sg_softmax_xent": (_i32, [_p, _i64, _i32, _p, _i64, _i64, _i64, _p, _p, _i64, _p, _p, _i64, _p]),
     "sg_sgd": (_i32, [_p, _p, _i64, _f32, _p]),
     "sg_check_finite": (_i32, [_i32, _p, _i64, _i64, _i64, _p, _p]),
     "sg_ewise": (_i32, [_i32, _i64, _i64, _p, _i64, _p, _i64, _i64, _i64, _p, _i64, _p]),

@@ -15,12 +15,12 @@ int grid_for(int64_t work, int per_block) {
 
 // softmax_cross_entropy (tensor.py:487-506): one warp per row.
 __global__ void xent_rows_kernel(const float* Z, int64_t ldz, int relu_input, const int64_t* lab,
-                                 int64_t n, int64_t C, float* dZ, int64_t lddz, float* logp_out,
-                                 int32_t* err) {
+                                 int64_t n, int64_t C, int64_t n_total, float* dZ, int64_t lddz,
+                                 float* logp_out, int32_t* err) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const float inv_n = 1.0f / (float)n;
+  const float inv_n = 1.0f / (float)n_total;
   for (int64_t r = warp; r < n; r += nwarps) {
     const float* z = Z + r * ldz;
     int64_t l = lab[r];
@@ -58,7 +58,7 @@ __global__ void xent_rows_kernel(const float* Z, int64_t ldz, int relu_input, co
 }
 
 // Deterministic mean: one block, fixed per-thread strided order, fixed tree.
-__global__ void xent_mean_kernel(const float* logp, int64_t n, float* loss) {
+__global__ void xent_mean_kernel(const float* logp, int64_t n, int64_t n_total, float* loss) {
   __shared__ double s[1024];
   double acc = 0.0;
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) acc += (double)logp[i];
@@ -68,7 +68,7 @@ __global__ void xent_mean_kernel(const float* logp, int64_t n, float* loss) {
     if ((int)threadIdx.x < w) s[threadIdx.x] += s[threadIdx.x + w];
     __syncthreads();
   }
-  if (threadIdx.x == 0) *loss = (float)(-s[0] / (double)n);
+  if (threadIdx.x == 0) *loss = (float)(-s[0] / (double)n_total);
 }
 
 __global__ void sgd_kernel(float* W, const float* dW, int64_t n, float lr) {
@@ -155,16 +155,17 @@ extern "C" {
 int64_t sg_xent_workspace_bytes(int64_t n) { return std::max<int64_t>(n, 1) * 4; }
 
 int sg_softmax_xent(const float* Z, int64_t ldz, int relu_input, const int64_t* labels, int64_t n,
-                    int64_t C, float* loss, float* dZ, int64_t lddz, int32_t* err_flag,
-                    void* workspace, int64_t workspace_bytes, void* stream) {
+                    int64_t C, int64_t n_total, float* loss, float* dZ, int64_t lddz,
+                    int32_t* err_flag, void* workspace, int64_t workspace_bytes, void* stream) {
+  if (n_total <= 0) n_total = n;
   SG_REQUIRE(n >= 1 && C >= 1, SG_ESHAPE, "logits must be [n, classes] with n, classes >= 1");
   SG_REQUIRE(workspace_bytes >= sg_xent_workspace_bytes(n), SG_EBUDGET, "xent workspace too small");
   cudaStream_t st = (cudaStream_t)stream;
   float* logp = (float*)workspace;
-  xent_rows_kernel<<<grid_for(n * 32, 256), 256, 0, st>>>(Z, ldz, relu_input, labels, n, C, dZ,
-                                                         lddz, logp, err_flag);
+  xent_rows_kernel<<<grid_for(n * 32, 256), 256, 0, st>>>(Z, ldz, relu_input, labels, n, C, n_total,
+                                                         dZ, lddz, logp, err_flag);
   SG_LAUNCH_CHECK("xent rows");
-  xent_mean_kernel<<<1, 1024, 0, st>>>(logp, n, loss);
+  xent_mean_kernel<<<1, 1024, 0, st>>>(logp, n, n_total, loss);
   SG_LAUNCH_CHECK("xent mean");
   sg::count_launch(2);
   return SG_OK;

@@ -80,11 +80,11 @@ def gemm(A, B, C, *, trans_a=False, trans_b=False, relu_out=None, prec=_lib.GEMM
                       buf.numel(), stream_handle(stream)))
 
 
-def softmax_xent(Z, labels, loss, dZ, err, *, relu_input=True, ws=None, stream=None):
+def softmax_xent(Z, labels, loss, dZ, err, *, relu_input=True, n_total=0, ws=None, stream=None):
     n, C = Z.shape
     wsb = int(lib.sg_xent_workspace_bytes(n))
     buf = ws.get(wsb) if ws is not None else torch.empty(wsb, dtype=torch.uint8, device=Z.device)
-    check(lib.sg_softmax_xent(tptr(Z), ld(Z), int(relu_input), tptr(labels), n, C, tptr(loss),
+    check(lib.sg_softmax_xent(tptr(Z), ld(Z), int(relu_input), tptr(labels), n, C, int(n_total), tptr(loss),
                               tptr(dZ), ld(dZ), tptr(err), tptr(buf), buf.numel(),
                               stream_handle(stream)))
 
