@@ -8,12 +8,12 @@
 // (SURVEY.md §7 "fp32 parity of the GEMM").
 //
 // CTA = 128 x BN output tile, K in blocks of 32, STAGES-deep shared-memory ring:
-//   warps 0-3  load A/B tiles with coalesced 128-bit LDG, split hi/lo and store them
+//   warps 0-7  load A/B tiles with coalesced 128-bit LDG, split hi/lo and store them
 //              in the UMMA canonical K-major SWIZZLE_128B layout (operands stored
 //              MN-contiguous in HBM, e.g. a^T in dW = a^T dz, are transposed 4x4 in
 //              registers on the way, never in memory); after the K loop they drain
 //              the TMEM accumulator with tcgen05.ld (epilogue).
-//   warp 4     allocates TMEM and is the single-thread tcgen05.mma issuer; each
+//   warp 8     allocates TMEM and is the single-thread tcgen05.mma issuer; each
 //              stage is released back to the loaders by tcgen05.commit -> mbarrier.
 // Long-K products (dW = a^T dz, K = |V|) are split over K; fp32 partials are
 // reduced in a fixed order, so results are deterministic.
@@ -27,7 +27,8 @@
 namespace {
 
 constexpr int BM = 128, BK = 32;
-constexpr int kLoadThreads = 128;
+constexpr int kLoadThreads = 256;                 // 8 loader / epilogue warps
+constexpr int kMmaWarp = kLoadThreads / 32;       // warp 8: TMEM allocator + UMMA issuer
 constexpr int kThreads = kLoadThreads + 32;
 
 template <int BN>
@@ -123,11 +124,12 @@ __device__ __forceinline__ void load_tile(const float* X, int64_t ld, int64_t mn
     // 4 consecutive m), transpose in registers and store K-major -- the shared-memory
     // operand is always K-major, so no operand is ever transposed in HBM.
     constexpr int BLOCKS = (R / 4) * (BK / 4);
-    constexpr int PER = BLOCKS / kLoadThreads;
+    constexpr int PER = (BLOCKS + kLoadThreads - 1) / kLoadThreads;
     float4 v[PER][4];
 #pragma unroll
     for (int i = 0; i < PER; ++i) {
       const int idx = t + kLoadThreads * i;
+      if (BLOCKS % kLoadThreads != 0 && idx >= BLOCKS) continue;
       const int mb = idx % (R / 4), kb = idx / (R / 4);
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -139,6 +141,7 @@ __device__ __forceinline__ void load_tile(const float* X, int64_t ld, int64_t mn
 #pragma unroll
     for (int i = 0; i < PER; ++i) {
       const int idx = t + kLoadThreads * i;
+      if (BLOCKS % kLoadThreads != 0 && idx >= BLOCKS) continue;
       const int mb = idx % (R / 4), kb = idx / (R / 4);
       store_split(hi_base, lo_base, kmajor_off(mb * 4 + 0, kb), make_float4(v[i][0].x, v[i][1].x, v[i][2].x, v[i][3].x));
       store_split(hi_base, lo_base, kmajor_off(mb * 4 + 1, kb), make_float4(v[i][0].y, v[i][1].y, v[i][2].y, v[i][3].y));
@@ -180,13 +183,13 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tf32x3_kernel(const TcArgs p
     sm100::mbar_init(done, 1);
     sm100::fence_mbar_init();
   }
-  if (warp == 4) sm100::tmem_alloc<C::TMEM_COLS>(tmem_slot);
+  if (warp == kMmaWarp) sm100::tmem_alloc<C::TMEM_COLS>(tmem_slot);
   sm100::tc_fence_before();
   __syncthreads();
   sm100::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp < 4) {
+  if (warp < kMmaWarp) {
     // ---------------- loaders: LDG -> split hi/lo -> swizzled STS
     const int t = threadIdx.x;
     for (int i = 0; i < nkb; ++i) {
@@ -204,11 +207,13 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tf32x3_kernel(const TcArgs p
     // ---------------- epilogue: TMEM -> registers -> global
     sm100::mbar_wait(done, 0);
     sm100::tc_fence_after();
-    const int64_t row = m0 + warp * 32 + lane;
+    // warp w reads TMEM lane quarter w % 4 (its rows) and column half w / 4
+    const int quarter = warp & 3, half = warp >> 2;
+    const int64_t row = m0 + quarter * 32 + lane;
 #pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 16) {
+    for (int c0 = half * (BN / 2); c0 < (half + 1) * (BN / 2); c0 += 16) {
       float v[16];
-      sm100::tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + c0, v);
+      sm100::tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + c0, v);
       if (row < p.M) {
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
@@ -224,7 +229,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tf32x3_kernel(const TcArgs p
         }
       }
     }
-  } else if (warp == 4) {
+  } else if (warp == kMmaWarp) {
     // ---------------- single-thread UMMA issuer
     if (lane == 0) {
       constexpr uint32_t idesc = sm100::idesc_tf32(BM, BN, false, false);  // smem always K-major
@@ -252,7 +257,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tf32x3_kernel(const TcArgs p
   }
   sm100::tc_fence_before();
   __syncthreads();
-  if (warp == 4) sm100::tmem_dealloc<C::TMEM_COLS>(tmem);
+  if (warp == kMmaWarp) sm100::tmem_dealloc<C::TMEM_COLS>(tmem);
 }
 
 __global__ void tc_splitk_reduce(const float* partial, int splits, int64_t M, int64_t N, float* C,

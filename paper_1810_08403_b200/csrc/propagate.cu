@@ -488,9 +488,46 @@ cudaError_t launch_tma(const PropArgs& a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+#include "propagate_async.cuh"
+
+// cp.async ring path for wide single-operand rows: opt-in (SG_PROP_ASYNC=1).  Measured
+// slower than the register path on the Reddit-shaped pass (20.1 vs 17.1 ms): that pass
+// is bound by L2 throughput (~72% of peak), not by per-warp loads in flight.
+bool async_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("SG_PROP_ASYNC");
+    on = (e && e[0] == '1') ? 1 : 0;
+  }
+  return on == 1;
+}
+
+template <int MODE, int DT, int VPL>
+cudaError_t launch_async(const PropArgs& a, cudaStream_t st) {
+  // ring depth S: as many rows in flight as ~100 KB of shared memory per 8-warp block
+  // allows while keeping two blocks (16 warps) per SM
+  constexpr int S = VPL <= 3 ? 8 : (VPL == 4 ? 6 : 4);
+  const size_t smem = (size_t)kAsyncWarps * S * VPL * 512;
+  auto kern = prop_async_kernel<MODE, DT, VPL, S>;
+  static int blocks_per_sm = 0;
+  if (!blocks_per_sm) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, kAsyncWarps * 32, smem);
+    if (blocks_per_sm <= 0) blocks_per_sm = 1;
+  }
+  int64_t want = ((int64_t)a.n_items + kAsyncWarps - 1) / kAsyncWarps;
+  int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)blocks_per_sm * sm_count()));
+  kern<<<grid, kAsyncWarps * 32, smem, st>>>(a);
+  sg::count_launch();
+  return cudaGetLastError();
+}
+
 template <int MODE, int DT, int W, int VPL, int LPR>
 cudaError_t launch_one(const PropArgs& a, cudaStream_t st) {
   constexpr int NG = ModeT<MODE>::NG;
+  if constexpr (LPR == 32 && VPL >= 2 && NG == 1 && W > 1) {
+    if (async_enabled() && !tma_enabled()) return launch_async<MODE, DT, VPL>(a, st);
+  }
   // rows in flight per warp: ~8 vectors per lane (DEPTH 3 at VPL 5 spills and runs 50% slower)
   constexpr int DEPTH = (VPL * NG) <= 4 ? 8 / (VPL * NG) : (NG > 1 ? 1 : 2);
   if constexpr (LPR == 32 && VPL >= 2 && NG == 1 && W > 1) {
