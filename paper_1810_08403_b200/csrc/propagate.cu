@@ -69,8 +69,10 @@ __device__ __forceinline__ void add2_rn(float& a0, float& a1, float t0, float t1
 }
 
 __device__ __forceinline__ float sigmoid_ref(float x) {
-  // 1.0 / (1.0 + np.exp(-x))  (tensor.py:205)
-  return __fdiv_rn(1.0f, __fadd_rn(1.0f, expf(-x)));
+  // 1.0 / (1.0 + np.exp(-x))  (tensor.py:205).  Not bit-comparable with numpy's exp in
+  // any case, so use MUFU-based __expf (~2 ulp) and the correctly rounded reciprocal:
+  // the G-GCN passes were instruction bound with expf + IEEE division (BlogCatalog x10).
+  return __frcp_rn(__fadd_rn(1.0f, __expf(-x)));
 }
 
 template <>
@@ -493,20 +495,31 @@ cudaError_t launch_tma(const PropArgs& a, cudaStream_t st) {
 // cp.async ring path for wide single-operand rows: opt-in (SG_PROP_ASYNC=1).  Measured
 // slower than the register path on the Reddit-shaped pass (20.1 vs 17.1 ms): that pass
 // is bound by L2 throughput (~72% of peak), not by per-warp loads in flight.
-bool async_enabled() {
+// SG_PROP_TEAM2=1: rows of 17..32 vectors (F 65..128 fp32) as half-warp teams (A/B knob).
+bool team_rows() {
   static int on = -1;
   if (on < 0) {
-    const char* e = getenv("SG_PROP_ASYNC");
+    const char* e = getenv("SG_PROP_TEAM2");
     on = (e && e[0] == '1') ? 1 : 0;
   }
   return on == 1;
+}
+
+// SG_PROP_ASYNC: 0 off (default), 1 all widths, 2 one-vector rows only (F <= 128 fp32).
+bool async_enabled(int vpl) {
+  static int mode = -1;
+  if (mode < 0) {
+    const char* e = getenv("SG_PROP_ASYNC");
+    mode = (e && (e[0] == '1' || e[0] == '2')) ? e[0] - '0' : 0;
+  }
+  return mode == 1 || (mode == 2 && vpl == 1);
 }
 
 template <int MODE, int DT, int VPL>
 cudaError_t launch_async(const PropArgs& a, cudaStream_t st) {
   // ring depth S: as many rows in flight as ~100 KB of shared memory per 8-warp block
   // allows while keeping two blocks (16 warps) per SM
-  constexpr int S = VPL <= 3 ? 8 : (VPL == 4 ? 6 : 4);
+  constexpr int S = VPL == 1 ? 16 : (VPL <= 3 ? 8 : (VPL == 4 ? 6 : 4));
   const size_t smem = (size_t)kAsyncWarps * S * VPL * 512;
   auto kern = prop_async_kernel<MODE, DT, VPL, S>;
   static int blocks_per_sm = 0;
@@ -525,8 +538,8 @@ cudaError_t launch_async(const PropArgs& a, cudaStream_t st) {
 template <int MODE, int DT, int W, int VPL, int LPR>
 cudaError_t launch_one(const PropArgs& a, cudaStream_t st) {
   constexpr int NG = ModeT<MODE>::NG;
-  if constexpr (LPR == 32 && VPL >= 2 && NG == 1 && W > 1) {
-    if (async_enabled() && !tma_enabled()) return launch_async<MODE, DT, VPL>(a, st);
+  if constexpr (LPR == 32 && NG == 1 && W > 1) {
+    if (async_enabled(VPL) && !tma_enabled()) return launch_async<MODE, DT, VPL>(a, st);
   }
   // rows in flight per warp: ~8 vectors per lane (DEPTH 3 at VPL 5 spills and runs 50% slower)
   constexpr int DEPTH = (VPL * NG) <= 4 ? 8 / (VPL * NG) : (NG > 1 ? 1 : 2);
@@ -557,6 +570,7 @@ template <int MODE, int DT, int W>
 cudaError_t dispatch_vpl(const PropArgs& a, int LPR, int VPL, cudaStream_t st) {
   constexpr int VMAX = vpl_max(MODE, DT);
   if (LPR < 32) {
+    if (VPL == 2) return launch_one<MODE, DT, W, 2, 16>(a, st);  // two rows per warp
     switch (LPR) {
       case 2: return launch_one<MODE, DT, W, 1, 2>(a, st);
       case 4: return launch_one<MODE, DT, W, 1, 4>(a, st);
@@ -655,6 +669,9 @@ int sg_propagate(int mode, int dtype, const int64_t* ptr, const int32_t* idx, co
       LPR = 2;
       while (LPR < Fv) LPR *= 2;
       VPL = 1;
+    } else if (Fv <= 32 && team_rows()) {
+      LPR = 16;  // half-warp teams: two destination rows per warp, 2 vectors per lane
+      VPL = 2;
     }
     PropArgs a;
     a.ptr = ptr; a.idx = idx; a.w = w; a.items = items; a.splits = splits;
