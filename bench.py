@@ -38,7 +38,9 @@ CONFIGS = {
     "blogcatalog10": dict(workload="2-layer G-GCN epoch, BlogCatalog-shaped graph x10 edges",
                           model="ggcn", graph="uniform", V=10312, E=6680000, F=128, H=128, C=39),
 }
-CPU_SAMPLE_EDGES = {"reddit": 300_000, "pubmed": 88_648, "blogcatalog10": 100_000}
+# bounded CPU samples: ~3-6 s per oracle epoch on one host core (propagation is
+# single-threaded numpy), so --impl reference with the default K/W ends in ~1-2 minutes
+CPU_SAMPLE_EDGES = {"reddit": 150_000, "pubmed": 88_648, "blogcatalog10": 50_000}
 METRIC = "GCN epoch throughput (whole-graph edges per second of 2-layer fwd+bwd epoch)"
 
 
