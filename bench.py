@@ -286,18 +286,23 @@ def run_ours(a, cfg):
     # ---- e2e through the public API with host buffers (H2D features+labels, D2H loss)
     e2e = None
     if not a.no_e2e:
-        times = []
-        for k in range(max(3, a.steps // 2)):
-            torch.cuda.synchronize()
-            t1 = time.perf_counter()
-            m.load_features(X_host)
-            m.load_labels(lab_host)
-            m.train_step(a.lr)
+        # every step: H2D of that step's features + labels from pinned host memory (staged
+        # on a copy stream while the previous step computes) and D2H of its loss
+        n_e2e = max(3, a.steps // 2)
+        m.capture(a.lr)  # one CUDA-graph launch per epoch (forward, backward, SGD)
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        m.prefetch_inputs(X_host, lab_host)
+        for k in range(n_e2e):
+            m.replay()
+            if k + 1 < n_e2e:
+                m.prefetch_inputs(X_host, lab_host)
             float(m.loss.item())
-            times.append(time.perf_counter() - t1)
-        e2e = {"value": E / float(np.mean(times)), "unit": "edges/s",
+        t_e2e = (time.perf_counter() - t1) / n_e2e
+        e2e = {"value": E / t_e2e, "unit": "edges/s",
                "h2d_bytes_per_step": int(X_host.numel() * 4 + lab_host.numel() * 8),
-               "d2h_bytes_per_step": 4, "ms_per_step": float(np.mean(times)) * 1e3}
+               "d2h_bytes_per_step": 4, "ms_per_step": t_e2e * 1e3,
+               "note": "wall clock incl. per-step H2D (pipelined on a copy stream) and loss D2H"}
 
     # ---- CPU baseline (oracle port) on a bounded sample, rank 0 only
     cpu = None

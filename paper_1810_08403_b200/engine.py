@@ -173,6 +173,41 @@ class SAGAModel:
     def load_labels(self, labels):
         self.labels.copy_(torch.as_tensor(np.asarray(labels, np.int64)), non_blocking=True)
 
+    def prefetch_inputs(self, X_host, labels_host):
+        """Stage the NEXT step's features and labels (pinned host tensors) on a copy stream.
+
+        The H2D copy overlaps the current step's kernels; the next ``train_step`` makes
+        the compute stream wait for it and moves the staged inputs into place (a D2D
+        copy), so input transfer is pipelined with compute (double buffering)."""
+        if getattr(self, "_copy_stream", None) is None:
+            self._copy_stream = torch.cuda.Stream(device=self.device)
+            self._stage_X = torch.empty((self.V, self.layers[0].F), dtype=torch.float32,
+                                        device=self.device)
+            self._stage_y = torch.empty_like(self.labels)
+            self._staged = None
+            self._consumed = None
+        cs = self._copy_stream
+        if self._consumed is not None:
+            cs.wait_event(self._consumed)  # previous staging buffer already moved into place
+        with torch.cuda.stream(cs):
+            self._stage_X.copy_(X_host[:, : self.layers[0].F], non_blocking=True)
+            self._stage_y.copy_(labels_host, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(cs)
+        self._staged = ev
+
+    def _take_staged(self):
+        if getattr(self, "_staged", None) is None:
+            return
+        cur = torch.cuda.current_stream(self.device)
+        cur.wait_event(self._staged)
+        self.X.copy_(self._stage_X)
+        self.labels.copy_(self._stage_y)
+        ev = torch.cuda.Event()
+        ev.record(cur)
+        self._consumed = ev
+        self._staged = None
+
     # ------------------------------------------------------------------ passes
     def _rows(self, t, k):
         b = self.grid.begin(k)
@@ -317,6 +352,7 @@ class SAGAModel:
         return out
 
     def train_step(self, lr=0.01):
+        self._take_staged()
         self.forward()
         self.backward()
         self.sgd(lr)
@@ -343,6 +379,7 @@ class SAGAModel:
         return self.graph
 
     def replay(self):
+        self._take_staged()
         self.graph.replay()
         return self.loss
 
