@@ -275,6 +275,12 @@ def run_ours(a, cfg):
     algo = gcn_pass_bytes(V, E, F) if cfg["model"] == "gcn" else \
         E * (4 + 2 * F * 4) + V * (4 + 2 * F * 4)
     achieved = algo / (k_ms / 1e3) / 1e9 if k_ms else None
+    l2_ceiling = None  # measured L2->SM gather ceiling for 2.4-KB rows (tools/l2bw.cu)
+    probe = os.path.join(ROOT, "profiles", "r01_l2_probe.txt")
+    if os.path.exists(probe):
+        vals = [json.loads(x)["GBps"] for x in open(probe) if x.startswith("{") and
+                '"buffer_MB": 48,' in x and '"row_bytes": 2432' in x]
+        l2_ceiling = max(vals) if vals else None
     traffic = None
     prof_json = os.path.join(ROOT, "profiles", "ncu_dram_bytes.json")
     if os.path.exists(prof_json):
@@ -323,7 +329,11 @@ def run_ours(a, cfg):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                      "kernel": "L0.fwd.propagate (sg_propagate GCN, F=%d)" % F,
-                     "algorithmic_bytes_per_launch": algo, "launch_ms": k_ms, "peak_source": peak_src},
+                     "algorithmic_bytes_per_launch": algo, "launch_ms": k_ms, "peak_source": peak_src,
+                     "note": "frac > 1: hot source rows are L2-resident (R-MAT); the pass is "
+                             "bound by L2->SM bandwidth, see l2_ceiling_gbs (tools/l2bw.cu)",
+                     "l2_ceiling_gbs": l2_ceiling,
+                     "frac_of_l2_ceiling": (achieved / l2_ceiling) if (achieved and l2_ceiling) else None},
         "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": int(launches),
         "clocks": clk,
         "stages_ms": {k: round(v, 4) for k, v in stages.items()},
