@@ -1,0 +1,71 @@
+"""SAGA-NN front end and optimizer passes, CPU only."""
+
+import pytest
+
+import paper_1810_08403_b200 as sg
+from paper_1810_08403_b200 import program as P
+
+
+def test_gcn_program_fuses_to_gcn_kernel():
+    q, reps = sg.optimize(sg.build_gcn(8, 4))
+    assert q.fused.kind == "gcn"
+    assert sg.validate_program(q) == []
+    assert P.vertex_kind(q) == "W"
+
+
+def test_ggcn_hoist_and_fuse():
+    p = sg.build_ggcn(6, 3)
+    assert P.matmul_rows(p.apply_edge, 30, 10) == 2 * 30          # 2|E| before
+    q, rep = sg.hoist_vertex_computation(p)
+    assert len(q.precompute) == 2 and sorted(s for s, _ in q.precompute.values()) == ["dest", "src"]
+    assert P.matmul_rows(q.apply_edge, 30, 10, q.precompute) == 2 * 10   # 2|V| after
+    assert not any(n.op == "matmul" for n in P.nodes(q.apply_edge))
+    q2, rep2 = sg.fuse_sag(q)
+    assert q2.fused.kind == "ggcn" and q2.fused.params == ("W_H", "W_C")
+
+
+def test_hoist_idempotent():
+    q, _ = sg.hoist_vertex_computation(sg.build_ggcn(5, 5))
+    q2, rep = sg.hoist_vertex_computation(q)
+    assert q2.apply_edge.key() == q.apply_edge.key() and rep.moved == []
+
+
+def test_commnet_passthrough_unchanged_and_fused():
+    p = sg.build_commnet(4, 4)
+    q, rep = sg.hoist_vertex_computation(p)
+    assert rep.moved == [] and q.apply_edge.key() == p.apply_edge.key()
+    assert sg.fuse_sag(q)[0].fused.kind == "pass"
+
+
+def test_mpgcn_matmul_blocks_fusion():
+    p = sg.make_program(lambda e, p: P.sigmoid(e.src @ p.W_pool),
+                        lambda v, acc, p: P.relu(acc @ p.W), "max",
+                        {"W_pool": (4, 6), "W": (6, 3)}, 4, 3)
+    q, rep = sg.fuse_sag(p)
+    assert q.fused is None and rep.blocker == "matmul"
+
+
+def test_scope_rules():  # accum is out of scope inside ApplyEdge
+    with pytest.raises(sg.ProgramError):
+        P.trace_udf(lambda e, p: P.Expr("input", name="accum", width=3), "edge", {}, 3)
+    with pytest.raises(sg.ProgramError):
+        P.trace_udf(lambda v, acc, p: P.Expr("input", name="edge.src", width=3), "vertex", {}, 3)
+
+
+def test_validate_reports_width_mismatch():
+    p = sg.make_program(lambda e, p: e.src, lambda v, acc, p: P.relu(acc @ p.W), "sum",
+                        {"W": (16, 4)}, 8, 4, acc_width=16)
+    diags = sg.validate_program(p)
+    assert any("gather width 8" in d for d in diags)
+
+
+def test_invalid_accumulator_and_dims():
+    with pytest.raises(sg.ProgramError):
+        sg.make_program(lambda e, p: e.src, lambda v, acc, p: acc, "mean", {}, 2, 2)
+    with pytest.raises(sg.ProgramError):
+        sg.build_gcn(0, 3)
+
+
+def test_matmul_shape_error():
+    with pytest.raises(sg.ProgramError):
+        sg.make_program(lambda e, p: e.src @ p.W, lambda v, acc, p: acc, "sum", {"W": (5, 2)}, 3, 2)
