@@ -47,9 +47,12 @@ class SAGAModel:
     gather (gcn / pass / ggcn) followed by ApplyVertex = ReLU(W accum)."""
 
     def __init__(self, programs, grid, weights=None, *, seed=2, gemm_prec=_lib.GEMM_TF32X3,
-                 device="cuda", strict=True):
+                 device="cuda", strict=True, schedule="locality"):
         if not torch.cuda.is_available():
             raise RuntimeError("SAGAModel needs a CUDA device (no CPU fallback)")
+        if schedule not in ("locality", "dest_order"):
+            raise ConfigError(f"unknown schedule '{schedule}'; valid: locality, dest_order")
+        self.schedule = schedule
         self.grid, self.device, self.strict = grid, torch.device(device), strict
         self.V = grid.V
         self.gemm_prec = gemm_prec
@@ -216,34 +219,47 @@ class SAGAModel:
     def _fwd_propagate(self, L, stream=None):
         g, P = self.grid, self.grid.P
         for j in range(P):
-            chain = [i for i in range(P) if (i, j) in g.csc]
-            if not chain:
+            if not any((i, j) in g.csc for i in range(P)):
                 self._rows(L.a, j).zero_()
-                continue
-            for k, i in enumerate(chain):
-                pi = g.csc[(i, j)]
-                if L.kind == "ggcn":
-                    K.propagate(pi, _lib.PROP_GGCN_FWD, self._rows(L.HP, i), self._rows(L.a, j), L.F,
-                                g_off=L.goff, R=self._rows(L.Qv, j), accumulate=k > 0, ws=self.ws,
-                                stream=stream)
-                else:
-                    mode = _lib.PROP_GCN if L.kind == "gcn" else _lib.PROP_PASS
-                    K.propagate(pi, mode, self._rows(L.hin, i), self._rows(L.a, j), L.F,
-                                accumulate=k > 0, ws=self.ws, stream=stream)
+        for (i, j), first, _ in self._chunk_order(list(g.csc), 1):
+            pi = g.csc[(i, j)]
+            if L.kind == "ggcn":
+                K.propagate(pi, _lib.PROP_GGCN_FWD, self._rows(L.HP, i), self._rows(L.a, j), L.F,
+                            g_off=L.goff, R=self._rows(L.Qv, j), accumulate=not first, ws=self.ws,
+                            stream=stream)
+            else:
+                mode = _lib.PROP_GCN if L.kind == "gcn" else _lib.PROP_PASS
+                K.propagate(pi, mode, self._rows(L.hin, i), self._rows(L.a, j), L.F,
+                            accumulate=not first, ws=self.ws, stream=stream)
+
+    def _chunk_order(self, keys, out_axis):
+        """Chunk visit order of the scheduler for a pass whose output
+        interval is key[out_axis].  'locality': output-interval outer, so the accumulator
+        A_j stays hot across its chunks; 'dest_order': input-interval outer.  Both visit the
+        chunks of one output interval in ascending input interval, so results are bitwise
+        identical.  Yields (key, first_for_output, last_for_output)."""
+        P = self.grid.P
+        inner = 1 - out_axis
+        per_out = {o: sorted(k for k in keys if k[out_axis] == o) for o in range(P)}
+        if self.schedule == "locality":
+            order = [k for o in range(P) for k in per_out[o]]
+        else:
+            order = sorted(keys, key=lambda k: (k[inner], k[out_axis]))
+        for k in order:
+            chain = per_out[k[out_axis]]
+            yield k, k == chain[0], k == chain[-1]
 
     def _bwd_propagate_gcn(self, L, out, mask, stream=None):
         """dH[v] = sum_{out(v)} w_e dA[u] over CSR chunks, j ascending; ReLU mask on the last."""
         g, P = self.grid, self.grid.P
         mode = _lib.PROP_GCN if L.kind == "gcn" else _lib.PROP_PASS
         for i in range(P):
-            chain = [j for j in range(P) if (i, j) in g.csr]
-            if not chain:
+            if not any((i, j) in g.csr for j in range(P)):
                 self._rows(out, i).zero_()
-                continue
-            for k, j in enumerate(chain):
-                K.propagate(g.csr[(i, j)], mode, self._rows(L.da, j), self._rows(out, i), L.F,
-                            mask=self._rows(mask, i) if k == len(chain) - 1 else None,
-                            accumulate=k > 0, ws=self.ws, stream=stream)
+        for (i, j), first, last in self._chunk_order(list(g.csr), 0):
+            K.propagate(g.csr[(i, j)], mode, self._rows(L.da, j), self._rows(out, i), L.F,
+                        mask=self._rows(mask, i) if last else None, accumulate=not first,
+                        ws=self.ws, stream=stream)
 
     def _bwd_propagate_ggcn(self, L, stream=None):
         g, P = self.grid, self.grid.P
