@@ -1,4 +1,4 @@
-"""Multi-GPU engine: destination-interval sharding with source-block all-gather.
+"""Multi-GPU engine: destination-interval sharding with streamed source blocks.
 
 SURVEY.md §8(e), replacing the reference's ring-streaming simulator
  with real collectives over NVLink/NVSwitch:
@@ -6,16 +6,18 @@ SURVEY.md §8(e), replacing the reference's ring-streaming simulator
 * the 2D grid uses P = world intervals; rank r owns destination interval D_r (and,
   since layer outputs are indexed like inputs, source interval S_r = D_r of the next
   layer), the CSC chunks C_{i,r} of its column and the CSR chunks C_{r,j} of its row;
-* forward, per layer: all-gather the source-feature blocks h_i (NCCL), then run the
-  fused gather over C_{i,r} in ascending i into the resident A_r -- the chunked
-  engine's Locality order, so the result equals the 1-GPU chunked run with P = world
-  bit for bit -- and ApplyVertex on the local rows;
+* forward, per layer: every source-feature block h_i is broadcast by its owner (NCCL,
+  posted asynchronously in ascending i); the fused gather over C_{i,r} waits only for
+  block i, so it overlaps the transfer of the later blocks, and accumulates into the
+  resident A_r in ascending i -- the chunked engine's Locality order, so the result
+  equals the 1-GPU chunked run with P = world bit for bit -- then ApplyVertex on the
+  local rows;
 * loss: softmax-CE over local rows normalised by the global |V|, loss all-reduced;
-* backward: dW_r = a_r^T dz_r all-reduced; dA_r = dz_r W^T all-gathered; the CSR duals
-  over C_{r,j} (ascending j) produce dz for the local sources with the ReLU mask of the
-  layer below fused.
+* backward: dW_r = a_r^T dz_r all-reduced; dA blocks streamed the same way; the CSR
+  duals over C_{r,j} (ascending j) produce dz for the local sources with the ReLU mask
+  of the layer below fused.
 NVSwitch gives every GPU full bandwidth to every peer, so the reference's fat-tree /
-ring ordering (built to avoid shared PCIe links) collapses to one all-gather.
+ring ordering (built to avoid shared PCIe links) reduces to per-block broadcasts.
 
 Compute is behind a small backend interface so the host-side logic (sharding,
 ordering, collectives) runs in CPU tests with the gloo backend; the product backend
@@ -114,8 +116,7 @@ class DistGCN:
         self.z = [compute.zeros(n, dims[k + 1]) for k in range(L)]
         self.dz = [compute.zeros(n, dims[k + 1]) for k in range(L)]
         self.da = [compute.zeros(n, dims[k]) for k in range(L)]
-        # all-gather landing buffer: world blocks of `size` rows (last block padded)
-        self.gbuf = torch.zeros((self.world * shard.size, _ld(max(dims))), dtype=dtype, device=dev)
+        self._blocks = {}  # (F, dtype) -> per-source-interval landing buffers
         self.labels = torch.zeros(n, dtype=torch.int64, device=dev)
         self.loss = torch.zeros(1, dtype=dtype, device=dev)
         self.err = torch.zeros(1, dtype=torch.int32, device=dev)
@@ -129,19 +130,22 @@ class DistGCN:
         self.labels.copy_(torch.as_tensor(np.asarray(y_local, np.int64)))
 
     # ---------------------------------------------------------------- collectives
-    def _all_gather(self, X, F):
-        """Every rank's [rows, F] block -> self.gbuf blocks (padded to `size` rows)."""
-        size = self.s.size
-        send = torch.zeros((size, F), dtype=X.dtype, device=X.device)
-        send[: X.shape[0]] = X
-        outs = [torch.empty((size, F), dtype=X.dtype, device=X.device) for _ in range(self.world)]
-        dist.all_gather(outs, send, group=self.group)
-        blocks = []
-        for i, o in enumerate(outs):
-            v = self.gbuf[i * size: i * size + self.s.sizes[i], :F]
-            v.copy_(o[: self.s.sizes[i]])
-            blocks.append(v)
-        return blocks
+    def _stream_blocks(self, X, F):
+        """Post one broadcast per source block (root = its owner), asynchronously and in
+        ascending block order, and return [(block view, work)].  The consumer waits for
+        block i only right before the gather over C_{i,r}, so the gather of block i
+        overlaps the NVLink transfer of blocks i+1.. (the paper's ring streaming,
+        PAPER.md:495-505, on NVSwitch).  Blocks are padded to 16-byte rows."""
+        ldF = _ld(F)
+        key = (F, X.dtype)
+        if key not in self._blocks:
+            self._blocks[key] = [torch.zeros((n, ldF), dtype=X.dtype, device=X.device)
+                                 for n in self.s.sizes]
+        blocks = self._blocks[key]
+        blocks[self.s.rank][:, :F].copy_(X)
+        works = [dist.broadcast(blocks[i], src=i, group=self.group, async_op=True)
+                 for i in range(self.world)]
+        return [(b[:, :F], w) for b, w in zip(blocks, works)]
 
     # ---------------------------------------------------------------- step
     def forward(self):
@@ -149,12 +153,15 @@ class DistGCN:
         L = len(self.dims) - 1
         for l in range(L):
             F = self.dims[l]
-            blocks = self._all_gather(self.h[l], F)
+            blocks = self._stream_blocks(self.h[l], F)
             chain = [i for i in range(self.world) if i in s.csc]
             if not chain:
                 self.a[l].zero_()
             for k, i in enumerate(chain):   # source intervals ascending (Locality order)
-                c.gather(s.csc[i], blocks[i], self.a[l], F, accumulate=k > 0)
+                blocks[i][1].wait()
+                c.gather(s.csc[i], blocks[i][0], self.a[l], F, accumulate=k > 0)
+            for _, w in blocks:
+                w.wait()
             c.gemm(self.a[l], self.W[l], self.z[l], relu_out=self.h[l + 1] if l + 1 < L else None)
         return self.z[-1]
 
@@ -169,13 +176,16 @@ class DistGCN:
             if l > 0:
                 F = self.dims[l]
                 c.gemm(self.dz[l], self.W[l], self.da[l], trans_b=True)
-                blocks = self._all_gather(self.da[l], F)
+                blocks = self._stream_blocks(self.da[l], F)
                 chain = [j for j in range(self.world) if j in s.csr]
                 if not chain:
                     self.dz[l - 1].zero_()
                 for k, j in enumerate(chain):  # destination intervals ascending
-                    c.gather(s.csr[j], blocks[j], self.dz[l - 1], F, accumulate=k > 0,
+                    blocks[j][1].wait()
+                    c.gather(s.csr[j], blocks[j][0], self.dz[l - 1], F, accumulate=k > 0,
                              mask=self.z[l - 1] if k == len(chain) - 1 else None)
+                for _, w in blocks:
+                    w.wait()
         return self.loss
 
     def train_step(self, lr=0.01):
