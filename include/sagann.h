@@ -133,6 +133,19 @@ int sg_segment_max(int dtype, const int64_t* ptr, const int32_t* idx, int64_t n_
 /* backward of segment_max: gx[argmax[r,f], f] = g[r, f] (gx pre-zeroed by caller). */
 int sg_segment_max_bwd(int dtype, const void* g, int64_t ldg, const int64_t* argmax, int64_t lda,
                        int64_t n_rows, void* gx, int64_t ldx, int64_t F, void* stream);
+/* Fused Gather(max) over a CSC index (MP-GCN ApplyEdge hoisted to Y, PAPER.md:574-586;
+ * segment_max, tensor.py:453-484): out[u] = max over in-edges of Y[idx_e]; argpos[u,f]
+ * = CSC position of the first maximum (int32), -1 and empty_fill for empty rows.
+ * fp32; Y rows with ld % 4 == 0 are read as 16-B vectors. */
+int sg_max_gather(const int64_t* ptr, const int32_t* idx, int64_t n_rows, const float* Y, int64_t ldy,
+                  float* out, int64_t ldo, int32_t* argpos, int64_t lda, int64_t F, float empty_fill,
+                  void* stream);
+/* Its backward over the transposed (CSR) index: out[v] = sum over out-edges k (CSR order)
+ * of G[idx_k] where argpos[idx_k] == pos_k (the edge's CSC position), else +0.0; optional
+ * ReLU mask.  Bitwise equal to segment_max's backward followed by take_rows' backward. */
+int sg_max_gather_bwd(const int64_t* ptr, const int32_t* idx, const int32_t* pos, int64_t n_rows,
+                      const float* G, int64_t ldg, const int32_t* argpos, int64_t lda, float* out,
+                      int64_t ldo, int64_t F, const float* mask, int64_t ldm, void* stream);
 /* Scatter (take_rows, tensor.py:424-436): out[k] = X[idx[k]] (int64 idx, bounds
  * checked on device: *err_flag set to 1 if any index is out of [0, n_src)). */
 int sg_take_rows(int dtype, const void* X, int64_t ldx, int64_t n_src, const int64_t* idx,
@@ -173,7 +186,8 @@ int sg_sgd(float* W, const float* dW, int64_t n, float lr, void* stream);
 int sg_check_finite(int dtype, const void* X, int64_t rows, int64_t cols, int64_t ld,
                     int32_t* flag, void* stream);
 /* Elementwise ops used by unfused ApplyEdge programs (tensor.py:204-303):
- * op 0 add, 1 sub, 2 mul, 3 div, 4 max, 5 sigmoid, 6 tanh, 7 relu, 8 relu-backward
+ * op 0 add, 1 sub, 2 mul, 3 div, 4 max, 5 sigmoid, 6 tanh, 7 relu, 8 relu-backward,
+ * 9 sigmoid-backward (a * b * (1 - b) with b = y, tensor.py:232)
  * (a * (b > 0), tensor.py:236); b is broadcast
  * per row when b_cols == 1 (the "b_row" kind, tensor.py:184-185), along the
  * leading axis when b_rows == 1 ("b_lead"). */

@@ -226,6 +226,52 @@ def ggcn_epoch(part, X, layers, labels, T=None):
     return dict(loss=loss, p=p, out=hs[1:], cache=cache, grads=grads)
 
 
+def mpgcn_epoch(part, X, layers, labels, args=None):
+    """2-layer MP-GCN, hoisted: Y = sigmoid(h W_pool + b) per vertex,
+    Gather(max) over in-edges (segment_max, tensor.py:453-484, argmax = first CSC
+    position), ApplyVertex ReLU(accum W).  ``layers`` = [(W_pool, b, W), ...].  P = 1.
+
+    ``args`` (optional, one [V, pool] CSC-position array per layer) pins the max
+    selection: max is discontinuous at ties, so a checker comparing an fp32 run with
+    this fp64 oracle routes both through the SAME argmax (after verifying separately
+    that every disagreement is a near-tie)."""
+    if part.P != 1:
+        raise ValueError("the MP-GCN oracle runs on a single chunk (P = 1)")
+    ch = part.chunk(0, 0)
+    src = ch["csc_idx"].astype(np.int64)
+    dst = local_rows(ch["csc_ptr"])
+    V = part.V
+    hs, cache = [X], []
+    for (Wp, b, W) in layers:
+        h = hs[-1]
+        Y = prim.sigmoid(prim.add(prim.matmul(h, Wp), b))
+        ys = prim.take_rows(Y, src)
+        a, arg = prim.segment_max(ys, dst, V)
+        if args is not None:
+            arg = np.asarray(args[len(cache)], dtype=np.int64)
+            cols = np.broadcast_to(np.arange(arg.shape[1]), arg.shape)
+            a = np.where(arg >= 0, ys[np.maximum(arg, 0), cols] if len(src) else 0, 0).astype(Y.dtype)
+        z = prim.matmul(a, W)
+        cache.append((h, Y, a, arg, z))
+        hs.append(prim.relu(z))
+    loss, p = prim.softmax_cross_entropy(hs[-1], labels)
+    g = prim.softmax_cross_entropy_bwd(np.asarray(1.0, dtype=X.dtype), p, labels)
+    grads = [None] * len(layers)
+    for l in range(len(layers) - 1, -1, -1):
+        Wp, b, W = layers[l]
+        h, Y, a, arg, z = cache[l]
+        gz = prim.relu_bwd(g, z)
+        ga, gW = prim.matmul_bwd(gz, a, W)
+        gys = prim.segment_max_bwd(ga, arg, len(src))          # tensor.py:473-482
+        gY = prim.take_rows_bwd(gys, src, V)                    # tensor.py:431-434
+        gpre = prim.sigmoid_bwd(gY, Y)
+        gb = gpre.sum(axis=0)                                   # _reduce_to b_lead (tensor.py:199)
+        gh, gWp = prim.matmul_bwd(gpre, h, Wp)
+        grads[l] = (gWp, gb, gW)
+        g = gh
+    return dict(loss=loss, out=hs[1:], cache=cache, grads=grads)
+
+
 def sgd(params, grads, lr):
     """W <- W - lr * dW (SPEC.md:598, :617)."""
     return [W - lr * g for W, g in zip(params, grads)]

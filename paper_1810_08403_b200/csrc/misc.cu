@@ -105,7 +105,7 @@ __global__ void ewise_kernel(int op, int64_t rows, int64_t cols, const float* a,
     const int64_t r = t / cols, c = t % cols;
     const float x = a[r * lda + c];
     float y = 0.f, w = 0.f;
-    if (op <= 4 || op == 8) w = b[(b_rows == 1 ? 0 : r) * ldb + (b_cols == 1 ? 0 : c)];
+    if (op <= 4 || op >= 8) w = b[(b_rows == 1 ? 0 : r) * ldb + (b_cols == 1 ? 0 : c)];
     switch (op) {  // tensor.py:204-303
       case 0: y = __fadd_rn(x, w); break;
       case 1: y = __fsub_rn(x, w); break;
@@ -115,7 +115,8 @@ __global__ void ewise_kernel(int op, int64_t rows, int64_t cols, const float* a,
       case 5: y = __fdiv_rn(1.0f, __fadd_rn(1.0f, expf(-x))); break;
       case 6: y = tanhf(x); break;
       case 7: y = fmaxf(x, 0.f); break;
-      default: y = __fmul_rn(x, w > 0.f ? 1.f : 0.f); break;  // relu bwd: g * (z > 0)
+      case 8: y = __fmul_rn(x, w > 0.f ? 1.f : 0.f); break;  // relu bwd: g * (z > 0)
+      default: y = __fmul_rn(__fmul_rn(x, w), __fsub_rn(1.0f, w)); break;  // sigmoid bwd g*y*(1-y)
     }
     out[r * ldo + c] = y;
   }
@@ -195,8 +196,8 @@ int sg_check_finite(int dtype, const void* X, int64_t rows, int64_t cols, int64_
 
 int sg_ewise(int op, int64_t rows, int64_t cols, const float* a, int64_t lda, const float* b,
              int64_t b_rows, int64_t b_cols, int64_t ldb, float* out, int64_t ldo, void* stream) {
-  SG_REQUIRE(op >= 0 && op <= 8, SG_EINVAL, "ewise: unknown op %d", op);
-  SG_REQUIRE((op > 4 && op != 8) || b, SG_EINVAL, "ewise: binary op needs b");
+  SG_REQUIRE(op >= 0 && op <= 9, SG_EINVAL, "ewise: unknown op %d", op);
+  SG_REQUIRE((op > 4 && op < 8) || b, SG_EINVAL, "ewise: binary op needs b");
   if (rows == 0 || cols == 0) return SG_OK;
   ewise_kernel<<<grid_for(rows * cols, 256), 256, 0, (cudaStream_t)stream>>>(
       op, rows, cols, a, lda, b, b_rows, b_cols, ldb, out, ldo);

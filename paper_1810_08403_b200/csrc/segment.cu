@@ -146,9 +146,105 @@ int grid_for(int64_t work, int per_block) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(g, 148 * 32));
 }
 
+// Fused Gather(max) over a CSC index (MP-GCN): out[u] = max over the
+// in-edges of Y[src] with the CSC position of the first maximum recorded as the argmax
+// ("ties broken by lowest CSC edge index"); empty rows -> fill, argmax -1.
+__global__ void maxgather_kernel(const int64_t* ptr, const int32_t* idx, int64_t n_rows,
+                                 const float* Y, int64_t ldy, float* out, int64_t ldo, int32_t* arg,
+                                 int64_t lda, int F, float fill, int vec) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int W = vec ? 4 : 1;
+  const int Fv = (F + W - 1) / W;
+  for (int64_t r = warp; r < n_rows; r += nwarps) {
+    const int64_t e0 = ptr[r], e1 = ptr[r + 1];
+    for (int cv = lane; cv < Fv; cv += 32) {
+      float best[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+      int32_t barg[4] = {-1, -1, -1, -1};
+      for (int64_t e = e0; e < e1; ++e) {
+        const float* row = Y + (int64_t)__ldg(idx + e) * ldy + (int64_t)cv * W;
+        float v[4];
+        if (vec) {
+          float4 q = __ldg(reinterpret_cast<const float4*>(row));
+          v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+        } else {
+          v[0] = __ldg(row);
+        }
+        for (int k = 0; k < W; ++k)
+          if (v[k] > best[k]) {  // strict '>' : the lowest position wins ties (tensor.py:467)
+            best[k] = v[k];
+            barg[k] = (int32_t)e;
+          }
+      }
+      for (int k = 0; k < W; ++k) {
+        const int c = cv * W + k;
+        if (c < F) {
+          out[r * ldo + c] = barg[k] < 0 ? fill : best[k];
+          arg[r * lda + c] = barg[k];
+        }
+      }
+    }
+  }
+}
+
+// Backward of the fused max gather over the transposed (CSR) index: dY[v] = sum over
+// out-edges k of v, in CSR order (= the forward edge-list order, tensor.py:431-434), of
+// dA[dst_k] where the destination's argmax is this edge (pos_k = its CSC position), else
+// +0.0 -- exactly tensor.py:473-482 followed by take_rows' backward.  No atomics.
+__global__ void maxgather_bwd_kernel(const int64_t* ptr, const int32_t* idx, const int32_t* pos,
+                                     int64_t n_rows, const float* G, int64_t ldg, const int32_t* arg,
+                                     int64_t lda, float* out, int64_t ldo, int F, const float* mask,
+                                     int64_t ldm) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = warp; r < n_rows; r += nwarps) {
+    const int64_t e0 = ptr[r], e1 = ptr[r + 1];
+    for (int c = lane; c < F; c += 32) {
+      float acc = 0.f;
+      for (int64_t k = e0; k < e1; ++k) {
+        const int64_t u = __ldg(idx + k);
+        const float g = __ldg(G + u * ldg + c);
+        const int32_t a = __ldg(arg + u * lda + c);
+        acc = __fadd_rn(acc, a == __ldg(pos + k) ? g : 0.f);
+      }
+      if (mask) acc = __fmul_rn(acc, __ldg(mask + r * ldm + c) > 0.f ? 1.f : 0.f);
+      out[r * ldo + c] = acc;
+    }
+  }
+}
+
 }  // namespace
 
 extern "C" {
+
+int sg_max_gather(const int64_t* ptr, const int32_t* idx, int64_t n_rows, const float* Y, int64_t ldy,
+                  float* out, int64_t ldo, int32_t* argpos, int64_t lda, int64_t F, float empty_fill,
+                  void* stream) {
+  if (n_rows == 0 || F == 0) return SG_OK;
+  SG_REQUIRE(ptr && idx && Y && out && argpos, SG_EINVAL, "max_gather: null pointer");
+  const int vec = (F % 4 == 0) && (ldy % 4 == 0) && aligned(Y, 16);
+  maxgather_kernel<<<grid_for(n_rows * 32, 256), 256, 0, (cudaStream_t)stream>>>(
+      ptr, idx, n_rows, Y, ldy, out, ldo, argpos, lda, (int)F, empty_fill, vec);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) SG_FAIL(SG_ECUDA, "max_gather launch: %s", cudaGetErrorString(e));
+  sg::count_launch(1);
+  return SG_OK;
+}
+
+int sg_max_gather_bwd(const int64_t* ptr, const int32_t* idx, const int32_t* pos, int64_t n_rows,
+                      const float* G, int64_t ldg, const int32_t* argpos, int64_t lda, float* out,
+                      int64_t ldo, int64_t F, const float* mask, int64_t ldm, void* stream) {
+  if (n_rows == 0 || F == 0) return SG_OK;
+  SG_REQUIRE(ptr && idx && pos && G && argpos && out, SG_EINVAL, "max_gather_bwd: null pointer");
+  maxgather_bwd_kernel<<<grid_for(n_rows * 32, 256), 256, 0, (cudaStream_t)stream>>>(
+      ptr, idx, pos, n_rows, G, ldg, argpos, lda, out, ldo, (int)F, mask, ldm);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) SG_FAIL(SG_ECUDA, "max_gather_bwd launch: %s", cudaGetErrorString(e));
+  sg::count_launch(1);
+  return SG_OK;
+}
 
 int sg_take_rows(int dtype, const void* X, int64_t ldx, int64_t n_src, const int64_t* idx,
                  int64_t n, void* out, int64_t ldo, int64_t F, int32_t* err_flag, void* stream) {

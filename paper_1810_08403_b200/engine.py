@@ -64,7 +64,7 @@ class SAGAModel:
             diags = prog.validate_program(q)
             if diags:
                 raise ProgramError("; ".join(diags))
-            if q.fused is None or q.fused.kind not in ("gcn", "pass", "ggcn"):
+            if q.fused is None or q.fused.kind not in ("gcn", "pass", "ggcn", "max", "max_pool"):
                 raise ProgramError(f"layer ApplyEdge {p.apply_edge!r} has no fused kernel "
                                    f"({reports[-1].blocker or (q.fused and q.fused.kind)})")
             wname = prog.vertex_kind(q)
@@ -73,6 +73,10 @@ class SAGAModel:
             L = _Layer()
             L.prog, L.kind, L.wname, L.F, L.O = q, q.fused.kind, wname, q.f_in, q.f_out
             L.gate = q.fused.params
+            # accumulator width: the pooled width for MP-GCN, else the input width
+            L.Aw = q.params[L.gate[0]][1] if L.kind == "max_pool" else q.f_in
+            if L.kind in ("max", "max_pool") and grid.P != 1:
+                raise ProgramError("the max-accumulator executor runs on a single chunk (P = 1)")
             self.layers.append(L)
             dims.append((q.f_in, q.f_out))
         for a, b in zip(dims, dims[1:]):
@@ -89,15 +93,22 @@ class SAGAModel:
         for L in self.layers:
             if L.kind == "ggcn":
                 out += [(L.F, L.F), (L.F, L.F), (L.F, L.O)]
+            elif L.kind == "max_pool":
+                out += [(L.F, L.Aw), (L.Aw,), (L.Aw, L.O)]
             else:
                 out += [(L.F, L.O)]
         return out
 
     def init_weights(self, seed=2):
-        """Glorot-uniform from default_rng(seed) in parameter order."""
+        """Glorot-uniform matrices (zero biases) from default_rng(seed) in parameter order
+        (SURVEY.md §8(d))."""
         rng = np.random.default_rng(seed)
         out = []
-        for fin, fout in self.param_shapes():
+        for shape in self.param_shapes():
+            if len(shape) == 1:
+                out.append(np.zeros(shape, np.float32))
+                continue
+            fin, fout = shape
             lim = np.sqrt(6.0 / (fin + fout))
             out.append(rng.uniform(-lim, lim, (fin, fout)).astype(np.float32))
         return out
@@ -110,24 +121,49 @@ class SAGAModel:
         for L in self.layers:
             for t in L.params:
                 w = torch.as_tensor(np.asarray(flat[k], np.float32))
+                if w.dim() == 1 and t.dim() == 2 and t.shape[0] == 1:
+                    w = w.reshape(1, -1)  # bias vector
                 if tuple(w.shape) != tuple(t.shape):
                     raise ShapeError(f"weight {k} has shape {tuple(w.shape)}, want {tuple(t.shape)}")
                 t.copy_(w)
                 k += 1
 
+    @staticmethod
+    def _host(t, L):
+        x = t.detach().cpu().numpy().copy()
+        return x.reshape(-1) if t is getattr(L, "bias", None) or t is getattr(L, "dbias", None) else x
+
     def weights(self):
-        return [t.detach().cpu().numpy().copy() for L in self.layers for t in L.params]
+        return [self._host(t, L) for L in self.layers for t in L.params]
 
     def grads(self):
-        return [t.detach().cpu().numpy().copy() for L in self.layers for t in L.dparams]
+        return [self._host(t, L) for L in self.layers for t in L.dparams]
 
     # ------------------------------------------------------------------ buffers
     def _alloc(self):
         V, dev = self.V, self.device
         for n, L in enumerate(self.layers):
             F, O = L.F, L.O
-            L.W = torch.zeros((F, O), dtype=torch.float32, device=dev)
+            L.W = torch.zeros((L.Aw, O), dtype=torch.float32, device=dev)
             L.dW = torch.zeros_like(L.W)
+            if L.kind in ("max", "max_pool"):
+                A = L.Aw
+                L.hin = None
+                L.arg = torch.zeros((V, _ld(A)), dtype=torch.int32, device=dev)[:, :A]
+                L.da = _mat(V, A, dev)
+                L.dY = _mat(V, A, dev)
+                L.params, L.dparams = [L.W], [L.dW]
+                if L.kind == "max_pool":
+                    L.Y = _mat(V, A, dev)
+                    L.Wp = torch.zeros((F, A), dtype=torch.float32, device=dev)
+                    L.bias = torch.zeros((1, A), dtype=torch.float32, device=dev)
+                    L.dWp, L.dbias = torch.zeros_like(L.Wp), torch.zeros_like(L.bias)
+                    L.params, L.dparams = [L.Wp, L.bias, L.W], [L.dWp, L.dbias, L.dW]
+                    self._ones = torch.ones((V, 1), dtype=torch.float32, device=dev)
+                L.a = _mat(V, A, dev)
+                L.z = _mat(V, O, dev)
+                L.dz = _mat(V, O, dev)
+                continue
             if L.kind == "ggcn":
                 L.goff = _ld(F)
                 L.HP = torch.zeros((V, 2 * L.goff), dtype=torch.float32, device=dev)
@@ -306,7 +342,21 @@ class SAGAModel:
                 self._gemm(L.hin, L.WH, L.Pv)   # hoisted P = h W_H
                 self._gemm(L.hin, L.WC, L.Qv)   # hoisted Q = h W_C
                 self._mark(f"L{n}.fwd.hoist_gemm")
-            self._fwd_propagate(L, stream)
+            if L.kind in ("max", "max_pool"):
+                Y = L.hin
+                if L.kind == "max_pool":       # hoisted edge network Y = sigmoid(h W_pool + b)
+                    self._gemm(L.hin, L.Wp, L.Y)
+                    K.ewise(0, L.Y, L.bias, L.Y, stream)
+                    K.ewise(5, L.Y, None, L.Y, stream)
+                    Y = L.Y
+                    self._mark(f"L{n}.fwd.hoist_gemm")
+                if (0, 0) in self.grid.csc:
+                    K.max_gather(self.grid.csc[(0, 0)], Y, L.a, L.arg, L.Aw, stream=stream)
+                else:
+                    L.a.zero_()
+                    L.arg.fill_(-1)
+            else:
+                self._fwd_propagate(L, stream)
             self._mark(f"L{n}.fwd.propagate")
             self._gemm(L.a, L.W, L.z, relu_out=L.hout)  # ApplyVertex: z = a W, h' = relu(z)
             self._mark(f"L{n}.fwd.apply_vertex")
@@ -322,6 +372,34 @@ class SAGAModel:
             L = self.layers[n]
             self._gemm(L.a, L.dz, L.dW, trans_a=True)           # dW = a^T dz
             below = self.layers[n - 1] if n > 0 else None
+            if L.kind in ("max", "max_pool"):
+                self._gemm(L.dz, L.W, L.da, trans_b=True)       # dA = dz W^T
+                self._mark(f"L{n}.bwd.apply_vertex")
+                pi = self.grid.csr.get((0, 0))
+                if L.kind == "max":
+                    if below is not None:
+                        if pi is None:
+                            below.dz.zero_()
+                        else:  # max routing + ReLU mask of the layer below, one pass
+                            K.max_gather_bwd(pi, self.grid.csr_positions(0, 0), L.da, L.arg,
+                                             below.dz, L.Aw, mask=below.z, stream=stream)
+                    self._mark(f"L{n}.bwd.propagate")
+                    continue
+                if pi is None:
+                    L.dY.zero_()
+                else:
+                    K.max_gather_bwd(pi, self.grid.csr_positions(0, 0), L.da, L.arg, L.dY, L.Aw,
+                                     stream=stream)
+                self._mark(f"L{n}.bwd.propagate")
+                K.ewise(9, L.dY, L.Y, L.dY, stream)                  # sigmoid bwd (tensor.py:232)
+                self._gemm(self._ones, L.dY, L.dbias, trans_a=True)  # db = column sums
+                self._gemm(L.hin, L.dY, L.dWp, trans_a=True)         # dW_pool = h^T dpre
+                if below is not None:
+                    t1 = self.tmp1[:, : L.F]
+                    self._gemm(L.dY, L.Wp, t1, trans_b=True)
+                    K.ewise(8, t1, below.z, below.dz, stream)
+                self._mark(f"L{n}.bwd.hoist_gemm")
+                continue
             if L.kind == "ggcn":
                 self._gemm(L.dz, L.W, L.dAv, trans_b=True)      # dA = dz W^T
                 self._mark(f"L{n}.bwd.apply_vertex")
@@ -416,10 +494,19 @@ def ggcn_model(grid, dims, **kw):
     return SAGAModel([prog.build_ggcn(a, b) for a, b in zip(dims, dims[1:])], grid, **kw)
 
 
+def mpgcn_model(grid, dims, pool=None, **kw):
+    """MP-GCN: per layer W_pool [F, pool], b [pool], W [pool, O].
+    ``pool`` defaults to each layer's input width."""
+    pool = list(pool) if pool is not None else list(dims[:-1])
+    if len(pool) != len(dims) - 1:
+        raise ShapeError("need one pool width per layer")
+    return SAGAModel([prog.build_mpgcn(a, p, b) for a, p, b in zip(dims, pool, dims[1:])], grid, **kw)
+
+
 def run_train(config):
     """SPEC.md:595-603 run_train on a synthetic graph; returns a metrics dict.
 
-    config keys (SPEC.md:622 subset + synthetic graph): model ('gcn'|'ggcn'),
+    config keys (SPEC.md:622 subset + synthetic graph): model ('gcn'|'ggcn'|'mpgcn'),
     graph ('rmat'|'uniform'), V, E, features F, hidden, classes, layers, epochs,
     lr, seed, interval_size."""
     from . import graph as G
@@ -430,8 +517,9 @@ def run_train(config):
     if bad:
         raise ConfigError(f"unknown config keys {sorted(bad)}")
     model = config.get("model", "gcn")
-    if model not in ("gcn", "ggcn"):
-        raise ConfigError(f"unknown model '{model}'; valid: gcn, ggcn")
+    builders = {"gcn": gcn_model, "ggcn": ggcn_model, "mpgcn": mpgcn_model}
+    if model not in builders:
+        raise ConfigError(f"unknown model '{model}'; valid: {', '.join(builders)}")
     V, E = int(config["V"]), int(config["E"])
     gen = G.rmat_graph if config.get("graph", "uniform") == "rmat" else G.uniform_graph
     g = gen(V, E, seed=int(config.get("seed", 0)))
@@ -440,7 +528,7 @@ def run_train(config):
     F, H, C = int(config["features"]), int(config.get("hidden", 16)), int(config["classes"])
     nl = int(config.get("layers", 2))
     dims = [F] + [H] * (nl - 1) + [C]
-    m = (gcn_model if model == "gcn" else ggcn_model)(grid, dims)
+    m = builders[model](grid, dims)
     m.load_features(torch.from_numpy(G.synthetic_features(V, F, seed=1)))
     m.load_labels(np.random.default_rng(3).integers(0, C, V))
     losses = []

@@ -229,6 +229,20 @@ class ChunkGrid:
     def size(self, k):
         return int(self.part.sizes[k])
 
+    def csr_positions(self, i, j):
+        """CSC position of every CSR edge of chunk C_ij (int32, device), for routing max
+        gradients to the argmax edge.  The CSR order is a stable sort of the CSC order by
+        local source, so this is argsort(csc_idx, stable)."""
+        if not hasattr(self, "_csr_pos"):
+            self._csr_pos = {}
+        if (i, j) not in self._csr_pos:
+            import torch
+
+            ch = self.part.chunk(i, j)
+            pos = np.argsort(ch["csc_idx"], kind="stable").astype(np.int32)
+            self._csr_pos[(i, j)] = torch.from_numpy(pos).to(self.device)
+        return self._csr_pos[(i, j)]
+
     def workspace_bytes(self, F, mode):
         m = 0
         for d in (self.csc, self.csr):

@@ -89,6 +89,26 @@ def softmax_xent(Z, labels, loss, dZ, err, *, relu_input=True, n_total=0, ws=Non
                               stream_handle(stream)))
 
 
+def max_gather(pi, Y, out, arg, F, empty_fill=0.0, stream=None):
+    """Fused Gather(max) over CSC pass index ``pi`` (argmax = CSC position, int32)."""
+    check(lib.sg_max_gather(tptr(pi.ptr), tptr(pi.idx), pi.n_rows, tptr(Y), ld(Y), tptr(out), ld(out),
+                            tptr(arg), ld(arg), F, float(empty_fill), stream_handle(stream)))
+
+
+def max_gather_bwd(pi, pos, G, arg, out, F, mask=None, stream=None):
+    """Backward of max_gather over CSR pass index ``pi`` (pos = CSC position per CSR edge)."""
+    check(lib.sg_max_gather_bwd(tptr(pi.ptr), tptr(pi.idx), tptr(pos), pi.n_rows, tptr(G), ld(G),
+                                tptr(arg), ld(arg), tptr(out), ld(out), F, tptr(mask),
+                                ld(mask) if mask is not None else 0, stream_handle(stream)))
+
+
+def ewise(op, a, b, out, stream=None):
+    """sg_ewise on 2-D views; b is [rows, cols], [rows, 1] (b_row) or [1, cols] (b_lead)."""
+    check(lib.sg_ewise(op, a.shape[0], a.shape[1], tptr(a), ld(a), tptr(b),
+                       b.shape[0] if b is not None else 0, b.shape[1] if b is not None else 0,
+                       ld(b) if b is not None else 0, tptr(out), ld(out), stream_handle(stream)))
+
+
 def sgd(W, dW, lr, stream=None):
     check(lib.sg_sgd(tptr(W), tptr(dW), W.numel(), float(lr), stream_handle(stream)))
 

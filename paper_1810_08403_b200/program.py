@@ -98,7 +98,7 @@ def matmul(a, b):
     """Row convention x @ W (tensor.py:313).  ``W @ x`` (the paper's W (x) x) means the same."""
     if a.op == "param" and b.op != "param":
         a, b = b, a
-    if b.op != "param" or b.width is None:
+    if b.op != "param" or not isinstance(b.width, tuple):
         raise ProgramError("matmul needs one per-row operand and one parameter matrix")
     rows, cols = b.width
     if a.width is not None and a.width != rows:
@@ -122,7 +122,9 @@ class _Params:
             raise AttributeError(k)
         if k not in self._shapes:
             raise ProgramError(f"unknown parameter '{k}'")
-        return Expr("param", name=k, width=tuple(self._shapes[k]))
+        shape = tuple(self._shapes[k])
+        # matrices keep their (rows, cols); a bias vector (n,) broadcasts like a row (b_lead)
+        return Expr("param", name=k, width=shape if len(shape) == 2 else shape[0])
 
 
 def trace_udf(udf, kind, params, f_in):
@@ -295,6 +297,16 @@ def fuse_sag(p):
         return LayerProgram(e, p.apply_vertex, p.accumulator, p.params, p.f_in, p.f_out,
                             p.precompute, None), rep
     kind, params = "generic", ()
+    if p.accumulator == "max":
+        if _is(e, "input", "edge.src"):
+            kind = "max"
+        elif e.op == "pre" and p.precompute[e.name][0] == "src":
+            x = p.precompute[e.name][1]
+            # sigmoid(vertex @ W_pool + b): MP-GCN's pooling edge network
+            if x.op == "sigmoid" and x.args[0].op == "add":
+                mm, bias = x.args[0].args
+                if mm.op == "matmul" and _is(mm.args[0], "input", "vertex") and bias.op == "param":
+                    kind, params = "max_pool", (mm.args[1].name, bias.name)
     if p.accumulator == "sum":
         if _is(e, "input", "edge.src"):
             kind = "pass"
@@ -392,4 +404,16 @@ def build_commnet(f_in, f_out):
                         {"W": (f_in, f_out)}, f_in, f_out)
 
 
-MODELS = {"gcn": build_gcn, "ggcn": build_ggcn, "commnet": build_commnet}
+def build_mpgcn(f_in, f_pool, f_out):
+    """MP-GCN: ApplyEdge = sigmoid(W_pool src + b), Gather.accumulator =
+    max, ApplyVertex = ReLU(W accum).  The edge network depends on src only, so the hoist
+    pass moves it to one per-vertex GEMM and the SAG phase becomes a fused max gather."""
+    if min(f_in, f_pool, f_out) < 1:
+        raise ProgramError("invalid dimensions")
+    return make_program(lambda e, p: sigmoid(matmul(e.src, p.W_pool) + p.b),
+                        lambda v, acc, p: relu(matmul(acc, p.W)), "max",
+                        {"W_pool": (f_in, f_pool), "b": (f_pool,), "W": (f_pool, f_out)},
+                        f_in, f_out, acc_width=f_pool)
+
+
+MODELS = {"gcn": build_gcn, "ggcn": build_ggcn, "commnet": build_commnet, "mpgcn": build_mpgcn}

@@ -95,6 +95,31 @@ def run_ggcn(X, layers, labels, src, dst, V, dtype, hoisted=True):
     return acts, loss.to_numpy(), [tuple(grads[m.tid] for m in L) for L in lt], counter.counts
 
 
+def run_mpgcn(X, layers, labels, src, dst, V, dtype, hoisted=True):
+    """MP-GCN: acc = sigmoid(W_pool src + b), Gather(max), ReLU(W accum)."""
+    tape = T.Tape()
+    lt = [tuple(tens(m, dtype) for m in L) for L in layers]
+    for L in lt:
+        for m in L:
+            tape.watch(m)
+    h = tens(X, dtype)
+    acts = []
+    for (Wp, b, W) in lt:
+        if hoisted:
+            Y = T.sigmoid(T.add(T.matmul(h, Wp, tape), b, tape), tape)
+            ys = T.take_rows(Y, src, tape)
+        else:
+            hs_ = T.take_rows(h, src, tape)
+            ys = T.sigmoid(T.add(T.matmul(hs_, Wp, tape), b, tape), tape)
+        accum = T.segment_max(ys, dst, V, tape=tape)
+        z = T.matmul(accum, W, tape)
+        h = T.relu(z, tape)
+        acts.append((accum.to_numpy(), z.to_numpy(), h.to_numpy()))
+    loss = T.softmax_cross_entropy(h, labels, tape)
+    grads = T.backward(tape, Seed(dtype))
+    return acts, loss.to_numpy(), [tuple(grads[m.tid] for m in L) for L in lt]
+
+
 CASES = [
     # name, V, E, F, H, C, generator, seed
     ("uniform_v40_e160", 40, 160, 12, 8, 3, "uniform", 11),
@@ -139,6 +164,21 @@ def make_case(name, V, E, F, H, C, gen, seed):
                 out[f"ggcn{hp}_{tag}_a{l}"], out[f"ggcn{hp}_{tag}_z{l}"], out[f"ggcn{hp}_{tag}_h{l}"] = acts[l]
             out[f"ggcn{hp}_{tag}_loss"] = loss
             out[f"ggcn{hp}_{tag}_mm_edge"] = counts.get("apply_edge", 0)
+        # MP-GCN: F -> pool 9 -> H ; H -> pool 7 -> C  (W_pool, b, W per layer)
+        r = np.random.default_rng(2)
+        Lm = []
+        for fi, fp, fo in ((F, 9, H), (H, 7, C)):
+            Lm.append((r.uniform(-0.5, 0.5, (fi, fp)).astype(dt), r.uniform(-0.2, 0.2, (fp,)).astype(dt),
+                       r.uniform(-0.5, 0.5, (fp, fo)).astype(dt)))
+        for hoisted in (True, False):
+            acts, loss, gL = run_mpgcn(X, Lm, lab, s, d, V, dt, hoisted)
+            hp = "h" if hoisted else "u"
+            for l, L in enumerate(Lm):
+                for k, m in enumerate(L):
+                    out[f"mpgcn_{tag}_L{l}_{k}"] = m
+                    out[f"mpgcn{hp}_{tag}_dL{l}_{k}"] = gL[l][k]
+                out[f"mpgcn{hp}_{tag}_a{l}"], out[f"mpgcn{hp}_{tag}_z{l}"], _ = acts[l]
+            out[f"mpgcn{hp}_{tag}_loss"] = loss
     np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
     print("wrote", name)
 

@@ -413,3 +413,117 @@ def test_run_train_entry_point(sg):
     assert out["epochs"] == 10 and all(b < a for a, b in zip(out["loss"], out["loss"][1:]))
     with pytest.raises(sg.ConfigError):
         sg.run_train({"model": "nope", "V": 2, "E": 1, "features": 1, "classes": 1})
+
+
+# ---------------------------------------------------------------- MP-GCN (max accumulator)
+@pytest.mark.parametrize("kind,V,E,F", [("rmat", 3000, 60000, 64), ("rmat", 800, 20000, 7),
+                                        ("uniform", 2000, 30000, 602), ("uniform", 60, 30, 9),
+                                        ("uniform", 50, 0, 16)])
+def test_max_gather_fwd_bwd_bitwise(sg, kind, V, E, F):
+    """Fused Gather(max) + its backward vs segment_max / take_rows_bwd (tensor.py:453-484)."""
+    from paper_1810_08403_b200 import kernels as K
+
+    s, d = _graph(kind, V, E, 21)
+    g = sg.Graph(V, s, d)
+    grid = sg.ChunkGrid(g, V, gcn_weights=False)
+    Y = rng.features(V, F, seed=5)
+    Y[::7] = Y[::7].round(1)  # plenty of ties: the lowest CSC position must win
+    G = rng.features(V, F, seed=6)
+    M = rng.features(V, F, seed=7)
+    out = _padded(np.zeros((V, F), np.float32))
+    arg = torch.full((V, F), -7, dtype=torch.int32, device="cuda")
+    dH = _padded(np.zeros((V, F), np.float32))
+    dHm = _padded(np.zeros((V, F), np.float32))
+    part = og.partition_2d(s, d, V, V)
+    if E:
+        K.max_gather(grid.csc[(0, 0)], _padded(Y), out, arg, F)
+        pos = grid.csr_positions(0, 0)
+        K.max_gather_bwd(grid.csr[(0, 0)], pos, _padded(G), arg, dH, F)
+        K.max_gather_bwd(grid.csr[(0, 0)], pos, _padded(G), arg, dHm, F, mask=_padded(M))
+        ch = part.chunk(0, 0)
+        src = ch["csc_idx"].astype(np.int64)
+        dst = np.repeat(np.arange(V), np.diff(ch["csc_ptr"]))
+    else:
+        src = dst = np.zeros(0, np.int64)
+    ref, ref_arg = prim.segment_max(prim.take_rows(Y, src), dst, V)
+    if E:
+        assert np.array_equal(out.cpu().numpy(), ref)
+        assert np.array_equal(arg.cpu().numpy().astype(np.int64), ref_arg)
+        ref_dh = prim.take_rows_bwd(prim.segment_max_bwd(G, ref_arg, len(src)), src, V)
+        assert np.array_equal(dH.cpu().numpy(), ref_dh)
+        assert np.array_equal(dHm.cpu().numpy(), prim.relu_bwd(ref_dh, M))
+
+
+@pytest.mark.parametrize("case", GOLDEN_CASES)
+def test_mpgcn_model_vs_reference_golden(sg, case):
+    """2-layer MP-GCN step vs the REAL reference's fp32/fp64 outputs (W_pool, b, W per layer)."""
+    g = load_golden(case)
+    V = int(g["V"])
+    graph = sg.Graph(V, g["src_in"], g["dst_in"])
+    grid = sg.ChunkGrid(graph, V, gcn_weights=False)
+    weights = [g[f"mpgcn_f32_L{l}_{k}"] for l in range(2) for k in range(3)]
+    m = sg.mpgcn_model(grid, [int(g["F"]), int(g["H"]), int(g["C"])], pool=[9, 7], weights=weights)
+    m.load_features(torch.from_numpy(g["gcn_f32_X"]))
+    m.load_labels(g["labels"])
+    m.forward()
+    m.backward()
+    m.check_status()
+    ref_loss = float(np.ravel(g["mpgcnh_f64_loss"])[0])
+    assert abs(m.loss.item() - ref_loss) <= 1e-4 * ref_loss
+    assert_close(m.layers[0].a.cpu().numpy(), g["mpgcnh_f64_a0"], 1e-5, "a0")
+    got = m.grads()
+    for l in range(2):
+        assert_close(m.layers[l].z.cpu().numpy(), g[f"mpgcnh_f64_z{l}"], 1e-4, f"z{l}")
+        for k in range(3):
+            assert_close(got[3 * l + k], g[f"mpgcnh_f64_dL{l}_{k}"], 1e-4, f"L{l}.{k}")
+
+
+@pytest.mark.parametrize("kind", ["rmat", "uniform"])
+def test_mpgcn_epoch_vs_oracle(sg, kind):
+    """MP-GCN epoch at a Pubmed-like shape (F=500, pool 64, H=16, C=3) vs the fp64 oracle."""
+    V, E, F, H, C = 4000, 18000, 500, 16, 3
+    s, d = _graph(kind, V, E, 0)
+    graph = sg.Graph(V, s, d)
+    grid = sg.ChunkGrid(graph, V, gcn_weights=False)
+    m = sg.mpgcn_model(grid, [F, H, C], pool=[64, 32])
+    r = np.random.default_rng(9)
+    W = m.weights()
+    W[1] = r.uniform(-0.2, 0.2, W[1].shape).astype(np.float32)  # non-zero biases
+    W[4] = r.uniform(-0.2, 0.2, W[4].shape).astype(np.float32)
+    m.set_weights(W)
+    X = rng.features(V, F, seed=1)
+    lab = rng.labels(V, C)
+    m.load_features(torch.from_numpy(X))
+    m.load_labels(lab)
+    m.forward()
+    m.backward()
+    m.check_status()
+    part = og.partition_2d(s, d, V, V)
+    layers = [tuple(x.astype(np.float64) for x in W[3 * l: 3 * l + 3]) for l in range(2)]
+    free = saga.mpgcn_epoch(part, X.astype(np.float64), layers, lab)
+    # max is discontinuous: an fp32 run may pick a different argmax only at a near-tie
+    args = [m.layers[l].arg.cpu().numpy().astype(np.int64) for l in range(2)]
+    ch = part.chunk(0, 0)
+    src = ch["csc_idx"].astype(np.int64)
+    for l in range(2):
+        ra = free["cache"][l][3]
+        diff = np.nonzero(args[l] != ra)
+        Y = free["cache"][l][1]
+        assert len(diff[0]) <= 1e-3 * ra.size, (l, len(diff[0]))
+        gap = np.abs(Y[src[args[l][diff]], diff[1]] - Y[src[ra[diff]], diff[1]])
+        assert np.all(gap <= 1e-5), (l, float(gap.max()))
+    ref = saga.mpgcn_epoch(part, X.astype(np.float64), layers, lab, args=args)
+    rl = float(np.ravel(ref["loss"])[0])
+    assert abs(m.loss.item() - rl) <= 1e-4 * rl
+    for k, (a, b) in enumerate(zip(m.grads(), [x for L in ref["grads"] for x in L])):
+        assert_close(a, b, 1e-4, f"grad {k}")
+
+
+def test_mpgcn_rejects_2d_grid_and_trains(sg):
+    s, d = _graph("rmat", 1000, 8000, 1)
+    graph = sg.Graph(1000, s, d)
+    with pytest.raises(sg.ProgramError):
+        sg.mpgcn_model(sg.ChunkGrid(graph, 500, gcn_weights=False), [16, 8, 3])
+    out = sg.run_train({"model": "mpgcn", "graph": "rmat", "V": 1000, "E": 8000, "features": 32,
+                        "classes": 4, "epochs": 5, "lr": 1.0})
+    assert out["loss"][-1] < out["loss"][0]

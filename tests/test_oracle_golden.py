@@ -107,3 +107,27 @@ def test_ggcn_chunked_grid_matches_reference(case):
     for l in range(2):
         for k in range(3):
             assert np.abs(r["grads"][l][k] - g[f"ggcnh_f64_dL{l}_{k}"]).max() <= 1e-10
+
+
+@pytest.mark.parametrize("case", GOLDEN_CASES)
+@pytest.mark.parametrize("tag", ["f64", "f32"])
+def test_mpgcn_oracle_bitwise(case, tag):
+    """MP-GCN (max accumulator) oracle == the real reference, bit for bit."""
+    g = load_golden(case)
+    V = int(g["V"])
+    part = _grid(g)
+    layers = [tuple(g[f"mpgcn_{tag}_L{l}_{k}"] for k in range(3)) for l in range(2)]
+    r = saga.mpgcn_epoch(part, g[f"gcn_{tag}_X"], layers, g["labels"])
+    assert np.array_equal(np.ravel(r["loss"]), np.ravel(g[f"mpgcnh_{tag}_loss"]))
+    for l in range(2):
+        for k in range(3):
+            assert np.array_equal(r["grads"][l][k], g[f"mpgcnh_{tag}_dL{l}_{k}"]), (l, k)
+
+
+@pytest.mark.parametrize("case", GOLDEN_CASES)
+def test_mpgcn_hoist_semantics_preserving(case):
+    g = load_golden(case)
+    assert abs(sc(g["mpgcnh_f64_loss"]) - sc(g["mpgcnu_f64_loss"])) <= 1e-12
+    for l in range(2):
+        for k in range(3):
+            assert np.abs(g[f"mpgcnh_f64_dL{l}_{k}"] - g[f"mpgcnu_f64_dL{l}_{k}"]).max() <= 1e-12
