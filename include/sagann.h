@@ -135,17 +135,24 @@ int sg_segment_max_bwd(int dtype, const void* g, int64_t ldg, const int64_t* arg
                        int64_t n_rows, void* gx, int64_t ldx, int64_t F, void* stream);
 /* Fused Gather(max) over a CSC index (MP-GCN ApplyEdge hoisted to Y, PAPER.md:574-586;
  * segment_max, tensor.py:453-484): out[u] = max over in-edges of Y[idx_e]; argpos[u,f]
- * = CSC position of the first maximum (int32), -1 and empty_fill for empty rows.
+ * = global position (pos_base + CSC position) of the first maximum (int32), -1 for
+ * empty rows.  2D grid: pos_base = the chunk's offset in the source-interval-major
+ * flattening; the chunks of one destination interval run in source order with
+ * accumulate = 1 after the first (running max/argmax read back from out/argpos), and
+ * finalize = 1 on the last writes empty_fill into rows that saw no edge.
  * fp32; Y rows with ld % 4 == 0 are read as 16-B vectors. */
 int sg_max_gather(const int64_t* ptr, const int32_t* idx, int64_t n_rows, const float* Y, int64_t ldy,
                   float* out, int64_t ldo, int32_t* argpos, int64_t lda, int64_t F, float empty_fill,
-                  void* stream);
-/* Its backward over the transposed (CSR) index: out[v] = sum over out-edges k (CSR order)
- * of G[idx_k] where argpos[idx_k] == pos_k (the edge's CSC position), else +0.0; optional
- * ReLU mask.  Bitwise equal to segment_max's backward followed by take_rows' backward. */
+                  int64_t pos_base, int accumulate, int finalize, void* stream);
+/* Its backward over the transposed (CSR) index: out[v] (+)= sum over out-edges k (CSR
+ * order) of G[idx_k] where argpos[idx_k] == pos_base + pos_k (the edge's global
+ * position), else +0.0; accumulate continues the previous chunk of the source interval;
+ * optional ReLU mask (pass it on the last chunk).  Bitwise equal to segment_max's
+ * backward followed by take_rows' backward (tensor.py:473-482, :431-434). */
 int sg_max_gather_bwd(const int64_t* ptr, const int32_t* idx, const int32_t* pos, int64_t n_rows,
                       const float* G, int64_t ldg, const int32_t* argpos, int64_t lda, float* out,
-                      int64_t ldo, int64_t F, const float* mask, int64_t ldm, void* stream);
+                      int64_t ldo, int64_t F, const float* mask, int64_t ldm, int64_t pos_base,
+                      int accumulate, void* stream);
 /* Scatter (take_rows, tensor.py:424-436): out[k] = X[idx[k]] (int64 idx, bounds
  * checked on device: *err_flag set to 1 if any index is out of [0, n_src)). */
 int sg_take_rows(int dtype, const void* X, int64_t ldx, int64_t n_src, const int64_t* idx,

@@ -229,17 +229,21 @@ def ggcn_epoch(part, X, layers, labels, T=None):
 def mpgcn_epoch(part, X, layers, labels, args=None):
     """2-layer MP-GCN, hoisted: Y = sigmoid(h W_pool + b) per vertex,
     Gather(max) over in-edges (segment_max, tensor.py:453-484, argmax = first CSC
-    position), ApplyVertex ReLU(accum W).  ``layers`` = [(W_pool, b, W), ...].  P = 1.
+    position), ApplyVertex ReLU(accum W).  ``layers`` = [(W_pool, b, W), ...].
+
+    The edge list is the 2D grid flattened source-interval-major (chunk C_ij for i, then
+    j, each in CSC order): per destination that is source interval ascending then
+    in-chunk CSC order, per source destination interval ascending
+    then CSR order -- the engine's chunk order in both directions.  Positions (argmax)
+    index this list; with P = 1 it is the plain CSC edge list.
 
     ``args`` (optional, one [V, pool] CSC-position array per layer) pins the max
     selection: max is discontinuous at ties, so a checker comparing an fp32 run with
     this fp64 oracle routes both through the SAME argmax (after verifying separately
     that every disagreement is a near-tie)."""
-    if part.P != 1:
-        raise ValueError("the MP-GCN oracle runs on a single chunk (P = 1)")
-    ch = part.chunk(0, 0)
-    src = ch["csc_idx"].astype(np.int64)
-    dst = local_rows(ch["csc_ptr"])
+    from .graph import flatten_edges
+
+    src, dst = flatten_edges(part)
     V = part.V
     hs, cache = [X], []
     for (Wp, b, W) in layers:

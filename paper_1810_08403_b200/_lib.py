@@ -54,9 +54,10 @@ _SIGS = {
                             _i64, _i32, _p, _i64, _p]),
     "sg_segment_max": (_i32, [_i32, _p, _p, _i64, _p, _i64, _p, _i64, _p, _i64, _i64, _f32, _p]),
     "sg_segment_max_bwd": (_i32, [_i32, _p, _i64, _p, _i64, _i64, _p, _i64, _i64, _p]),
-    "sg_max_gather": (_i32, [_p, _p, _i64, _p, _i64, _p, _i64, _p, _i64, _i64, _f32, _p]),
+    "sg_max_gather": (_i32, [_p, _p, _i64, _p, _i64, _p, _i64, _p, _i64, _i64, _f32, _i64, _i32,
+                             _i32, _p]),
     "sg_max_gather_bwd": (_i32, [_p, _p, _p, _i64, _p, _i64, _p, _i64, _p, _i64, _i64, _p, _i64,
-                                 _p]),
+                                 _i64, _i32, _p]),
     "sg_take_rows":(_i32, [_i32, _p, _i64, _i64, _p, _i64, _p, _i64, _i64, _p, _p]),
     "sg_sort_workspace_bytes": (_i64, [_i64, _i64]),
     "sg_segment_sort": (_i32, [_p, _i64, _i64, _p, _p, _p, _p, _i64, _p]),

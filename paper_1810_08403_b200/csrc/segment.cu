@@ -147,41 +147,86 @@ int grid_for(int64_t work, int per_block) {
 }
 
 // Fused Gather(max) over a CSC index (MP-GCN): out[u] = max over the
-// in-edges of Y[src] with the CSC position of the first maximum recorded as the argmax
+// in-edges of Y[src] with the position of the first maximum recorded as the argmax
 // ("ties broken by lowest CSC edge index"); empty rows -> fill, argmax -1.
-__global__ void maxgather_kernel(const int64_t* ptr, const int32_t* idx, int64_t n_rows,
-                                 const float* Y, int64_t ldy, float* out, int64_t ldo, int32_t* arg,
-                                 int64_t lda, int F, float fill, int vec) {
-  const int lane = threadIdx.x & 31;
+//
+// Positions are global: base + in-chunk CSC position, base = the chunk's offset in the
+// source-interval-major flattening of the 2D grid, so for a destination interval the
+// chunks C_0j, C_1j, ... (visited in that order, `accumulate` carrying the running
+// max/argmax in out/arg) produce exactly segment_max over the flattened edge list.
+// `finalize` applies the empty fill on the last chunk of the chain.
+//
+// TEAM lanes per destination row (narrow pooled widths pack 32/TEAM rows per warp);
+// 4 source rows are loaded before any is compared so 4 row reads are in flight per lane.
+template <int W, int TEAM>
+__global__ void __launch_bounds__(256) maxgather_kernel(
+    const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx, int64_t n_rows,
+    const float* __restrict__ Y, int64_t ldy, float* __restrict__ out, int64_t ldo,
+    int32_t* __restrict__ arg, int64_t lda, int F, float fill, int64_t base, int accumulate,
+    int finalize) {
+  constexpr int RPW = 32 / TEAM;
+  const int lane = threadIdx.x & 31, tl = lane % TEAM;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int W = vec ? 4 : 1;
+  const int64_t nteams = (((int64_t)gridDim.x * blockDim.x) >> 5) * RPW;
   const int Fv = (F + W - 1) / W;
-  for (int64_t r = warp; r < n_rows; r += nwarps) {
-    const int64_t e0 = ptr[r], e1 = ptr[r + 1];
-    for (int cv = lane; cv < Fv; cv += 32) {
-      float best[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-      int32_t barg[4] = {-1, -1, -1, -1};
-      for (int64_t e = e0; e < e1; ++e) {
-        const float* row = Y + (int64_t)__ldg(idx + e) * ldy + (int64_t)cv * W;
-        float v[4];
-        if (vec) {
-          float4 q = __ldg(reinterpret_cast<const float4*>(row));
-          v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+  for (int64_t r = warp * RPW + lane / TEAM; r < n_rows; r += nteams) {
+    const int64_t e0 = __ldg(ptr + r), e1 = __ldg(ptr + r + 1);
+    for (int cv = tl; cv < Fv; cv += TEAM) {
+      const int c0 = cv * W;
+      float best[W];
+      int32_t barg[W];
+#pragma unroll
+      for (int k = 0; k < W; ++k) {
+        best[k] = -INFINITY;
+        barg[k] = -1;
+        if (accumulate && c0 + k < F) {
+          barg[k] = arg[r * lda + c0 + k];
+          if (barg[k] >= 0) best[k] = out[r * ldo + c0 + k];
+        }
+      }
+      int64_t e = e0;
+      for (; e + 4 <= e1; e += 4) {
+        float v[4][W];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float* row = Y + (int64_t)__ldg(idx + e + u) * ldy + c0;
+          if (W == 4) {
+            const float4 q = __ldg(reinterpret_cast<const float4*>(row));
+            v[u][0] = q.x; v[u][1 % W] = q.y; v[u][2 % W] = q.z; v[u][3 % W] = q.w;
+          } else {
+            v[u][0] = __ldg(row);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int k = 0; k < W; ++k)
+            if (v[u][k] > best[k]) {  // strict '>' : the lowest position wins (tensor.py:467)
+              best[k] = v[u][k];
+              barg[k] = (int32_t)(base + e + u);
+            }
+      }
+      for (; e < e1; ++e) {
+        const float* row = Y + (int64_t)__ldg(idx + e) * ldy + c0;
+        float v[W];
+        if (W == 4) {
+          const float4 q = __ldg(reinterpret_cast<const float4*>(row));
+          v[0] = q.x; v[1 % W] = q.y; v[2 % W] = q.z; v[3 % W] = q.w;
         } else {
           v[0] = __ldg(row);
         }
+#pragma unroll
         for (int k = 0; k < W; ++k)
-          if (v[k] > best[k]) {  // strict '>' : the lowest position wins ties (tensor.py:467)
+          if (v[k] > best[k]) {
             best[k] = v[k];
-            barg[k] = (int32_t)e;
+            barg[k] = (int32_t)(base + e);
           }
       }
+#pragma unroll
       for (int k = 0; k < W; ++k) {
-        const int c = cv * W + k;
-        if (c < F) {
-          out[r * ldo + c] = barg[k] < 0 ? fill : best[k];
-          arg[r * lda + c] = barg[k];
+        if (c0 + k < F) {
+          out[r * ldo + c0 + k] = (finalize && barg[k] < 0) ? fill : best[k];
+          arg[r * lda + c0 + k] = barg[k];
         }
       }
     }
@@ -190,29 +235,76 @@ __global__ void maxgather_kernel(const int64_t* ptr, const int32_t* idx, int64_t
 
 // Backward of the fused max gather over the transposed (CSR) index: dY[v] = sum over
 // out-edges k of v, in CSR order (= the forward edge-list order, tensor.py:431-434), of
-// dA[dst_k] where the destination's argmax is this edge (pos_k = its CSC position), else
-// +0.0 -- exactly tensor.py:473-482 followed by take_rows' backward.  No atomics.
-__global__ void maxgather_bwd_kernel(const int64_t* ptr, const int32_t* idx, const int32_t* pos,
-                                     int64_t n_rows, const float* G, int64_t ldg, const int32_t* arg,
-                                     int64_t lda, float* out, int64_t ldo, int F, const float* mask,
-                                     int64_t ldm) {
-  const int lane = threadIdx.x & 31;
+// dA[dst_k] where the destination's argmax is this edge (pos_base + pos_k = its global
+// position), else +0.0 -- exactly tensor.py:473-482 followed by take_rows' backward.
+// `accumulate` continues the sum of the previous chunk of the same source interval
+// (chunks C_i0, C_i1, ... in that order).  No atomics.
+template <int W, int TEAM>
+__global__ void __launch_bounds__(256) maxgather_bwd_kernel(
+    const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx, const int32_t* __restrict__ pos,
+    int64_t n_rows, const float* __restrict__ G, int64_t ldg, const int32_t* __restrict__ arg,
+    int64_t lda, float* __restrict__ out, int64_t ldo, int F, const float* __restrict__ mask,
+    int64_t ldm, int64_t pos_base, int accumulate) {
+  constexpr int RPW = 32 / TEAM;
+  const int lane = threadIdx.x & 31, tl = lane % TEAM;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t r = warp; r < n_rows; r += nwarps) {
-    const int64_t e0 = ptr[r], e1 = ptr[r + 1];
-    for (int c = lane; c < F; c += 32) {
-      float acc = 0.f;
-      for (int64_t k = e0; k < e1; ++k) {
-        const int64_t u = __ldg(idx + k);
-        const float g = __ldg(G + u * ldg + c);
-        const int32_t a = __ldg(arg + u * lda + c);
-        acc = __fadd_rn(acc, a == __ldg(pos + k) ? g : 0.f);
+  const int64_t nteams = (((int64_t)gridDim.x * blockDim.x) >> 5) * RPW;
+  const int Fv = (F + W - 1) / W;
+  for (int64_t r = warp * RPW + lane / TEAM; r < n_rows; r += nteams) {
+    const int64_t e0 = __ldg(ptr + r), e1 = __ldg(ptr + r + 1);
+    for (int cv = tl; cv < Fv; cv += TEAM) {
+      const int c0 = cv * W;
+      float acc[W];
+#pragma unroll
+      for (int k = 0; k < W; ++k) acc[k] = (accumulate && c0 + k < F) ? out[r * ldo + c0 + k] : 0.f;
+      int64_t e = e0;
+      for (; e + 2 <= e1; e += 2) {  // 2 edges' rows in flight (each is a G and an arg read)
+        float g[2][W];
+        int32_t a[2][W], p[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int64_t d = __ldg(idx + e + u);
+          p[u] = (int32_t)(pos_base + __ldg(pos + e + u));
+          if (W == 4) {
+            const float4 q = __ldg(reinterpret_cast<const float4*>(G + d * ldg + c0));
+            const int4 t = __ldg(reinterpret_cast<const int4*>(arg + d * lda + c0));
+            g[u][0] = q.x; g[u][1 % W] = q.y; g[u][2 % W] = q.z; g[u][3 % W] = q.w;
+            a[u][0] = t.x; a[u][1 % W] = t.y; a[u][2 % W] = t.z; a[u][3 % W] = t.w;
+          } else {
+            g[u][0] = __ldg(G + d * ldg + c0);
+            a[u][0] = __ldg(arg + d * lda + c0);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+          for (int k = 0; k < W; ++k) acc[k] = __fadd_rn(acc[k], a[u][k] == p[u] ? g[u][k] : 0.f);
       }
-      if (mask) acc = __fmul_rn(acc, __ldg(mask + r * ldm + c) > 0.f ? 1.f : 0.f);
-      out[r * ldo + c] = acc;
+      for (; e < e1; ++e) {
+        const int64_t d = __ldg(idx + e);
+        const int32_t pp = (int32_t)(pos_base + __ldg(pos + e));
+#pragma unroll
+        for (int k = 0; k < W; ++k) {
+          const int c = min(c0 + k, F - 1);
+          acc[k] = __fadd_rn(acc[k], __ldg(arg + d * lda + c) == pp ? __ldg(G + d * ldg + c) : 0.f);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < W; ++k) {
+        if (c0 + k < F) {
+          float v = acc[k];
+          if (mask) v = __fmul_rn(v, __ldg(mask + r * ldm + c0 + k) > 0.f ? 1.f : 0.f);
+          out[r * ldo + c0 + k] = v;
+        }
+      }
     }
   }
+}
+
+int team_for(int Fv) {
+  int t = 1;
+  while (t < Fv && t < 32) t <<= 1;
+  return t;
 }
 
 }  // namespace
@@ -221,12 +313,32 @@ extern "C" {
 
 int sg_max_gather(const int64_t* ptr, const int32_t* idx, int64_t n_rows, const float* Y, int64_t ldy,
                   float* out, int64_t ldo, int32_t* argpos, int64_t lda, int64_t F, float empty_fill,
-                  void* stream) {
+                  int64_t pos_base, int accumulate, int finalize, void* stream) {
   if (n_rows == 0 || F == 0) return SG_OK;
   SG_REQUIRE(ptr && idx && Y && out && argpos, SG_EINVAL, "max_gather: null pointer");
-  const int vec = (F % 4 == 0) && (ldy % 4 == 0) && aligned(Y, 16);
-  maxgather_kernel<<<grid_for(n_rows * 32, 256), 256, 0, (cudaStream_t)stream>>>(
-      ptr, idx, n_rows, Y, ldy, out, ldo, argpos, lda, (int)F, empty_fill, vec);
+  const bool vec = (F % 4 == 0) && (ldy % 4 == 0) && aligned(Y, 16);
+  const int team = team_for(vec ? (int)(F / 4) : (int)F);
+  const int g = grid_for(n_rows * team, 256);
+  cudaStream_t st = (cudaStream_t)stream;
+#define SG_MG(Wv, T)                                                                        \
+  maxgather_kernel<Wv, T><<<g, 256, 0, st>>>(ptr, idx, n_rows, Y, ldy, out, ldo, argpos, lda, \
+                                             (int)F, empty_fill, pos_base, accumulate, finalize)
+#define SG_MG_TEAMS(Wv)                         \
+  switch (team) {                               \
+    case 1: SG_MG(Wv, 1); break;                \
+    case 2: SG_MG(Wv, 2); break;                \
+    case 4: SG_MG(Wv, 4); break;                \
+    case 8: SG_MG(Wv, 8); break;                \
+    case 16: SG_MG(Wv, 16); break;              \
+    default: SG_MG(Wv, 32); break;              \
+  }
+  if (vec) {
+    SG_MG_TEAMS(4)
+  } else {
+    SG_MG_TEAMS(1)
+  }
+#undef SG_MG_TEAMS
+#undef SG_MG
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) SG_FAIL(SG_ECUDA, "max_gather launch: %s", cudaGetErrorString(e));
   sg::count_launch(1);
@@ -235,11 +347,34 @@ int sg_max_gather(const int64_t* ptr, const int32_t* idx, int64_t n_rows, const 
 
 int sg_max_gather_bwd(const int64_t* ptr, const int32_t* idx, const int32_t* pos, int64_t n_rows,
                       const float* G, int64_t ldg, const int32_t* argpos, int64_t lda, float* out,
-                      int64_t ldo, int64_t F, const float* mask, int64_t ldm, void* stream) {
+                      int64_t ldo, int64_t F, const float* mask, int64_t ldm, int64_t pos_base,
+                      int accumulate, void* stream) {
   if (n_rows == 0 || F == 0) return SG_OK;
   SG_REQUIRE(ptr && idx && pos && G && argpos && out, SG_EINVAL, "max_gather_bwd: null pointer");
-  maxgather_bwd_kernel<<<grid_for(n_rows * 32, 256), 256, 0, (cudaStream_t)stream>>>(
-      ptr, idx, pos, n_rows, G, ldg, argpos, lda, out, ldo, (int)F, mask, ldm);
+  const bool vec = (F % 4 == 0) && (ldg % 4 == 0) && (lda % 4 == 0) && aligned(G, 16) &&
+                   aligned(argpos, 16);
+  const int team = team_for(vec ? (int)(F / 4) : (int)F);
+  const int g = grid_for(n_rows * team, 256);
+  cudaStream_t st = (cudaStream_t)stream;
+#define SG_MB(Wv, T)                                                                              \
+  maxgather_bwd_kernel<Wv, T><<<g, 256, 0, st>>>(ptr, idx, pos, n_rows, G, ldg, argpos, lda, out, \
+                                                 ldo, (int)F, mask, ldm, pos_base, accumulate)
+#define SG_MB_TEAMS(Wv)                         \
+  switch (team) {                               \
+    case 1: SG_MB(Wv, 1); break;                \
+    case 2: SG_MB(Wv, 2); break;                \
+    case 4: SG_MB(Wv, 4); break;                \
+    case 8: SG_MB(Wv, 8); break;                \
+    case 16: SG_MB(Wv, 16); break;              \
+    default: SG_MB(Wv, 32); break;              \
+  }
+  if (vec) {
+    SG_MB_TEAMS(4)
+  } else {
+    SG_MB_TEAMS(1)
+  }
+#undef SG_MB_TEAMS
+#undef SG_MB
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) SG_FAIL(SG_ECUDA, "max_gather_bwd launch: %s", cudaGetErrorString(e));
   sg::count_launch(1);

@@ -75,8 +75,6 @@ class SAGAModel:
             L.gate = q.fused.params
             # accumulator width: the pooled width for MP-GCN, else the input width
             L.Aw = q.params[L.gate[0]][1] if L.kind == "max_pool" else q.f_in
-            if L.kind in ("max", "max_pool") and grid.P != 1:
-                raise ProgramError("the max-accumulator executor runs on a single chunk (P = 1)")
             self.layers.append(L)
             dims.append((q.f_in, q.f_out))
         for a, b in zip(dims, dims[1:]):
@@ -318,6 +316,33 @@ class SAGAModel:
                             r_off=L.goff, out1=self._rows(L.dHt, i), accumulate=k > 0, ws=self.ws,
                             stream=stream)
 
+    def _fwd_max(self, L, Y, stream=None):
+        """Gather(max) over the CSC chunks of each destination interval, source intervals
+        ascending, carrying the running max/argmax (global positions = chunk base + CSC
+        position, so the result is segment_max over the flattened edge list)."""
+        g, P = self.grid, self.grid.P
+        for j in range(P):
+            if not any((i, j) in g.csc for i in range(P)):
+                self._rows(L.a, j).zero_()
+                self._rows(L.arg, j).fill_(-1)
+        for (i, j), first, last in self._chunk_order(list(g.csc), 1):
+            K.max_gather(g.csc[(i, j)], self._rows(Y, i), self._rows(L.a, j), self._rows(L.arg, j),
+                         L.Aw, pos_base=g.edge_base[(i, j)], accumulate=not first, finalize=last,
+                         stream=stream)
+
+    def _bwd_max(self, L, out, mask, stream=None):
+        """dY[v] = sum over out-edges (destination intervals ascending, CSR order) of dA[dst]
+        routed to the argmax edge; ReLU mask of the layer below fused on the last chunk."""
+        g, P = self.grid, self.grid.P
+        for i in range(P):
+            if not any((i, j) in g.csr for j in range(P)):
+                self._rows(out, i).zero_()
+        for (i, j), first, last in self._chunk_order(list(g.csr), 0):
+            K.max_gather_bwd(g.csr[(i, j)], g.csr_positions(i, j), self._rows(L.da, j),
+                             self._rows(L.arg, j), self._rows(out, i), L.Aw,
+                             mask=self._rows(mask, i) if (last and mask is not None) else None,
+                             pos_base=g.edge_base[(i, j)], accumulate=not first, stream=stream)
+
     def _gemm(self, A, B, C, **kw):
         K.gemm(A, B, C, prec=self.gemm_prec, ws=self.ws, **kw)
 
@@ -350,11 +375,7 @@ class SAGAModel:
                     K.ewise(5, L.Y, None, L.Y, stream)
                     Y = L.Y
                     self._mark(f"L{n}.fwd.hoist_gemm")
-                if (0, 0) in self.grid.csc:
-                    K.max_gather(self.grid.csc[(0, 0)], Y, L.a, L.arg, L.Aw, stream=stream)
-                else:
-                    L.a.zero_()
-                    L.arg.fill_(-1)
+                self._fwd_max(L, Y, stream)
             else:
                 self._fwd_propagate(L, stream)
             self._mark(f"L{n}.fwd.propagate")
@@ -375,21 +396,12 @@ class SAGAModel:
             if L.kind in ("max", "max_pool"):
                 self._gemm(L.dz, L.W, L.da, trans_b=True)       # dA = dz W^T
                 self._mark(f"L{n}.bwd.apply_vertex")
-                pi = self.grid.csr.get((0, 0))
                 if L.kind == "max":
-                    if below is not None:
-                        if pi is None:
-                            below.dz.zero_()
-                        else:  # max routing + ReLU mask of the layer below, one pass
-                            K.max_gather_bwd(pi, self.grid.csr_positions(0, 0), L.da, L.arg,
-                                             below.dz, L.Aw, mask=below.z, stream=stream)
+                    if below is not None:  # max routing + ReLU mask of the layer below, one pass
+                        self._bwd_max(L, below.dz, below.z, stream)
                     self._mark(f"L{n}.bwd.propagate")
                     continue
-                if pi is None:
-                    L.dY.zero_()
-                else:
-                    K.max_gather_bwd(pi, self.grid.csr_positions(0, 0), L.da, L.arg, L.dY, L.Aw,
-                                     stream=stream)
+                self._bwd_max(L, L.dY, None, stream)
                 self._mark(f"L{n}.bwd.propagate")
                 K.ewise(9, L.dY, L.Y, L.dY, stream)                  # sigmoid bwd (tensor.py:232)
                 self._gemm(self._ones, L.dY, L.dbias, trans_a=True)  # db = column sums

@@ -211,9 +211,15 @@ class ChunkGrid:
         self.device = device
         degs = g.degrees() if gcn_weights else None
         self.csc, self.csr = {}, {}
+        # offset of each chunk's edges in the source-interval-major flattening (global
+        # edge positions, e.g. the max-gather argmax)
+        self.edge_base = {}
+        total = 0
         for i in range(self.P):
             for j in range(self.P):
                 ch = self.part.chunk(i, j)
+                self.edge_base[(i, j)] = total
+                total += int(ch["nnz"])
                 if ch["nnz"] == 0:
                     continue
                 wc = g.gcn_weights(ch["csc_eid"], degs) if gcn_weights else None

@@ -89,17 +89,20 @@ def softmax_xent(Z, labels, loss, dZ, err, *, relu_input=True, n_total=0, ws=Non
                               stream_handle(stream)))
 
 
-def max_gather(pi, Y, out, arg, F, empty_fill=0.0, stream=None):
-    """Fused Gather(max) over CSC pass index ``pi`` (argmax = CSC position, int32)."""
+def max_gather(pi, Y, out, arg, F, empty_fill=0.0, *, pos_base=0, accumulate=False, finalize=True,
+               stream=None):
+    """Fused Gather(max) over CSC pass index ``pi`` (argmax = pos_base + CSC position, int32)."""
     check(lib.sg_max_gather(tptr(pi.ptr), tptr(pi.idx), pi.n_rows, tptr(Y), ld(Y), tptr(out), ld(out),
-                            tptr(arg), ld(arg), F, float(empty_fill), stream_handle(stream)))
+                            tptr(arg), ld(arg), F, float(empty_fill), int(pos_base),
+                            int(bool(accumulate)), int(bool(finalize)), stream_handle(stream)))
 
 
-def max_gather_bwd(pi, pos, G, arg, out, F, mask=None, stream=None):
+def max_gather_bwd(pi, pos, G, arg, out, F, mask=None, *, pos_base=0, accumulate=False, stream=None):
     """Backward of max_gather over CSR pass index ``pi`` (pos = CSC position per CSR edge)."""
     check(lib.sg_max_gather_bwd(tptr(pi.ptr), tptr(pi.idx), tptr(pos), pi.n_rows, tptr(G), ld(G),
                                 tptr(arg), ld(arg), tptr(out), ld(out), F, tptr(mask),
-                                ld(mask) if mask is not None else 0, stream_handle(stream)))
+                                ld(mask) if mask is not None else 0, int(pos_base),
+                                int(bool(accumulate)), stream_handle(stream)))
 
 
 def ewise(op, a, b, out, stream=None):

@@ -416,42 +416,62 @@ def test_run_train_entry_point(sg):
 
 
 # ---------------------------------------------------------------- MP-GCN (max accumulator)
-@pytest.mark.parametrize("kind,V,E,F", [("rmat", 3000, 60000, 64), ("rmat", 800, 20000, 7),
-                                        ("uniform", 2000, 30000, 602), ("uniform", 60, 30, 9),
-                                        ("uniform", 50, 0, 16)])
-def test_max_gather_fwd_bwd_bitwise(sg, kind, V, E, F):
-    """Fused Gather(max) + its backward vs segment_max / take_rows_bwd (tensor.py:453-484)."""
+def _gpu_max_chunked(sg, grid, Y, G, M, F):
+    """Chunk loops of the engine: forward per destination interval over source intervals
+    ascending; backward per source interval over destination intervals ascending."""
     from paper_1810_08403_b200 import kernels as K
 
-    s, d = _graph(kind, V, E, 21)
-    g = sg.Graph(V, s, d)
-    grid = sg.ChunkGrid(g, V, gcn_weights=False)
-    Y = rng.features(V, F, seed=5)
-    Y[::7] = Y[::7].round(1)  # plenty of ties: the lowest CSC position must win
-    G = rng.features(V, F, seed=6)
-    M = rng.features(V, F, seed=7)
+    V = grid.V
     out = _padded(np.zeros((V, F), np.float32))
     arg = torch.full((V, F), -7, dtype=torch.int32, device="cuda")
     dH = _padded(np.zeros((V, F), np.float32))
     dHm = _padded(np.zeros((V, F), np.float32))
-    part = og.partition_2d(s, d, V, V)
-    if E:
-        K.max_gather(grid.csc[(0, 0)], _padded(Y), out, arg, F)
-        pos = grid.csr_positions(0, 0)
-        K.max_gather_bwd(grid.csr[(0, 0)], pos, _padded(G), arg, dH, F)
-        K.max_gather_bwd(grid.csr[(0, 0)], pos, _padded(G), arg, dHm, F, mask=_padded(M))
-        ch = part.chunk(0, 0)
-        src = ch["csc_idx"].astype(np.int64)
-        dst = np.repeat(np.arange(V), np.diff(ch["csc_ptr"]))
-    else:
-        src = dst = np.zeros(0, np.int64)
+    rows = lambda t, k: t[grid.begin(k): grid.begin(k) + grid.size(k)]  # noqa: E731
+    for j in range(grid.P):
+        chain = [i for i in range(grid.P) if (i, j) in grid.csc]
+        if not chain:
+            rows(out, j).zero_()
+            rows(arg, j).fill_(-1)
+        for k, i in enumerate(chain):
+            K.max_gather(grid.csc[(i, j)], rows(Y, i), rows(out, j), rows(arg, j), F,
+                         pos_base=grid.edge_base[(i, j)], accumulate=k > 0,
+                         finalize=k == len(chain) - 1)
+    for i in range(grid.P):
+        chain = [j for j in range(grid.P) if (i, j) in grid.csr]
+        if not chain:
+            rows(dH, i).zero_()
+            rows(dHm, i).zero_()
+        for k, j in enumerate(chain):
+            for o, m in ((dH, None), (dHm, M)):
+                K.max_gather_bwd(grid.csr[(i, j)], grid.csr_positions(i, j), rows(G, j), rows(arg, j),
+                                 rows(o, i), F, mask=rows(m, i) if (m is not None and k == len(chain) - 1)
+                                 else None, pos_base=grid.edge_base[(i, j)], accumulate=k > 0)
+    return out, arg, dH, dHm
+
+
+@pytest.mark.parametrize("kind,V,E,F,P", [("rmat", 3000, 60000, 64, 1), ("rmat", 800, 20000, 7, 1),
+                                          ("uniform", 2000, 30000, 602, 1), ("uniform", 60, 30, 9, 1),
+                                          ("uniform", 50, 0, 16, 1), ("rmat", 3000, 60000, 64, 3),
+                                          ("rmat", 1000, 30000, 9, 4), ("uniform", 700, 500, 128, 5)])
+def test_max_gather_fwd_bwd_bitwise(sg, kind, V, E, F, P):
+    """Fused Gather(max) + its backward vs segment_max / take_rows_bwd (tensor.py:453-484) over
+    the flattened edge list; P > 1 runs the engine's chunk loops over the 2D grid."""
+    s, d = _graph(kind, V, E, 21)
+    g = sg.Graph(V, s, d)
+    size = -(-V // P)
+    grid = sg.ChunkGrid(g, size, gcn_weights=False)
+    Y = rng.features(V, F, seed=5)
+    Y[::7] = Y[::7].round(1)  # plenty of ties: the lowest position must win
+    G = rng.features(V, F, seed=6)
+    M = rng.features(V, F, seed=7)
+    out, arg, dH, dHm = _gpu_max_chunked(sg, grid, _padded(Y), _padded(G), _padded(M), F)
+    src, dst = og.flatten_edges(og.partition_2d(s, d, V, size))
     ref, ref_arg = prim.segment_max(prim.take_rows(Y, src), dst, V)
-    if E:
-        assert np.array_equal(out.cpu().numpy(), ref)
-        assert np.array_equal(arg.cpu().numpy().astype(np.int64), ref_arg)
-        ref_dh = prim.take_rows_bwd(prim.segment_max_bwd(G, ref_arg, len(src)), src, V)
-        assert np.array_equal(dH.cpu().numpy(), ref_dh)
-        assert np.array_equal(dHm.cpu().numpy(), prim.relu_bwd(ref_dh, M))
+    assert np.array_equal(out.cpu().numpy(), ref)
+    assert np.array_equal(arg.cpu().numpy().astype(np.int64), ref_arg)
+    ref_dh = prim.take_rows_bwd(prim.segment_max_bwd(G, ref_arg, len(src)), src, V)
+    assert np.array_equal(dH.cpu().numpy(), ref_dh)
+    assert np.array_equal(dHm.cpu().numpy(), prim.relu_bwd(ref_dh, M))
 
 
 @pytest.mark.parametrize("case", GOLDEN_CASES)
@@ -478,14 +498,17 @@ def test_mpgcn_model_vs_reference_golden(sg, case):
             assert_close(got[3 * l + k], g[f"mpgcnh_f64_dL{l}_{k}"], 1e-4, f"L{l}.{k}")
 
 
-@pytest.mark.parametrize("kind", ["rmat", "uniform"])
-def test_mpgcn_epoch_vs_oracle(sg, kind):
-    """MP-GCN epoch at a Pubmed-like shape (F=500, pool 64, H=16, C=3) vs the fp64 oracle."""
+@pytest.mark.parametrize("kind,P,schedule", [("rmat", 1, "locality"), ("uniform", 1, "locality"),
+                                             ("rmat", 3, "locality"), ("rmat", 3, "dest_order")])
+def test_mpgcn_epoch_vs_oracle(sg, kind, P, schedule):
+    """MP-GCN epoch at a Pubmed-like shape (F=500, pool 64/32, H=16, C=3) vs the fp64 oracle,
+    on one chunk and on a 3x3 grid."""
     V, E, F, H, C = 4000, 18000, 500, 16, 3
     s, d = _graph(kind, V, E, 0)
     graph = sg.Graph(V, s, d)
-    grid = sg.ChunkGrid(graph, V, gcn_weights=False)
-    m = sg.mpgcn_model(grid, [F, H, C], pool=[64, 32])
+    size = -(-V // P)
+    grid = sg.ChunkGrid(graph, size, gcn_weights=False)
+    m = sg.mpgcn_model(grid, [F, H, C], pool=[64, 32], schedule=schedule)
     r = np.random.default_rng(9)
     W = m.weights()
     W[1] = r.uniform(-0.2, 0.2, W[1].shape).astype(np.float32)  # non-zero biases
@@ -498,13 +521,12 @@ def test_mpgcn_epoch_vs_oracle(sg, kind):
     m.forward()
     m.backward()
     m.check_status()
-    part = og.partition_2d(s, d, V, V)
+    part = og.partition_2d(s, d, V, size)
     layers = [tuple(x.astype(np.float64) for x in W[3 * l: 3 * l + 3]) for l in range(2)]
     free = saga.mpgcn_epoch(part, X.astype(np.float64), layers, lab)
     # max is discontinuous: an fp32 run may pick a different argmax only at a near-tie
     args = [m.layers[l].arg.cpu().numpy().astype(np.int64) for l in range(2)]
-    ch = part.chunk(0, 0)
-    src = ch["csc_idx"].astype(np.int64)
+    src, _ = og.flatten_edges(part)
     for l in range(2):
         ra = free["cache"][l][3]
         diff = np.nonzero(args[l] != ra)
@@ -519,11 +541,7 @@ def test_mpgcn_epoch_vs_oracle(sg, kind):
         assert_close(a, b, 1e-4, f"grad {k}")
 
 
-def test_mpgcn_rejects_2d_grid_and_trains(sg):
-    s, d = _graph("rmat", 1000, 8000, 1)
-    graph = sg.Graph(1000, s, d)
-    with pytest.raises(sg.ProgramError):
-        sg.mpgcn_model(sg.ChunkGrid(graph, 500, gcn_weights=False), [16, 8, 3])
+def test_mpgcn_trains(sg):
     out = sg.run_train({"model": "mpgcn", "graph": "rmat", "V": 1000, "E": 8000, "features": 32,
-                        "classes": 4, "epochs": 5, "lr": 1.0})
+                        "classes": 4, "epochs": 5, "lr": 1.0, "interval_size": 300})
     assert out["loss"][-1] < out["loss"][0]

@@ -131,3 +131,21 @@ def test_mpgcn_hoist_semantics_preserving(case):
     for l in range(2):
         for k in range(3):
             assert np.abs(g[f"mpgcnh_f64_dL{l}_{k}"] - g[f"mpgcnu_f64_dL{l}_{k}"]).max() <= 1e-12
+
+
+@pytest.mark.parametrize("case", GOLDEN_CASES)
+def test_mpgcn_oracle_2d_grid_matches_one_chunk(case):
+    """The 2D-grid edge order (source-interval-major flattening) changes only summation
+    order and tie positions: loss and gradients agree with P = 1 to fp64 round-off."""
+    g = load_golden(case)
+    V = int(g["V"])
+    layers = [tuple(g[f"mpgcn_f64_L{l}_{k}"] for k in range(3)) for l in range(2)]
+    r1 = saga.mpgcn_epoch(og.partition_2d(g["src_in"], g["dst_in"], V, V), g["gcn_f64_X"], layers,
+                          g["labels"])
+    r3 = saga.mpgcn_epoch(og.partition_2d(g["src_in"], g["dst_in"], V, -(-V // 3)), g["gcn_f64_X"],
+                          layers, g["labels"])
+    assert abs(sc(r1["loss"]) - sc(r3["loss"])) <= 1e-12
+    for l in range(2):
+        assert np.array_equal(r1["cache"][l][2], r3["cache"][l][2])  # max values are order-free
+        for k in range(3):
+            assert np.abs(r1["grads"][l][k] - r3["grads"][l][k]).max() <= 1e-12
