@@ -226,6 +226,34 @@ def ggcn_epoch(part, X, layers, labels, T=None):
     return dict(loss=loss, p=p, out=hs[1:], cache=cache, grads=grads)
 
 
+def commnet_epoch(part, X, layers, labels, T=None):
+    """2-layer CommNet: ApplyEdge = edge.src (passthrough), Gather(sum),
+    ApplyVertex = ReLU(h W_H + accum W_C) (tensor.py:274 add of the two matmuls).
+    ``layers`` = [(W_H, W_C), ...].  The gradient of h sums the direct (W_H) partial and
+    the take_rows partial in the tape's reverse order (tensor.py:109-116)."""
+    hs, cache = [X], []
+    for (WH, WC) in layers:
+        h = hs[-1]
+        a = gcn_propagate_fwd(part, h, None, T)
+        z = prim.add(prim.matmul(h, WH), prim.matmul(a, WC))
+        cache.append((h, a, z))
+        hs.append(prim.relu(z))
+    loss, p = prim.softmax_cross_entropy(hs[-1], labels)
+    g = prim.softmax_cross_entropy_bwd(np.asarray(1.0, dtype=X.dtype), p, labels)
+    grads = [None] * len(layers)
+    for l in range(len(layers) - 1, -1, -1):
+        WH, WC = layers[l]
+        h, a, z = cache[l]
+        gz = prim.relu_bwd(g, z)
+        ga, gWC = prim.matmul_bwd(gz, a, WC)
+        gh, gWH = prim.matmul_bwd(gz, h, WH)
+        grads[l] = (gWH, gWC)
+        if l > 0:
+            g = gh + gcn_propagate_bwd(part, ga, None, T)
+    return dict(loss=loss, a=[c[1] for c in cache], z=[c[2] for c in cache], out=hs[1:],
+                grads=grads)
+
+
 def mpgcn_epoch(part, X, layers, labels, args=None):
     """2-layer MP-GCN, hoisted: Y = sigmoid(h W_pool + b) per vertex,
     Gather(max) over in-edges (segment_max, tensor.py:453-484, argmax = first CSC

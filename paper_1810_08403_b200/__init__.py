@@ -15,7 +15,7 @@ from .graph import (ChunkGrid, Graph, Partition, partition_2d, reencode_balance,
 from .program import (FusedGather, LayerProgram, PassReport, build_commnet, build_gcn, build_ggcn,
                       build_mpgcn,
                       evaluate_expr, fuse_sag, hoist_vertex_computation, make_program, matmul_rows,
-                      optimize, trace_udf, validate_program)
+                      optimize, trace_udf, validate_program, vertex_form)
 
 __all__ = [
     "errors", "BudgetError", "ConfigError", "EngineError", "GraphFormatError", "NumericError",
@@ -23,14 +23,14 @@ __all__ = [
     "reencode_balance", "rmat_graph", "synthetic_features", "uniform_graph", "FusedGather",
     "LayerProgram", "PassReport", "build_commnet", "build_gcn", "build_ggcn", "build_mpgcn", "evaluate_expr",
     "fuse_sag", "hoist_vertex_computation", "make_program", "matmul_rows", "optimize", "trace_udf",
-    "validate_program", "SAGAModel", "gcn_model", "ggcn_model", "mpgcn_model", "run_train",
+    "validate_program", "vertex_form", "SAGAModel", "gcn_model", "ggcn_model", "mpgcn_model", "commnet_model", "run_train",
 ]
 
 
 def __getattr__(name):
     # the executor needs torch + CUDA; import it lazily so the host-side graph store
     # and front end stay importable on a CPU-only machine
-    if name in ("SAGAModel", "gcn_model", "ggcn_model", "mpgcn_model", "run_train"):
+    if name in ("SAGAModel", "gcn_model", "ggcn_model", "mpgcn_model", "commnet_model", "run_train"):
         from . import engine
 
         return getattr(engine, name)

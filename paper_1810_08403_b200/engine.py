@@ -67,11 +67,15 @@ class SAGAModel:
             if q.fused is None or q.fused.kind not in ("gcn", "pass", "ggcn", "max", "max_pool"):
                 raise ProgramError(f"layer ApplyEdge {p.apply_edge!r} has no fused kernel "
                                    f"({reports[-1].blocker or (q.fused and q.fused.kind)})")
-            wname = prog.vertex_kind(q)
-            if wname is None:
-                raise ProgramError("ApplyVertex must be ReLU(W accum) for the fused executor")
+            form = prog.vertex_form(q)
+            if form is None:
+                raise ProgramError("ApplyVertex must be ReLU(W accum) or ReLU(W_H vertex + "
+                                   "W_C accum) for the fused executor")
+            if form[0] == "hc" and q.fused.kind not in ("gcn", "pass"):
+                raise ProgramError("ReLU(W_H vertex + W_C accum) is lowered for sum gathers only")
             L = _Layer()
-            L.prog, L.kind, L.wname, L.F, L.O = q, q.fused.kind, wname, q.f_in, q.f_out
+            L.prog, L.kind, L.F, L.O = q, q.fused.kind, q.f_in, q.f_out
+            L.vform, L.wname = form[0], form[1:]
             L.gate = q.fused.params
             # accumulator width: the pooled width for MP-GCN, else the input width
             L.Aw = q.params[L.gate[0]][1] if L.kind == "max_pool" else q.f_in
@@ -93,6 +97,8 @@ class SAGAModel:
                 out += [(L.F, L.F), (L.F, L.F), (L.F, L.O)]
             elif L.kind == "max_pool":
                 out += [(L.F, L.Aw), (L.Aw,), (L.Aw, L.O)]
+            elif L.vform == "hc":
+                out += [(L.F, L.O), (L.F, L.O)]
             else:
                 out += [(L.F, L.O)]
         return out
@@ -144,6 +150,24 @@ class SAGAModel:
             F, O = L.F, L.O
             L.W = torch.zeros((L.Aw, O), dtype=torch.float32, device=dev)
             L.dW = torch.zeros_like(L.W)
+            if L.vform == "hc":
+                # CommNet: z = [h | accum] @ [W_H; W_C] as ONE GEMM over a per-vertex [h | a]
+                # buffer (16-B padded halves, zero pad rows in the stacked weights); its
+                # backward dz @ [W_H; W_C]^T writes [dh_direct | da] in one pass too.
+                ldF = _ld(F)
+                L.HA = torch.zeros((V, 2 * ldF), dtype=torch.float32, device=dev)
+                L.hin, L.a = L.HA[:, :F], L.HA[:, ldF:ldF + F]
+                L.W = torch.zeros((2 * ldF, O), dtype=torch.float32, device=dev)
+                L.dW = torch.zeros_like(L.W)
+                L.WH, L.WC = L.W[:F], L.W[ldF:ldF + F]
+                L.dWH, L.dWC = L.dW[:F], L.dW[ldF:ldF + F]
+                L.dHA = torch.zeros((V, 2 * ldF), dtype=torch.float32, device=dev)
+                L.da = L.dHA[:, ldF:ldF + F]
+                L.gin = L.HA
+                L.params, L.dparams = [L.WH, L.WC], [L.dWH, L.dWC]
+                L.z = _mat(V, O, dev)
+                L.dz = _mat(V, O, dev)
+                continue
             if L.kind in ("max", "max_pool"):
                 A = L.Aw
                 L.hin = None
@@ -184,6 +208,13 @@ class SAGAModel:
             L.a = _mat(V, F, dev)
             L.z = _mat(V, O, dev)
             L.dz = _mat(V, O, dev)
+        for n, L in enumerate(self.layers):
+            if getattr(L, "gin", None) is None:
+                L.gin = L.a  # the ApplyVertex GEMM operand
+            if L.vform == "hc" and n > 0:
+                # the layer below's dz IS the direct half of this layer's [dh | da] buffer:
+                # the CSR pass then accumulates the gathered half onto it in place
+                self.layers[n - 1].dz = L.dHA[:, : L.F]
         for n, L in enumerate(self.layers):
             if L.hin is None:
                 L.hin = _mat(V, L.F, dev) if n == 0 else None
@@ -283,16 +314,21 @@ class SAGAModel:
             chain = per_out[k[out_axis]]
             yield k, k == chain[0], k == chain[-1]
 
-    def _bwd_propagate_gcn(self, L, out, mask, stream=None):
-        """dH[v] = sum_{out(v)} w_e dA[u] over CSR chunks, j ascending; ReLU mask on the last."""
+    def _bwd_propagate_gcn(self, L, out, mask, stream=None, onto=False):
+        """dH[v] = sum_{out(v)} w_e dA[u] over CSR chunks, j ascending; ReLU mask on the last.
+        ``onto``: continue from the value already in ``out`` (CommNet's direct W_H term)."""
         g, P = self.grid, self.grid.P
         mode = _lib.PROP_GCN if L.kind == "gcn" else _lib.PROP_PASS
         for i in range(P):
             if not any((i, j) in g.csr for j in range(P)):
-                self._rows(out, i).zero_()
+                if onto:
+                    o = self._rows(out, i)
+                    K.ewise(8, o, self._rows(mask, i), o, stream)
+                else:
+                    self._rows(out, i).zero_()
         for (i, j), first, last in self._chunk_order(list(g.csr), 0):
             K.propagate(g.csr[(i, j)], mode, self._rows(L.da, j), self._rows(out, i), L.F,
-                        mask=self._rows(mask, i) if last else None, accumulate=not first,
+                        mask=self._rows(mask, i) if last else None, accumulate=onto or not first,
                         ws=self.ws, stream=stream)
 
     def _bwd_propagate_ggcn(self, L, stream=None):
@@ -379,7 +415,7 @@ class SAGAModel:
             else:
                 self._fwd_propagate(L, stream)
             self._mark(f"L{n}.fwd.propagate")
-            self._gemm(L.a, L.W, L.z, relu_out=L.hout)  # ApplyVertex: z = a W, h' = relu(z)
+            self._gemm(L.gin, L.W, L.z, relu_out=L.hout)  # ApplyVertex: z = a W, h' = relu(z)
             self._mark(f"L{n}.fwd.apply_vertex")
         return self.layers[-1].z
 
@@ -391,7 +427,7 @@ class SAGAModel:
         self._mark("loss")
         for n in range(len(self.layers) - 1, -1, -1):
             L = self.layers[n]
-            self._gemm(L.a, L.dz, L.dW, trans_a=True)           # dW = a^T dz
+            self._gemm(L.gin, L.dz, L.dW, trans_a=True)         # dW = a^T dz
             below = self.layers[n - 1] if n > 0 else None
             if L.kind in ("max", "max_pool"):
                 self._gemm(L.dz, L.W, L.da, trans_b=True)       # dA = dz W^T
@@ -427,6 +463,14 @@ class SAGAModel:
                     self._ewise(0, t1, t2, t1, stream)          # + P part (tape order)
                     self._ewise(8, t1, below.z, below.dz, stream)  # relu bwd of the layer below
                 self._mark(f"L{n}.bwd.hoist_gemm")
+            elif L.vform == "hc":
+                if below is not None:  # [dh_direct | da] = dz [W_H; W_C]^T, then += gathered da
+                    self._gemm(L.dz, L.W, L.dHA, trans_b=True)
+                    self._mark(f"L{n}.bwd.apply_vertex")
+                    self._bwd_propagate_gcn(L, below.dz, below.z, stream, onto=True)
+                    self._mark(f"L{n}.bwd.propagate")
+                else:
+                    self._mark(f"L{n}.bwd.apply_vertex")
             else:
                 if below is not None:
                     self._gemm(L.dz, L.W, L.da, trans_b=True)   # dA = dz W^T
@@ -506,6 +550,11 @@ def ggcn_model(grid, dims, **kw):
     return SAGAModel([prog.build_ggcn(a, b) for a, b in zip(dims, dims[1:])], grid, **kw)
 
 
+def commnet_model(grid, dims, **kw):
+    """CommNet: params per layer [W_H, W_C]."""
+    return SAGAModel([prog.build_commnet(a, b) for a, b in zip(dims, dims[1:])], grid, **kw)
+
+
 def mpgcn_model(grid, dims, pool=None, **kw):
     """MP-GCN: per layer W_pool [F, pool], b [pool], W [pool, O].
     ``pool`` defaults to each layer's input width."""
@@ -518,7 +567,7 @@ def mpgcn_model(grid, dims, pool=None, **kw):
 def run_train(config):
     """SPEC.md:595-603 run_train on a synthetic graph; returns a metrics dict.
 
-    config keys (SPEC.md:622 subset + synthetic graph): model ('gcn'|'ggcn'|'mpgcn'),
+    config keys (SPEC.md:622 subset + synthetic graph): model ('gcn'|'ggcn'|'mpgcn'|'commnet'),
     graph ('rmat'|'uniform'), V, E, features F, hidden, classes, layers, epochs,
     lr, seed, interval_size."""
     from . import graph as G
@@ -529,7 +578,8 @@ def run_train(config):
     if bad:
         raise ConfigError(f"unknown config keys {sorted(bad)}")
     model = config.get("model", "gcn")
-    builders = {"gcn": gcn_model, "ggcn": ggcn_model, "mpgcn": mpgcn_model}
+    builders = {"gcn": gcn_model, "ggcn": ggcn_model, "mpgcn": mpgcn_model,
+                "commnet": commnet_model}
     if model not in builders:
         raise ConfigError(f"unknown model '{model}'; valid: {', '.join(builders)}")
     V, E = int(config["V"]), int(config["E"])

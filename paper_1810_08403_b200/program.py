@@ -378,6 +378,30 @@ def vertex_kind(p):
     return None
 
 
+def vertex_form(p):
+    """The ApplyVertex forms the executor lowers onto GEMMs:
+    ('w', W)         ReLU(W (x) accum)                    GCN / G-GCN / MP-GCN (PAPER.md:563)
+    ('hc', W_H, W_C) ReLU(W_H (x) vertex + W_C (x) accum) CommNet (PAPER.md:529-541)
+    or None."""
+    W = vertex_kind(p)
+    if W is not None:
+        return ("w", W)
+    v = p.apply_vertex
+    if v.op == "relu" and v.args[0].op == "add":
+        def mm(t, name):
+            if t.op == "matmul" and _is(t.args[0], "input", name) and t.args[1].op == "param":
+                return t.args[1].name
+            return None
+
+        a, b = v.args[0].args
+        wh, wc = mm(a, "vertex"), mm(b, "accum")
+        if wh is None or wc is None:
+            wh, wc = mm(b, "vertex"), mm(a, "accum")
+        if wh is not None and wc is not None:
+            return ("hc", wh, wc)
+    return None
+
+
 # ------------------------------------------------------------------ model zoo (SPEC.md:521-550)
 def build_gcn(f_in, f_out):
     """GCN: ApplyEdge = src x edge.data, sum, ReLU(W accum)."""
@@ -399,9 +423,13 @@ def build_ggcn(f_in, f_out):
 
 
 def build_commnet(f_in, f_out):
-    """CommNet-style passthrough edge with ReLU(W accum) vertex."""
-    return make_program(lambda e, p: e.src, lambda v, acc, p: relu(matmul(acc, p.W)), "sum",
-                        {"W": (f_in, f_out)}, f_in, f_out)
+    """CommNet: ApplyEdge = edge.src (no edge-parallel compute), sum,
+    ApplyVertex = ReLU(W_H (x) vertex + W_C (x) accum); params p = [W_H, W_C]."""
+    if f_in < 1 or f_out < 1:
+        raise ProgramError("invalid dimensions")
+    return make_program(lambda e, p: e.src,
+                        lambda v, acc, p: relu(matmul(v, p.W_H) + matmul(acc, p.W_C)), "sum",
+                        {"W_H": (f_in, f_out), "W_C": (f_in, f_out)}, f_in, f_out)
 
 
 def build_mpgcn(f_in, f_pool, f_out):

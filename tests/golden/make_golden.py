@@ -120,6 +120,26 @@ def run_mpgcn(X, layers, labels, src, dst, V, dtype, hoisted=True):
     return acts, loss.to_numpy(), [tuple(grads[m.tid] for m in L) for L in lt]
 
 
+def run_commnet(X, layers, labels, src, dst, V, dtype):
+    """CommNet: acc = edge.src, Gather(sum), ReLU(W_H vertex + W_C accum)."""
+    tape = T.Tape()
+    lt = [tuple(tens(m, dtype) for m in L) for L in layers]
+    for L in lt:
+        for m in L:
+            tape.watch(m)
+    h = tens(X, dtype)
+    acts = []
+    for (WH, WC) in lt:
+        es = T.take_rows(h, src, tape)                    # Scatter; ApplyEdge = passthrough
+        accum = T.segment_sum(es, dst, V, tape)           # Gather(sum)
+        z = T.add(T.matmul(h, WH, tape), T.matmul(accum, WC, tape), tape)
+        h = T.relu(z, tape)
+        acts.append((accum.to_numpy(), z.to_numpy(), h.to_numpy()))
+    loss = T.softmax_cross_entropy(h, labels, tape)
+    grads = T.backward(tape, Seed(dtype))
+    return acts, loss.to_numpy(), [tuple(grads[m.tid] for m in L) for L in lt]
+
+
 CASES = [
     # name, V, E, F, H, C, generator, seed
     ("uniform_v40_e160", 40, 160, 12, 8, 3, "uniform", 11),
@@ -179,6 +199,16 @@ def make_case(name, V, E, F, H, C, gen, seed):
                     out[f"mpgcn{hp}_{tag}_dL{l}_{k}"] = gL[l][k]
                 out[f"mpgcn{hp}_{tag}_a{l}"], out[f"mpgcn{hp}_{tag}_z{l}"], _ = acts[l]
             out[f"mpgcn{hp}_{tag}_loss"] = loss
+        # CommNet: F -> H -> C, params [W_H, W_C] per layer
+        Lc = rng.glorot([(F, H), (F, H), (H, C), (H, C)], seed=2, dtype=dt)
+        layers = [tuple(Lc[0:2]), tuple(Lc[2:4])]
+        acts, loss, gL = run_commnet(X, layers, lab, s, d, V, dt)
+        for l, L in enumerate(layers):
+            for k, m in enumerate(L):
+                out[f"commnet_{tag}_L{l}_{k}"] = m
+                out[f"commnet_{tag}_dL{l}_{k}"] = gL[l][k]
+            out[f"commnet_{tag}_a{l}"], out[f"commnet_{tag}_z{l}"], _ = acts[l]
+        out[f"commnet_{tag}_loss"] = loss
     np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
     print("wrote", name)
 

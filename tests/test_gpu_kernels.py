@@ -545,3 +545,56 @@ def test_mpgcn_trains(sg):
     out = sg.run_train({"model": "mpgcn", "graph": "rmat", "V": 1000, "E": 8000, "features": 32,
                         "classes": 4, "epochs": 5, "lr": 1.0, "interval_size": 300})
     assert out["loss"][-1] < out["loss"][0]
+
+
+# ---------------------------------------------------------------- CommNet (passthrough, W_H/W_C)
+@pytest.mark.parametrize("case", GOLDEN_CASES)
+def test_commnet_model_vs_reference_golden(sg, case):
+    g = load_golden(case)
+    V = int(g["V"])
+    graph = sg.Graph(V, g["src_in"], g["dst_in"])
+    grid = sg.ChunkGrid(graph, V, gcn_weights=False)
+    weights = [g[f"commnet_f32_L{l}_{k}"] for l in range(2) for k in range(2)]
+    m = sg.commnet_model(grid, [int(g["F"]), int(g["H"]), int(g["C"])], weights=weights)
+    m.load_features(torch.from_numpy(g["gcn_f32_X"]))
+    m.load_labels(g["labels"])
+    m.forward()
+    m.backward()
+    m.check_status()
+    assert np.array_equal(m.layers[0].a.cpu().numpy(), g["commnet_f32_a0"])  # PASS gather bitwise
+    ref_loss = float(np.ravel(g["commnet_f64_loss"])[0])
+    assert abs(m.loss.item() - ref_loss) <= 1e-4 * ref_loss
+    got = m.grads()
+    for l in range(2):
+        assert_close(m.layers[l].z.cpu().numpy(), g[f"commnet_f64_z{l}"], 1e-4, f"z{l}")
+        for k in range(2):
+            assert_close(got[2 * l + k], g[f"commnet_f64_dL{l}_{k}"], 1e-4, f"L{l}.{k}")
+
+
+@pytest.mark.parametrize("P,T", [(1, 4096), (3, 64)])
+def test_commnet_epoch_vs_oracle(sg, P, T):
+    V, E, F, H, C = 4000, 30000, 96, 32, 5
+    s, d = _graph("rmat", V, E, 4)
+    graph = sg.Graph(V, s, d)
+    size = -(-V // P)
+    grid = sg.ChunkGrid(graph, size, split_edges=T, gcn_weights=False)
+    m = sg.commnet_model(grid, [F, H, C])
+    X = rng.features(V, F, seed=1)
+    lab = rng.labels(V, C)
+    m.load_features(torch.from_numpy(X))
+    m.load_labels(lab)
+    W = m.weights()
+    m.forward()
+    m.backward()
+    m.check_status()
+    part = og.partition_2d(s, d, V, size)
+    layers = [tuple(x.astype(np.float64) for x in W[2 * l: 2 * l + 2]) for l in range(2)]
+    ref = saga.commnet_epoch(part, X.astype(np.float64), layers, lab, T=T)
+    rl = float(np.ravel(ref["loss"])[0])
+    assert abs(m.loss.item() - rl) <= 1e-4 * rl
+    for k, (a, b) in enumerate(zip(m.grads(), [x for L in ref["grads"] for x in L])):
+        assert_close(a, b, 1e-4, f"grad {k}")
+    # unnormalised sums: a small step (SPEC.md:601 uses lr 0.01)
+    out = sg.run_train({"model": "commnet", "graph": "uniform", "V": 1000, "E": 8000, "features": 32,
+                        "classes": 4, "epochs": 5, "lr": 0.01})
+    assert out["loss"][-1] < out["loss"][0]

@@ -149,3 +149,20 @@ def test_mpgcn_oracle_2d_grid_matches_one_chunk(case):
         assert np.array_equal(r1["cache"][l][2], r3["cache"][l][2])  # max values are order-free
         for k in range(3):
             assert np.abs(r1["grads"][l][k] - r3["grads"][l][k]).max() <= 1e-12
+
+
+@pytest.mark.parametrize("case", GOLDEN_CASES)
+@pytest.mark.parametrize("tag", ["f64", "f32"])
+def test_commnet_oracle_bitwise(case, tag):
+    """CommNet (passthrough edge, ReLU(W_H h + W_C accum)) oracle ==
+    the real reference, bit for bit."""
+    g = load_golden(case)
+    part = _grid(g)
+    layers = [tuple(g[f"commnet_{tag}_L{l}_{k}"] for k in range(2)) for l in range(2)]
+    r = saga.commnet_epoch(part, g[f"gcn_{tag}_X"], layers, g["labels"])
+    assert np.array_equal(np.ravel(r["loss"]), np.ravel(g[f"commnet_{tag}_loss"]))
+    for l in range(2):
+        assert np.array_equal(r["a"][l], g[f"commnet_{tag}_a{l}"])
+        assert np.array_equal(r["z"][l], g[f"commnet_{tag}_z{l}"])
+        for k in range(2):
+            assert np.array_equal(r["grads"][l][k], g[f"commnet_{tag}_dL{l}_{k}"]), (l, k)

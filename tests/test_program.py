@@ -69,3 +69,15 @@ def test_invalid_accumulator_and_dims():
 def test_matmul_shape_error():
     with pytest.raises(sg.ProgramError):
         sg.make_program(lambda e, p: e.src @ p.W, lambda v, acc, p: acc, "sum", {"W": (5, 2)}, 3, 2)
+
+
+def test_vertex_forms():
+    assert P.vertex_form(sg.build_gcn(4, 3)) == ("w", "W")
+    assert P.vertex_form(sg.build_commnet(4, 3)) == ("hc", "W_H", "W_C")
+    swapped = sg.make_program(lambda e, p: e.src,
+                              lambda v, acc, p: P.relu(acc @ p.B + v @ p.A), "sum",
+                              {"A": (4, 3), "B": (4, 3)}, 4, 3)
+    assert P.vertex_form(swapped) == ("hc", "A", "B")
+    odd = sg.make_program(lambda e, p: e.src, lambda v, acc, p: P.sigmoid(acc @ p.W), "sum",
+                          {"W": (4, 3)}, 4, 3)
+    assert P.vertex_form(odd) is None
