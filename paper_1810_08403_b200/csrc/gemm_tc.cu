@@ -51,7 +51,7 @@ struct TcArgs {
   int64_t M, N, K;
   int kb_per_split, n_kb;
   int epilogue;
-  int vec_a, vec_b;
+  int vec_a, vec_b, vec_c, vec_d;
 };
 
 __device__ __forceinline__ void split_tf32(float4 x, float4& hi, float4& lo) {
@@ -101,55 +101,79 @@ __device__ __forceinline__ void store_split(uint32_t hi_base, uint32_t lo_base, 
   sts128(lo_base + off, lo);
 }
 
+// One operand tile (R rows of the operand x 32 k) held in registers between its global
+// load and its split/store, so the next stage's loads are in flight while this stage is
+// written to shared memory (register double buffering in the loader loop).
 template <bool MN_MAJOR, int R>
-__device__ __forceinline__ void load_tile(const float* X, int64_t ld, int64_t mn0, int64_t k0,
-                                          int64_t MNmax, int64_t Kmax, bool vec, uint32_t hi_base,
-                                          uint32_t lo_base, int t) {
-  if constexpr (!MN_MAJOR) {
-    // rows contiguous along k: one 16-B chunk per LDG.128 / STS.128
-    constexpr int PER = R * BK / 4 / kLoadThreads;
-    float4 v[PER];
+struct TileRegs {
+  // K-major: one 16-B chunk (row, 4 k) per slot; MN-major: one 4x4 (4 k x 4 rows) block
+  static constexpr int PER_K = R * BK / 4 / kLoadThreads;
+  static constexpr int BLOCKS = (R / 4) * (BK / 4);
+  static constexpr int PER_MN = (BLOCKS + kLoadThreads - 1) / kLoadThreads;
+  static constexpr int N4 = MN_MAJOR ? PER_MN * 4 : PER_K;
+  float4 v[N4];
+
+  // MN-major block -> (mb, kb).  Thread bits: b0 = mb & 1 (two threads cover a full 32-B
+  // sector of a k-row), b1-b2 = kb & 3, rest = mb >> 1 | kb >> 2.  For a fixed q the 32
+  // swizzled STS.128 of a warp then hit 8 distinct 16-B bank groups (4 wavefronts, no
+  // conflicts): chunk = kb ^ (row & 7) with row & 7 = (mb & 1) * 4 + q.
+  __device__ __forceinline__ static void mn_coords(int idx, int& mb, int& kb) {
+    const int rest = idx >> 3;
+    mb = (rest % (R / 8)) * 2 + (idx & 1);
+    kb = ((idx >> 1) & 3) + 4 * (rest / (R / 8));
+  }
+
+  __device__ __forceinline__ void load(const float* X, int64_t ld, int64_t mn0, int64_t k0,
+                                       int64_t MNmax, int64_t Kmax, bool vec, int t) {
+    if constexpr (!MN_MAJOR) {
 #pragma unroll
-    for (int i = 0; i < PER; ++i) {
-      const int idx = t + kLoadThreads * i;
-      v[i] = ld4(X, ld, mn0 + idx / 8, k0 + (idx % 8) * 4, MNmax, Kmax, vec);
-    }
+      for (int i = 0; i < PER_K; ++i) {
+        const int idx = t + kLoadThreads * i;
+        v[i] = ld4(X, ld, mn0 + idx / 8, k0 + (idx % 8) * 4, MNmax, Kmax, vec);
+      }
+    } else {
 #pragma unroll
-    for (int i = 0; i < PER; ++i) {
-      const int idx = t + kLoadThreads * i;
-      store_split(hi_base, lo_base, kmajor_off(idx / 8, idx % 8), v[i]);
-    }
-  } else {
-    // memory contiguous along the operand rows (X[k, m]): load 4x4 blocks (4 k-rows of
-    // 4 consecutive m), transpose in registers and store K-major -- the shared-memory
-    // operand is always K-major, so no operand is ever transposed in HBM.
-    constexpr int BLOCKS = (R / 4) * (BK / 4);
-    constexpr int PER = (BLOCKS + kLoadThreads - 1) / kLoadThreads;
-    float4 v[PER][4];
+      for (int i = 0; i < PER_MN; ++i) {
+        const int idx = t + kLoadThreads * i;
+        if (BLOCKS % kLoadThreads != 0 && idx >= BLOCKS) continue;
+        int mb, kb;
+        mn_coords(idx, mb, kb);
 #pragma unroll
-    for (int i = 0; i < PER; ++i) {
-      const int idx = t + kLoadThreads * i;
-      if (BLOCKS % kLoadThreads != 0 && idx >= BLOCKS) continue;
-      const int mb = idx % (R / 4), kb = idx / (R / 4);
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int64_t k = k0 + kb * 4 + q;
-        v[i][q] = k < Kmax ? ld4(X, ld, k, mn0 + mb * 4, Kmax, MNmax, vec)
-                           : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int q = 0; q < 4; ++q) {
+          const int64_t k = k0 + kb * 4 + q;
+          v[i * 4 + q] = k < Kmax ? ld4(X, ld, k, mn0 + mb * 4, Kmax, MNmax, vec)
+                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
       }
     }
+  }
+
+  // split hi/lo and store in the K-major SWIZZLE_128B canonical layout (operands stored
+  // MN-contiguous in HBM are transposed 4x4 in registers: the shared-memory operand is
+  // always K-major, no operand is ever transposed in HBM)
+  __device__ __forceinline__ void store(uint32_t hi_base, uint32_t lo_base, int t) const {
+    if constexpr (!MN_MAJOR) {
 #pragma unroll
-    for (int i = 0; i < PER; ++i) {
-      const int idx = t + kLoadThreads * i;
-      if (BLOCKS % kLoadThreads != 0 && idx >= BLOCKS) continue;
-      const int mb = idx % (R / 4), kb = idx / (R / 4);
-      store_split(hi_base, lo_base, kmajor_off(mb * 4 + 0, kb), make_float4(v[i][0].x, v[i][1].x, v[i][2].x, v[i][3].x));
-      store_split(hi_base, lo_base, kmajor_off(mb * 4 + 1, kb), make_float4(v[i][0].y, v[i][1].y, v[i][2].y, v[i][3].y));
-      store_split(hi_base, lo_base, kmajor_off(mb * 4 + 2, kb), make_float4(v[i][0].z, v[i][1].z, v[i][2].z, v[i][3].z));
-      store_split(hi_base, lo_base, kmajor_off(mb * 4 + 3, kb), make_float4(v[i][0].w, v[i][1].w, v[i][2].w, v[i][3].w));
+      for (int i = 0; i < PER_K; ++i) {
+        const int idx = t + kLoadThreads * i;
+        store_split(hi_base, lo_base, kmajor_off(idx / 8, idx % 8), v[i]);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < PER_MN; ++i) {
+        const int idx = t + kLoadThreads * i;
+        if (BLOCKS % kLoadThreads != 0 && idx >= BLOCKS) continue;
+        int mb, kb;
+        mn_coords(idx, mb, kb);
+        const float4* b = v + i * 4;
+        store_split(hi_base, lo_base, kmajor_off(mb * 4 + 0, kb), make_float4(b[0].x, b[1].x, b[2].x, b[3].x));
+        store_split(hi_base, lo_base, kmajor_off(mb * 4 + 1, kb), make_float4(b[0].y, b[1].y, b[2].y, b[3].y));
+        store_split(hi_base, lo_base, kmajor_off(mb * 4 + 2, kb), make_float4(b[0].z, b[1].z, b[2].z, b[3].z));
+        store_split(hi_base, lo_base, kmajor_off(mb * 4 + 3, kb), make_float4(b[0].w, b[1].w, b[2].w, b[3].w));
+      }
     }
   }
-}
+};
 
 // one tf32 UMMA consumes K = 8 = 32 B of each K-major row: advance the start address
 __device__ __forceinline__ uint64_t tile_desc(uint32_t base, int kk) {
@@ -190,19 +214,34 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tf32x3_kernel(const TcArgs p
   const uint32_t tmem = *tmem_slot;
 
   if (warp < kMmaWarp) {
-    // ---------------- loaders: LDG -> split hi/lo -> swizzled STS
+    // ---------------- loaders: LDG -> split hi/lo -> swizzled STS, one stage ahead
     const int t = threadIdx.x;
-    for (int i = 0; i < nkb; ++i) {
-      const int s = i % C::STAGES;
-      const uint32_t use = i / C::STAGES;
-      sm100::mbar_wait(empty + s, (use & 1) ^ 1);
-      const uint32_t st = base + s * C::STAGE;
-      const int64_t k0 = (int64_t)(kb0 + i) * BK;
-      load_tile<A_MN, BM>(p.A, p.lda, m0, k0, p.M, p.K, p.vec_a, st, st + C::A_TILE, t);
-      load_tile<B_MN, BN>(p.B, p.ldb, n0, k0, p.N, p.K, p.vec_b, st + 2 * C::A_TILE,
-                          st + 2 * C::A_TILE + C::B_TILE, t);
-      sm100::fence_proxy_async_smem();
-      sm100::mbar_arrive(full + s);
+    TileRegs<A_MN, BM> ra[2];
+    TileRegs<B_MN, BN> rb[2];
+    if (nkb > 0) {
+      ra[0].load(p.A, p.lda, m0, (int64_t)kb0 * BK, p.M, p.K, p.vec_a, t);
+      rb[0].load(p.B, p.ldb, n0, (int64_t)kb0 * BK, p.N, p.K, p.vec_b, t);
+    }
+#pragma unroll 1
+    for (int i = 0; i < nkb; i += 2) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {  // static register-set index (no dynamic indexing)
+        const int ii = i + h;
+        if (ii >= nkb) break;
+        if (ii + 1 < nkb) {
+          const int64_t kn = (int64_t)(kb0 + ii + 1) * BK;
+          ra[h ^ 1].load(p.A, p.lda, m0, kn, p.M, p.K, p.vec_a, t);
+          rb[h ^ 1].load(p.B, p.ldb, n0, kn, p.N, p.K, p.vec_b, t);
+        }
+        const int s = ii % C::STAGES;
+        const uint32_t use = ii / C::STAGES;
+        sm100::mbar_wait(empty + s, (use & 1) ^ 1);
+        const uint32_t st = base + s * C::STAGE;
+        ra[h].store(st, st + C::A_TILE, t);
+        rb[h].store(st + 2 * C::A_TILE, st + 2 * C::A_TILE + C::B_TILE, t);
+        sm100::fence_proxy_async_smem();
+        sm100::mbar_arrive(full + s);
+      }
     }
     // ---------------- epilogue: TMEM -> registers -> global
     sm100::mbar_wait(done, 0);
@@ -210,20 +249,34 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tf32x3_kernel(const TcArgs p
     // warp w reads TMEM lane quarter w % 4 (its rows) and column half w / 4
     const int quarter = warp & 3, half = warp >> 2;
     const int64_t row = m0 + quarter * 32 + lane;
+    // each thread owns 16 consecutive columns of one row: 4 x 16-B stores (full sectors)
+    float* dst = p.partial ? p.partial + (int64_t)blockIdx.z * p.M * p.N : p.C;
+    const int64_t ldo = p.partial ? p.N : p.ldc;
+    const bool relu = !p.partial && p.epilogue == SG_EPI_RELU_DUAL;
+    const bool vec_o = p.partial ? (p.N % 4 == 0) : p.vec_c;
 #pragma unroll 1
     for (int c0 = half * (BN / 2); c0 < (half + 1) * (BN / 2); c0 += 16) {
       float v[16];
       sm100::tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + c0, v);
       if (row < p.M) {
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
+        for (int j = 0; j < 16; j += 4) {
           const int64_t col = n0 + c0 + j;
-          if (col < p.N) {
-            if (p.partial) {
-              p.partial[((int64_t)blockIdx.z * p.M + row) * p.N + col] = v[j];
+          if (vec_o && col + 3 < p.N) {
+            *reinterpret_cast<float4*>(dst + row * ldo + col) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+          } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              if (col + q < p.N) dst[row * ldo + col + q] = v[j + q];
+          }
+          if (relu) {
+            if (p.vec_d && col + 3 < p.N) {
+              *reinterpret_cast<float4*>(p.D + row * p.ldd + col) =
+                  make_float4(fmaxf(v[j], 0.f), fmaxf(v[j + 1], 0.f), fmaxf(v[j + 2], 0.f), fmaxf(v[j + 3], 0.f));
             } else {
-              p.C[row * p.ldc + col] = v[j];
-              if (p.epilogue == SG_EPI_RELU_DUAL) p.D[row * p.ldd + col] = fmaxf(v[j], 0.f);
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                if (col + q < p.N) p.D[row * p.ldd + col + q] = fmaxf(v[j + q], 0.f);
             }
           }
         }
@@ -330,6 +383,8 @@ int sg_gemm_tc(int prec, int trans_a, int trans_b, int64_t M, int64_t N, int64_t
   p.epilogue = epilogue;
   p.vec_a = (lda % 4 == 0) && ((uintptr_t)A % 16 == 0);
   p.vec_b = (ldb % 4 == 0) && ((uintptr_t)B % 16 == 0);
+  p.vec_c = (ldc % 4 == 0) && ((uintptr_t)C % 16 == 0);
+  p.vec_d = D != nullptr && (ldd % 4 == 0) && ((uintptr_t)D % 16 == 0);
   p.n_kb = (int)((K + BK - 1) / BK);
   const int splits = tc_splits(M, N, K);
   p.kb_per_split = (p.n_kb + splits - 1) / splits;
