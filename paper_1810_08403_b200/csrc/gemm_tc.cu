@@ -359,6 +359,10 @@ cudaError_t dispatch_major(bool a_mn, bool b_mn, const TcArgs& p, dim3 grid, cud
 
 }  // namespace
 
+int sg_gemm_tma_try(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,
+                    const float* B, int64_t ldb, float* C, int64_t ldc, int epilogue, float* D, int64_t ldd,
+                    float* partial, int kb_per_split, int n_kb, int gz, cudaStream_t st, cudaError_t* err);
+
 int64_t sg_gemm_tc_workspace_bytes(int64_t M, int64_t N, int64_t K, int prec) {
   (void)prec;
   const int s = tc_splits(M, N, K);
@@ -397,8 +401,12 @@ int sg_gemm_tc(int prec, int trans_a, int trans_b, int64_t M, int64_t N, int64_t
   }
   const int BN = pick_bn(N);
   dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM), (unsigned)gz);
-  cudaError_t e = BN == 64 ? dispatch_major<64>(a_mn, b_mn, p, grid, st)
-                           : dispatch_major<128>(a_mn, b_mn, p, grid, st);
+  cudaError_t e = cudaSuccess;
+  // TMA-fed kernel (gemm_tma.cu) when the operands meet the tensor-map constraints;
+  // otherwise the LDG-fed kernel above (any alignment)
+  if (!sg_gemm_tma_try(trans_a, trans_b, M, N, K, A, lda, B, ldb, C, ldc, epilogue, D, ldd, p.partial,
+                       p.kb_per_split, p.n_kb, gz, st, &e))
+    e = BN == 64 ? dispatch_major<64>(a_mn, b_mn, p, grid, st) : dispatch_major<128>(a_mn, b_mn, p, grid, st);
   if (e != cudaSuccess) SG_FAIL(SG_ECUDA, "tcgen05 gemm launch: %s", cudaGetErrorString(e));
   if (gz > 1) {
     const int64_t total = M * N;

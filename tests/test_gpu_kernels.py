@@ -187,17 +187,21 @@ def test_gemm_f32(sg, M, N, K, ta, tb):
                                          (3000, 41, 128, 0, 1), (7, 5, 3, 0, 0), (130, 3, 1, 1, 1),
                                          (300, 200, 77, 1, 1), (4096, 64, 604, 0, 0),
                                          (128, 41, 40000, 1, 0)])
-def test_gemm_tcgen05_tf32x3(sg, M, N, K, ta, tb):
-    """tcgen05/TMEM 3xTF32 GEMM (all four operand majors, split-K) vs fp64."""
+@pytest.mark.parametrize("aligned", [False, True])
+def test_gemm_tcgen05_tf32x3(sg, M, N, K, ta, tb, aligned):
+    """tcgen05/TMEM 3xTF32 GEMM (all four operand majors, split-K) vs fp64.  16-B aligned rows
+    take the TMA-fed kernel (K-major SW128 / MN-major SW128_BASE32B tiles), others the
+    LDG-fed one."""
     from paper_1810_08403_b200 import _lib
     from paper_1810_08403_b200 import kernels as Kn
 
     r = np.random.default_rng(M * 7 + N + K)
     A = r.uniform(-1, 1, (K, M) if ta else (M, K)).astype(np.float32)
     B = r.uniform(-1, 1, (N, K) if tb else (K, N)).astype(np.float32)
-    C = torch.empty((M, N), device="cuda")
-    D = torch.empty((M, N), device="cuda")
-    Kn.gemm(_dev(A), _dev(B), C, trans_a=bool(ta), trans_b=bool(tb), relu_out=D,
+    mk = _padded if aligned else _dev
+    C = mk(np.zeros((M, N), np.float32))
+    D = mk(np.zeros((M, N), np.float32))
+    Kn.gemm(mk(A), mk(B), C, trans_a=bool(ta), trans_b=bool(tb), relu_out=D,
             prec=_lib.GEMM_TF32X3)
     A64 = (A.T if ta else A).astype(np.float64)
     B64 = (B.T if tb else B).astype(np.float64)

@@ -36,13 +36,16 @@ def main():
     dev = torch.device("cuda")
     ws = K.Workspace(dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def pad(r, c):
+        return (torch.rand((r, (c + 3) // 4 * 4), device=dev) - 0.5)[:, :c]
     for name, (M, N, Kd, ta, tb, relu) in SHAPES.items():
         if a.only and a.only not in name:
             continue
-        A = torch.rand((Kd, M) if ta else (M, Kd), device=dev) - 0.5
-        B = torch.rand((N, Kd) if tb else (Kd, N), device=dev) - 0.5
-        Cm = torch.empty((M, N), device=dev)
-        D = torch.empty((M, N), device=dev) if relu else None
+        A = pad(*((Kd, M) if ta else (M, Kd)))  # 16-B aligned rows, as the engine allocates
+        B = pad(*((N, Kd) if tb else (Kd, N)))
+        Cm = pad(M, N)
+        D = pad(M, N) if relu else None
         for _ in range(3):
             K.gemm(A, B, Cm, trans_a=bool(ta), trans_b=bool(tb), relu_out=D, prec=prec, ws=ws)
         ts = []
