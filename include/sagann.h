@@ -124,6 +124,21 @@ int sg_propagate(int mode, int dtype, const int64_t* ptr, const int32_t* idx, co
                  int64_t ld1, const void* mask, int64_t ldm, int64_t F, int accumulate,
                  void* workspace, int64_t workspace_bytes, void* stream);
 
+/* sg_propagate with a hub-row cache (GCN / PASS modes, rows wider than 16 vectors).
+ * The n_hub most referenced gathered rows (hub_rows[0..n_hub), int32 row ids of G) are
+ * copied into each block's shared memory once; idx must be the hub-encoded index in
+ * which an edge to hub slot k carries (int32)(k | 0x80000000) instead of its row id.
+ * Results are bitwise identical to sg_propagate over the plain index.
+ * n_hub <= sg_propagate_hub_capacity(F, dtype); n_hub = 0 is plain sg_propagate. */
+int64_t sg_propagate_hub_capacity(int64_t F, int dtype);
+int sg_propagate_hub(int mode, int dtype, const int64_t* ptr, const int32_t* idx, const float* w,
+                     int64_t n_rows, const sg_item* items, int64_t n_items, const sg_split* splits,
+                     int64_t n_splits, int64_t n_slots, const void* G, int64_t ldg, int64_t g_off,
+                     const void* R, int64_t ldr, int64_t r_off, void* out0, int64_t ld0, void* out1,
+                     int64_t ld1, const void* mask, int64_t ldm, int64_t F, int accumulate,
+                     const int32_t* hub_rows, int64_t n_hub, void* workspace, int64_t workspace_bytes,
+                     void* stream);
+
 /* Gather(max) with argmax (segment_max, tensor.py:453-484):
  * out[r] = max over rows X[idx_e] (strict >, lowest edge position wins), -inf
  * init, empty rows get empty_fill and argmax -1; argmax holds idx_e (int64). */

@@ -52,6 +52,10 @@ _SIGS = {
     "sg_propagate": (_i32, [_i32, _i32, _p, _p, _p, _i64, _p, _i64, _p, _i64, _i64,
                             _p, _i64, _i64, _p, _i64, _i64, _p, _i64, _p, _i64, _p, _i64,
                             _i64, _i32, _p, _i64, _p]),
+    "sg_propagate_hub_capacity": (_i64, [_i64, _i32]),
+    "sg_propagate_hub": (_i32, [_i32, _i32, _p, _p, _p, _i64, _p, _i64, _p, _i64, _i64,
+                                _p, _i64, _i64, _p, _i64, _i64, _p, _i64, _p, _i64, _p, _i64,
+                                _i64, _i32, _p, _i64, _p, _i64, _p]),
     "sg_segment_max": (_i32, [_i32, _p, _p, _i64, _p, _i64, _p, _i64, _p, _i64, _i64, _f32, _p]),
     "sg_segment_max_bwd": (_i32, [_i32, _p, _i64, _p, _i64, _i64, _p, _i64, _i64, _p]),
     "sg_max_gather": (_i32, [_p, _p, _i64, _p, _i64, _p, _i64, _p, _i64, _i64, _f32, _i64, _i32,

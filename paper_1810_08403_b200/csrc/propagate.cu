@@ -29,6 +29,20 @@ namespace {
 using sg::VecIO;
 
 constexpr int kWarpsPerBlock = 8;
+// shared memory given to the hub-row cache (SG_HUB_KB overrides; the rest of the 256 KB
+// L1/shared array stays L1 for the in-flight row loads)
+// rows of >= 4 vectors per lane (F > 384 fp32): the cache measured slower on 1-vector
+// rows (F = 128: 3.6 -> 5.0 ms, the hub branch breaks the 8-deep load batching)
+constexpr int kHubMinVpl = 4;
+
+int64_t hub_smem_bytes() {
+  static int64_t v = -1;
+  if (v < 0) {
+    const char* e = getenv("SG_HUB_KB");
+    v = (e ? atoll(e) : 64) * 1024;
+  }
+  return v;
+}
 
 // ------------------------------------------------------------------ modes
 template <int MODE>
@@ -140,9 +154,11 @@ struct PropArgs {
   int32_t Fv;        // vectors per row in this column slice
   int32_t Fcols;     // valid columns in this column slice
   int32_t accumulate;
+  const int32_t* hub_rows;  // hub-row cache: idx < 0 means slot (idx & 0x7fffffff) in smem
+  int32_t n_hub;
 };
 
-template <int MODE, int DT, int W, int VPL, int LPR, int DEPTH>
+template <int MODE, int DT, int W, int VPL, int LPR, int DEPTH, bool HUB = false>
 struct Prop {
   using M = ModeT<MODE>;
   using IO = VecIO<DT, W>;
@@ -155,14 +171,21 @@ struct Prop {
   // their terms in edge order.  FULL: all DEPTH edges valid (no per-edge predicates).
   // `gl` is G advanced to this lane's first column; only the last vector needs a bound check.
   template <bool FULL>
-  static __device__ __forceinline__ void step(const PropArgs& a, const Elem* gl, bool last_ok,
-                                              const int (&s)[DEPTH], const float (&wv)[DEPTH],
-                                              int n, const float (&rs)[NR > 0 ? NR : 1][VPL][W],
+  static __device__ __forceinline__ void step(const PropArgs& a, const Elem* gl, const Raw* hl,
+                                              bool last_ok, const int (&s)[DEPTH],
+                                              const float (&wv)[DEPTH], int n,
+                                              const float (&rs)[NR > 0 ? NR : 1][VPL][W],
                                               float (&acc)[NOUT][VPL][W]) {
     Raw g[DEPTH][NG][VPL];
 #pragma unroll
     for (int d = 0; d < DEPTH; ++d) {
-      if (FULL || d < n) {
+      if (HUB && (FULL || d < n) && s[d] < 0) {
+        // hub row: served from the CTA's shared-memory copy (same bits as the HBM row)
+        const Raw* hrow = hl + (s[d] & 0x7fffffff) * a.Fv;
+#pragma unroll
+        for (int v = 0; v < VPL; ++v)
+          if (v < VPL - 1 || last_ok) g[d][0][v] = hrow[v * LPR];
+      } else if (FULL || d < n) {
         // 32x32->64 IMAD.WIDE row address; column offsets are immediates
         const Elem* row = gl + (uint64_t)(uint32_t)s[d] * (uint32_t)a.ldg;
 #pragma unroll
@@ -211,8 +234,9 @@ struct Prop {
   static __device__ __forceinline__ void run_edges(const PropArgs& a, int64_t e0, int64_t e1,
                                                    const float (&rs)[NR > 0 ? NR : 1][VPL][W],
                                                    float (&acc)[NOUT][VPL][W], unsigned tmask,
-                                                   int tl) {
+                                                   int tl, const Raw* hs) {
     const Elem* gl = static_cast<const Elem*>(a.G) + tl * W;
+    const Raw* hl = hs + tl;
     const bool last_ok = (VPL - 1) * LPR + tl < a.Fv;
     if constexpr (LPR == 32) {
       // warp-wide index window: 32 (src, w) pairs loaded coalesced, broadcast by shuffle;
@@ -244,7 +268,7 @@ struct Prop {
             s[d] = __shfl_sync(0xffffffffu, my_src, d0 + d);
             wv[d] = M::USE_W ? __shfl_sync(0xffffffffu, my_w, d0 + d) : 0.f;
           }
-          step<true>(a, gl, last_ok, s, wv, DEPTH, rs, acc);
+          step<true>(a, gl, hl, last_ok, s, wv, DEPTH, rs, acc);
         }
         if (d0 < n) {
           int s[DEPTH];
@@ -254,7 +278,7 @@ struct Prop {
             s[d] = __shfl_sync(0xffffffffu, my_src, (d0 + d) & 31);
             wv[d] = M::USE_W ? __shfl_sync(0xffffffffu, my_w, (d0 + d) & 31) : 0.f;
           }
-          step<false>(a, gl, last_ok, s, wv, n - d0, rs, acc);
+          step<false>(a, gl, hl, last_ok, s, wv, n - d0, rs, acc);
         }
       }
     } else {
@@ -269,7 +293,7 @@ struct Prop {
           s[d] = __ldcs(a.idx + e + d);
           wv[d] = M::USE_W ? __ldcs(a.w + e + d) : 0.f;
         }
-        step<true>(a, gl, last_ok, s, wv, DEPTH, rs, acc);
+        step<true>(a, gl, hl, last_ok, s, wv, DEPTH, rs, acc);
       }
       if (e < e1) {
         const int n = (int)(e1 - e);
@@ -280,7 +304,7 @@ struct Prop {
           s[d] = d < n ? __ldcs(a.idx + e + d) : 0;
           wv[d] = (M::USE_W && d < n) ? __ldcs(a.w + e + d) : 0.f;
         }
-        step<false>(a, gl, last_ok, s, wv, n, rs, acc);
+        step<false>(a, gl, hl, last_ok, s, wv, n, rs, acc);
       }
     }
     (void)tmask;
@@ -350,10 +374,26 @@ constexpr int prop_min_blocks() {
   return regs <= 80 ? 3 : 2;
 }
 
-template <int MODE, int DT, int W, int VPL, int LPR, int DEPTH>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, (prop_min_blocks<MODE, W, VPL, DEPTH>()))
+// HUB: the block first copies the pass's hub rows (most-referenced source rows, listed in
+// a.hub_rows; their edges carry idx = slot | 0x80000000) into shared memory, so those
+// gathers are served on-chip instead of through L2.  One block of NWB warps per SM.
+template <int MODE, int DT, int W, int VPL, int LPR, int DEPTH, bool HUB = false, int NWB = kWarpsPerBlock>
+__global__ void __launch_bounds__(NWB * 32, (HUB ? 1 : prop_min_blocks<MODE, W, VPL, DEPTH>()))
     prop_kernel(const PropArgs a) {
-  using K = Prop<MODE, DT, W, VPL, LPR, DEPTH>;
+  using K = Prop<MODE, DT, W, VPL, LPR, DEPTH, HUB>;
+  using Raw = typename K::Raw;
+  extern __shared__ __align__(16) unsigned char prop_smem[];
+  const Raw* hs = reinterpret_cast<const Raw*>(prop_smem);
+  if constexpr (HUB) {
+    Raw* hw = reinterpret_cast<Raw*>(prop_smem);
+    const int total = a.n_hub * a.Fv;
+    for (int i = threadIdx.x; i < total; i += blockDim.x) {
+      const int r = i / a.Fv, c = i - r * a.Fv;
+      hw[i] = K::IO::ld_raw(static_cast<const typename K::Elem*>(a.G) +
+                            (int64_t)__ldg(a.hub_rows + r) * a.ldg + (int64_t)c * W);
+    }
+    __syncthreads();
+  }
   constexpr int NOUT = K::NOUT;
   constexpr int NRr = K::NR > 0 ? K::NR : 1;
   constexpr int NT = 32 / LPR;
@@ -379,7 +419,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, (prop_min_blocks<MODE, W,
       const int64_t e1 = split ? item.e_end : __ldg(a.ptr + r + 1);
       K::load_row_state(a, r, tl, rs);
       K::init_acc(a, r, tl, acc, a.accumulate != 0 && !split);
-      K::run_edges(a, e0, e1, rs, acc, tmask, tl);
+      K::run_edges(a, e0, e1, rs, acc, tmask, tl, hs);
       if (!split) {
         K::store_row(a, r, tl, acc);
       } else {
@@ -546,6 +586,25 @@ cudaError_t launch_one(const PropArgs& a, cudaStream_t st) {
   if constexpr (LPR == 32 && VPL >= 2 && NG == 1 && W > 1) {
     if (tma_enabled()) return launch_tma<MODE, DT, VPL>(a, st);
   }
+  if constexpr (LPR == 32 && NG == 1 && W > 1 && VPL >= kHubMinVpl) {
+    if (a.n_hub > 0) {
+      // hub-cache kernel: one block per SM holding the hub rows, as many warps as the
+      // register budget allowed the default kernel (2-3 blocks of 8 warps)
+      constexpr int NWB = kWarpsPerBlock * prop_min_blocks<MODE, W, VPL, DEPTH>();
+      auto hk = prop_kernel<MODE, DT, W, VPL, LPR, DEPTH, true, NWB>;
+      const size_t smem = (size_t)a.n_hub * a.Fv * 16;
+      static int hub_cfg = 0;
+      if (!hub_cfg) {
+        cudaFuncSetAttribute(hk, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        hub_cfg = 1;
+      }
+      int64_t want = ((int64_t)a.n_items + NWB - 1) / NWB;
+      int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, sm_count()));
+      hk<<<grid, NWB * 32, smem, st>>>(a);
+      sg::count_launch();
+      return cudaGetLastError();
+    }
+  }
   auto kern = prop_kernel<MODE, DT, W, VPL, LPR, DEPTH>;
   static int blocks_per_sm = 0;
   if (!blocks_per_sm) {
@@ -630,6 +689,30 @@ int sg_propagate(int mode, int dtype, const int64_t* ptr, const int32_t* idx, co
                  const void* R, int64_t ldr, int64_t r_off, void* out0, int64_t ld0, void* out1,
                  int64_t ld1, const void* mask, int64_t ldm, int64_t F, int accumulate,
                  void* workspace, int64_t workspace_bytes, void* stream) {
+  return sg_propagate_hub(mode, dtype, ptr, idx, w, n_rows, items, n_items, splits, n_splits, n_slots,
+                          G, ldg, g_off, R, ldr, r_off, out0, ld0, out1, ld1, mask, ldm, F, accumulate,
+                          nullptr, 0, workspace, workspace_bytes, stream);
+}
+
+int64_t sg_propagate_hub_capacity(int64_t F, int dtype) {
+  if (dtype != SG_F32 && dtype != SG_BF16) return 0;
+  const int VW = dtype == SG_F32 ? 4 : 8;
+  const int64_t max_cols = (int64_t)32 * vpl_max(SG_PROP_GCN, dtype) * VW;
+  const int64_t slice_cols = std::min<int64_t>(F, max_cols);
+  const int64_t row_bytes = (slice_cols + VW - 1) / VW * 16;
+  // every column slice must be wide enough for the hub kernel (the index is encoded)
+  const int64_t last_cols = F % max_cols == 0 ? std::min(F, max_cols) : F % max_cols;
+  if (last_cols <= (int64_t)32 * (kHubMinVpl - 1) * VW) return 0;
+  return std::min<int64_t>(hub_smem_bytes() / row_bytes, INT32_MAX);
+}
+
+int sg_propagate_hub(int mode, int dtype, const int64_t* ptr, const int32_t* idx, const float* w,
+                     int64_t n_rows, const sg_item* items, int64_t n_items, const sg_split* splits,
+                     int64_t n_splits, int64_t n_slots, const void* G, int64_t ldg, int64_t g_off,
+                     const void* R, int64_t ldr, int64_t r_off, void* out0, int64_t ld0, void* out1,
+                     int64_t ld1, const void* mask, int64_t ldm, int64_t F, int accumulate,
+                     const int32_t* hub_rows, int64_t n_hub, void* workspace, int64_t workspace_bytes,
+                     void* stream) {
   SG_REQUIRE(mode >= SG_PROP_PASS && mode <= SG_PROP_GGCN_BWD_SRC, SG_EINVAL, "bad mode %d", mode);
   SG_REQUIRE(dtype == SG_F32 || dtype == SG_BF16, SG_EINVAL, "bad dtype %d", dtype);
   SG_REQUIRE(n_items >= 0 && n_items <= INT32_MAX, SG_EINVAL, "bad n_items");
@@ -683,6 +766,16 @@ int sg_propagate(int mode, int dtype, const int64_t* ptr, const int32_t* idx, co
     a.out1 = out1 ? static_cast<char*>(out1) + c0 * esz : nullptr; a.ld1 = ld1;
     a.mask = mask ? static_cast<const char*>(mask) + c0 * esz : nullptr; a.ldm = ldm;
     a.n_items = (int32_t)n_items; a.Fv = Fv; a.Fcols = (int32_t)cols; a.accumulate = accumulate;
+    a.hub_rows = hub_rows;
+    a.n_hub = 0;
+    if (n_hub > 0) {
+      // an index encoded for hubs must run the hub kernel (negative entries are slots)
+      SG_REQUIRE(hub_rows && vec && mode <= SG_PROP_GCN && LPR == 32 && VPL >= kHubMinVpl &&
+                     n_hub <= sg_propagate_hub_capacity(F, dtype),
+                 SG_EINVAL, "hub cache not applicable (mode %d, F %lld, n_hub %lld)", mode, (long long)F,
+                 (long long)n_hub);
+      a.n_hub = (int32_t)n_hub;
+    }
     cudaError_t e = cudaMemsetAsync(ws, 0, 256 + align_up(4 * std::max<int64_t>(n_splits, 1), 256), st);
     if (e != cudaSuccess) SG_FAIL(SG_ECUDA, "memset: %s", cudaGetErrorString(e));
     switch (mode) {

@@ -18,6 +18,7 @@ from .errors import GraphFormatError, ShapeError
 
 RMAT_ABC = (0.57, 0.19, 0.19)
 DEFAULT_SPLIT_EDGES = 4096     # subgroup size T for heavy rows
+HUB_MIN_COVER = 0.03           # use the hub-row cache when its rows cover >= 3% of a pass's edges
 
 
 class Graph:
@@ -195,6 +196,38 @@ class PassIndex:
 
     def workspace_bytes(self, F, mode):
         return int(lib.sg_propagate_workspace_bytes(self.n_items, self.n_splits, self.n_slots, F, mode))
+
+    def hub(self, n_cap, min_cover=HUB_MIN_COVER):
+        """Hub-row cache of this pass for at most ``n_cap`` rows (sg_propagate_hub).
+
+        The most referenced gathered rows (count >= 2; descending count, ties by row id)
+        get slots 0..n-1; returns (encoded idx, hub rows, n, edge coverage) with each edge
+        to slot k carrying k | 0x80000000, or None when the hubs would cover fewer than
+        ``min_cover`` of the edges (e.g. uniform graphs).  Built on the device, cached."""
+        import torch
+
+        if not hasattr(self, "_hubs"):
+            self._hubs = {}
+        if n_cap in self._hubs:
+            return self._hubs[n_cap]
+        res = None
+        if self.nnz > 0 and n_cap > 0:
+            idx = self.idx.long()
+            counts = torch.bincount(idx)
+            vals, order = torch.sort(counts, descending=True, stable=True)
+            n = min(int(n_cap), int((vals >= 2).sum().item()))
+            cover = float(vals[:n].sum().item()) / self.nnz if n else 0.0
+            if n > 0 and cover >= min_cover:
+                rows = order[:n]
+                slot = torch.full((counts.numel(),), -1, dtype=torch.int64, device=idx.device)
+                slot[rows] = torch.arange(n, device=idx.device)
+                s = slot[idx]
+                enc = torch.where(s >= 0, s - (1 << 31), idx).to(torch.int32)
+                res = (enc, rows.to(torch.int32).contiguous(), n, cover)
+                del s, slot
+            del idx, counts
+        self._hubs[n_cap] = res
+        return res
 
 
 class ChunkGrid:

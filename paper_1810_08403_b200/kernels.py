@@ -5,6 +5,8 @@ current torch stream (or the given one) and raises the mirrored reference
 exception on a bad status.  torch is used only for device memory and streams.
 """
 
+import os
+
 import torch
 
 from . import _lib
@@ -45,19 +47,40 @@ class Workspace:
         return self.buf
 
 
+HUB_CACHE = os.environ.get("SG_HUB", "1") != "0"
+
+
+def _vec_ok(t, vw):
+    return t is None or (ld(t) % vw == 0 and t.data_ptr() % 16 == 0)
+
+
+def _hub_for(pi, mode, dt, G, out0, mask, F, g_off):
+    """The pass's hub-row cache if this call can use it (GCN / PASS, 16-B rows, > 16 vectors)."""
+    if not HUB_CACHE or mode not in (_lib.PROP_PASS, _lib.PROP_GCN) or not hasattr(pi, "hub"):
+        return None
+    vw = 4 if dt == _lib.SG_F32 else 8
+    if g_off % vw or not (_vec_ok(G, vw) and _vec_ok(out0, vw) and _vec_ok(mask, vw)):
+        return None
+    cap = int(lib.sg_propagate_hub_capacity(F, dt))
+    return pi.hub(cap) if cap > 0 else None
+
+
 def propagate(pi, mode, G, out0, F, *, g_off=0, R=None, r_off=0, out1=None, mask=None,
-              accumulate=False, ws=None, stream=None):
-    """One fused Scatter-ApplyEdge-Gather pass over PassIndex ``pi`` (sg_propagate)."""
+              accumulate=False, ws=None, stream=None, hub=True):
+    """One fused Scatter-ApplyEdge-Gather pass over PassIndex ``pi`` (sg_propagate; with the
+    hub-row cache, sg_propagate_hub, when the pass has hubs -- bitwise identical)."""
     dt = dtype_code(G)
     wsb = pi.workspace_bytes(F, mode)
     buf = ws.get(wsb) if ws is not None else torch.empty(wsb, dtype=torch.uint8, device=G.device)
-    check(lib.sg_propagate(
-        mode, dt, tptr(pi.ptr), tptr(pi.idx), tptr(pi.w), pi.n_rows, tptr(pi.items), pi.n_items,
+    h = _hub_for(pi, mode, dt, G, out0, mask, F, g_off) if hub and R is None and out1 is None else None
+    idx, rows, n_hub = (h[0], h[1], h[2]) if h is not None else (pi.idx, None, 0)
+    check(lib.sg_propagate_hub(
+        mode, dt, tptr(pi.ptr), tptr(idx), tptr(pi.w), pi.n_rows, tptr(pi.items), pi.n_items,
         tptr(pi.splits), pi.n_splits, pi.n_slots, tptr(G), ld(G), g_off,
         tptr(R), ld(R) if R is not None else 0, r_off, tptr(out0), ld(out0),
         tptr(out1), ld(out1) if out1 is not None else 0, tptr(mask),
-        ld(mask) if mask is not None else 0, F, int(bool(accumulate)), tptr(buf), buf.numel(),
-        stream_handle(stream)))
+        ld(mask) if mask is not None else 0, F, int(bool(accumulate)), tptr(rows), n_hub,
+        tptr(buf), buf.numel(), stream_handle(stream)))
 
 
 def gemm(A, B, C, *, trans_a=False, trans_b=False, relu_out=None, prec=_lib.GEMM_F32, ws=None,

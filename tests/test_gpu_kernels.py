@@ -602,3 +602,43 @@ def test_commnet_epoch_vs_oracle(sg, P, T):
     out = sg.run_train({"model": "commnet", "graph": "uniform", "V": 1000, "E": 8000, "features": 32,
                         "classes": 4, "epochs": 5, "lr": 0.01})
     assert out["loss"][-1] < out["loss"][0]
+
+
+@pytest.mark.parametrize("F,P,T,mode", [(602, 1, 4096, "gcn"), (500, 1, 256, "gcn"), (512, 3, 64, "pass"),
+                                        (2048, 1, 4096, "gcn")])
+def test_hub_cache_bitwise(sg, F, P, T, mode):
+    """sg_propagate_hub (hub rows served from shared memory) == the plain pass == the oracle."""
+    from paper_1810_08403_b200 import _lib
+    from paper_1810_08403_b200 import kernels as K
+
+    V, E = 6000, 150000
+    for narrow in (128, 1100):  # 1-vector rows / a narrow last column slice: no hub path
+        assert _lib.lib.sg_propagate_hub_capacity(narrow, _lib.SG_F32) == 0
+    s, d = _graph("rmat", V, E, 11)
+    g = sg.Graph(V, s, d)
+    size = -(-V // P)
+    grid = sg.ChunkGrid(g, size, split_edges=T, gcn_weights=(mode == "gcn"))
+    pmode = _lib.PROP_GCN if mode == "gcn" else _lib.PROP_PASS
+    X = _padded(rng.features(V, F, seed=1))
+    used = [pi.hub(int(_lib.lib.sg_propagate_hub_capacity(F, _lib.SG_F32))) is not None
+            for pi in grid.csc.values()]
+    assert any(used)
+    K.HUB_CACHE = True
+    try:
+        with_hub = _gpu_prop_fwd(sg, grid, X, F, pmode)
+        K.HUB_CACHE = False
+        plain = _gpu_prop_fwd(sg, grid, X, F, pmode)
+    finally:
+        K.HUB_CACHE = True
+    assert torch.equal(with_hub, plain)
+    part = og.partition_2d(s, d, V, size)
+    w = og.gcn_edge_weights(s, d, V, np.float32) if mode == "gcn" else None
+    ref = saga.gcn_propagate_fwd(part, X.cpu().numpy(), w, T=T)
+    assert np.array_equal(with_hub.cpu().numpy(), ref)
+    # backward dual over CSR with the ReLU mask (its hubs are high in-degree destinations)
+    Gr = _padded(rng.features(V, F, seed=4))
+    Z = _padded(rng.features(V, F, seed=8))
+    if mode == "gcn":
+        bw = _gpu_prop_bwd(sg, grid, Gr, F, mask=Z)
+        ref_b = prim.relu_bwd(saga.gcn_propagate_bwd(part, Gr.cpu().numpy(), w, T=T), Z.cpu().numpy())
+        assert np.array_equal(bw.cpu().numpy(), ref_b)
