@@ -31,7 +31,8 @@ enum sg_status {
   SG_EBUDGET = 3,  /* BudgetError  (errors.py:24) */
   SG_ECUDA = 4,
   SG_ENCCL = 5,
-  SG_EINVAL = 6
+  SG_EINVAL = 6,
+  SG_EFORMAT = 7   /* GraphFormatError (errors.py): malformed input file, line named */
 };
 
 enum sg_dtype { SG_F32 = 0, SG_BF16 = 1 };
@@ -102,6 +103,25 @@ int sg_host_gcn_weights(const int32_t* src, const int32_t* dst, const int64_t* d
 int sg_host_plan(const int64_t* ptr, int64_t n_rows, int64_t pack_edges, int64_t max_rows,
                  int64_t split_edges, sg_item* items, sg_split* splits, int64_t* n_items,
                  int64_t* n_splits, int64_t* n_slots);
+
+/* ---------------------------------------------------------------- host: ingestion
+ * load_graph's file formats.  Edge file: one "src dest
+ * [edge_value]" per line, whitespace separated (blank, '#' and '%' lines skipped).
+ * Feature file: text CSV or binary (u64 rows, u64 cols, row-major f64, little endian).
+ * Label file: one integer per line.  Scan first (sizes; vertex_limit >= 0 bounds-checks
+ * ids), then read into caller buffers.  Errors (SG_EFORMAT) name the 1-based line. */
+int sg_host_scan_edges(const char* path, int64_t vertex_limit, int64_t* n_edges, int64_t* max_id,
+                       int* has_value);
+int sg_host_read_edges(const char* path, int64_t n_edges, int32_t* src, int32_t* dst, double* value);
+int sg_host_scan_matrix_text(const char* path, int64_t* rows, int64_t* cols);
+int sg_host_read_matrix_text(const char* path, int64_t rows, int64_t cols, double* out);
+int sg_host_read_matrix_bin_header(const char* path, int64_t* rows, int64_t* cols);
+int sg_host_read_matrix_bin(const char* path, int64_t rows, int64_t cols, double* out);
+int sg_host_write_matrix_bin(const char* path, int64_t rows, int64_t cols, const double* data);
+int sg_host_scan_labels(const char* path, int64_t* n);
+int sg_host_read_labels(const char* path, int64_t n, int64_t* out);
+/* Order-sensitive 64-bit content hash (keys the on-disk partition cache). */
+uint64_t sg_host_hash64(const void* data, int64_t nbytes, uint64_t seed);
 
 /* ---------------------------------------------------------------- device: propagation
  * One fused Scatter-ApplyEdge-Gather pass over a CSC (forward) or CSR (backward)

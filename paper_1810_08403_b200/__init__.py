@@ -10,8 +10,8 @@ from . import errors
 from ._lib import lib as _native  # noqa: F401  (fails loudly if libsagann.so is missing)
 from .errors import (BudgetError, ConfigError, EngineError, GraphFormatError, NumericError,
                      ProgramError, ShapeError)
-from .graph import (ChunkGrid, Graph, Partition, partition_2d, reencode_balance, rmat_graph,
-                    synthetic_features, uniform_graph)
+from .graph import (ChunkGrid, Graph, Partition, load_graph, partition_2d, read_features, read_labels,
+                    reencode_balance, rmat_graph, synthetic_features, uniform_graph, write_features_bin)
 from .program import (FusedGather, LayerProgram, PassReport, build_commnet, build_gcn, build_ggcn,
                       build_mpgcn,
                       evaluate_expr, fuse_sag, hoist_vertex_computation, make_program, matmul_rows,
@@ -19,7 +19,8 @@ from .program import (FusedGather, LayerProgram, PassReport, build_commnet, buil
 
 __all__ = [
     "errors", "BudgetError", "ConfigError", "EngineError", "GraphFormatError", "NumericError",
-    "ProgramError", "ShapeError", "ChunkGrid", "Graph", "Partition", "partition_2d",
+    "ProgramError", "ShapeError", "ChunkGrid", "Graph", "Partition", "partition_2d", "load_graph",
+    "read_features", "read_labels", "write_features_bin",
     "reencode_balance", "rmat_graph", "synthetic_features", "uniform_graph", "FusedGather",
     "LayerProgram", "PassReport", "build_commnet", "build_gcn", "build_ggcn", "build_mpgcn", "evaluate_expr",
     "fuse_sag", "hoist_vertex_computation", "make_program", "matmul_rows", "optimize", "trace_udf",

@@ -20,7 +20,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libsagann.so")
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "sagann.h")
 
-SG_OK, SG_ESHAPE, SG_ENUMERIC, SG_EBUDGET, SG_ECUDA, SG_ENCCL, SG_EINVAL = range(7)
+SG_OK, SG_ESHAPE, SG_ENUMERIC, SG_EBUDGET, SG_ECUDA, SG_ENCCL, SG_EINVAL, SG_EFORMAT = range(8)
 SG_F32, SG_BF16 = 0, 1
 PROP_PASS, PROP_GCN, PROP_GGCN_FWD, PROP_GGCN_BWD_DST, PROP_GGCN_BWD_SRC = range(5)
 EPI_NONE, EPI_RELU_DUAL = 0, 1
@@ -33,6 +33,7 @@ assert ITEM_DTYPE.itemsize == 32 and SPLIT_DTYPE.itemsize == 16
 
 _i64, _i32, _f64, _f32 = ctypes.c_int64, ctypes.c_int, ctypes.c_double, ctypes.c_float
 _u64, _p = ctypes.c_uint64, ctypes.c_void_p
+_s = ctypes.c_char_p
 
 _SIGS = {
     "sg_last_error": (ctypes.c_char_p, []),
@@ -48,6 +49,16 @@ _SIGS = {
     "sg_host_partition_2d": (_i32, [_p, _p, _i64, _i64, _i64] + [_p] * 9),
     "sg_host_gcn_weights": (_i32, [_p, _p, _p, _p, _p, _i64, _p]),
     "sg_host_plan": (_i32, [_p, _i64, _i64, _i64, _i64, _p, _p, _p, _p, _p]),
+    "sg_host_scan_edges": (_i32, [_s, _i64, _p, _p, _p]),
+    "sg_host_read_edges": (_i32, [_s, _i64, _p, _p, _p]),
+    "sg_host_scan_matrix_text": (_i32, [_s, _p, _p]),
+    "sg_host_read_matrix_text": (_i32, [_s, _i64, _i64, _p]),
+    "sg_host_read_matrix_bin_header": (_i32, [_s, _p, _p]),
+    "sg_host_read_matrix_bin": (_i32, [_s, _i64, _i64, _p]),
+    "sg_host_write_matrix_bin": (_i32, [_s, _i64, _i64, _p]),
+    "sg_host_scan_labels": (_i32, [_s, _p]),
+    "sg_host_read_labels": (_i32, [_s, _i64, _p]),
+    "sg_host_hash64": (_u64, [_p, _i64, _u64]),
     "sg_propagate_workspace_bytes": (_i64, [_i64, _i64, _i64, _i64, _i32]),
     "sg_propagate": (_i32, [_i32, _i32, _p, _p, _p, _i64, _p, _i64, _p, _i64, _i64,
                             _p, _i64, _i64, _p, _i64, _i64, _p, _i64, _p, _i64, _p, _i64,
@@ -99,6 +110,7 @@ def _load():
 lib = _load()
 
 _EXC = {
+    SG_EFORMAT: errors.GraphFormatError,
     SG_ESHAPE: errors.ShapeError,
     SG_ENUMERIC: errors.NumericError,
     SG_EBUDGET: errors.BudgetError,

@@ -138,9 +138,147 @@ class Partition:
                     csr_idx=self.csr_idx[e0:e1], csr_eid=self.csr_eid[e0:e1])
 
 
-def partition_2d(g, interval_size):
-    """P = ceil(V / interval_size), explicit empty chunks."""
-    return Partition(g, interval_size)
+    # ---------------------------------------------------------------- on-disk cache
+    _ARRAYS = ("sizes", "edge_off", "cptr_off", "rptr_off", "csc_ptr", "csr_ptr", "csc_idx", "csr_idx",
+               "csc_eid", "csr_eid")
+
+    def save(self, path):
+        """Write the partition as a directory of .npy arrays (memory-mappable on load)."""
+        import os
+
+        os.makedirs(path, exist_ok=True)
+        for k in self._ARRAYS:
+            np.save(os.path.join(path, k + ".npy"), getattr(self, k))
+        np.save(os.path.join(path, "meta.npy"),
+                np.array([self.V, self.E, self.P, self.interval_size], np.int64))
+
+    @classmethod
+    def load(cls, path, mmap=True):
+        import os
+
+        self = cls.__new__(cls)
+        V, E, P, isz = (int(x) for x in np.load(os.path.join(path, "meta.npy")))
+        self.V, self.E, self.P, self.interval_size = V, E, P, isz
+        for k in self._ARRAYS:
+            setattr(self, k, np.load(os.path.join(path, k + ".npy"), mmap_mode="r" if mmap else None))
+        return self
+
+
+def graph_key(g, interval_size):
+    """Content key of (graph, interval_size) for the partition cache (native 64-bit hash)."""
+    h = lib.sg_host_hash64(nptr(g.src), g.src.nbytes, np.uint64(g.V).item())
+    h = lib.sg_host_hash64(nptr(g.dst), g.dst.nbytes, h)
+    return f"v{g.V}_e{g.E}_i{int(interval_size)}_{h:016x}"
+
+
+def partition_2d(g, interval_size, cache_dir=None):
+    """P = ceil(V / interval_size), explicit empty chunks.
+
+    ``cache_dir``: reuse a partition saved there for the same edge list and interval
+    size (content hash of src/dst), else build and save it ("partition
+    cache")."""
+    if cache_dir is None:
+        return Partition(g, interval_size)
+    import os
+
+    path = os.path.join(cache_dir, "partition_" + graph_key(g, interval_size))
+    if os.path.exists(os.path.join(path, "meta.npy")):
+        part = Partition.load(path)
+        part.cache_hit = True
+        return part
+    part = Partition(g, interval_size)
+    tmp = path + f".tmp{os.getpid()}"
+    part.save(tmp)
+    if not os.path.exists(path):
+        os.replace(tmp, path)  # atomic publish; a concurrent writer's copy is equivalent
+    part.cache_hit = False
+    return part
+
+
+# ------------------------------------------------------------------ ingestion
+def _path(p):
+    return str(p).encode()
+
+
+def read_features(path, fmt="auto"):
+    """Feature file: text CSV (row v = features of vertex v) or raw binary
+    (u64 rows, u64 cols, row-major f64).  ``fmt`` = 'csv' | 'bin' | 'auto' (by content)."""
+    if fmt == "auto":
+        fmt = "csv"
+        try:
+            r = np.zeros(1, np.int64)
+            c = np.zeros(1, np.int64)
+            if lib.sg_host_read_matrix_bin_header(_path(path), nptr(r), nptr(c)) == _lib.SG_OK:
+                fmt = "bin"
+        except Exception:  # noqa: BLE001
+            fmt = "csv"
+    r = np.zeros(1, np.int64)
+    c = np.zeros(1, np.int64)
+    if fmt == "bin":
+        check(lib.sg_host_read_matrix_bin_header(_path(path), nptr(r), nptr(c)))
+        out = np.empty((int(r[0]), int(c[0])), np.float64)
+        check(lib.sg_host_read_matrix_bin(_path(path), int(r[0]), int(c[0]), nptr(out)))
+        return out
+    if fmt != "csv":
+        raise GraphFormatError(f"unknown feature format '{fmt}' (csv | bin | auto)")
+    check(lib.sg_host_scan_matrix_text(_path(path), nptr(r), nptr(c)))
+    out = np.empty((int(r[0]), int(c[0])), np.float64)
+    check(lib.sg_host_read_matrix_text(_path(path), int(r[0]), int(c[0]), nptr(out)))
+    return out
+
+
+def write_features_bin(path, X):
+    X = np.ascontiguousarray(X, np.float64)
+    if X.ndim != 2:
+        raise ShapeError("features must be a 2-D matrix")
+    check(lib.sg_host_write_matrix_bin(_path(path), X.shape[0], X.shape[1], nptr(X)))
+
+
+def read_labels(path):
+    n = np.zeros(1, np.int64)
+    check(lib.sg_host_scan_labels(_path(path), nptr(n)))
+    out = np.empty(int(n[0]), np.int64)
+    check(lib.sg_host_read_labels(_path(path), int(n[0]), nptr(out)))
+    return out
+
+
+def load_graph(edge_file, feature_file=None, label_file=None, *, num_vertices=None,
+               feature_format="auto"):
+    """load_graph: edge list + optional features / labels.
+
+    V = ``num_vertices`` if given, else the feature row count, else max id + 1.  Ids are
+    bounds-checked against V with the offending line named; self-loops and multi-edges
+    are kept as given.  Returns a Graph with ``features`` (f64 [V, F] or None),
+    ``labels`` (int64 [V] or None) and ``edge_values`` (f64 [E] or None) attached."""
+    X = read_features(feature_file, feature_format) if feature_file is not None else None
+    if num_vertices is not None:
+        V = int(num_vertices)
+        if X is not None and X.shape[0] != V:
+            raise GraphFormatError(f"feature file has {X.shape[0]} rows, expected {V} vertices")
+    elif X is not None:
+        V = X.shape[0]
+    else:
+        V = -1
+    E = np.zeros(1, np.int64)
+    mx = np.zeros(1, np.int64)
+    hv = np.zeros(1, np.int32)
+    check(lib.sg_host_scan_edges(_path(edge_file), V, nptr(E), nptr(mx), nptr(hv)))
+    E = int(E[0])
+    if V < 0:
+        V = int(mx[0]) + 1
+    src = np.empty(E, np.int32)
+    dst = np.empty(E, np.int32)
+    val = np.empty(E, np.float64) if hv[0] else None
+    check(lib.sg_host_read_edges(_path(edge_file), E, nptr(src), nptr(dst), nptr(val)))
+    g = Graph(V, src, dst)
+    g.features, g.edge_values = X, val
+    g.labels = None
+    if label_file is not None:
+        y = read_labels(label_file)
+        if y.shape[0] != V:
+            raise GraphFormatError(f"label file has {y.shape[0]} rows, expected {V} vertices")
+        g.labels = y
+    return g
 
 
 def plan(ptr, split_edges=DEFAULT_SPLIT_EDGES, pack_edges=None, max_rows=256):
