@@ -35,6 +35,16 @@ def _mat(V, n, device, align=4):
     return torch.zeros((V, _ld(n, align)), dtype=torch.float32, device=device)[:, :n]
 
 
+def _param(L, r, c, device):
+    """A parameter and its gradient as [r, c] views of zero-padded [r, ld] buffers (16-B
+    rows, so the tensor-core GEMM takes the TMA path); SGD runs over the whole buffers
+    (the padding columns of W and dW stay zero)."""
+    wb = torch.zeros((r, _ld(c)), dtype=torch.float32, device=device)
+    gb = torch.zeros_like(wb)
+    L.sgd_pairs.append((wb, gb))
+    return wb[:, :c], gb[:, :c]
+
+
 class _Layer:
     pass
 
@@ -148,8 +158,9 @@ class SAGAModel:
         V, dev = self.V, self.device
         for n, L in enumerate(self.layers):
             F, O = L.F, L.O
-            L.W = torch.zeros((L.Aw, O), dtype=torch.float32, device=dev)
-            L.dW = torch.zeros_like(L.W)
+            L.sgd_pairs = []
+            if L.vform != "hc":
+                L.W, L.dW = _param(L, L.Aw, O, dev)
             if L.vform == "hc":
                 # CommNet: z = [h | accum] @ [W_H; W_C] as ONE GEMM over a per-vertex [h | a]
                 # buffer (16-B padded halves, zero pad rows in the stacked weights); its
@@ -157,8 +168,7 @@ class SAGAModel:
                 ldF = _ld(F)
                 L.HA = torch.zeros((V, 2 * ldF), dtype=torch.float32, device=dev)
                 L.hin, L.a = L.HA[:, :F], L.HA[:, ldF:ldF + F]
-                L.W = torch.zeros((2 * ldF, O), dtype=torch.float32, device=dev)
-                L.dW = torch.zeros_like(L.W)
+                L.W, L.dW = _param(L, 2 * ldF, O, dev)
                 L.WH, L.WC = L.W[:F], L.W[ldF:ldF + F]
                 L.dWH, L.dWC = L.dW[:F], L.dW[ldF:ldF + F]
                 L.dHA = torch.zeros((V, 2 * ldF), dtype=torch.float32, device=dev)
@@ -177,9 +187,8 @@ class SAGAModel:
                 L.params, L.dparams = [L.W], [L.dW]
                 if L.kind == "max_pool":
                     L.Y = _mat(V, A, dev)
-                    L.Wp = torch.zeros((F, A), dtype=torch.float32, device=dev)
-                    L.bias = torch.zeros((1, A), dtype=torch.float32, device=dev)
-                    L.dWp, L.dbias = torch.zeros_like(L.Wp), torch.zeros_like(L.bias)
+                    L.Wp, L.dWp = _param(L, F, A, dev)
+                    L.bias, L.dbias = _param(L, 1, A, dev)
                     L.params, L.dparams = [L.Wp, L.bias, L.W], [L.dWp, L.dbias, L.dW]
                     self._ones = torch.ones((V, 1), dtype=torch.float32, device=dev)
                 L.a = _mat(V, A, dev)
@@ -194,9 +203,8 @@ class SAGAModel:
                 L.Pv = L.HP[:, L.goff:L.goff + F]
                 L.Qv = L.GQ[:, L.goff:L.goff + F]
                 L.dAv = L.GQ[:, :F]
-                L.WH = torch.zeros((F, F), dtype=torch.float32, device=dev)
-                L.WC = torch.zeros((F, F), dtype=torch.float32, device=dev)
-                L.dWH, L.dWC = torch.zeros_like(L.WH), torch.zeros_like(L.WC)
+                L.WH, L.dWH = _param(L, F, F, dev)
+                L.WC, L.dWC = _param(L, F, F, dev)
                 L.dQ, L.dP, L.dHt = _mat(V, F, dev), _mat(V, F, dev), _mat(V, F, dev)
                 L.params = [L.WH, L.WC, L.W]
                 L.dparams = [L.dWH, L.dWC, L.dW]
@@ -489,7 +497,7 @@ class SAGAModel:
 
     def sgd(self, lr, stream=None):
         for L in self.layers:
-            for W, dW in zip(L.params, L.dparams):
+            for W, dW in L.sgd_pairs:  # whole padded buffers (padding stays zero)
                 K.sgd(W, dW, lr, stream)
         self._mark("sgd")
 
