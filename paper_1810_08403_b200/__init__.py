@@ -25,6 +25,7 @@ __all__ = [
     "LayerProgram", "PassReport", "build_commnet", "build_gcn", "build_ggcn", "build_mpgcn", "evaluate_expr",
     "fuse_sag", "hoist_vertex_computation", "make_program", "matmul_rows", "optimize", "trace_udf",
     "validate_program", "vertex_form", "SAGAModel", "gcn_model", "ggcn_model", "mpgcn_model", "commnet_model", "run_train",
+    "StreamingGCN", "HostGrid",
 ]
 
 
@@ -35,4 +36,8 @@ def __getattr__(name):
         from . import engine
 
         return getattr(engine, name)
+    if name in ("StreamingGCN", "HostGrid"):
+        from . import stream
+
+        return getattr(stream, name)
     raise AttributeError(name)

@@ -642,3 +642,46 @@ def test_hub_cache_bitwise(sg, F, P, T, mode):
         bw = _gpu_prop_bwd(sg, grid, Gr, F, mask=Z)
         ref_b = prim.relu_bwd(saga.gcn_propagate_bwd(part, Gr.cpu().numpy(), w, T=T), Z.cpu().numpy())
         assert np.array_equal(bw.cpu().numpy(), ref_b)
+
+
+# ---------------------------------------------------------------- out-of-core streaming
+@pytest.mark.parametrize("P,T", [(1, 4096), (3, 256), (4, 64)])
+def test_streaming_gcn_matches_resident(sg, P, T):
+    """Host-resident graph streamed chunk by chunk (prefetch depth 1) == the resident executor:
+    layer aggregates bitwise, loss / gradients / updated weights to fp32 round-off."""
+    V, E, dims = 5000, 100000, [96, 32, 7]
+    s, d = _graph("rmat", V, E, 2)
+    g = sg.Graph(V, s, d)
+    size = -(-V // P)
+    X = rng.features(V, dims[0], seed=1)
+    lab = rng.labels(V, dims[-1])
+    res = sg.gcn_model(sg.ChunkGrid(g, size, split_edges=T), dims)
+    W = res.weights()
+    res.load_features(torch.from_numpy(X))
+    res.load_labels(lab)
+    st = sg.StreamingGCN(sg.HostGrid(g, size, split_edges=T), dims, weights=W)
+    st.load_features(torch.from_numpy(X))
+    st.load_labels(lab)
+    res.forward()
+    res.backward()
+    st.forward()
+    st.backward()
+    st.check_status()
+    res.check_status()
+    for l in range(2):
+        assert np.array_equal(st.A[l][:, : dims[l]].numpy(), res.layers[l].a.cpu().numpy()), l
+    assert abs(st.loss.item() - res.loss.item()) <= 1e-6 * res.loss.item()
+    for a, b in zip(st.grads(), res.grads()):
+        assert_close(a, b, 1e-5, "dW")
+    assert st.h2d_bytes > 0 and st.d2h_bytes > 0
+    res.sgd(0.5)
+    st.sgd(0.5)
+    for a, b in zip(st.weights(), res.weights()):
+        assert_close(a, b, 1e-6, "W")
+
+
+def test_streaming_budget_error(sg):
+    s, d = _graph("rmat", 2000, 20000, 3)
+    g = sg.Graph(2000, s, d)
+    with pytest.raises(sg.BudgetError, match="interval_size"):
+        sg.StreamingGCN(sg.HostGrid(g, 1000), [64, 16, 4], budget=1 << 16)
