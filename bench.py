@@ -37,10 +37,16 @@ CONFIGS = {
                    graph="uniform", V=19717, E=88648, F=500, H=16, C=3),
     "blogcatalog10": dict(workload="2-layer G-GCN epoch, BlogCatalog-shaped graph x10 edges",
                           model="ggcn", graph="uniform", V=10312, E=6680000, F=128, H=128, C=39),
+    # BASELINE.json configs[3]: the multi-GPU power-law graph (runs on 1 GPU too)
+    "powerlaw_gcn": dict(workload="2-layer GCN epoch, synthetic power-law graph 4M V / 1B E",
+                         model="gcn", graph="rmat", V=4000000, E=1000000000, F=128, H=128, C=16),
+    "powerlaw_ggcn": dict(workload="2-layer G-GCN epoch, synthetic power-law graph 4M V / 1B E",
+                          model="ggcn", graph="rmat", V=4000000, E=1000000000, F=128, H=128, C=16),
 }
 # bounded CPU samples: ~3-6 s per oracle epoch on one host core (propagation is
 # single-threaded numpy), so --impl reference with the default K/W ends in ~1-2 minutes
-CPU_SAMPLE_EDGES = {"reddit": 150_000, "pubmed": 88_648, "blogcatalog10": 50_000}
+CPU_SAMPLE_EDGES = {"reddit": 150_000, "pubmed": 88_648, "blogcatalog10": 50_000,
+                    "powerlaw_gcn": 300_000, "powerlaw_ggcn": 60_000}
 METRIC = "GCN epoch throughput (whole-graph edges per second of 2-layer fwd+bwd epoch)"
 
 
@@ -56,6 +62,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--split-edges", type=int, default=4096)
+    ap.add_argument("--engine", choices=["auto", "dist"], default="auto",
+                    help="dist: run the sharded multi-GPU engine (NCCL) even at N=1")
     return ap.parse_args()
 
 
@@ -157,8 +165,10 @@ def run_reference(a, cfg):
 def config_of(cfg, a, world):
     return {"workload": cfg["workload"], "graph": cfg["graph"] + (" (0.57,0.19,0.19,0.05)" if cfg["graph"] == "rmat" else ""),
             "V": cfg["V"], "E": cfg["E"], "F": cfg["F"], "H": cfg["H"], "C": cfg["C"],
-            "layers": 2, "interval_size": cfg["V"], "split_edges": a.split_edges,
-            "parallelism": "single GPU" if world == 1 else f"dest-interval sharding x{world}",
+            "layers": 2, "split_edges": a.split_edges,
+            "interval_size": cfg["V"] if (world == 1 and a.engine != "dist") else -(-cfg["V"] // world),
+            "parallelism": ("single GPU" if world == 1 and a.engine != "dist" else
+                            f"dest-interval sharding x{world} (reencode_balance, NCCL block broadcasts)"),
             "l2": "256 MiB L2 flush between timed steps; inputs (X, edge index) > L2"}
 
 
@@ -215,10 +225,14 @@ def run_ours(a, cfg):
     from paper_1810_08403_b200 import _lib
 
     rank, local, world = dist_env()
-    if world > 1:
+    if world > 1 or a.engine == "dist":
         from paper_1810_08403_b200 import dist
 
-        return dist.bench_main(a, cfg, METRIC, config_of(cfg, a, world))
+        for k, v in (("MASTER_ADDR", "127.0.0.1"), ("MASTER_PORT", "29533"), ("RANK", "0"),
+                     ("WORLD_SIZE", "1"), ("LOCAL_RANK", "0")):
+            os.environ.setdefault(k, v)
+        return dist.bench_main(a, cfg, METRIC, config_of(cfg, a, world),
+                               {"Clocks": Clocks, "measured_peaks": measured_peaks})
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     V, E, F, H, C = cfg["V"], cfg["E"], cfg["F"], cfg["H"], cfg["C"]

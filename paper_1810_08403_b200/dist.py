@@ -3,25 +3,30 @@
 SURVEY.md §8(e), replacing the reference's ring-streaming simulator
  with real collectives over NVLink/NVSwitch:
 
+* vertices are first re-encoded with ``reencode_balance`` for
+  P = world intervals, so every rank owns about |V|/world vertices AND about |E|/world
+  edge endpoints (R-MAT concentrates edges on low ids; without it rank 0 would own
+  most in-edges);
 * the 2D grid uses P = world intervals; rank r owns destination interval D_r (and,
   since layer outputs are indexed like inputs, source interval S_r = D_r of the next
   layer), the CSC chunks C_{i,r} of its column and the CSR chunks C_{r,j} of its row;
-* forward, per layer: every source-feature block h_i is broadcast by its owner (NCCL,
-  posted asynchronously in ascending i); the fused gather over C_{i,r} waits only for
-  block i, so it overlaps the transfer of the later blocks, and accumulates into the
-  resident A_r in ascending i -- the chunked engine's Locality order, so the result
-  equals the 1-GPU chunked run with P = world bit for bit -- then ApplyVertex on the
-  local rows;
+* forward, per layer: every source-feature block (h_i for GCN, [h_i | P_i] for G-GCN)
+  is broadcast by its owner (NCCL, posted asynchronously in ascending i); the fused
+  gather over C_{i,r} waits only for block i, so it overlaps the transfer of the later
+  blocks, and accumulates into the resident A_r in ascending i -- the chunked engine's
+  Locality order, so the aggregate equals the 1-GPU chunked run with P = world bit for
+  bit -- then ApplyVertex on the local rows;
 * loss: softmax-CE over local rows normalised by the global |V|, loss all-reduced;
-* backward: dW_r = a_r^T dz_r all-reduced; dA blocks streamed the same way; the CSR
-  duals over C_{r,j} (ascending j) produce dz for the local sources with the ReLU mask
-  of the layer below fused.
+* backward: dW_r = a_r^T dz_r all-reduced; GCN streams the dA blocks and runs the CSR
+  duals over C_{r,j} (ascending j) with the ReLU mask of the layer below fused; G-GCN
+  runs pass A (CSC, dQ) over the [h | P] blocks kept from the forward, streams the
+  [dA | Q] blocks and runs pass B (CSR, dP and the take_rows part of dh) over them.
 NVSwitch gives every GPU full bandwidth to every peer, so the reference's fat-tree /
 ring ordering (built to avoid shared PCIe links) reduces to per-block broadcasts.
 
 Compute is behind a small backend interface so the host-side logic (sharding,
 ordering, collectives) runs in CPU tests with the gloo backend; the product backend
-is ``CudaCompute`` (libsagann kernels + NCCL).
+is ``CudaCompute`` (libsagann kernels; NCCL for the collectives).
 """
 
 import time
@@ -39,18 +44,30 @@ def _ld(n, align=4):
 
 
 class ShardIndex:
-    """Rank ``rank``'s share of the P = world chunk grid (device pass indices)."""
+    """Rank ``rank``'s share of the P = world chunk grid (device pass indices).
+
+    ``balance``: re-encode the graph with reencode_balance(world) first; ``perm`` maps
+    old -> new vertex ids and ``vertices`` lists the ORIGINAL ids of the local rows
+    (select features / labels with it)."""
 
     def __init__(self, g, world, rank, split_edges=G.DEFAULT_SPLIT_EDGES, device="cuda",
-                 gcn_weights=True):
+                 gcn_weights=True, balance=True):
         size = -(-g.V // world)
+        if balance and world > 1:
+            g, perm = G.reencode_balance(g, world)
+        else:
+            perm = np.arange(g.V, dtype=np.int64)
+        inv = np.empty_like(perm)
+        inv[perm] = np.arange(g.V, dtype=np.int64)
         part = G.partition_2d(g, size)
         if part.P != world:
             raise ValueError(f"V={g.V} too small to shard over {world} ranks")
+        self.graph, self.perm = g, perm
         self.V, self.E, self.world, self.rank, self.size = g.V, g.E, world, rank, size
         self.sizes = [int(s) for s in part.sizes]
         self.begin = rank * size
         self.rows = self.sizes[rank]
+        self.vertices = inv[self.begin: self.begin + self.rows]
         degs = g.degrees() if gcn_weights else None
         self.csc, self.csr = {}, {}
         for i in range(world):
@@ -78,12 +95,20 @@ class CudaCompute:
     def zeros(self, rows, cols):
         return torch.zeros((rows, _ld(cols)), dtype=torch.float32, device=self.device)[:, :cols]
 
-    def gather(self, pi, H, out, F, accumulate, mask=None):
-        self.K.propagate(pi, _lib.PROP_GCN, H, out, F, accumulate=accumulate, mask=mask, ws=self.ws)
+    def propagate(self, pi, mode, Gm, out, F, *, g_off=0, R=None, r_off=0, out1=None, mask=None,
+                  accumulate=False):
+        self.K.propagate(pi, mode, Gm, out, F, g_off=g_off, R=R, r_off=r_off, out1=out1, mask=mask,
+                         accumulate=accumulate, ws=self.ws)
 
     def gemm(self, A, B, C, trans_a=False, trans_b=False, relu_out=None):
         self.K.gemm(A, B, C, trans_a=trans_a, trans_b=trans_b, relu_out=relu_out, prec=self.prec,
                     ws=self.ws)
+
+    def add(self, a, b, out):
+        self.K.ewise(0, a, b, out)
+
+    def relu_bwd(self, g, z, out):
+        self.K.ewise(8, g, z, out)
 
     def xent(self, Z, labels, loss, dZ, err, n_total):
         self.K.softmax_xent(Z, labels, loss, dZ, err, relu_input=True, n_total=n_total, ws=self.ws)
@@ -91,78 +116,161 @@ class CudaCompute:
     def sgd(self, W, dW, lr):
         self.K.sgd(W, dW, lr)
 
+    def launches(self):
+        return int(_lib.lib.sg_launch_count())
 
-class DistGCN:
-    """L-layer GCN (dims = [F, H, ..., C]) sharded over the ranks of ``group``."""
 
-    def __init__(self, shard, dims, compute, weights=None, seed=2, group=None, dtype=torch.float32):
-        self.s, self.c, self.dims, self.group = shard, compute, list(dims), group
+class DistSAGA:
+    """L-layer GCN or G-GCN (dims = [F, H, ..., C]) sharded over the ranks of ``group``.
+
+    Parameters per layer: GCN [W]; G-GCN [W_H, W_C, W] (the single-GPU executor's order).
+    Parameter buffers are 16-B padded (the tensor-core GEMM's TMA path)."""
+
+    def __init__(self, shard, dims, compute, model="gcn", weights=None, seed=2, group=None,
+                 dtype=torch.float32):
+        if model not in ("gcn", "ggcn"):
+            raise ValueError(f"unknown model '{model}' (gcn | ggcn)")
+        self.s, self.c, self.dims, self.group, self.model = shard, compute, list(dims), group, model
         self.dtype = dtype
         self.world = shard.world
         n, dev = shard.rows, compute.device
-        self.W, self.dW = [], []
-        rng = np.random.default_rng(seed)
-        for k, (fi, fo) in enumerate(zip(dims, dims[1:])):
-            if weights is None:
-                lim = np.sqrt(6.0 / (fi + fo))
-                w = rng.uniform(-lim, lim, (fi, fo)).astype(np.float32)
-            else:
-                w = np.asarray(weights[k])
-            self.W.append(torch.from_numpy(w.copy()).to(dev, dtype))
-            self.dW.append(torch.zeros((fi, fo), dtype=dtype, device=dev))
         L = len(dims) - 1
-        self.h = [compute.zeros(n, dims[0])] + [compute.zeros(n, dims[k + 1]) for k in range(L - 1)]
-        self.a = [compute.zeros(n, dims[k]) for k in range(L)]
-        self.z = [compute.zeros(n, dims[k + 1]) for k in range(L)]
-        self.dz = [compute.zeros(n, dims[k + 1]) for k in range(L)]
-        self.da = [compute.zeros(n, dims[k]) for k in range(L)]
-        self._blocks = {}  # (F, dtype) -> per-source-interval landing buffers
+        shapes = []
+        for fi, fo in zip(dims, dims[1:]):
+            shapes += ([(fi, fi), (fi, fi)] if model == "ggcn" else []) + [(fi, fo)]
+        if weights is None:
+            rng = np.random.default_rng(seed)
+            weights = []
+            for fi, fo in shapes:
+                lim = np.sqrt(6.0 / (fi + fo))
+                weights.append(rng.uniform(-lim, lim, (fi, fo)).astype(np.float32))
+        if len(weights) != len(shapes):
+            raise ValueError("wrong number of weight matrices")
+        self.params, self.grads_, self._bufs = [], [], []
+        for (fi, fo), w in zip(shapes, weights):
+            wb = torch.zeros((fi, _ld(fo)), dtype=dtype, device=dev)
+            gb = torch.zeros_like(wb)
+            wb[:, :fo].copy_(torch.as_tensor(np.asarray(w)).to(dtype))
+            self._bufs.append((wb, gb))
+            self.params.append(wb[:, :fo])
+            self.grads_.append(gb[:, :fo])
+        k = 3 if model == "ggcn" else 1
+        self.W = [self.params[k * l + k - 1] for l in range(L)]
+        self.dW = [self.grads_[k * l + k - 1] for l in range(L)]
+        self.h = [compute.zeros(n, dims[0])] + [compute.zeros(n, dims[l + 1]) for l in range(L - 1)]
+        self.a = [compute.zeros(n, dims[l]) for l in range(L)]
+        self.z = [compute.zeros(n, dims[l + 1]) for l in range(L)]
+        self.dz = [compute.zeros(n, dims[l + 1]) for l in range(L)]
+        self.da = [compute.zeros(n, dims[l]) for l in range(L)]
+        if model == "ggcn":
+            self.WH = [self.params[3 * l] for l in range(L)]
+            self.WC = [self.params[3 * l + 1] for l in range(L)]
+            self.dWH = [self.grads_[3 * l] for l in range(L)]
+            self.dWC = [self.grads_[3 * l + 1] for l in range(L)]
+            self.goff = [_ld(dims[l]) for l in range(L)]
+            # per-vertex [h | P] (forward gather operand) and [dA | Q] (backward pass B operand)
+            self.HP = [compute.zeros(n, 2 * self.goff[l]) for l in range(L)]
+            self.GQ = [compute.zeros(n, 2 * self.goff[l]) for l in range(L)]
+            self.dQ = [compute.zeros(n, dims[l]) for l in range(L)]
+            self.dP = [compute.zeros(n, dims[l]) for l in range(L)]
+            self.dHt = [compute.zeros(n, dims[l]) for l in range(L)]
+            F0 = max(dims[:-1])
+            self.t1, self.t2 = compute.zeros(n, F0), compute.zeros(n, F0)
+            self.h[0] = self.HP[0][:, : dims[0]]
+            for l in range(1, L):
+                self.h[l] = self.HP[l][:, : dims[l]]
+        self._blocks = {}  # key -> per-source-interval landing buffers
         self.labels = torch.zeros(n, dtype=torch.int64, device=dev)
         self.loss = torch.zeros(1, dtype=dtype, device=dev)
         self.err = torch.zeros(1, dtype=torch.int32, device=dev)
-        self.comm_s = 0.0
+        self.prof = None
 
     # ---------------------------------------------------------------- data
     def load_features(self, X_local):
-        self.h[0].copy_(torch.as_tensor(X_local)[:, : self.dims[0]])
+        self.h[0].copy_(torch.as_tensor(X_local)[:, : self.dims[0]], non_blocking=True)
 
     def load_labels(self, y_local):
-        self.labels.copy_(torch.as_tensor(np.asarray(y_local, np.int64)))
+        self.labels.copy_(torch.as_tensor(np.asarray(y_local, np.int64)), non_blocking=True)
+
+    def weights(self):
+        return [p.detach().cpu().numpy().copy() for p in self.params]
+
+    def grads(self):
+        return [g.detach().cpu().numpy().copy() for g in self.grads_]
+
+    # ---------------------------------------------------------------- profiling
+    def _mark(self, name):
+        if self.prof is not None:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()
+            self.prof.append((name, e))
+
+    def stage_times(self):
+        out = {}
+        for (_, a), (name, b) in zip(self.prof, self.prof[1:]):
+            if name != "start":
+                out[name] = out.get(name, 0.0) + a.elapsed_time(b)
+        return out
 
     # ---------------------------------------------------------------- collectives
-    def _stream_blocks(self, X, F):
+    def _stream_blocks(self, key, X, width):
         """Post one broadcast per source block (root = its owner), asynchronously and in
-        ascending block order, and return [(block view, work)].  The consumer waits for
-        block i only right before the gather over C_{i,r}, so the gather of block i
+        ascending block order, and return [(block, work)].  The consumer waits for
+        block i only right before the gather over chunk i, so the gather of block i
         overlaps the NVLink transfer of blocks i+1.. (the paper's ring streaming,
-        PAPER.md:495-505, on NVSwitch).  Blocks are padded to 16-byte rows."""
-        ldF = _ld(F)
-        key = (F, X.dtype)
+        PAPER.md:495-505, on NVSwitch).  Blocks are padded to 16-byte rows; the own
+        block is copied in place (its broadcast is the send)."""
+        ldw = _ld(width)
         if key not in self._blocks:
-            self._blocks[key] = [torch.zeros((n, ldF), dtype=X.dtype, device=X.device)
+            self._blocks[key] = [torch.zeros((n, ldw), dtype=X.dtype, device=X.device)
                                  for n in self.s.sizes]
         blocks = self._blocks[key]
-        blocks[self.s.rank][:, :F].copy_(X)
+        blocks[self.s.rank][:, :width].copy_(X[:, :width])
         works = [dist.broadcast(blocks[i], src=i, group=self.group, async_op=True)
                  for i in range(self.world)]
-        return [(b[:, :F], w) for b, w in zip(blocks, works)]
+        return [(b[:, :width], w) for b, w in zip(blocks, works)]
+
+    def _allreduce(self, t):
+        """Sum a parameter gradient over ranks: the whole 16-B padded buffer behind the view
+        (collectives need contiguous memory; the padding columns are zero on every rank)."""
+        dist.all_reduce(t if t.is_contiguous() else t._base, group=self.group)
+
+    @staticmethod
+    def _drain(blocks):
+        for _, w in blocks:
+            w.wait()
 
     # ---------------------------------------------------------------- step
     def forward(self):
         s, c = self.s, self.c
         L = len(self.dims) - 1
+        self._mark("start")
         for l in range(L):
             F = self.dims[l]
-            blocks = self._stream_blocks(self.h[l], F)
             chain = [i for i in range(self.world) if i in s.csc]
+            if self.model == "ggcn":
+                go = self.goff[l]
+                HP = self.HP[l]
+                c.gemm(self.h[l], self.WH[l], HP[:, go: go + F])          # P = h W_H (hoisted)
+                c.gemm(self.h[l], self.WC[l], self.GQ[l][:, go: go + F])  # Q = h W_C
+                self._mark(f"L{l}.fwd.hoist_gemm")
+                blocks = self._stream_blocks(("HP", l), HP, go + F)
+                for k, i in enumerate(chain):
+                    blocks[i][1].wait()
+                    c.propagate(s.csc[i], _lib.PROP_GGCN_FWD, blocks[i][0], self.a[l], F, g_off=go,
+                                R=self.GQ[l][:, go: go + F], accumulate=k > 0)
+            else:
+                blocks = self._stream_blocks(("h", F), self.h[l], F)
+                for k, i in enumerate(chain):   # source intervals ascending (Locality order)
+                    blocks[i][1].wait()
+                    c.propagate(s.csc[i], _lib.PROP_GCN, blocks[i][0], self.a[l], F,
+                                accumulate=k > 0)
             if not chain:
                 self.a[l].zero_()
-            for k, i in enumerate(chain):   # source intervals ascending (Locality order)
-                blocks[i][1].wait()
-                c.gather(s.csc[i], blocks[i][0], self.a[l], F, accumulate=k > 0)
-            for _, w in blocks:
-                w.wait()
+            self._drain(blocks)
+            self._mark(f"L{l}.fwd.propagate")
             c.gemm(self.a[l], self.W[l], self.z[l], relu_out=self.h[l + 1] if l + 1 < L else None)
+            self._mark(f"L{l}.fwd.apply_vertex")
         return self.z[-1]
 
     def backward(self):
@@ -170,72 +278,220 @@ class DistGCN:
         L = len(self.dims) - 1
         c.xent(self.z[-1], self.labels, self.loss, self.dz[-1], self.err, n_total=s.V)
         dist.all_reduce(self.loss, group=self.group)
+        self._mark("loss")
         for l in range(L - 1, -1, -1):
+            F = self.dims[l]
             c.gemm(self.a[l], self.dz[l], self.dW[l], trans_a=True)
-            dist.all_reduce(self.dW[l], group=self.group)
-            if l > 0:
-                F = self.dims[l]
-                c.gemm(self.dz[l], self.W[l], self.da[l], trans_b=True)
-                blocks = self._stream_blocks(self.da[l], F)
-                chain = [j for j in range(self.world) if j in s.csr]
-                if not chain:
-                    self.dz[l - 1].zero_()
-                for k, j in enumerate(chain):  # destination intervals ascending
-                    blocks[j][1].wait()
-                    c.gather(s.csr[j], blocks[j][0], self.dz[l - 1], F, accumulate=k > 0,
-                             mask=self.z[l - 1] if k == len(chain) - 1 else None)
-                for _, w in blocks:
-                    w.wait()
+            self._allreduce(self.dW[l])
+            if self.model == "ggcn":
+                self._backward_ggcn(l)
+                continue
+            if l == 0:
+                self._mark(f"L{l}.bwd.apply_vertex")
+                continue
+            c.gemm(self.dz[l], self.W[l], self.da[l], trans_b=True)
+            self._mark(f"L{l}.bwd.apply_vertex")
+            blocks = self._stream_blocks(("h", F), self.da[l], F)
+            chain = [j for j in range(self.world) if j in s.csr]
+            if not chain:
+                self.dz[l - 1].zero_()
+            for k, j in enumerate(chain):  # destination intervals ascending
+                blocks[j][1].wait()
+                c.propagate(s.csr[j], _lib.PROP_GCN, blocks[j][0], self.dz[l - 1], F,
+                            accumulate=k > 0, mask=self.z[l - 1] if k == len(chain) - 1 else None)
+            self._drain(blocks)
+            self._mark(f"L{l}.bwd.propagate")
         return self.loss
+
+    def _backward_ggcn(self, l):
+        s, c = self.s, self.c
+        F, go = self.dims[l], self.goff[l]
+        GQ = self.GQ[l]
+        c.gemm(self.dz[l], self.W[l], GQ[:, :F], trans_b=True)          # dA = dz W^T
+        self._mark(f"L{l}.bwd.apply_vertex")
+        # pass A over the local CSC column: dQ[u], with the [h | P] blocks of the forward
+        hp_blocks = self._blocks[("HP", l)]
+        chain = [i for i in range(self.world) if i in s.csc]
+        if not chain:
+            self.dQ[l].zero_()
+        for k, i in enumerate(chain):
+            c.propagate(s.csc[i], _lib.PROP_GGCN_BWD_DST, hp_blocks[i][:, : go + F], self.dQ[l], F,
+                        g_off=go, R=GQ, r_off=go, accumulate=k > 0)
+        # pass B over the local CSR row: dP[v], dh_take[v], with streamed [dA | Q] blocks
+        blocks = self._stream_blocks(("GQ", l), GQ, go + F)
+        chain = [j for j in range(self.world) if j in s.csr]
+        if not chain:
+            self.dP[l].zero_()
+            self.dHt[l].zero_()
+        for k, j in enumerate(chain):
+            blocks[j][1].wait()
+            c.propagate(s.csr[j], _lib.PROP_GGCN_BWD_SRC, blocks[j][0], self.dP[l], F, g_off=go,
+                        R=self.HP[l], r_off=go, out1=self.dHt[l], accumulate=k > 0)
+        self._drain(blocks)
+        self._mark(f"L{l}.bwd.propagate")
+        c.gemm(self.h[l], self.dQ[l], self.dWC[l], trans_a=True)        # dW_C = h^T dQ
+        c.gemm(self.h[l], self.dP[l], self.dWH[l], trans_a=True)        # dW_H = h^T dP
+        self._allreduce(self.dWC[l])
+        self._allreduce(self.dWH[l])
+        if l > 0:
+            t1, t2 = self.t1[:, :F], self.t2[:, :F]
+            c.gemm(self.dQ[l], self.WC[l], t1, trans_b=True)
+            c.add(self.dHt[l], t1, t1)                                  # take_rows part + Q part
+            c.gemm(self.dP[l], self.WH[l], t2, trans_b=True)
+            c.add(t1, t2, t1)                                           # + P part (tape order)
+            c.relu_bwd(t1, self.z[l - 1], self.dz[l - 1])
+        self._mark(f"L{l}.bwd.hoist_gemm")
+
+    def sgd(self, lr):
+        for wb, gb in self._bufs:
+            self.c.sgd(wb, gb, lr)
+        self._mark("sgd")
 
     def train_step(self, lr=0.01):
         self.forward()
         self.backward()
-        for W, dW in zip(self.W, self.dW):
-            self.c.sgd(W, dW, lr)
+        self.sgd(lr)
         return self.loss
 
 
-def bench_main(a, cfg, metric, config):
-    """bench.py --gpus N under torchrun: one process per GPU, NCCL over NVLink."""
+DistGCN = DistSAGA  # the GCN engine of earlier revisions
+
+
+def pass_bytes(model, nnz, rows, F, s=4):
+    """SURVEY.md §8(d) algorithmic bytes of one forward gather pass over a chunk."""
+    if model == "gcn":
+        return nnz * (4 + 4 + F * s) + rows * (4 + F * s)
+    return nnz * (4 + 2 * F * s) + rows * (4 + 2 * F * s)
+
+
+def bench_main(a, cfg, metric, config, helpers):
+    """bench.py --gpus N under torchrun: one process per GPU, NCCL over NVLink.
+
+    Timing: W warm-up steps; K timed steps bracketed by barrier + synchronize, CUDA
+    events per step with an L2 flush between steps, max over ranks; the per-stage
+    times (and the roofline of the layer-1 gather) are max over ranks too."""
     import json
     import os
 
-    rank, local = int(os.environ["RANK"]), int(os.environ.get("LOCAL_RANK", 0))
-    world = int(os.environ["WORLD_SIZE"])
+    rank, local = int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl")
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
     V, E, F, H, C = cfg["V"], cfg["E"], cfg["F"], cfg["H"], cfg["C"]
-    if cfg["model"] != "gcn":
-        raise SystemExit("multi-GPU bench implements the GCN workload")
+    t0 = time.perf_counter()
     g = (G.rmat_graph if cfg["graph"] == "rmat" else G.uniform_graph)(V, E, seed=0)
-    shard = ShardIndex(g, world, rank, split_edges=a.split_edges, device=f"cuda:{local}")
-    model = DistGCN(shard, [F, H, C], CudaCompute(f"cuda:{local}"))
-    X = G.synthetic_features(V, F, seed=1)[shard.begin: shard.begin + shard.rows]
-    y = np.random.default_rng(3).integers(0, C, V)[shard.begin: shard.begin + shard.rows]
-    model.load_features(torch.from_numpy(X))
-    model.load_labels(y)
+    shard = ShardIndex(g, world, rank, split_edges=a.split_edges, device=dev,
+                       gcn_weights=cfg["model"] == "gcn")
+    del g
+    t_setup = time.perf_counter() - t0
+    comp = CudaCompute(dev)
+    model = DistSAGA(shard, [F, H, C], comp, model=cfg["model"])
+    X_all = G.synthetic_features(V, F, seed=1)
+    y_all = np.random.default_rng(3).integers(0, C, V)
+    X_host = torch.from_numpy(np.ascontiguousarray(X_all[shard.vertices])).pin_memory()
+    y_host = torch.from_numpy(np.ascontiguousarray(y_all[shard.vertices])).pin_memory()
+    del X_all, y_all
+    model.load_features(X_host)
+    model.load_labels(y_host)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     for _ in range(a.warmup):
         model.train_step(a.lr)
     torch.cuda.synchronize()
+
+    clocks = helpers["Clocks"](local)
+    clocks.start()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
+    marks = []
+    n0 = comp.launches()
     dist.barrier()
-    t0 = time.perf_counter()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev0.record()
-    for _ in range(a.steps):
+    torch.cuda.synchronize()
+    for k in range(a.steps):
+        flush.zero_()
+        model.prof = []
+        starts[k].record()
         model.train_step(a.lr)
-    ev1.record()
+        ends[k].record()
+        marks.append(model.prof)
     torch.cuda.synchronize()
     dist.barrier()
-    ms = torch.tensor([ev0.elapsed_time(ev1) / a.steps], device=f"cuda:{local}")
-    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    t = float(ms.item()) / 1e3
+    launches = comp.launches() - n0
+    clk = clocks.stop()
+    step_ms = [s_.elapsed_time(e) for s_, e in zip(starts, ends)]
+    stages = {}
+    for mk in marks:
+        model.prof = mk
+        for kname, v in model.stage_times().items():
+            stages[kname] = stages.get(kname, 0.0) + v / a.steps
+    model.prof = None
+    names = sorted(stages)
+    vec = torch.tensor([float(np.mean(step_ms))] + [stages[k] for k in names], device=dev,
+                       dtype=torch.float64)
+    dist.all_reduce(vec, op=dist.ReduceOp.MAX)
+    t_step = float(vec[0].item()) / 1e3
+    stages_max = {k: float(v) for k, v in zip(names, vec[1:].tolist())}
+    if int(model.err.item()):
+        raise RuntimeError("label out of range")
+
+    # roofline of the layer-1 forward gather: all ranks' algorithmic bytes over the
+    # slowest rank's stage time (it includes waiting for streamed blocks)
+    my_bytes = sum(pass_bytes(cfg["model"], pi.nnz, pi.n_rows, F) for pi in shard.csc.values())
+    tb = torch.tensor([float(my_bytes)], device=dev, dtype=torch.float64)
+    dist.all_reduce(tb)
+    k_ms = stages_max.get("L0.fwd.propagate")
+    peak, peak_src = helpers["measured_peaks"]()
+    achieved = float(tb.item()) / (k_ms / 1e3) / 1e9 if k_ms else None
+
+    # e2e: per step H2D of the local feature/label shard from pinned memory, the step,
+    # and the loss read back; wall clock, max over ranks
+    e2e = None
+    if not a.no_e2e:
+        n_e2e = max(3, a.steps // 2)
+        torch.cuda.synchronize()
+        dist.barrier()
+        t1 = time.perf_counter()
+        for _ in range(n_e2e):
+            model.load_features(X_host)
+            model.load_labels(y_host)
+            model.train_step(a.lr)
+            float(model.loss.item())
+        te = torch.tensor([(time.perf_counter() - t1) / n_e2e], device=dev, dtype=torch.float64)
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        bi = torch.tensor([float(X_host.numel() * 4 + y_host.numel() * 8)], device=dev,
+                          dtype=torch.float64)
+        dist.all_reduce(bi)
+        t_e2e = float(te.item())
+        e2e = {"value": E / t_e2e, "unit": "edges/s", "h2d_bytes_per_step": int(bi.item()),
+               "d2h_bytes_per_step": 4 * world, "ms_per_step": t_e2e * 1e3,
+               "note": "wall clock, max over ranks: per-step H2D of every rank's feature/label "
+                       "shard, the step, loss D2H"}
+    lt = torch.tensor([float(launches)], device=dev, dtype=torch.float64)
+    dist.all_reduce(lt)
+    shard_edges = _gather_ints(shard.local_edges, world, dev)
     if rank == 0:
-        line = {"metric": metric, "value": E / t, "unit": "edges/s", "n_gpus": world,
-                "steps": a.steps, "warmup": a.warmup, "ms_per_step": t * 1e3,
+        line = {"metric": metric, "value": E / t_step, "unit": "edges/s", "n_gpus": world,
+                "steps": a.steps, "warmup": a.warmup, "ms_per_step": t_step * 1e3,
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
                 "dtype": "f32", "data": "synthetic", "config": config,
-                "wall_s": time.perf_counter() - t0,
-                "gpu_launches": None, "e2e": None, "roofline": None, "cpu_baseline": None}
+                "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak * world,
+                             "unit": "GB/s", "frac": achieved / (peak * world) if achieved else None,
+                             "traffic": None,
+                             "kernel": f"L0.fwd.propagate ({cfg['model']} gather, F={F}), all ranks",
+                             "algorithmic_bytes_per_launch": float(tb.item()), "launch_ms": k_ms,
+                             "peak_source": peak_src + f" x {world} GPUs"},
+                "e2e": e2e, "cpu_baseline": None, "gpu_launches": int(lt.item()),
+                "clocks": clk, "stages_ms": {k: round(v, 4) for k, v in stages_max.items()},
+                "shard_edges": [int(x) for x in shard_edges],
+                "setup_s": round(t_setup, 2),
+                "step_ms_all": [round(x, 3) for x in step_ms]}
         print(json.dumps(line), flush=True)
+    dist.barrier()
     dist.destroy_process_group()
+
+
+def _gather_ints(x, world, dev):
+    t = torch.zeros(world, dtype=torch.int64, device=dev)
+    t[dist.get_rank()] = int(x)
+    dist.all_reduce(t)
+    return t.tolist()

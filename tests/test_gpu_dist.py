@@ -1,0 +1,106 @@
+"""Multi-GPU engine with the REAL product backend (libsagann kernels) on one GPU.
+
+NCCL refuses two ranks on one device, so these tests run the sharded engine of
+paper_1810_08403_b200.dist with world_size 2 over gloo (which moves CUDA tensors through
+host memory) with both ranks on cuda:0 and ``CudaCompute`` doing every gather, GEMM and
+loss.  The result must equal the single-GPU chunked executor with P = world on the same
+re-encoded graph: layer-1 aggregates bitwise (same kernels, same chunk order), the rest
+within fp32 reduction-order tolerance (dW is a sum of per-rank partials).
+"""
+
+import os
+import socket
+import tempfile
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from conftest import assert_close
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    with socket.socket() as sck:
+        sck.bind(("127.0.0.1", 0))
+        return sck.getsockname()[1]
+
+
+def _graph(gen, V, E):
+    import paper_1810_08403_b200 as sg
+
+    return (sg.rmat_graph if gen == "rmat" else sg.uniform_graph)(V, E, seed=5)
+
+
+def _worker(rank, world, port, case, outdir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_1810_08403_b200 as sg
+    from paper_1810_08403_b200 import dist as D
+
+    model, V, E, F, H, C, gen, T = case
+    g = _graph(gen, V, E)
+    shard = D.ShardIndex(g, world, rank, split_edges=T, device="cuda:0", gcn_weights=model == "gcn")
+    m = D.DistSAGA(shard, [F, H, C], D.CudaCompute("cuda:0"), model=model, seed=2)
+    X = sg.synthetic_features(V, F, seed=1)
+    y = np.random.default_rng(3).integers(0, C, V)
+    m.load_features(torch.from_numpy(X[shard.vertices]))
+    m.load_labels(y[shard.vertices])
+    n0 = sg._lib.lib.sg_launch_count()
+    m.forward()
+    m.backward()
+    torch.cuda.synchronize()
+    launched = sg._lib.lib.sg_launch_count() - n0
+    out = dict(loss=m.loss.cpu().numpy(), a0=m.a[0].cpu().numpy(), z1=m.z[1].cpu().numpy(),
+               begin=shard.begin, perm=shard.perm, launched=launched)
+    for k, gr in enumerate(m.grads()):
+        out[f"g{k}"] = gr
+    np.savez(os.path.join(outdir, f"r{rank}.npz"), **out)
+    dist.destroy_process_group()
+
+
+CASES = [("gcn", 3000, 60000, 37, 16, 5, "rmat", 4096), ("gcn", 2500, 40000, 130, 24, 7, "uniform", 64),
+         ("ggcn", 2000, 30000, 32, 16, 5, "rmat", 128)]
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_dist_world2_cuda_matches_single_gpu_chunked(case):
+    import paper_1810_08403_b200 as sg
+
+    world = 2
+    with tempfile.TemporaryDirectory() as outdir:
+        mp.start_processes(_worker, args=(world, _free_port(), case, outdir), nprocs=world,
+                           join=True, start_method="spawn")
+        res = [dict(np.load(os.path.join(outdir, f"r{r}.npz"))) for r in range(world)]
+    model, V, E, F, H, C, gen, T = case
+    g = _graph(gen, V, E)
+    g2, perm = sg.reencode_balance(g, world)
+    assert np.array_equal(res[0]["perm"], perm)
+    inv = np.argsort(perm)
+    grid = sg.ChunkGrid(g2, -(-V // world), split_edges=T, gcn_weights=model == "gcn")
+    build = sg.gcn_model if model == "gcn" else sg.ggcn_model
+    m = build(grid, [F, H, C], seed=2)
+    m.load_features(torch.from_numpy(sg.synthetic_features(V, F, seed=1)[inv]))
+    m.load_labels(np.random.default_rng(3).integers(0, C, V)[inv])
+    m.forward()
+    m.backward()
+    torch.cuda.synchronize()
+    a0 = m.layers[0].a.cpu().numpy()
+    z1 = m.layers[1].z.cpu().numpy()
+    grads = m.grads()
+    for r in range(world):
+        assert res[r]["launched"] > 0
+        b = int(res[r]["begin"])
+        n = res[r]["a0"].shape[0]
+        if model == "gcn":
+            assert np.array_equal(res[r]["a0"], a0[b: b + n]), "sharded aggregate differs"
+        else:
+            assert_close(res[r]["a0"], a0[b: b + n], rel=1e-5, what="a0")
+        assert_close(res[r]["z1"], z1[b: b + n], rel=1e-5, what="z1")
+        assert abs(float(res[r]["loss"][0]) - m.loss.item()) <= 1e-5 * m.loss.item()
+        for k, gw in enumerate(grads):
+            assert_close(res[r][f"g{k}"], gw, rel=1e-5, what=f"grad {k}")
