@@ -50,7 +50,7 @@ struct ModeT;
 
 template <>
 struct ModeT<SG_PROP_PASS> {
-  static constexpr int NG = 1, NR = 0, NOUT = 1;
+  static constexpr int NG = 1, NR = 0, NOUT = 1, GATE_ROW = -1;
   static constexpr bool USE_W = false;
   static __device__ __forceinline__ void term(const float* g0, const float*, const float*,
                                               const float*, float, float* t0, float*) {
@@ -60,7 +60,7 @@ struct ModeT<SG_PROP_PASS> {
 
 template <>
 struct ModeT<SG_PROP_GCN> {
-  static constexpr int NG = 1, NR = 0, NOUT = 1;
+  static constexpr int NG = 1, NR = 0, NOUT = 1, GATE_ROW = -1;
   static constexpr bool USE_W = true;
   // mul(take_rows(H, src), w): x * w (tensor.py:249); mul bwd g * w (tensor.py:263)
   static __device__ __forceinline__ void term(const float* g0, const float*, const float*,
@@ -82,34 +82,52 @@ __device__ __forceinline__ void add2_rn(float& a0, float& a1, float t0, float t1
       : "f"(t0), "f"(t1));
 }
 
-__device__ __forceinline__ float sigmoid_ref(float x) {
-  // 1.0 / (1.0 + np.exp(-x))  (tensor.py:205).  Not bit-comparable with numpy's exp in
-  // any case, so use MUFU-based __expf (~2 ulp) and the correctly rounded reciprocal:
-  // the G-GCN passes were instruction bound with expf + IEEE division (BlogCatalog x10).
-  return __frcp_rn(__fadd_rn(1.0f, __expf(-x)));
+// Gate sigmoid.  The reference computes 1.0 / (1.0 + np.exp(-x)) (tensor.py:205); device exp
+// is not bit-comparable with numpy's anyway, so the gate uses the SFU: eta = rcp(1 + 2^t)
+// with t = -log2(e) * (P + Q) formed by ONE fma from the pre-scaled row operand
+// (rs = -log2(e) * Q, scaled once per row in load_row_state).  ex2.approx / rcp.approx are
+// within 2 ulp; 2^t -> inf gives eta = 0 and 2^t -> 0 gives 1 with no special-case path
+// (the IEEE __frcp_rn's slow path cost 2x on saturated gates).
+constexpr float kNegLog2e = -1.4426950408889634f;
+
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// sigmoid(p + q) given p and qs = -log2(e) * q
+__device__ __forceinline__ float gate(float p, float qs) {
+  return rcp_approx(__fadd_rn(1.0f, ex2_approx(__fmaf_rn(p, kNegLog2e, qs))));
 }
 
 template <>
 struct ModeT<SG_PROP_GGCN_FWD> {
-  static constexpr int NG = 2, NR = 1, NOUT = 1;
+  static constexpr int NG = 2, NR = 1, NOUT = 1, GATE_ROW = 0;
   static constexpr bool USE_W = false;
   // G = [h | P] row of v, R = Q row of u: eta = sigmoid(P[v] + Q[u]); t = eta * h[v]
   static __device__ __forceinline__ void term(const float* g0, const float* g1, const float* r0,
                                               const float*, float, float* t0, float*) {
-    float eta = sigmoid_ref(__fadd_rn(g1[0], r0[0]));
+    float eta = gate(g1[0], r0[0]);
     t0[0] = __fmul_rn(eta, g0[0]);
   }
 };
 
 template <>
 struct ModeT<SG_PROP_GGCN_BWD_DST> {
-  static constexpr int NG = 2, NR = 2, NOUT = 1;
+  static constexpr int NG = 2, NR = 2, NOUT = 1, GATE_ROW = 1;
   static constexpr bool USE_W = false;
   // CSC row u.  G = [h | P] of v, R = [dA | Q] of u.
   // g_eta = dA[u] * h[v] (mul bwd, tensor.py:263); t = (g_eta * eta) * (1 - eta) (tensor.py:232)
   static __device__ __forceinline__ void term(const float* g0, const float* g1, const float* r0,
                                               const float* r1, float, float* t0, float*) {
-    float eta = sigmoid_ref(__fadd_rn(g1[0], r1[0]));
+    float eta = gate(g1[0], r1[0]);
     float ge = __fmul_rn(r0[0], g0[0]);
     t0[0] = __fmul_rn(__fmul_rn(ge, eta), __fsub_rn(1.0f, eta));
   }
@@ -117,13 +135,13 @@ struct ModeT<SG_PROP_GGCN_BWD_DST> {
 
 template <>
 struct ModeT<SG_PROP_GGCN_BWD_SRC> {
-  static constexpr int NG = 2, NR = 2, NOUT = 2;
+  static constexpr int NG = 2, NR = 2, NOUT = 2, GATE_ROW = 1;
   static constexpr bool USE_W = false;
-  // CSR row v.  G = [dA | Q] of u, R = [h | P] of v.
+  // CSR row v.  G = [dA | Q] of u, R = [h | P] of v (gate operand: the row's P, pre-scaled).
   // dP[v] += (dA[u]*h[v]*eta)*(1-eta);  dH[v] += dA[u] * eta  (g_hs = g * eta)
   static __device__ __forceinline__ void term(const float* g0, const float* g1, const float* r0,
                                               const float* r1, float, float* t0, float* t1) {
-    float eta = sigmoid_ref(__fadd_rn(r1[0], g1[0]));
+    float eta = gate(g1[0], r1[0]);
     float ge = __fmul_rn(g0[0], r0[0]);
     t0[0] = __fmul_rn(__fmul_rn(ge, eta), __fsub_rn(1.0f, eta));
     t1[0] = __fmul_rn(g0[0], eta);
@@ -318,8 +336,13 @@ struct Prop {
       const int cv = v * LPR + tl;
       if (cv < a.Fv) {
 #pragma unroll
-        for (int q = 0; q < NR; ++q)
+        for (int q = 0; q < NR; ++q) {
           IO::ld_cs(a.R, r * a.ldr + (q ? a.r_off : 0) + (int64_t)cv * W, rs[q][v]);
+          if (q == M::GATE_ROW) {  // gate operand pre-scaled by -log2(e), once per row
+#pragma unroll
+            for (int k = 0; k < W; ++k) rs[q][v][k] = __fmul_rn(rs[q][v][k], kNegLog2e);
+          }
+        }
       }
     }
   }
