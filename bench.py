@@ -62,6 +62,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--split-edges", type=int, default=4096)
+    ap.add_argument("--no-reorder", action="store_true",
+                    help="skip the secondary reorder_linear_gather measurement")
     ap.add_argument("--engine", choices=["auto", "dist"], default="auto",
                     help="dist: run the sharded multi-GPU engine (NCCL) even at N=1")
     return ap.parse_args()
@@ -308,7 +310,7 @@ def run_ours(a, cfg):
     if not a.no_e2e:
         # every step: H2D of that step's features + labels from pinned host memory (staged
         # on a copy stream while the previous step computes) and D2H of its loss
-        n_e2e = max(3, a.steps // 2)
+        n_e2e = max(5, a.steps)
         m.capture(a.lr)  # one CUDA-graph launch per epoch (forward, backward, SGD)
         torch.cuda.synchronize()
         t1 = time.perf_counter()
@@ -323,6 +325,44 @@ def run_ours(a, cfg):
                "h2d_bytes_per_step": int(X_host.numel() * 4 + lab_host.numel() * 8),
                "d2h_bytes_per_step": 4, "ms_per_step": t_e2e * 1e3,
                "note": "wall clock incl. per-step H2D (pipelined on a copy stream) and loss D2H"}
+
+    # ---- secondary: the same epoch with reorder_linear_gather (Y = h W, then propagate Y):
+    # the same function re-associated (fp32-rounding-equal, not bitwise), gathers at the
+    # narrower output widths.  Reported beside the headline, which keeps the reference's
+    # stage order (the F-wide fused gather the roofline is judged on).
+    reordered = None
+    if cfg["model"] == "gcn" and not a.no_reorder:
+        m2 = build(grid, [F, H, C], reorder=True)
+        m2.load_features(X_host)
+        m2.load_labels(lab_host)
+        for _ in range(a.warmup):
+            m2.train_step(a.lr)
+        torch.cuda.synchronize()
+        m2.check_status()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(a.steps)]
+        marks2 = []
+        for k in range(a.steps):
+            flush.zero_()
+            m2.prof = []
+            ev[k][0].record()
+            m2.train_step(a.lr)
+            ev[k][1].record()
+            marks2.append(m2.prof)
+        torch.cuda.synchronize()
+        ms2 = float(np.mean([s_.elapsed_time(e_) for s_, e_ in ev]))
+        st2 = {}
+        for mk in marks2:
+            m2.prof = mk
+            for kname, v in m2.stage_times().items():
+                st2[kname] = st2.get(kname, 0.0) + v / a.steps
+        reordered = {"ms_per_step": ms2, "value": E / (ms2 / 1e3), "unit": "edges/s",
+                     "layers_reordered": [bool(L.reorder) for L in m2.layers],
+                     "stages_ms": {k: round(v, 4) for k, v in st2.items()},
+                     "note": "optimizer pass reorder_linear_gather: ReLU((A h) W) computed as "
+                             "ReLU(A (h W)); loss/gradients within fp32 tolerance of the reference "
+                             "order (tests/test_gpu_kernels.py::test_reordered_gcn_epoch_vs_oracle)"}
+        del m2
 
     # ---- CPU baseline (oracle port) on a bounded sample, rank 0 only
     cpu = None
@@ -349,6 +389,7 @@ def run_ours(a, cfg):
                      "l2_ceiling_gbs": l2_ceiling,
                      "frac_of_l2_ceiling": (achieved / l2_ceiling) if (achieved and l2_ceiling) else None},
         "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": int(launches),
+        "reordered_apply_vertex": reordered,
         "clocks": clk,
         "stages_ms": {k: round(v, 4) for k, v in stages.items()},
         "scatter_gather_edges_per_s": (E / (k_ms / 1e3)) if k_ms else None,

@@ -300,32 +300,79 @@ struct Prop {
         }
       }
     } else {
-      // narrow rows: every team lane reads the (broadcast) index directly
-      int64_t e = e0;
-      #pragma unroll 1
-      for (; e + DEPTH <= e1; e += DEPTH) {
-        int s[DEPTH];
-        float wv[DEPTH];
+      // narrow rows (teams of LPR lanes, one row each): the team loads a window of WIN
+      // (src, w) pairs coalesced -- WPL per lane -- and broadcasts them inside the team by
+      // width-LPR shuffles; the next window is prefetched while this one is consumed, so
+      // the index load latency no longer serialises with the row loads.
+      constexpr int WIN = LPR > DEPTH ? LPR : DEPTH;
+      constexpr int WPL = WIN / LPR;
+      int src_next[WPL];
+      float w_next[WPL];
+      int n_next = (int)min((int64_t)WIN, e1 - e0);
 #pragma unroll
-        for (int d = 0; d < DEPTH; ++d) {
-          s[d] = __ldcs(a.idx + e + d);
-          wv[d] = M::USE_W ? __ldcs(a.w + e + d) : 0.f;
-        }
-        step<true>(a, gl, hl, last_ok, s, wv, DEPTH, rs, acc);
+      for (int q = 0; q < WPL; ++q) {
+        const int k = q * LPR + tl;
+        src_next[q] = k < n_next ? __ldcs(a.idx + e0 + k) : 0;
+        w_next[q] = (M::USE_W && k < n_next) ? __ldcs(a.w + e0 + k) : 0.f;
       }
-      if (e < e1) {
-        const int n = (int)(e1 - e);
-        int s[DEPTH];
-        float wv[DEPTH];
+      #pragma unroll 1
+      for (int64_t eb = e0; eb < e1; eb += WIN) {
+        const int n = n_next;
+        int my_src[WPL];
+        float my_w[WPL];
 #pragma unroll
-        for (int d = 0; d < DEPTH; ++d) {
-          s[d] = d < n ? __ldcs(a.idx + e + d) : 0;
-          wv[d] = (M::USE_W && d < n) ? __ldcs(a.w + e + d) : 0.f;
+        for (int q = 0; q < WPL; ++q) {
+          my_src[q] = src_next[q];
+          my_w[q] = w_next[q];
         }
-        step<false>(a, gl, hl, last_ok, s, wv, n, rs, acc);
+        n_next = (int)min((int64_t)WIN, e1 - (eb + WIN));
+#pragma unroll
+        for (int q = 0; q < WPL; ++q) {
+          const int k = q * LPR + tl;
+          if (k < n_next) {
+            src_next[q] = __ldcs(a.idx + eb + WIN + k);
+            if (M::USE_W) w_next[q] = __ldcs(a.w + eb + WIN + k);
+          }
+        }
+        if constexpr (WPL > 1) {
+          // WIN == DEPTH: one step per window, edge d sits in slot d / LPR of lane d % LPR
+          int s[DEPTH];
+          float wv[DEPTH];
+#pragma unroll
+          for (int d = 0; d < DEPTH; ++d) {
+            s[d] = __shfl_sync(tmask, my_src[d / LPR], d % LPR, LPR);
+            wv[d] = M::USE_W ? __shfl_sync(tmask, my_w[d / LPR], d % LPR, LPR) : 0.f;
+          }
+          if (n == DEPTH)
+            step<true>(a, gl, hl, last_ok, s, wv, DEPTH, rs, acc);
+          else
+            step<false>(a, gl, hl, last_ok, s, wv, n, rs, acc);
+        } else {
+          int d0 = 0;
+          #pragma unroll 1
+          for (; d0 + DEPTH <= n; d0 += DEPTH) {
+            int s[DEPTH];
+            float wv[DEPTH];
+#pragma unroll
+            for (int d = 0; d < DEPTH; ++d) {
+              s[d] = __shfl_sync(tmask, my_src[0], d0 + d, LPR);
+              wv[d] = M::USE_W ? __shfl_sync(tmask, my_w[0], d0 + d, LPR) : 0.f;
+            }
+            step<true>(a, gl, hl, last_ok, s, wv, DEPTH, rs, acc);
+          }
+          if (d0 < n) {
+            int s[DEPTH];
+            float wv[DEPTH];
+#pragma unroll
+            for (int d = 0; d < DEPTH; ++d) {
+              s[d] = __shfl_sync(tmask, my_src[0], (d0 + d) & (LPR - 1), LPR);
+              wv[d] = M::USE_W ? __shfl_sync(tmask, my_w[0], (d0 + d) & (LPR - 1), LPR) : 0.f;
+            }
+            step<false>(a, gl, hl, last_ok, s, wv, n - d0, rs, acc);
+          }
+        }
       }
     }
-    (void)tmask;
   }
 
   static __device__ __forceinline__ void load_row_state(const PropArgs& a, int64_t r, int tl,
@@ -559,6 +606,17 @@ cudaError_t launch_tma(const PropArgs& a, cudaStream_t st) {
 // slower than the register path on the Reddit-shaped pass (20.1 vs 17.1 ms): that pass
 // is bound by L2 throughput (~72% of peak), not by per-warp loads in flight.
 // SG_PROP_TEAM2=1: rows of 17..32 vectors (F 65..128 fp32) as half-warp teams (A/B knob).
+// SG_PROP_TEAM_MAXV: widest row (in 16-B vectors) still given to a lane team of < 32 lanes;
+// wider rows take one warp per row (A/B knob, default 16).
+int team_max_vectors() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SG_PROP_TEAM_MAXV");
+    v = e ? atoi(e) : 16;
+  }
+  return v;
+}
+
 bool team_rows() {
   static int on = -1;
   if (on < 0) {
@@ -771,7 +829,13 @@ int sg_propagate_hub(int mode, int dtype, const int64_t* ptr, const int32_t* idx
     const int64_t cols = std::min(slice_cols, F - c0);
     const int Fv = (int)((cols + W - 1) / W);
     int LPR = 32, VPL = (Fv + 31) / 32;
-    if (Fv <= 16) {
+    // Lane teams (one narrow row per team, 32/LPR rows per warp) pay off when items hold
+    // many similar rows (uniform graphs: 2-4x, tools/sweep.py).  When split subgroups are
+    // half the plan's items or more (R-MAT hubs: Reddit 56% of edges in rows > T), only
+    // team 0 works on split items and heavy packed rows leave teams idle: one warp per row
+    // measured 17% faster there (tools/narrow_ab.py), so teams are not used.
+    const bool hub_heavy = n_slots * 2 >= n_items;
+    if (Fv <= team_max_vectors() && Fv <= 16 && !hub_heavy) {
       LPR = 2;
       while (LPR < Fv) LPR *= 2;
       VPL = 1;

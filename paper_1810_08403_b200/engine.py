@@ -57,7 +57,7 @@ class SAGAModel:
     gather (gcn / pass / ggcn) followed by ApplyVertex = ReLU(W accum)."""
 
     def __init__(self, programs, grid, weights=None, *, seed=2, gemm_prec=_lib.GEMM_TF32X3,
-                 device="cuda", strict=True, schedule="locality"):
+                 device="cuda", strict=True, schedule="locality", reorder=False):
         if not torch.cuda.is_available():
             raise RuntimeError("SAGAModel needs a CUDA device (no CPU fallback)")
         if schedule not in ("locality", "dest_order"):
@@ -69,8 +69,9 @@ class SAGAModel:
         self.ws = K.Workspace(self.device)
         self.layers = []
         dims = []
+        self.reorder = bool(reorder)
         for p in programs:
-            q, reports = prog.optimize(p)
+            q, reports = prog.optimize(p, reorder=self.reorder)
             diags = prog.validate_program(q)
             if diags:
                 raise ProgramError("; ".join(diags))
@@ -87,6 +88,8 @@ class SAGAModel:
             L.prog, L.kind, L.F, L.O = q, q.fused.kind, q.f_in, q.f_out
             L.vform, L.wname = form[0], form[1:]
             L.gate = q.fused.params
+            # reorder_linear_gather: Y = h W per vertex, then propagate Y (width O)
+            L.reorder = bool(getattr(q, "reorder", False))
             # accumulator width: the pooled width for MP-GCN, else the input width
             L.Aw = q.params[L.gate[0]][1] if L.kind == "max_pool" else q.f_in
             self.layers.append(L)
@@ -210,10 +213,12 @@ class SAGAModel:
                 L.dparams = [L.dWH, L.dWC, L.dW]
             else:
                 L.hin = None  # set below (previous layer's ReLU output or X)
-                L.da = _mat(V, F, dev)
+                L.da = _mat(V, F, dev) if not L.reorder else None
                 L.params = [L.W]
                 L.dparams = [L.dW]
-            L.a = _mat(V, F, dev)
+                if L.reorder:
+                    L.Y, L.dY = _mat(V, O, dev), _mat(V, O, dev)
+            L.a = _mat(V, F, dev) if not getattr(L, "reorder", False) else None
             L.z = _mat(V, O, dev)
             L.dz = _mat(V, O, dev)
         for n, L in enumerate(self.layers):
@@ -289,11 +294,15 @@ class SAGAModel:
         b = self.grid.begin(k)
         return t[b: b + self.grid.size(k)]
 
-    def _fwd_propagate(self, L, stream=None):
+    def _fwd_propagate(self, L, stream=None, src=None, out=None, F=None):
+        """Forward gather over the CSC chunks: src (default L.hin) -> out (default L.a)."""
         g, P = self.grid, self.grid.P
+        src = L.hin if src is None else src
+        out = L.a if out is None else out
+        F = L.F if F is None else F
         for j in range(P):
             if not any((i, j) in g.csc for i in range(P)):
-                self._rows(L.a, j).zero_()
+                self._rows(out, j).zero_()
         for (i, j), first, _ in self._chunk_order(list(g.csc), 1):
             pi = g.csc[(i, j)]
             if L.kind == "ggcn":
@@ -302,7 +311,7 @@ class SAGAModel:
                             stream=stream)
             else:
                 mode = _lib.PROP_GCN if L.kind == "gcn" else _lib.PROP_PASS
-                K.propagate(pi, mode, self._rows(L.hin, i), self._rows(L.a, j), L.F,
+                K.propagate(pi, mode, self._rows(src, i), self._rows(out, j), F,
                             accumulate=not first, ws=self.ws, stream=stream)
 
     def _chunk_order(self, keys, out_axis):
@@ -322,10 +331,13 @@ class SAGAModel:
             chain = per_out[k[out_axis]]
             yield k, k == chain[0], k == chain[-1]
 
-    def _bwd_propagate_gcn(self, L, out, mask, stream=None, onto=False):
+    def _bwd_propagate_gcn(self, L, out, mask, stream=None, onto=False, src=None, F=None):
         """dH[v] = sum_{out(v)} w_e dA[u] over CSR chunks, j ascending; ReLU mask on the last.
-        ``onto``: continue from the value already in ``out`` (CommNet's direct W_H term)."""
+        ``onto``: continue from the value already in ``out`` (CommNet's direct W_H term).
+        ``src`` (default L.da) / ``F`` (default L.F): the gathered gradient and its width."""
         g, P = self.grid, self.grid.P
+        src = L.da if src is None else src
+        F = L.F if F is None else F
         mode = _lib.PROP_GCN if L.kind == "gcn" else _lib.PROP_PASS
         for i in range(P):
             if not any((i, j) in g.csr for j in range(P)):
@@ -335,9 +347,9 @@ class SAGAModel:
                 else:
                     self._rows(out, i).zero_()
         for (i, j), first, last in self._chunk_order(list(g.csr), 0):
-            K.propagate(g.csr[(i, j)], mode, self._rows(L.da, j), self._rows(out, i), L.F,
-                        mask=self._rows(mask, i) if last else None, accumulate=onto or not first,
-                        ws=self.ws, stream=stream)
+            K.propagate(g.csr[(i, j)], mode, self._rows(src, j), self._rows(out, i), F,
+                        mask=self._rows(mask, i) if (last and mask is not None) else None,
+                        accumulate=onto or not first, ws=self.ws, stream=stream)
 
     def _bwd_propagate_ggcn(self, L, stream=None):
         g, P = self.grid, self.grid.P
@@ -411,6 +423,14 @@ class SAGAModel:
                 self._gemm(L.hin, L.WH, L.Pv)   # hoisted P = h W_H
                 self._gemm(L.hin, L.WC, L.Qv)   # hoisted Q = h W_C
                 self._mark(f"L{n}.fwd.hoist_gemm")
+            if L.reorder:  # Y = h W, then z = A Y (reorder_linear_gather)
+                self._gemm(L.hin, L.W, L.Y)
+                self._mark(f"L{n}.fwd.apply_vertex")
+                self._fwd_propagate(L, stream, src=L.Y, out=L.z, F=L.O)
+                if L.hout is not None:
+                    K.ewise(7, L.z, None, L.hout, stream)   # h' = relu(z)
+                self._mark(f"L{n}.fwd.propagate")
+                continue
             if L.kind in ("max", "max_pool"):
                 Y = L.hin
                 if L.kind == "max_pool":       # hoisted edge network Y = sigmoid(h W_pool + b)
@@ -435,8 +455,18 @@ class SAGAModel:
         self._mark("loss")
         for n in range(len(self.layers) - 1, -1, -1):
             L = self.layers[n]
-            self._gemm(L.gin, L.dz, L.dW, trans_a=True)         # dW = a^T dz
             below = self.layers[n - 1] if n > 0 else None
+            if L.reorder:
+                # dY = A^T dz (CSR pass), dW = h^T dY, dh = dY W^T (+ ReLU mask of the layer below)
+                self._bwd_propagate_gcn(L, L.dY, None, stream, src=L.dz, F=L.O)
+                self._mark(f"L{n}.bwd.propagate")
+                self._gemm(L.hin, L.dY, L.dW, trans_a=True)
+                if below is not None:
+                    self._gemm(L.dY, L.W, below.dz, trans_b=True)
+                    K.ewise(8, below.dz, below.z, below.dz, stream)
+                self._mark(f"L{n}.bwd.apply_vertex")
+                continue
+            self._gemm(L.gin, L.dz, L.dW, trans_a=True)         # dW = a^T dz
             if L.kind in ("max", "max_pool"):
                 self._gemm(L.dz, L.W, L.da, trans_b=True)       # dA = dz W^T
                 self._mark(f"L{n}.bwd.apply_vertex")

@@ -361,11 +361,42 @@ def evaluate_expr(e, bindings):
     return ev(e)
 
 
-def optimize(p):
-    """hoist then fuse (the paper's pipeline)."""
+def optimize(p, reorder=False):
+    """hoist then fuse (the paper's pipeline); optionally then
+    ``reorder_linear_gather``."""
     q, r1 = hoist_vertex_computation(p)
     q, r2 = fuse_sag(q)
-    return q, [r1, r2]
+    if not reorder:
+        return q, [r1, r2]
+    q, r3 = reorder_linear_gather(q)
+    return q, [r1, r2, r3]
+
+
+def reorder_linear_gather(p):
+    """Move ApplyVertex's weight in front of the Gather when that narrows the propagation.
+
+    For a fused sum gather whose ApplyEdge is linear in edge.src (GCN: src * edge.data;
+    passthrough) and ApplyVertex = ReLU(W (x) accum):
+        ReLU((sum_e w_e h[src_e]) W) == ReLU(sum_e w_e (h W)[src_e])
+    so the layer can run Y = h W per vertex (a GEMM) and propagate Y at width f_out
+    instead of h at width f_in -- the same function, re-associated: results agree with
+    the reference order to fp32 rounding, not bitwise (the aggregate a = A h is never
+    formed).  Applied only when f_out < f_in (the propagation is the dominant cost,
+    SURVEY.md §8(d)).  Sets ``p.reorder`` (an attribute the executor reads)."""
+    ok = (p.fused is not None and p.fused.kind in ("gcn", "pass") and p.accumulator == "sum"
+          and vertex_kind(p) is not None)
+    q = LayerProgram(p.apply_edge, p.apply_vertex, p.accumulator, p.params, p.f_in, p.f_out,
+                     p.precompute, p.fused)
+    if not ok:
+        q.reorder = False
+        return q, PassReport("reorder_linear_gather", blocker="not a linear sum gather + ReLU(W accum)")
+    if p.f_out >= p.f_in:
+        q.reorder = False
+        return q, PassReport("reorder_linear_gather", blocker=f"f_out {p.f_out} >= f_in {p.f_in}")
+    q.reorder = True
+    return q, PassReport("reorder_linear_gather", [f"{vertex_kind(p)} before Gather"],
+                         matmul_rows_before=f"gather width {p.f_in}",
+                         matmul_rows_after=f"gather width {p.f_out}")
 
 
 def vertex_kind(p):

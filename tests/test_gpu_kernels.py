@@ -343,6 +343,38 @@ def test_model_epoch_vs_oracle_pubmed_like(sg, model, P, T):
         assert_close(a, b, 1e-4, f"grad {k}")
 
 
+@pytest.mark.parametrize("P,T", [(1, 4096), (3, 64)])
+@pytest.mark.parametrize("dims", [(500, 16, 3), (130, 64, 7), (37, 40, 5)])
+def test_reordered_gcn_epoch_vs_oracle(sg, P, T, dims):
+    """reorder_linear_gather (Y = h W, then propagate Y) is the same function as the
+    reference order: loss, logits and every gradient vs the fp64 oracle (reference order)
+    within the fp32 tolerance.  (37, 40, 5): layer 0 widens, so only layer 1 reorders."""
+    V, E = 3000, 30000
+    F, H, C = dims
+    s, d = _graph("rmat", V, E, 0)
+    graph = sg.Graph(V, s, d)
+    size = -(-V // P)
+    grid = sg.ChunkGrid(graph, size, split_edges=T)
+    m = sg.gcn_model(grid, [F, H, C], reorder=True)
+    assert [L.reorder for L in m.layers] == [H < F, C < H]
+    X = rng.features(V, F, seed=1)
+    lab = rng.labels(V, C)
+    m.load_features(torch.from_numpy(X))
+    m.load_labels(lab)
+    W = m.weights()
+    m.forward()
+    m.backward()
+    m.check_status()
+    part = og.partition_2d(s, d, V, size)
+    w = og.gcn_edge_weights(s, d, V, np.float64)
+    ref = saga.gcn_epoch(part, X.astype(np.float64), [x.astype(np.float64) for x in W], lab, w, T=T)
+    rl = float(np.ravel(ref["loss"])[0])
+    assert abs(m.loss.item() - rl) <= 1e-4 * rl
+    assert_close(m.layers[1].z.cpu().numpy(), ref["z"][1], 1e-4, "logits")
+    for k, (a, b) in enumerate(zip(m.grads(), ref["grads"])):
+        assert_close(a, b, 1e-4, f"grad {k}")
+
+
 def test_fused_equals_unfused_gcn_bitwise(sg):
     """fused GCN gather == Scatter -> ApplyEdge -> Gather, bit for bit.
 

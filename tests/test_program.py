@@ -81,3 +81,19 @@ def test_vertex_forms():
     odd = sg.make_program(lambda e, p: e.src, lambda v, acc, p: P.sigmoid(acc @ p.W), "sum",
                           {"W": (4, 3)}, 4, 3)
     assert P.vertex_form(odd) is None
+
+
+def test_reorder_linear_gather_pass():
+    from paper_1810_08403_b200 import program as prog
+
+    q, reps = prog.optimize(prog.build_gcn(602, 128), reorder=True)
+    assert q.reorder and reps[-1].name == "reorder_linear_gather" and not reps[-1].blocker
+    assert reps[-1].matmul_rows_after == "gather width 128"
+    q, reps = prog.optimize(prog.build_gcn(16, 64), reorder=True)   # widening: keep the order
+    assert not q.reorder and "f_out" in reps[-1].blocker
+    q, reps = prog.optimize(prog.build_ggcn(64, 16), reorder=True)  # gated ApplyEdge: nonlinear
+    assert not q.reorder and reps[-1].blocker
+    q, reps = prog.optimize(prog.build_commnet(64, 16), reorder=True)  # ApplyVertex not ReLU(W accum)
+    assert not q.reorder
+    q, _ = prog.optimize(prog.build_gcn(602, 128))  # off by default
+    assert not getattr(q, "reorder", False)
