@@ -17,7 +17,8 @@ import numpy as np
 from . import errors
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsagann.so")
+# SG_LIB_PATH: an alternate in-tree build for A/B timing (e.g. libsagann_ab.so)
+LIB_PATH = os.environ.get("SG_LIB_PATH") or os.path.join(_HERE, "libsagann.so")
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "sagann.h")
 
 SG_OK, SG_ESHAPE, SG_ENUMERIC, SG_EBUDGET, SG_ECUDA, SG_ENCCL, SG_EINVAL, SG_EFORMAT = range(8)

@@ -436,8 +436,12 @@ struct Prop {
 
 // Resident blocks per SM to ask ptxas for: in-flight raw vectors (4 regs each) plus
 // fp32 accumulators and row state decide the register budget (64 / 80 / 128 regs).
+#ifndef SG_VPL1_BLOCKS
+#define SG_VPL1_BLOCKS 2
+#endif
 template <int MODE, int W, int VPL, int DEPTH>
 constexpr int prop_min_blocks() {
+  if (VPL == 1 && ModeT<MODE>::NG == 1 && SG_VPL1_BLOCKS != 2) return SG_VPL1_BLOCKS;
   // per in-flight edge: raw vectors + 64-bit row pointer + shuffled (src, w)
   constexpr int regs = DEPTH * (ModeT<MODE>::NG * VPL * 4 + 4) +
                        (ModeT<MODE>::NOUT + ModeT<MODE>::NR) * VPL * W + 40;
@@ -659,13 +663,17 @@ cudaError_t launch_async(const PropArgs& a, cudaStream_t st) {
 template <int MODE, int DT, int W, int VPL, int LPR>
 cudaError_t launch_one(const PropArgs& a, cudaStream_t st) {
   constexpr int NG = ModeT<MODE>::NG;
+  // (the opt-in ring paths read raw indices: never with a hub-encoded index)
   if constexpr (LPR == 32 && NG == 1 && W > 1) {
-    if (async_enabled(VPL) && !tma_enabled()) return launch_async<MODE, DT, VPL>(a, st);
+    if (async_enabled(VPL) && !tma_enabled() && a.n_hub == 0) return launch_async<MODE, DT, VPL>(a, st);
   }
   // rows in flight per warp: ~8 vectors per lane (DEPTH 3 at VPL 5 spills and runs 50% slower)
-  constexpr int DEPTH = (VPL * NG) <= 4 ? 8 / (VPL * NG) : (NG > 1 ? 1 : 2);
+#ifndef SG_DEPTH1
+#define SG_DEPTH1 8
+#endif
+  constexpr int DEPTH = (VPL * NG) == 1 ? SG_DEPTH1 : ((VPL * NG) <= 4 ? 8 / (VPL * NG) : (NG > 1 ? 1 : 2));
   if constexpr (LPR == 32 && VPL >= 2 && NG == 1 && W > 1) {
-    if (tma_enabled()) return launch_tma<MODE, DT, VPL>(a, st);
+    if (tma_enabled() && a.n_hub == 0) return launch_tma<MODE, DT, VPL>(a, st);
   }
   if constexpr (LPR == 32 && NG == 1 && W > 1 && VPL >= kHubMinVpl) {
     if (a.n_hub > 0) {
