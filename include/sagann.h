@@ -204,8 +204,9 @@ int sg_segment_sort(const int64_t* seg, int64_t n, int64_t n_seg, int64_t* ptr, 
  * ApplyVertex GEMM (matmul, tensor.py:306-319): C[M,N] = op(A)[M,K] . op(B)[K,N],
  * row-major; trans_a: A is stored [K,M]; trans_b: B is stored [N,K].  Epilogue
  * RELU_DUAL also writes D = relu(C) (tensor.py:207).  Split-K reductions are
- * deterministic (fixed order).  prec: SG_GEMM_F32 (SIMT fp32), SG_GEMM_TF32X3 /
- * SG_GEMM_BF16 (tcgen05 tensor cores, TMEM accumulators). */
+ * deterministic (fixed order).  prec: SG_GEMM_F32 (SIMT fp32), SG_GEMM_TF32X3
+ * (tcgen05 tensor cores, TMEM accumulators).  SG_GEMM_BF16 is reserved: not implemented,
+ * returns SG_EINVAL. */
 int64_t sg_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K, int prec);
 int sg_gemm(int prec, int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, const float* A,
             int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc, int epilogue,
