@@ -304,6 +304,145 @@ def mpgcn_epoch(part, X, layers, labels, args=None):
     return dict(loss=loss, out=hs[1:], cache=cache, grads=grads)
 
 
+# ------------------------------------------------------------------ GG-NN
+def typed_csc_rows(part, i, j, types_in, n_types):
+    """Rows of the per-type table Y (viewed [V * n_types, F], row v * n_types + t) that the
+    CSC edges of chunk C_ij gather: (begin_i + local src) * n_types + type."""
+    ch = part.chunk(i, j)
+    return (part.begin(i) + ch["csc_idx"].astype(np.int64)) * n_types + \
+        np.asarray(types_in, np.int64)[ch["csc_eid"]]
+
+
+def typed_csr(part, i, j, types_in, n_types):
+    """Per-type CSR of chunk C_ij: rows keyed (local src) * n_types + type, each row's edges
+    in CSR order (stable), i.e. the order take_rows' backward adds them (tensor.py:431-434).
+    Returns (ptr [n_i * n_types + 1], local destination per edge)."""
+    ch = part.chunk(i, j)
+    n_i = int(part.sizes[i])
+    src_local = local_rows(ch["csr_ptr"])
+    key = src_local * n_types + np.asarray(types_in, np.int64)[ch["csr_eid"]]
+    order = np.argsort(key, kind="stable")
+    ptr = np.zeros(n_i * n_types + 1, np.int64)
+    np.add.at(ptr, key + 1, 1)
+    return np.cumsum(ptr), ch["csr_idx"].astype(np.int64)[order]
+
+
+def ggnn_propagate_fwd(part, Yflat, types_in, n_types, T=None):
+    """GG-NN Scatter + ApplyEdge + Gather after the per-type hoist:
+    a[u] = sum_{e in in(u)} Y_{type_e}[src_e] with Y stacked per vertex ([V, n_types*F],
+    row v holds Y_0[v] | Y_1[v] | ...), Locality order over the grid."""
+    V, F = part.V, Yflat.shape[1] // n_types
+    Yrows = Yflat.reshape(V * n_types, F)
+    A = np.zeros((V, F), dtype=Yflat.dtype)
+    for j in range(part.P):
+        Aj = np.zeros((int(part.sizes[j]), F), dtype=Yflat.dtype)
+        for i in range(part.P):
+            ch = part.chunk(i, j)
+            if ch["nnz"] == 0:
+                continue
+            Aj = seq_sum_rows(ch["csc_ptr"], Yrows[typed_csc_rows(part, i, j, types_in, n_types)], Aj, T)
+        A[part.begin(j): part.begin(j) + int(part.sizes[j])] = Aj
+    return A
+
+
+def ggnn_propagate_bwd(part, Ga, types_in, n_types, T=None):
+    """Backward of the typed gather: dY_t[v] = sum_{e in out(v), type_e = t} Ga[dst_e]
+    (segment_sum bwd tensor.py:447-448, select_rows bwd :380-386, take_rows bwd :431-434),
+    over the per-type CSR, destination intervals ascending.  Returns [V, n_types*F]."""
+    V, F = part.V, Ga.shape[1]
+    out = np.zeros((V * n_types, F), dtype=Ga.dtype)
+    for i in range(part.P):
+        n_i = int(part.sizes[i])
+        acc = np.zeros((n_i * n_types, F), dtype=Ga.dtype)
+        for j in range(part.P):
+            if part.chunk(i, j)["nnz"] == 0:
+                continue
+            ptr, dst_local = typed_csr(part, i, j, types_in, n_types)
+            Gj = Ga[part.begin(j): part.begin(j) + int(part.sizes[j])]
+            acc = seq_sum_rows(ptr, Gj[dst_local], acc, T)
+        b = part.begin(i) * n_types
+        out[b: b + n_i * n_types] = acc
+    return out.reshape(V, n_types * F)
+
+
+def gru_fwd(a, h, Wz, Uz, Wr, Ur, Wh, Uh):
+    """GRU(vertex, accum) in the Li et al. (GG-NN) form, no biases, with the
+    reference's op order (tensor.py add / sigmoid / tanh / mul / sub):
+    z = s(aWz + hUz); r = s(aWr + hUr); c = tanh(aWh + (r*h)Uh); h' = (1 - z)*h + z*c."""
+    z = prim.sigmoid(prim.add(prim.matmul(a, Wz), prim.matmul(h, Uz)))
+    r = prim.sigmoid(prim.add(prim.matmul(a, Wr), prim.matmul(h, Ur)))
+    rh = prim.mul(r, h)
+    c = prim.tanh(prim.add(prim.matmul(a, Wh), prim.matmul(rh, Uh)))
+    omz = prim.finalize(np.ones_like(z) - z, "sub")
+    hn = prim.add(prim.mul(omz, h), prim.mul(z, c))
+    return hn, (z, r, rh, c, omz)
+
+
+def gru_bwd(g, a, h, params, cache):
+    """Reverse sweep of gru_fwd in tape order (tensor.py:106-117): returns (g_a, g_h,
+    [gWz, gUz, gWr, gUr, gWh, gUh]); partials of h and a are summed in the order the tape
+    visits their consumers."""
+    Wz, Uz, Wr, Ur, Wh, Uh = params
+    z, r, rh, c, omz = cache
+    g_z = g * c                                   # mul(z, c)
+    g_c = g * z
+    g_omz = g * h                                 # mul(omz, h)
+    g_h = g * omz
+    g_z = g_z + (-g_omz)                          # sub(ones, z)
+    g_cp = g_c * (1.0 - c * c)                    # tanh bwd (tensor.py:234)
+    g_rh, gUh = prim.matmul_bwd(g_cp, rh, Uh)     # matmul(rh, Uh)
+    g_r = g_rh * h                                # mul(r, h)
+    g_h = g_h + g_rh * r
+    g_a, gWh = prim.matmul_bwd(g_cp, a, Wh)       # matmul(a, Wh)
+    g_rp = prim.sigmoid_bwd(g_r, r)
+    gh_r, gUr = prim.matmul_bwd(g_rp, h, Ur)      # matmul(h, Ur)
+    g_h = g_h + gh_r
+    ga_r, gWr = prim.matmul_bwd(g_rp, a, Wr)      # matmul(a, Wr)
+    g_a = g_a + ga_r
+    g_zp = prim.sigmoid_bwd(g_z, z)
+    gh_z, gUz = prim.matmul_bwd(g_zp, h, Uz)      # matmul(h, Uz)
+    g_h = g_h + gh_z
+    ga_z, gWz = prim.matmul_bwd(g_zp, a, Wz)      # matmul(a, Wz)
+    g_a = g_a + ga_z
+    return g_a, g_h, [gWz, gUz, gWr, gUr, gWh, gUh]
+
+
+def ggnn_epoch(part, X, layers, Wo, types_in, labels, T=None):
+    """GG-NN: per layer (As, Wz, Uz, Wr, Ur, Wh, Uh) with
+    As the n_types edge-type matrices; Y_t = h A_t hoisted per vertex, typed Gather(sum),
+    GRU ApplyVertex; readout logits = h_L Wo (no ReLU), softmax-CE.  ``types_in``: edge
+    type per INPUT edge id.  Returns dict(loss, logits, a, out, grads) with grads per layer
+    ([dA_t...], dWz, dUz, dWr, dUr, dWh, dUh) and grads_Wo."""
+    nt = len(layers[0][0])
+    hs, cache = [X], []
+    for (As, *gp) in layers:
+        h = hs[-1]
+        Yflat = np.concatenate([prim.matmul(h, A) for A in As], axis=1)
+        a = ggnn_propagate_fwd(part, Yflat, types_in, nt, T)
+        hn, gc = gru_fwd(a, h, *gp)
+        cache.append((h, a, gc))
+        hs.append(hn)
+    logits = prim.matmul(hs[-1], Wo)
+    loss, p = prim.softmax_cross_entropy(logits, labels)
+    g_logits = prim.softmax_cross_entropy_bwd(np.asarray(1.0, dtype=X.dtype), p, labels)
+    g, gWo = prim.matmul_bwd(g_logits, hs[-1], Wo)
+    grads = [None] * len(layers)
+    for l in range(len(layers) - 1, -1, -1):
+        As, *gp = layers[l]
+        h, a, gc = cache[l]
+        g_a, g_h, gps = gru_bwd(g, a, h, gp, gc)
+        F = h.shape[1]
+        dY = ggnn_propagate_bwd(part, g_a, types_in, nt, T)
+        gAs = [None] * nt
+        for t in range(nt - 1, -1, -1):            # matmul(h, A_t) visited last-first
+            gh_t, gAs[t] = prim.matmul_bwd(dY[:, t * F:(t + 1) * F], h, As[t])
+            g_h = g_h + gh_t
+        grads[l] = (gAs, *gps)
+        g = g_h
+    return dict(loss=loss, logits=logits, a=[c[1] for c in cache], out=hs[1:], grads=grads,
+                grads_Wo=gWo)
+
+
 def sgd(params, grads, lr):
     """W <- W - lr * dW (SPEC.md:598, :617)."""
     return [W - lr * g for W, g in zip(params, grads)]

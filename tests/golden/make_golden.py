@@ -140,6 +140,44 @@ def run_commnet(X, layers, labels, src, dst, V, dtype):
     return acts, loss.to_numpy(), [tuple(grads[m.tid] for m in L) for L in lt]
 
 
+def run_ggnn(X, layers, Wo, types, n_types, labels, src, dst, V, dtype):
+    """GG-NN (PAPER.md:597-612; SPEC.md:526-540): acc = A(edge.data) (x) edge.src with the
+    per-type matmul hoisted to the vertices (Y_t = h A_t, then a per-type
+    Scatter routed by select_rows_by_label, tensor.py:358-386), Gather(sum), ApplyVertex =
+    GRU(vertex, accum) in the Li et al. form without biases:
+        z = s(a Wz + h Uz), r = s(a Wr + h Ur), c = tanh(a Wh + (r*h) Uh),
+        h' = (1 - z)*h + z*c
+    then a linear readout logits = h_L Wo and softmax-CE (no ReLU)."""
+    tape = T.Tape()
+    lt = []
+    for (As, Wz, Uz, Wr, Ur, Wh, Uh) in layers:
+        lt.append(([tens(m, dtype) for m in As],) + tuple(tens(m, dtype) for m in (Wz, Uz, Wr, Ur, Wh, Uh)))
+    Wot = tens(Wo, dtype)
+    for L in lt:
+        for m in L[0]:
+            tape.watch(m)
+        for m in L[1:]:
+            tape.watch(m)
+    tape.watch(Wot)
+    h = tens(X, dtype)
+    ones = tens(np.ones(X.shape), dtype)
+    acts = []
+    for (As, Wz, Uz, Wr, Ur, Wh, Uh) in lt:
+        Ys = [T.matmul(h, A, tape) for A in As]
+        acc = T.select_rows_by_label(types, [T.take_rows(Y, src, tape) for Y in Ys], tape)
+        a = T.segment_sum(acc, dst, V, tape)
+        z = T.sigmoid(T.add(T.matmul(a, Wz, tape), T.matmul(h, Uz, tape), tape), tape)
+        r = T.sigmoid(T.add(T.matmul(a, Wr, tape), T.matmul(h, Ur, tape), tape), tape)
+        c = T.tanh(T.add(T.matmul(a, Wh, tape), T.matmul(T.mul(r, h, tape), Uh, tape), tape), tape)
+        h = T.add(T.mul(T.sub(ones, z, tape), h, tape), T.mul(z, c, tape), tape)
+        acts.append((a.to_numpy(), h.to_numpy()))
+    logits = T.matmul(h, Wot, tape)
+    loss = T.softmax_cross_entropy(logits, labels, tape)
+    grads = T.backward(tape, Seed(dtype))
+    gl = [([grads[m.tid] for m in L[0]],) + tuple(grads[m.tid] for m in L[1:]) for L in lt]
+    return acts, logits.to_numpy(), loss.to_numpy(), gl, grads[Wot.tid]
+
+
 CASES = [
     # name, V, E, F, H, C, generator, seed
     ("uniform_v40_e160", 40, 160, 12, 8, 3, "uniform", 11),
@@ -209,6 +247,30 @@ def make_case(name, V, E, F, H, C, gen, seed):
                 out[f"commnet_{tag}_dL{l}_{k}"] = gL[l][k]
             out[f"commnet_{tag}_a{l}"], out[f"commnet_{tag}_z{l}"], _ = acts[l]
         out[f"commnet_{tag}_loss"] = loss
+        # GG-NN: 2 propagation steps at state width F, 3 edge types, readout F -> C
+        nt = 3
+        types_in = rng.labels(E, nt, seed=5)
+        types = types_in[order]
+        out["ggnn_types"] = types
+        r = np.random.default_rng(7)
+        Lg = []
+        for _ in range(2):
+            As = [r.uniform(-0.4, 0.4, (F, F)).astype(dt) for _ in range(nt)]
+            Lg.append((As,) + tuple(r.uniform(-0.4, 0.4, (F, F)).astype(dt) for _ in range(6)))
+        Wo = r.uniform(-0.5, 0.5, (F, C)).astype(dt)
+        acts, logits, loss, gl, gWo = run_ggnn(X, Lg, Wo, types, nt, lab, s, d, V, dt)
+        for l, L in enumerate(Lg):
+            for t, A in enumerate(L[0]):
+                out[f"ggnn_{tag}_L{l}_A{t}"] = A
+                out[f"ggnn_{tag}_dL{l}_A{t}"] = gl[l][0][t]
+            for k in range(6):
+                out[f"ggnn_{tag}_L{l}_{k}"] = L[1 + k]
+                out[f"ggnn_{tag}_dL{l}_{k}"] = gl[l][1 + k]
+            out[f"ggnn_{tag}_a{l}"], out[f"ggnn_{tag}_h{l}"] = acts[l]
+        out[f"ggnn_{tag}_Wo"] = Wo
+        out[f"ggnn_{tag}_dWo"] = gWo
+        out[f"ggnn_{tag}_logits"] = logits
+        out[f"ggnn_{tag}_loss"] = loss
     np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
     print("wrote", name)
 

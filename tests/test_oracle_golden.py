@@ -166,3 +166,54 @@ def test_commnet_oracle_bitwise(case, tag):
         assert np.array_equal(r["z"][l], g[f"commnet_{tag}_z{l}"])
         for k in range(2):
             assert np.array_equal(r["grads"][l][k], g[f"commnet_{tag}_dL{l}_{k}"]), (l, k)
+
+
+def _ggnn_layers(g, tag):
+    layers = []
+    for l in range(2):
+        As = [g[f"ggnn_{tag}_L{l}_A{t}"] for t in range(3)]
+        layers.append((As,) + tuple(g[f"ggnn_{tag}_L{l}_{k}"] for k in range(6)))
+    return layers
+
+
+@pytest.mark.parametrize("name", GOLDEN_CASES)
+@pytest.mark.parametrize("tag", ["f64", "f32"])
+def test_ggnn_oracle_bitwise(name, tag):
+    """GG-NN oracle (P = 1, no split) == the real reference's tape (typed per-vertex hoist +
+    select_rows_by_label + GRU) bit for bit: loss, logits, aggregates, every gradient."""
+    g = load_golden(name)
+    V = int(g["V"])
+    types_in = np.empty_like(g["ggnn_types"])
+    part = og.partition_2d(g["src_in"], g["dst_in"], V, V)
+    types_in[part.csc_eid] = g["ggnn_types"]
+    layers = _ggnn_layers(g, tag)
+    res = saga.ggnn_epoch(part, g[f"gcn_{tag}_X"], layers, g[f"ggnn_{tag}_Wo"], types_in, g["labels"])
+    assert np.array_equal(np.ravel(res["loss"]), np.ravel(g[f"ggnn_{tag}_loss"]))
+    assert np.array_equal(res["logits"], g[f"ggnn_{tag}_logits"])
+    for l in range(2):
+        assert np.array_equal(res["a"][l], g[f"ggnn_{tag}_a{l}"])
+        assert np.array_equal(res["out"][l], g[f"ggnn_{tag}_h{l}"])
+        for t in range(3):
+            assert np.array_equal(res["grads"][l][0][t], g[f"ggnn_{tag}_dL{l}_A{t}"]), (l, t)
+        for k in range(6):
+            assert np.array_equal(res["grads"][l][1 + k], g[f"ggnn_{tag}_dL{l}_{k}"]), (l, k)
+    assert np.array_equal(res["grads_Wo"], g[f"ggnn_{tag}_dWo"])
+
+
+@pytest.mark.parametrize("name", GOLDEN_CASES)
+def test_ggnn_oracle_2d_grid_matches_reference(name):
+    """P = 3 grid with split subgroups: same function, fp64 rounding only."""
+    g = load_golden(name)
+    V = int(g["V"])
+    part1 = og.partition_2d(g["src_in"], g["dst_in"], V, V)
+    types_in = np.empty_like(g["ggnn_types"])
+    types_in[part1.csc_eid] = g["ggnn_types"]
+    part = og.partition_2d(g["src_in"], g["dst_in"], V, -(-V // 3))
+    res = saga.ggnn_epoch(part, g["gcn_f64_X"], _ggnn_layers(g, "f64"), g["ggnn_f64_Wo"], types_in,
+                          g["labels"], T=3)
+    assert abs(float(np.ravel(res["loss"])[0]) - float(np.ravel(g["ggnn_f64_loss"])[0])) < 1e-12
+    for l in range(2):
+        for k in range(6):
+            assert np.allclose(res["grads"][l][1 + k], g[f"ggnn_f64_dL{l}_{k}"], rtol=1e-9, atol=1e-12)
+        for t in range(3):
+            assert np.allclose(res["grads"][l][0][t], g[f"ggnn_f64_dL{l}_A{t}"], rtol=1e-9, atol=1e-12)
