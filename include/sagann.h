@@ -236,6 +236,25 @@ int sg_check_finite(int dtype, const void* X, int64_t rows, int64_t cols, int64_
  * leading axis when b_rows == 1 ("b_lead"). */
 int sg_ewise(int op, int64_t rows, int64_t cols, const float* a, int64_t lda, const float* b,
              int64_t b_rows, int64_t b_cols, int64_t ldb, float* out, int64_t ldo, void* stream);
+/* GG-NN ApplyVertex = GRU(vertex, accum) (Li et al. form,
+ * no biases), the element-wise stages around the ApplyVertex GEMMs.  G1 = a [Wz|Wr|Wh],
+ * G2 = h [Uz|Ur], G3 = (r*h) Uh, gate blocks at column stride bs (>= F); z/r/rh/c share ldo.
+ *   gates: z = s(G1z + G2z), r = s(G1r + G2r), rh = r*h       (s = 1/(1+exp(-x)), tensor.py:205)
+ *   out:   c = tanh(G1h + G3), hn = (1-z)*h + z*c
+ *   bwd1:  D3[:,0] = gzp, D3[:,2bs] = gcp, gh = g*(1-z)       (tape reverse order, tensor.py:231-263)
+ *   bwd2:  gh += grh*r, D3[:,bs] = grp                        (grh = gcp Uh^T) */
+int sg_gru_gates(int64_t V, int64_t F, const float* G1, int64_t ld1, const float* G2, int64_t ld2,
+                 int64_t bs, const float* h, int64_t ldh, float* z, float* r, float* rh, int64_t ldo,
+                 void* stream);
+int sg_gru_out(int64_t V, int64_t F, const float* G1, int64_t ld1, int64_t bs, const float* G3,
+               int64_t ld3, const float* z, const float* h, int64_t ldh, float* c, float* hn,
+               int64_t ldo, int64_t ldn, void* stream);
+int sg_gru_bwd1(int64_t V, int64_t F, const float* g, int64_t ldg, const float* z, const float* c,
+                int64_t ldo, const float* h, int64_t ldh, float* D3, int64_t ld3, int64_t bs, float* gh,
+                int64_t ldgh, void* stream);
+int sg_gru_bwd2(int64_t V, int64_t F, const float* grh, int64_t ldr, const float* r, int64_t ldo,
+                const float* h, int64_t ldh, float* gh, int64_t ldgh, float* D3, int64_t ld3, int64_t bs,
+                void* stream);
 /* fp32 <-> bf16 row copy with padding (feature staging). */
 int sg_convert(int src_dtype, int dst_dtype, const void* X, int64_t ldx, void* Y, int64_t ldy,
                int64_t rows, int64_t cols, void* stream);

@@ -13,7 +13,7 @@ from .errors import (BudgetError, ConfigError, EngineError, GraphFormatError, Nu
 from .graph import (ChunkGrid, Graph, Partition, load_graph, partition_2d, read_features, read_labels,
                     reencode_balance, rmat_graph, synthetic_features, uniform_graph, write_features_bin)
 from .program import (FusedGather, LayerProgram, PassReport, build_commnet, build_gcn, build_ggcn,
-                      build_mpgcn,
+                      build_ggnn, build_mpgcn,
                       evaluate_expr, fuse_sag, hoist_vertex_computation, make_program, matmul_rows,
                       optimize, trace_udf, validate_program, vertex_form)
 
@@ -25,7 +25,7 @@ __all__ = [
     "LayerProgram", "PassReport", "build_commnet", "build_gcn", "build_ggcn", "build_mpgcn", "evaluate_expr",
     "fuse_sag", "hoist_vertex_computation", "make_program", "matmul_rows", "optimize", "trace_udf",
     "validate_program", "vertex_form", "SAGAModel", "gcn_model", "ggcn_model", "mpgcn_model", "commnet_model", "run_train",
-    "StreamingGCN", "HostGrid",
+    "StreamingGCN", "HostGrid", "GGNNModel", "ggnn_model", "build_ggnn",
 ]
 
 
@@ -36,6 +36,10 @@ def __getattr__(name):
         from . import engine
 
         return getattr(engine, name)
+    if name in ("GGNNModel", "ggnn_model"):
+        from . import ggnn
+
+        return getattr(ggnn, name)
     if name in ("StreamingGCN", "HostGrid"):
         from . import stream
 

@@ -605,19 +605,19 @@ def mpgcn_model(grid, dims, pool=None, **kw):
 def run_train(config):
     """SPEC.md:595-603 run_train on a synthetic graph; returns a metrics dict.
 
-    config keys (SPEC.md:622 subset + synthetic graph): model ('gcn'|'ggcn'|'mpgcn'|'commnet'),
+    config keys (SPEC.md:622 subset + synthetic graph): model ('gcn'|'ggcn'|'mpgcn'|'commnet'|'ggnn'),
     graph ('rmat'|'uniform'), V, E, features F, hidden, classes, layers, epochs,
     lr, seed, interval_size."""
     from . import graph as G
 
     known = {"model", "graph", "V", "E", "features", "hidden", "classes", "layers", "epochs", "lr",
-             "seed", "interval_size", "split_edges"}
+             "seed", "interval_size", "split_edges", "edge_types"}
     bad = set(config) - known
     if bad:
         raise ConfigError(f"unknown config keys {sorted(bad)}")
     model = config.get("model", "gcn")
     builders = {"gcn": gcn_model, "ggcn": ggcn_model, "mpgcn": mpgcn_model,
-                "commnet": commnet_model}
+                "commnet": commnet_model, "ggnn": None}
     if model not in builders:
         raise ConfigError(f"unknown model '{model}'; valid: {', '.join(builders)}")
     V, E = int(config["V"]), int(config["E"])
@@ -628,7 +628,16 @@ def run_train(config):
     F, H, C = int(config["features"]), int(config.get("hidden", 16)), int(config["classes"])
     nl = int(config.get("layers", 2))
     dims = [F] + [H] * (nl - 1) + [C]
-    m = builders[model](grid, dims)
+    if model == "ggnn":  # GG-NN: state width F, synthetic edge labels, readout to C classes
+        from .ggnn import ggnn_model
+
+        nt = int(config.get("edge_types", 3))
+        types = np.random.default_rng(5).integers(0, nt, E)
+        grid = G.ChunkGrid(g, config.get("interval_size") or V, gcn_weights=False,
+                           split_edges=int(config.get("split_edges", G.DEFAULT_SPLIT_EDGES)))
+        m = ggnn_model(grid, F, nt, C, types, layers=nl)
+    else:
+        m = builders[model](grid, dims)
     m.load_features(torch.from_numpy(G.synthetic_features(V, F, seed=1)))
     m.load_labels(np.random.default_rng(3).integers(0, C, V))
     losses = []

@@ -106,6 +106,33 @@ def matmul(a, b):
     return Expr("matmul", (a, b), width=cols)
 
 
+def typed_matmul(x, labels, A):
+    """GG-NN's A(edge.data) (x) edge.src (tensor.py:322-355 typed_matmul):
+    row e times the parameter matrix A[labels[e]] of a (types, rows, cols) family."""
+    if A.op != "param" or not isinstance(A.width, tuple) or len(A.width) != 3:
+        raise ProgramError("typed_matmul needs a (types, rows, cols) parameter family")
+    if labels.op != "input" or labels.name != "edge.data":
+        raise ProgramError("typed_matmul selects its matrix by the integer edge label edge.data")
+    _, rows, cols = A.width
+    if x.width is not None and x.width != rows:
+        raise ProgramError(f"typed_matmul inner extents differ: {x.width} vs {rows}")
+    return Expr("typed_matmul", (x, labels, A), width=cols)
+
+
+def gru(vertex, accum, Wz, Uz, Wr, Ur, Wh, Uh):
+    """GRU(vertex, accum) ApplyVertex of GG-NN (Li et al.
+    form, no biases): z = s(a Wz + h Uz), r = s(a Wr + h Ur), c = tanh(a Wh + (r*h) Uh),
+    h' = (1 - z)*h + z*c."""
+    ps = (Wz, Uz, Wr, Ur, Wh, Uh)
+    for w in ps:
+        if w.op != "param" or not isinstance(w.width, tuple) or len(w.width) != 2:
+            raise ProgramError("gru needs six (F, F) parameter matrices")
+    F = vertex.width
+    if any(w.width != (F, F) for w in ps) or accum.width not in (None, F):
+        raise ProgramError("gru state, input and parameter widths must all equal F")
+    return Expr("gru", (vertex, accum) + ps, width=F)
+
+
 class _Edge:
     def __init__(self, f_src, f_dest):
         self.src = Expr("input", name="edge.src", width=f_src)
@@ -123,8 +150,9 @@ class _Params:
         if k not in self._shapes:
             raise ProgramError(f"unknown parameter '{k}'")
         shape = tuple(self._shapes[k])
-        # matrices keep their (rows, cols); a bias vector (n,) broadcasts like a row (b_lead)
-        return Expr("param", name=k, width=shape if len(shape) == 2 else shape[0])
+        # matrices keep their (rows, cols) (a typed family (types, rows, cols)); a bias
+        # vector (n,) broadcasts like a row (b_lead)
+        return Expr("param", name=k, width=shape if len(shape) >= 2 else shape[0])
 
 
 def trace_udf(udf, kind, params, f_in):
@@ -233,8 +261,9 @@ def validate_program(p):
 
 def matmul_rows(e, n_edges, n_vertices, precompute=None):
     """Matmul row applications of one layer's ApplyEdge (tensor.py:133-158 counting)."""
-    per_edge = sum(1 for n in nodes(e) if n.op == "matmul")
-    per_vertex = sum(sum(1 for n in nodes(x) if n.op == "matmul") for _, x in (precompute or {}).values())
+    per_edge = sum(1 for n in nodes(e) if n.op in ("matmul", "typed_matmul"))
+    per_vertex = sum(sum(1 if n.op == "matmul" else (n.args[1].width[0] if n.op == "typed_table" else 0)
+                         for n in nodes(x)) for _, x in (precompute or {}).values())
     return per_edge * n_edges + per_vertex * n_vertices
 
 
@@ -253,9 +282,18 @@ def hoist_vertex_computation(p):
         return None
 
     def has_mm(x):
-        return any(n.op == "matmul" for n in nodes(x))
+        return any(n.op in ("matmul", "typed_matmul") for n in nodes(x))
 
     def rewrite(x):
+        if x.op == "typed_matmul" and side_of(x.args[0]) == "src":
+            # per-type hoist: Y_t = vertex A_t for every type t per vertex,
+            # the edge then selects Y_{edge.data}[src] -- a typed per-vertex scatter
+            name = f"pre_src_typed{len(pre)}"
+            vx = Expr("typed_table", (_to_vertex(x.args[0]), x.args[2]), width=x.width)
+            pre[name] = ("src", vx)
+            moved.append(f"{x!r} -> per-vertex per-type {name}")
+            return Expr("select_type", (Expr("pre", name=name, width=x.width), x.args[1]),
+                        width=x.width)
         s = side_of(x)
         if s is not None and has_mm(x):
             name = f"pre_{s}{len(pre)}"
@@ -269,10 +307,14 @@ def hoist_vertex_computation(p):
 
     new_edge = rewrite(p.apply_edge)
     q = LayerProgram(new_edge, p.apply_vertex, p.accumulator, p.params, p.f_in, p.f_out, pre, p.fused)
+    def per_vertex(v):
+        return sum(1 if n.op == "matmul" else (n.args[1].width[0] if n.op == "typed_table" else 0)
+                   for n in nodes(v))
+
     rep = PassReport("hoist_vertex_computation", moved,
-                     f"{sum(1 for n in nodes(p.apply_edge) if n.op == 'matmul')}*|E|",
-                     f"{sum(1 for n in nodes(new_edge) if n.op == 'matmul')}*|E| + "
-                     f"{sum(sum(1 for n in nodes(v) if n.op == 'matmul') for _, v in pre.values())}*|V|")
+                     f"{sum(1 for n in nodes(p.apply_edge) if n.op in ('matmul', 'typed_matmul'))}*|E|",
+                     f"{sum(1 for n in nodes(new_edge) if n.op in ('matmul', 'typed_matmul'))}*|E| + "
+                     f"{sum(per_vertex(v) for _, v in pre.values())}*|V|")
     return q, rep
 
 
@@ -291,7 +333,7 @@ def _is(x, op, *names):
 def fuse_sag(p):
     """an element-wise-only (post-hoist) ApplyEdge becomes a FusedGather."""
     e = p.apply_edge
-    mm = [n for n in nodes(e) if n.op == "matmul"]
+    mm = [n for n in nodes(e) if n.op in ("matmul", "typed_matmul")]
     if mm:
         rep = PassReport("fuse_sag", blocker="matmul")
         return LayerProgram(e, p.apply_vertex, p.accumulator, p.params, p.f_in, p.f_out,
@@ -308,7 +350,10 @@ def fuse_sag(p):
                 if mm.op == "matmul" and _is(mm.args[0], "input", "vertex") and bias.op == "param":
                     kind, params = "max_pool", (mm.args[1].name, bias.name)
     if p.accumulator == "sum":
-        if _is(e, "input", "edge.src"):
+        if e.op == "select_type" and e.args[0].op == "pre" and p.precompute[e.args[0].name][0] == "src":
+            kind = "typed"   # GG-NN: PASS gather over the per-type table (row src*T + type)
+            params = (p.precompute[e.args[0].name][1].args[1].name,)
+        elif _is(e, "input", "edge.src"):
             kind = "pass"
         elif e.op == "mul" and {a.name for a in e.args if a.op == "input"} == {"edge.src", "edge.data"}:
             kind = "gcn"
@@ -418,6 +463,8 @@ def vertex_form(p):
     if W is not None:
         return ("w", W)
     v = p.apply_vertex
+    if v.op == "gru" and _is(v.args[0], "input", "vertex") and _is(v.args[1], "input", "accum"):
+        return ("gru",) + tuple(w.name for w in v.args[2:])
     if v.op == "relu" and v.args[0].op == "add":
         def mm(t, name):
             if t.op == "matmul" and _is(t.args[0], "input", name) and t.args[1].op == "param":
@@ -475,4 +522,17 @@ def build_mpgcn(f_in, f_pool, f_out):
                         f_in, f_out, acc_width=f_pool)
 
 
-MODELS = {"gcn": build_gcn, "ggcn": build_ggcn, "commnet": build_commnet, "mpgcn": build_mpgcn}
+def build_ggnn(f, edge_types):
+    """GG-NN (PAPER.md:597-612; SPEC.md:526-540): ApplyEdge = A(edge.data) (x) edge.src with
+    one (f, f) matrix per edge type, Gather(sum), ApplyVertex = GRU(vertex, accum)."""
+    if f < 1 or edge_types < 1:
+        raise ProgramError("invalid dimensions")
+    shapes = {"A": (edge_types, f, f)}
+    shapes.update({k: (f, f) for k in ("W_z", "U_z", "W_r", "U_r", "W_h", "U_h")})
+    return make_program(lambda e, p: typed_matmul(e.src, e.data, p.A),
+                        lambda v, acc, p: gru(v, acc, p.W_z, p.U_z, p.W_r, p.U_r, p.W_h, p.U_h),
+                        "sum", shapes, f, f)
+
+
+MODELS = {"gcn": build_gcn, "ggcn": build_ggcn, "commnet": build_commnet, "mpgcn": build_mpgcn,
+          "ggnn": build_ggnn}

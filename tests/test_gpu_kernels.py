@@ -449,6 +449,9 @@ def test_run_train_entry_point(sg):
     assert out["epochs"] == 10 and all(b < a for a, b in zip(out["loss"], out["loss"][1:]))
     with pytest.raises(sg.ConfigError):
         sg.run_train({"model": "nope", "V": 2, "E": 1, "features": 1, "classes": 1})
+    out = sg.run_train({"model": "ggnn", "graph": "rmat", "V": 300, "E": 3000, "features": 8,
+                        "classes": 3, "edge_types": 4, "epochs": 5, "lr": 0.5})
+    assert out["epochs"] == 5 and all(b < a for a, b in zip(out["loss"], out["loss"][1:]))
 
 
 # ---------------------------------------------------------------- MP-GCN (max accumulator)
@@ -717,3 +720,128 @@ def test_streaming_budget_error(sg):
     g = sg.Graph(2000, s, d)
     with pytest.raises(sg.BudgetError, match="interval_size"):
         sg.StreamingGCN(sg.HostGrid(g, 1000), [64, 16, 4], budget=1 << 16)
+
+
+# ------------------------------------------------------------------ GG-NN
+def _types_in(g):
+    """Golden edge types are stored in CSC order; map them back to input edge ids."""
+    V = int(g["V"])
+    part = og.partition_2d(g["src_in"], g["dst_in"], V, V)
+    t = np.empty_like(g["ggnn_types"])
+    t[part.csc_eid] = g["ggnn_types"]
+    return t
+
+
+@pytest.mark.parametrize("P,T", [(1, 4096), (3, 32)])
+def test_ggnn_typed_gather_fwd_bwd_bitwise(sg, P, T):
+    """GG-NN's typed gather (PASS over Y viewed [V*types, bs], row src*types + type) and its
+    per-type CSR dual == oracle ggnn_propagate_fwd / _bwd, bit for bit."""
+    V, E, F, nt = 2000, 40000, 24, 3
+    s, d = _graph("rmat", V, E, 2)
+    types = rng.labels(E, nt, seed=9)
+    grid = sg.ChunkGrid(sg.Graph(V, s, d), -(-V // P), split_edges=T, gcn_weights=False)
+    m = sg.ggnn_model(grid, F, nt, 4, types)
+    Y = rng.features(V, nt * F, seed=3)
+    Ga = rng.features(V, F, seed=4)
+    bs = m.bs
+    Yb = m.Y[0]
+    for t in range(nt):
+        Yb[:, t * bs: t * bs + F] = torch.from_numpy(Y[:, t * F:(t + 1) * F]).cuda()
+    from paper_1810_08403_b200 import _lib
+    from paper_1810_08403_b200 import kernels as K
+
+    out = _padded(np.zeros((V, F), np.float32))
+    for j in range(grid.P):
+        chain = [i for i in range(grid.P) if (i, j) in m.tcsc]
+        for k, i in enumerate(chain):
+            K.propagate(m.tcsc[(i, j)], _lib.PROP_PASS, m._typed_rows(Yb, i), m._rows(out, j), F,
+                        accumulate=k > 0)
+    part = og.partition_2d(s, d, V, -(-V // P))
+    ref = saga.ggnn_propagate_fwd(part, Y, types, nt, T)
+    assert np.array_equal(out.cpu().numpy(), ref)
+    Gd = _padded(Ga)
+    dY = torch.zeros_like(m.dY)
+    for i in range(grid.P):
+        chain = [j for j in range(grid.P) if (i, j) in m.tcsr]
+        for k, j in enumerate(chain):
+            K.propagate(m.tcsr[(i, j)], _lib.PROP_PASS, m._rows(Gd, j), m._typed_rows(dY, i), F,
+                        accumulate=k > 0)
+    got = np.concatenate([dY[:, t * bs: t * bs + F].cpu().numpy() for t in range(nt)], 1)
+    assert np.array_equal(got, saga.ggnn_propagate_bwd(part, Ga, types, nt, T))
+
+
+@pytest.mark.parametrize("name", GOLDEN_CASES)
+def test_ggnn_model_vs_reference_golden(sg, name):
+    """GG-NN step (typed hoist + gather, GRU, readout, softmax-CE) vs the REAL reference's
+    fp64 outputs: loss, logits and every gradient within the fp32 tolerance."""
+    g = load_golden(name)
+    V, F, C = int(g["V"]), int(g["F"]), int(g["C"])
+    grid = sg.ChunkGrid(sg.Graph(V, g["src_in"], g["dst_in"]), V, gcn_weights=False)
+    layers = []
+    for l in range(2):
+        As = [g[f"ggnn_f32_L{l}_A{t}"] for t in range(3)]
+        layers.append((As,) + tuple(g[f"ggnn_f32_L{l}_{k}"] for k in range(6)))
+    m = sg.ggnn_model(grid, F, 3, C, _types_in(g), weights=(layers, g["ggnn_f32_Wo"]))
+    m.load_features(torch.from_numpy(g["gcn_f32_X"]))
+    m.load_labels(g["labels"])
+    m.forward()
+    m.backward()
+    m.check_status()
+    rl = float(np.ravel(g["ggnn_f64_loss"])[0])
+    assert abs(m.loss.item() - rl) <= 1e-4 * abs(rl)
+    assert_close(m.logits.cpu().numpy(), g["ggnn_f64_logits"], 1e-4, "logits")
+    gl, gWo = m.grads()
+    for l in range(2):
+        for t in range(3):
+            assert_close(gl[l][0][t], g[f"ggnn_f64_dL{l}_A{t}"], 1e-4, f"L{l} dA{t}")
+        for k in range(6):
+            assert_close(gl[l][1 + k], g[f"ggnn_f64_dL{l}_{k}"], 1e-4, f"L{l} d{k}")
+    assert_close(gWo, g["ggnn_f64_dWo"], 1e-4, "dWo")
+
+
+@pytest.mark.parametrize("P,T", [(1, 4096), (2, 64)])
+def test_ggnn_epoch_vs_oracle(sg, P, T):
+    """GG-NN at a larger size on the 2D grid with split subgroups vs the fp64 oracle
+    (normwise 1e-4; elementwise floor 0.5e-4 of the tensor scale: the weight gradients are
+    K = V = 3000-row reductions at the end of a GRU + typed-gather chain)."""
+    V, E, F, nt, C = 3000, 40000, 32, 4, 5
+    s, d = _graph("rmat", V, E, 1)
+    types = rng.labels(E, nt, seed=9)
+    size = -(-V // P)
+    grid = sg.ChunkGrid(sg.Graph(V, s, d), size, split_edges=T, gcn_weights=False)
+    m = sg.ggnn_model(grid, F, nt, C, types)
+    X = rng.features(V, F, seed=1)
+    lab = rng.labels(V, C)
+    m.load_features(torch.from_numpy(X))
+    m.load_labels(lab)
+    layers, Wo = m.weights()
+    m.forward()
+    m.backward()
+    m.check_status()
+    part = og.partition_2d(s, d, V, size)
+    L64 = [([a.astype(np.float64) for a in L[0]],) + tuple(x.astype(np.float64) for x in L[1:]) for L in layers]
+    ref = saga.ggnn_epoch(part, X.astype(np.float64), L64, Wo.astype(np.float64), types, lab, T=T)
+    rl = float(np.ravel(ref["loss"])[0])
+    assert abs(m.loss.item() - rl) <= 1e-4 * abs(rl)
+    gl, gWo = m.grads()
+    for l in range(2):
+        for t in range(nt):
+            assert_close(gl[l][0][t], ref["grads"][l][0][t], 1e-4, f"L{l} dA{t}", floor=0.5)
+        for k in range(6):
+            assert_close(gl[l][1 + k], ref["grads"][l][1 + k], 1e-4, f"L{l} d{k}", floor=0.5)
+    assert_close(gWo, ref["grads_Wo"], 1e-4, "dWo", floor=0.5)
+
+
+def test_ggnn_trains(sg):
+    V, E, F, nt, C = 1500, 20000, 16, 3, 4
+    s, d = _graph("uniform", V, E, 3)
+    grid = sg.ChunkGrid(sg.Graph(V, s, d), V, gcn_weights=False)
+    m = sg.ggnn_model(grid, F, nt, C, rng.labels(E, nt, seed=9))
+    m.load_features(torch.from_numpy(rng.features(V, F, seed=1)))
+    m.load_labels(rng.labels(V, C))
+    losses = []
+    for _ in range(10):
+        m.train_step(0.5)
+        losses.append(m.loss.item())
+    m.check_status()
+    assert all(b < a for a, b in zip(losses, losses[1:])), losses

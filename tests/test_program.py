@@ -4,6 +4,7 @@ import pytest
 
 import paper_1810_08403_b200 as sg
 from paper_1810_08403_b200 import program as P
+from paper_1810_08403_b200.errors import ProgramError
 
 
 def test_gcn_program_fuses_to_gcn_kernel():
@@ -97,3 +98,23 @@ def test_reorder_linear_gather_pass():
     assert not q.reorder
     q, _ = prog.optimize(prog.build_gcn(602, 128))  # off by default
     assert not getattr(q, "reorder", False)
+
+
+def test_ggnn_program_typed_hoist_and_gru():
+    """GG-NN's edge stage is reduced to a per-type pre-computed scatter
+    (A(type) (x) src hoisted per edge type); ApplyVertex is recognised as the GRU."""
+    from paper_1810_08403_b200 import program as prog
+
+    p = prog.build_ggnn(8, 3)
+    assert prog.validate_program(p) == []
+    q, (h, f) = prog.optimize(p)
+    assert h.matmul_rows_before == "1*|E|" and h.matmul_rows_after == "0*|E| + 3*|V|"
+    assert q.fused.kind == "typed" and q.fused.params == ("A",)
+    assert prog.vertex_form(q) == ("gru", "W_z", "U_z", "W_r", "U_r", "W_h", "U_h")
+    assert prog.matmul_rows(p.apply_edge, 100, 10) == 100
+    assert prog.matmul_rows(q.apply_edge, 100, 10, q.precompute) == 30
+    with pytest.raises(ProgramError):
+        prog.build_ggnn(8, 0)
+    with pytest.raises(ProgramError):   # the family is selected by edge.data only
+        prog.make_program(lambda e, p: prog.typed_matmul(e.src, e.dest, p.A), lambda v, a, p: a, "sum",
+                          {"A": (2, 4, 4)}, 4, 4)
