@@ -17,6 +17,8 @@ All device buffers are allocated once; ``capture()`` records a whole training
 step into a CUDA graph, so an epoch is one graph launch.
 """
 
+import os
+
 import numpy as np
 import torch
 
@@ -408,8 +410,13 @@ class SAGAModel:
                                      out.data_ptr(), out.stride(0), _lib.stream_handle(stream)))
 
     # ------------------------------------------------------------------ step
+    _NVTX = os.environ.get("SG_NVTX", "0") == "1"
+
     def _mark(self, name):
-        """Stage boundary event (enabled by setting ``self.prof = []``)."""
+        """Stage boundary event (enabled by setting ``self.prof = []``); with SG_NVTX=1 also
+        an NVTX marker per SAGA stage for timeline tools (SURVEY.md §5 tracing)."""
+        if self._NVTX:
+            torch.cuda.nvtx.mark(f"sg:{name}")
         if self.prof is not None:
             e = torch.cuda.Event(enable_timing=True)
             e.record()
@@ -540,11 +547,38 @@ class SAGAModel:
         return out
 
     def train_step(self, lr=0.01):
+        if self._NVTX:
+            torch.cuda.nvtx.range_push("sg:train_step")
         self._take_staged()
         self.forward()
         self.backward()
         self.sgd(lr)
+        if self._NVTX:
+            torch.cuda.nvtx.range_pop()
         return self.loss
+
+    # ------------------------------------------------------------------ checkpoint
+    def save_checkpoint(self, path, epoch=0):
+        """Parameters + epoch (+ the graph's content key, so a resume on another graph is
+        refused) as one .npz (SURVEY.md §5 checkpoint/resume)."""
+        from . import graph as G
+
+        g = self.grid.graph
+        arrs = {f"p{k}": w for k, w in enumerate(self.weights())}
+        np.savez(path, epoch=np.int64(epoch), graph_key=np.array(G.graph_key(g, self.grid.part.interval_size)),
+                 n_params=np.int64(len(arrs)), **arrs)
+
+    def load_checkpoint(self, path):
+        """Restore parameters saved by save_checkpoint; returns the saved epoch."""
+        from . import graph as G
+
+        with np.load(path) as z:
+            key = str(z["graph_key"])
+            if key != G.graph_key(self.grid.graph, self.grid.part.interval_size):
+                raise ConfigError(f"checkpoint {path} was written for another graph ({key})")
+            n = int(z["n_params"])
+            self.set_weights([z[f"p{k}"] for k in range(n)])
+            return int(z["epoch"])
 
     # ------------------------------------------------------------------ CUDA graph
     def capture(self, lr=0.01, warmup=1):
@@ -611,7 +645,7 @@ def run_train(config):
     from . import graph as G
 
     known = {"model", "graph", "V", "E", "features", "hidden", "classes", "layers", "epochs", "lr",
-             "seed", "interval_size", "split_edges", "edge_types"}
+             "seed", "interval_size", "split_edges", "edge_types", "checkpoint"}
     bad = set(config) - known
     if bad:
         raise ConfigError(f"unknown config keys {sorted(bad)}")
@@ -640,9 +674,16 @@ def run_train(config):
         m = builders[model](grid, dims)
     m.load_features(torch.from_numpy(G.synthetic_features(V, F, seed=1)))
     m.load_labels(np.random.default_rng(3).integers(0, C, V))
+    ckpt = config.get("checkpoint")
+    start = 0
+    if ckpt and os.path.exists(ckpt) and hasattr(m, "load_checkpoint"):
+        start = m.load_checkpoint(ckpt)   # resume: parameters and epoch counter
     losses = []
-    for _ in range(int(config.get("epochs", 10))):
+    for _ in range(start, int(config.get("epochs", 10))):
         m.train_step(float(config.get("lr", 0.01)))
         m.check_status()
         losses.append(float(m.loss.item()))
-    return {"model": model, "V": V, "E": E, "epochs": len(losses), "loss": losses}
+    if ckpt and hasattr(m, "save_checkpoint"):
+        m.save_checkpoint(ckpt, start + len(losses))
+    return {"model": model, "V": V, "E": E, "epochs": len(losses), "start_epoch": start,
+            "loss": losses}

@@ -449,6 +449,18 @@ def test_run_train_entry_point(sg):
     assert out["epochs"] == 10 and all(b < a for a, b in zip(out["loss"], out["loss"][1:]))
     with pytest.raises(sg.ConfigError):
         sg.run_train({"model": "nope", "V": 2, "E": 1, "features": 1, "classes": 1})
+    import tempfile
+
+    with tempfile.TemporaryDirectory() as d:
+        cfg = {"model": "gcn", "graph": "rmat", "V": 200, "E": 2000, "features": 6, "hidden": 8,
+               "classes": 3, "epochs": 4, "lr": 0.01, "checkpoint": d + "/ck.npz"}
+        full = sg.run_train(dict(cfg, checkpoint=d + "/full.npz", epochs=8))
+        first = sg.run_train(cfg)                   # epochs 0-3, saves
+        rest = sg.run_train(dict(cfg, epochs=8))     # resumes at epoch 4
+        assert first["start_epoch"] == 0 and rest["start_epoch"] == 4
+        assert first["loss"] + rest["loss"] == full["loss"]   # bit-reproducible resume
+        with pytest.raises(sg.ConfigError):          # checkpoint of another graph
+            sg.run_train(dict(cfg, E=2001, epochs=9))
     out = sg.run_train({"model": "ggnn", "graph": "rmat", "V": 300, "E": 3000, "features": 8,
                         "classes": 3, "edge_types": 4, "epochs": 5, "lr": 0.5})
     assert out["epochs"] == 5 and all(b < a for a, b in zip(out["loss"], out["loss"][1:]))
