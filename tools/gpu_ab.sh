@@ -1,2 +1,2 @@
-timeout 300 python tools/narrow_ab.py 16 64 128
-SG_LIB_PATH=$PWD/paper_1810_08403_b200/libsagann_ab.so timeout 300 python tools/narrow_ab.py 16 64 128
+timeout 600 python tools/tile_ab.py reddit 1 2 4 8
+timeout 900 python tools/tile_ab.py powerlaw_gcn 1 4 16
