@@ -44,6 +44,48 @@ int64_t hub_smem_bytes() {
   return v;
 }
 
+// Thread-block-cluster hub cache: the hub rows are spread round-robin over the shared memory
+// of the CS CTAs of a cluster (slot k lives in CTA k % CS at row k / CS) and read through
+// DSMEM (ld.shared::cluster), so a cluster holds CS x the rows one CTA can.  Opt-in A/B knob
+// SG_HUB_CLUSTER = 1 | 2 | 4 | 8 | 16, default 1: on the Reddit L0 pass it measured SLOWER
+// (CSC 17.5 / 18.0 / 19.0 / 20.5 / 23.0 ms for CS = 1 / 2 / 4 / 8 / 16, profiles/r01_hub_cluster_ab.txt):
+// DSMEM (~20 B/clk/SM, served from the owner's shared-memory port) is slower than the L2 path
+// it replaces for 2.4-KB rows, and clusters leave SMs idle.
+int hub_cluster() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SG_HUB_CLUSTER");
+    v = e ? atoi(e) : 1;
+    if (v != 1 && v != 2 && v != 4 && v != 8 && v != 16) v = 1;
+  }
+  return v;
+}
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// 16 bytes of CTA `rank`'s shared memory at the address `local` has in this CTA
+template <typename Raw>
+__device__ __forceinline__ Raw ld_dsmem(uint32_t local, uint32_t rank) {
+  uint32_t remote, x, y, z, w;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local), "r"(rank));
+  asm volatile("ld.shared::cluster.v4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(x), "=r"(y), "=r"(z), "=r"(w)
+               : "r"(remote)
+               : "memory");
+  Raw out;
+  uint32_t* o = reinterpret_cast<uint32_t*>(&out);
+  o[0] = x; o[1] = y; o[2] = z; o[3] = w;
+  return out;
+}
+
 // ------------------------------------------------------------------ modes
 template <int MODE>
 struct ModeT;
@@ -176,7 +218,7 @@ struct PropArgs {
   int32_t n_hub;
 };
 
-template <int MODE, int DT, int W, int VPL, int LPR, int DEPTH, bool HUB = false>
+template <int MODE, int DT, int W, int VPL, int LPR, int DEPTH, bool HUB = false, int CS = 1>
 struct Prop {
   using M = ModeT<MODE>;
   using IO = VecIO<DT, W>;
@@ -198,11 +240,21 @@ struct Prop {
 #pragma unroll
     for (int d = 0; d < DEPTH; ++d) {
       if (HUB && (FULL || d < n) && s[d] < 0) {
-        // hub row: served from the CTA's shared-memory copy (same bits as the HBM row)
-        const Raw* hrow = hl + (s[d] & 0x7fffffff) * a.Fv;
+        // hub row: served from shared memory (same bits as the HBM row) -- this CTA's copy,
+        // or with CS > 1 the owning cluster CTA's, through DSMEM
+        const int slot = s[d] & 0x7fffffff;
+        if constexpr (CS == 1) {
+          const Raw* hrow = hl + slot * a.Fv;
 #pragma unroll
-        for (int v = 0; v < VPL; ++v)
-          if (v < VPL - 1 || last_ok) g[d][0][v] = hrow[v * LPR];
+          for (int v = 0; v < VPL; ++v)
+            if (v < VPL - 1 || last_ok) g[d][0][v] = hrow[v * LPR];
+        } else {
+          const uint32_t local = (uint32_t)__cvta_generic_to_shared(hl) +
+                                 (uint32_t)((slot / CS) * a.Fv) * 16u;
+#pragma unroll
+          for (int v = 0; v < VPL; ++v)
+            if (v < VPL - 1 || last_ok) g[d][0][v] = ld_dsmem<Raw>(local + v * LPR * 16u, slot % CS);
+        }
       } else if (FULL || d < n) {
         // 32x32->64 IMAD.WIDE row address; column offsets are immediates
         const Elem* row = gl + (uint64_t)(uint32_t)s[d] * (uint32_t)a.ldg;
@@ -451,22 +503,29 @@ constexpr int prop_min_blocks() {
 // HUB: the block first copies the pass's hub rows (most-referenced source rows, listed in
 // a.hub_rows; their edges carry idx = slot | 0x80000000) into shared memory, so those
 // gathers are served on-chip instead of through L2.  One block of NWB warps per SM.
-template <int MODE, int DT, int W, int VPL, int LPR, int DEPTH, bool HUB = false, int NWB = kWarpsPerBlock>
+template <int MODE, int DT, int W, int VPL, int LPR, int DEPTH, bool HUB = false, int NWB = kWarpsPerBlock,
+          int CS = 1>
 __global__ void __launch_bounds__(NWB * 32, (HUB ? 1 : prop_min_blocks<MODE, W, VPL, DEPTH>()))
     prop_kernel(const PropArgs a) {
-  using K = Prop<MODE, DT, W, VPL, LPR, DEPTH, HUB>;
+  using K = Prop<MODE, DT, W, VPL, LPR, DEPTH, HUB, CS>;
   using Raw = typename K::Raw;
   extern __shared__ __align__(16) unsigned char prop_smem[];
   const Raw* hs = reinterpret_cast<const Raw*>(prop_smem);
   if constexpr (HUB) {
+    // this CTA's hub rows: slots rank, rank + CS, rank + 2 CS, ... (all of them for CS = 1)
     Raw* hw = reinterpret_cast<Raw*>(prop_smem);
-    const int total = a.n_hub * a.Fv;
+    const int rank = CS > 1 ? (int)cluster_rank() : 0;
+    const int mine = (a.n_hub - rank + CS - 1) / CS;
+    const int total = mine * a.Fv;
     for (int i = threadIdx.x; i < total; i += blockDim.x) {
       const int r = i / a.Fv, c = i - r * a.Fv;
       hw[i] = K::IO::ld_raw(static_cast<const typename K::Elem*>(a.G) +
-                            (int64_t)__ldg(a.hub_rows + r) * a.ldg + (int64_t)c * W);
+                            (int64_t)__ldg(a.hub_rows + r * CS + rank) * a.ldg + (int64_t)c * W);
     }
-    __syncthreads();
+    if constexpr (CS > 1)
+      cluster_sync_all();  // every CTA's rows visible cluster-wide before any DSMEM read
+    else
+      __syncthreads();
   }
   constexpr int NOUT = K::NOUT;
   constexpr int NRr = K::NR > 0 ? K::NR : 1;
@@ -545,6 +604,8 @@ __global__ void __launch_bounds__(NWB * 32, (HUB ? 1 : prop_min_blocks<MODE, W, 
       }
     }
   }
+  if constexpr (HUB && CS > 1)
+    cluster_sync_all();  // no CTA leaves while a peer may still read its shared memory
 }
 
 // ------------------------------------------------------------------ dispatch
@@ -660,6 +721,51 @@ cudaError_t launch_async(const PropArgs& a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// hub-cache kernel: one block per SM holding (its share of) the hub rows; CS > 1 launches
+// clusters of CS blocks sharing the rows through DSMEM
+template <int MODE, int DT, int W, int VPL, int LPR, int DEPTH, int NWB, int CS>
+cudaError_t launch_hub(const PropArgs& a, cudaStream_t st) {
+  auto hk = prop_kernel<MODE, DT, W, VPL, LPR, DEPTH, true, NWB, CS>;
+  const int per_cta = (a.n_hub + CS - 1) / CS;
+  const size_t smem = (size_t)per_cta * a.Fv * 16;
+  static int hub_cfg = 0;
+  if (!hub_cfg) {
+    cudaFuncSetAttribute(hk, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (CS > 8) cudaFuncSetAttribute(hk, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    hub_cfg = 1;
+  }
+  int64_t want = ((int64_t)a.n_items + NWB - 1) / NWB;
+  if constexpr (CS == 1) {
+    int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, sm_count()));
+    hk<<<grid, NWB * 32, smem, st>>>(a);
+  } else {
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CS;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.blockDim = dim3(NWB * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    static int max_clusters = 0;
+    if (!max_clusters) {
+      cfg.gridDim = dim3(CS * ((sm_count() + CS - 1) / CS));
+      if (cudaOccupancyMaxActiveClusters(&max_clusters, hk, &cfg) != cudaSuccess || max_clusters <= 0)
+        max_clusters = sm_count() / CS;
+      if (max_clusters <= 0) max_clusters = 1;
+    }
+    const int64_t clusters = std::max<int64_t>(1, std::min<int64_t>((want + CS - 1) / CS, max_clusters));
+    cfg.gridDim = dim3((unsigned)(clusters * CS));
+    cudaError_t e = cudaLaunchKernelEx(&cfg, hk, a);
+    if (e != cudaSuccess) return e;
+  }
+  sg::count_launch();
+  return cudaGetLastError();
+}
+
 template <int MODE, int DT, int W, int VPL, int LPR>
 cudaError_t launch_one(const PropArgs& a, cudaStream_t st) {
   constexpr int NG = ModeT<MODE>::NG;
@@ -680,18 +786,13 @@ cudaError_t launch_one(const PropArgs& a, cudaStream_t st) {
       // hub-cache kernel: one block per SM holding the hub rows, as many warps as the
       // register budget allowed the default kernel (2-3 blocks of 8 warps)
       constexpr int NWB = kWarpsPerBlock * prop_min_blocks<MODE, W, VPL, DEPTH>();
-      auto hk = prop_kernel<MODE, DT, W, VPL, LPR, DEPTH, true, NWB>;
-      const size_t smem = (size_t)a.n_hub * a.Fv * 16;
-      static int hub_cfg = 0;
-      if (!hub_cfg) {
-        cudaFuncSetAttribute(hk, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        hub_cfg = 1;
+      switch (hub_cluster()) {
+        case 2: return launch_hub<MODE, DT, W, VPL, LPR, DEPTH, NWB, 2>(a, st);
+        case 4: return launch_hub<MODE, DT, W, VPL, LPR, DEPTH, NWB, 4>(a, st);
+        case 8: return launch_hub<MODE, DT, W, VPL, LPR, DEPTH, NWB, 8>(a, st);
+        case 16: return launch_hub<MODE, DT, W, VPL, LPR, DEPTH, NWB, 16>(a, st);
+        default: return launch_hub<MODE, DT, W, VPL, LPR, DEPTH, NWB, 1>(a, st);
       }
-      int64_t want = ((int64_t)a.n_items + NWB - 1) / NWB;
-      int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, sm_count()));
-      hk<<<grid, NWB * 32, smem, st>>>(a);
-      sg::count_launch();
-      return cudaGetLastError();
     }
   }
   auto kern = prop_kernel<MODE, DT, W, VPL, LPR, DEPTH>;
@@ -792,7 +893,7 @@ int64_t sg_propagate_hub_capacity(int64_t F, int dtype) {
   // every column slice must be wide enough for the hub kernel (the index is encoded)
   const int64_t last_cols = F % max_cols == 0 ? std::min(F, max_cols) : F % max_cols;
   if (last_cols <= (int64_t)32 * (kHubMinVpl - 1) * VW) return 0;
-  return std::min<int64_t>(hub_smem_bytes() / row_bytes, INT32_MAX);
+  return std::min<int64_t>((hub_smem_bytes() / row_bytes) * hub_cluster(), INT32_MAX);
 }
 
 int sg_propagate_hub(int mode, int dtype, const int64_t* ptr, const int32_t* idx, const float* w,
