@@ -82,7 +82,8 @@ class Partition:
     * ``edge_off[c]:edge_off[c+1]`` -- the chunk's edges in ``csc_*`` / ``csr_*``;
     * ``csc_ptr[cptr_off[c] : cptr_off[c] + n_j + 1]`` -- chunk-local column
       pointers by local destination; ``csc_idx`` = local source id,
-      ``csc_eid`` = input edge id.  Stable by input order within a destination.
+      ``csc_eid`` = input edge id.  Canonical: sorted by local source within a
+      destination, multi-edges (same source) in input order.
     * ``csr_ptr[rptr_off[c] : rptr_off[c] + n_i + 1]`` -- chunk-local row
       pointers by local source; ``csr_idx`` = local destination id,
       ``csr_eid`` = input edge id.  Stable by CSC position within a source
@@ -120,8 +121,10 @@ def partition_2d(src, dst, V, interval_size):
     si, sj = src // interval_size, dst // interval_size
     ls, ld = src - si * interval_size, dst - sj * interval_size
     cid = si * P + sj
-    # CSC: stable by (chunk, local dst), ties in input order
-    csc_eid = np.argsort(cid * interval_size + ld, kind="stable").astype(np.int64)
+    # canonical CSC: by (chunk, local dst), then local src ("CSC sorted by local
+    # dest id" with row indices sorted inside a column); multi-edges keep input order
+    by_src = np.argsort(ls, kind="stable")
+    csc_eid = by_src[np.argsort((cid * interval_size + ld)[by_src], kind="stable")].astype(np.int64)
     # CSR: stable by (chunk, local src) over the CSC order
     csr_perm = np.argsort((cid * interval_size + ls)[csc_eid], kind="stable")
     csr_eid = csc_eid[csr_perm]

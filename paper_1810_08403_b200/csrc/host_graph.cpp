@@ -2,7 +2,8 @@
 // partition_2d and propagation work plans.  Native C++ (OpenMP), no GPU needed.
 //
 // Semantics follow /root/reference/SPEC.md graph-store (:96-165) with the pins
-// of SURVEY.md Appendix B.4-B.5; the generator is the counter-based splitmix64
+// of SURVEY.md Appendix B.5 and a canonical CSC (ties within a destination by local source,
+// multi-edges in input order); the generator is the counter-based splitmix64
 // scheme restated in oracle/rng.py.  tests/test_host_graph.py checks every
 // output array byte for byte against the oracle.
 #include <omp.h>
@@ -215,13 +216,20 @@ int sg_host_partition_2d(const int32_t* src, const int32_t* dst, int64_t E, int6
     cptr_off[c + 1] = cptr_off[c] + nsz(c % P) + 1;
     rptr_off[c + 1] = rptr_off[c] + nsz(c / P) + 1;
   }
-  // 2) per chunk: CSC by local dst (stable), then CSR by local src over CSC order
+  // 2) per chunk: canonical CSC -- by local dst, then local src ("CSC sorted by
+  //    local dest id"; row indices sorted within a column as in a canonical sparse matrix,
+  //    multi-edges in input order) as two stable counting sorts (src, then dst); then CSR by
+  //    local src over the CSC order (so by dst within a source row)
   for (int64_t c = 0; c < P * P; ++c) {
     const int64_t i = c / P, j = c % P, e0 = edge_off[c], e1 = edge_off[c + 1], n = e1 - e0;
     const int64_t bi = i * size, bj = j * size;
     int64_t* cp = csc_ptr + cptr_off[c];
     int64_t* rp = csr_ptr + rptr_off[c];
-    stable_counting_sort(by_chunk.data() + e0, n, nsz(j), [&](int64_t e) { return dst[e] - bj; },
+    // src-sorted order staged in csr_eid (overwritten by the CSR sort below); its pointer
+    // array goes to rp, rewritten below as well
+    stable_counting_sort(by_chunk.data() + e0, n, nsz(i), [&](int64_t e) { return src[e] - bi; },
+                         csr_eid + e0, rp);
+    stable_counting_sort(csr_eid + e0, n, nsz(j), [&](int64_t e) { return dst[e] - bj; },
                          csc_eid + e0, cp);
     stable_counting_sort(csc_eid + e0, n, nsz(i), [&](int64_t e) { return src[e] - bi; },
                          csr_eid + e0, rp);

@@ -96,7 +96,8 @@ class Partition:
     """P x P grid of EdgeChunks; chunk id c = i * P + j.
 
     Same flattened layout as the oracle's ``Partition``: chunk-local CSC
-    pointers by local destination (stable by input order) and chunk-local CSR
+    pointers by local destination (canonical: by local source, multi-edges in input
+    order) and chunk-local CSR
     pointers by local source (stable by CSC position)."""
 
     def __init__(self, g, interval_size):
