@@ -47,7 +47,10 @@ class Workspace:
         return self.buf
 
 
-HUB_CACHE = os.environ.get("SG_HUB", "1") != "0"
+# hub-row cache: opt-in (SG_HUB=1).  With the canonical (source-sorted) CSC the L1 serves the
+# hot rows and the 64-KB shared-memory carve-out cost more than it saved (Reddit L0 15.5 vs
+# 14.2 ms, profiles/r01_hub_cluster_ab.txt)
+HUB_CACHE = os.environ.get("SG_HUB", "0") == "1"
 
 
 def _vec_ok(t, vw):

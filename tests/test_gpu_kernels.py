@@ -670,13 +670,14 @@ def test_hub_cache_bitwise(sg, F, P, T, mode):
     used = [pi.hub(int(_lib.lib.sg_propagate_hub_capacity(F, _lib.SG_F32))) is not None
             for pi in grid.csc.values()]
     assert any(used)
+    saved = K.HUB_CACHE
     K.HUB_CACHE = True
     try:
         with_hub = _gpu_prop_fwd(sg, grid, X, F, pmode)
         K.HUB_CACHE = False
         plain = _gpu_prop_fwd(sg, grid, X, F, pmode)
     finally:
-        K.HUB_CACHE = True
+        K.HUB_CACHE = saved
     assert torch.equal(with_hub, plain)
     part = og.partition_2d(s, d, V, size)
     w = og.gcn_edge_weights(s, d, V, np.float32) if mode == "gcn" else None
@@ -686,7 +687,11 @@ def test_hub_cache_bitwise(sg, F, P, T, mode):
     Gr = _padded(rng.features(V, F, seed=4))
     Z = _padded(rng.features(V, F, seed=8))
     if mode == "gcn":
-        bw = _gpu_prop_bwd(sg, grid, Gr, F, mask=Z)
+        K.HUB_CACHE = True
+        try:
+            bw = _gpu_prop_bwd(sg, grid, Gr, F, mask=Z)
+        finally:
+            K.HUB_CACHE = saved
         ref_b = prim.relu_bwd(saga.gcn_propagate_bwd(part, Gr.cpu().numpy(), w, T=T), Z.cpu().numpy())
         assert np.array_equal(bw.cpu().numpy(), ref_b)
 
