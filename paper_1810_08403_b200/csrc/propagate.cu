@@ -777,7 +777,11 @@ cudaError_t launch_one(const PropArgs& a, cudaStream_t st) {
 #ifndef SG_DEPTH1
 #define SG_DEPTH1 8
 #endif
-  constexpr int DEPTH = (VPL * NG) == 1 ? SG_DEPTH1 : ((VPL * NG) <= 4 ? 8 / (VPL * NG) : (NG > 1 ? 1 : 2));
+#ifndef SG_DEPTH_WIDE
+#define SG_DEPTH_WIDE 2
+#endif
+  constexpr int DEPTH = (VPL * NG) == 1 ? SG_DEPTH1
+                                        : ((VPL * NG) <= 4 ? 8 / (VPL * NG) : (NG > 1 ? 1 : SG_DEPTH_WIDE));
   if constexpr (LPR == 32 && VPL >= 2 && NG == 1 && W > 1) {
     if (tma_enabled() && a.n_hub == 0) return launch_tma<MODE, DT, VPL>(a, st);
   }
