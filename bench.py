@@ -384,8 +384,11 @@ def run_ours(a, cfg):
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                      "kernel": "L0.fwd.propagate (sg_propagate GCN, F=%d)" % F,
                      "algorithmic_bytes_per_launch": algo, "launch_ms": k_ms, "peak_source": peak_src,
-                     "note": "frac > 1: hot source rows are L2-resident (R-MAT); the pass is "
-                             "bound by L2->SM bandwidth, see l2_ceiling_gbs (tools/l2bw.cu)",
+                     "note": "frac > 1: the algorithmic bytes count one source row per edge, but "
+                             "R-MAT's hot rows are re-served from L1/L2 (canonical CSC: sources "
+                             "ascending within a destination); DRAM bytes per launch are in "
+                             "'traffic' (ncu); l2_ceiling_gbs = measured L2->SM ceiling for random "
+                             "2.4-KB row gathers (tools/l2bw.cu)",
                      "l2_ceiling_gbs": l2_ceiling,
                      "frac_of_l2_ceiling": (achieved / l2_ceiling) if (achieved and l2_ceiling) else None},
         "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": int(launches),
