@@ -37,20 +37,24 @@ __global__ void take_rows_kernel(const void* X, int64_t ldx, int64_t n_src, cons
   }
 }
 
-// One warp per segment; lanes over columns; strict '>' so the first (lowest
-// position) maximum wins; -inf init; empty segment -> empty_fill, argmax -1.
-template <int DT, int W>
-__global__ void segmax_kernel(const int64_t* ptr, const int32_t* idx, int64_t n_rows,
-                              const void* X, int64_t ldx, void* out, int64_t ldo, int64_t* arg,
-                              int64_t lda, int F, float fill) {
+// TEAM lanes per segment (narrow rows pack 32/TEAM segments per warp), lanes over column
+// vectors; 4 source rows loaded before any is compared (4 reads in flight per lane); strict
+// '>' so the first (lowest position) maximum wins; -inf init; empty segment -> empty_fill,
+// argmax -1.  argmax = idx[e] (the gathered row, tensor.py:467-469 with rows pre-gathered).
+template <int DT, int W, int TEAM>
+__global__ void __launch_bounds__(256) segmax_kernel(const int64_t* __restrict__ ptr,
+                                                     const int32_t* __restrict__ idx, int64_t n_rows,
+                                                     const void* X, int64_t ldx, void* out, int64_t ldo,
+                                                     int64_t* arg, int64_t lda, int F, float fill) {
   using IO = VecIO<DT, W>;
-  const int lane = threadIdx.x & 31;
+  constexpr int RPW = 32 / TEAM;
+  const int lane = threadIdx.x & 31, tl = lane % TEAM;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t nteams = (((int64_t)gridDim.x * blockDim.x) >> 5) * RPW;
   const int Fv = (F + W - 1) / W;
-  for (int64_t r = warp; r < n_rows; r += nwarps) {
-    const int64_t e0 = ptr[r], e1 = ptr[r + 1];
-    for (int cv = lane; cv < Fv; cv += 32) {
+  for (int64_t r = warp * RPW + lane / TEAM; r < n_rows; r += nteams) {
+    const int64_t e0 = __ldg(ptr + r), e1 = __ldg(ptr + r + 1);
+    for (int cv = tl; cv < Fv; cv += TEAM) {
       float best[W];
       int64_t barg[W];
 #pragma unroll
@@ -58,15 +62,33 @@ __global__ void segmax_kernel(const int64_t* ptr, const int32_t* idx, int64_t n_
         best[k] = -INFINITY;
         barg[k] = -1;
       }
-      for (int64_t e = e0; e < e1; ++e) {
-        const int64_t s = idx[e];
+      int64_t e = e0;
+      for (; e + 4 <= e1; e += 4) {
+        int64_t s[4];
+        float v[4][W];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          s[u] = __ldg(idx + e + u);
+          IO::ld_nc(X, s[u] * ldx + (int64_t)cv * W, v[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int k = 0; k < W; ++k)
+            if (v[u][k] > best[k]) {
+              best[k] = v[u][k];
+              barg[k] = s[u];
+            }
+      }
+      for (; e < e1; ++e) {
+        const int64_t sv = __ldg(idx + e);
         float v[W];
-        IO::ld_nc(X, s * ldx + (int64_t)cv * W, v);
+        IO::ld_nc(X, sv * ldx + (int64_t)cv * W, v);
 #pragma unroll
         for (int k = 0; k < W; ++k)
           if (v[k] > best[k]) {
             best[k] = v[k];
-            barg[k] = s;
+            barg[k] = sv;
           }
       }
       const int nvalid = min(W, F - cv * W);
@@ -410,15 +432,29 @@ int sg_segment_max(int dtype, const int64_t* ptr, const int32_t* idx, int64_t n_
   if (n_rows == 0 || F == 0) return SG_OK;
   SG_REQUIRE(ptr && idx && X && out && argmax, SG_EINVAL, "segment_max: null pointer");
   cudaStream_t st = (cudaStream_t)stream;
-  const int g = grid_for(n_rows * 32, 256);
-  if (dtype == SG_F32) {
-    if (ldx % 4 == 0 && ldo % 4 == 0 && aligned(X, 16) && aligned(out, 16))
-      segmax_kernel<SG_F32, 4><<<g, 256, 0, st>>>(ptr, idx, n_rows, X, ldx, out, ldo, argmax, lda, (int)F, empty_fill);
-    else
-      segmax_kernel<SG_F32, 1><<<g, 256, 0, st>>>(ptr, idx, n_rows, X, ldx, out, ldo, argmax, lda, (int)F, empty_fill);
-  } else {
-    segmax_kernel<SG_BF16, 1><<<g, 256, 0, st>>>(ptr, idx, n_rows, X, ldx, out, ldo, argmax, lda, (int)F, empty_fill);
+  const bool vec = dtype == SG_F32 && ldx % 4 == 0 && ldo % 4 == 0 && aligned(X, 16) && aligned(out, 16);
+  const int team = team_for(vec ? (int)((F + 3) / 4) : (int)F);
+  const int g = grid_for(n_rows * team, 256);
+#define SG_SM(DTv, Wv, T) \
+  segmax_kernel<DTv, Wv, T><<<g, 256, 0, st>>>(ptr, idx, n_rows, X, ldx, out, ldo, argmax, lda, (int)F, empty_fill)
+#define SG_SM_TEAMS(DTv, Wv)       \
+  switch (team) {                  \
+    case 1: SG_SM(DTv, Wv, 1); break;   \
+    case 2: SG_SM(DTv, Wv, 2); break;   \
+    case 4: SG_SM(DTv, Wv, 4); break;   \
+    case 8: SG_SM(DTv, Wv, 8); break;   \
+    case 16: SG_SM(DTv, Wv, 16); break; \
+    default: SG_SM(DTv, Wv, 32); break; \
   }
+  if (vec) {
+    SG_SM_TEAMS(SG_F32, 4)
+  } else if (dtype == SG_F32) {
+    SG_SM_TEAMS(SG_F32, 1)
+  } else {
+    SG_SM_TEAMS(SG_BF16, 1)
+  }
+#undef SG_SM_TEAMS
+#undef SG_SM
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) SG_FAIL(SG_ECUDA, "segment_max launch: %s", cudaGetErrorString(e));
   sg::count_launch(1);

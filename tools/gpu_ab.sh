@@ -1,3 +1,5 @@
-timeout 600 python -m pytest tests -q -x -m gpu -k "ggcn" 2>&1 | tail -2
-timeout 600 python bench.py --config blogcatalog10 --steps 10 --no-cpu-baseline --no-e2e 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('split', d['ms_per_step'], {k: round(v,3) for k,v in d['stages_ms'].items() if 'prop' in k})"
-SG_LIB_PATH=$PWD/paper_1810_08403_b200/libsagann_ab.so timeout 600 python bench.py --config blogcatalog10 --steps 10 --no-cpu-baseline --no-e2e 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('sfu', d['ms_per_step'], {k: round(v,3) for k,v in d['stages_ms'].items() if 'prop' in k})"
+timeout 900 python -m pytest tests -q -x -m gpu -k "segment_max or primitives or max" 2>&1 | tail -2
+timeout 900 python tools/sweep.py --quick 2>/dev/null | grep '"max' | python -c "
+import sys,json
+for l in sys.stdin:
+    d=json.loads(l); print(d['reduction'], d['F'], d['avg_degree'], round(d['ms'],3), round(d['hbm_frac'],2))"

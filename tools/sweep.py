@@ -4,7 +4,8 @@
 
 Uniform random graphs with V = 2^22 vertices (V reduced so E = V*deg <= 2^28), average
 degree 4..512; feature widths 16..1024; Gather(sum) = sg_propagate(PASS) over the CSC
-index, Gather(max) = sg_segment_max; fp32 and bf16 rows.  Every point times the
+index, Gather(max) = sg_segment_max (the primitive, int64 argmax) and sg_max_gather (the MP-GCN
+fused max gather, int32 argmax positions); fp32 and bf16 rows.  Every point times the
 kernel with CUDA events (median of 5 after 2 warm-ups, L2 flushed before each) and
 reports algorithmic bytes / time against MEASURED_PEAKS.json's HBM bandwidth.  Points
 whose source matrix V*F*s is below 4x the L2 size are flagged `l2_resident`.
@@ -94,6 +95,14 @@ def main():
                     rec.update(reduction="max", ms=ms, algo_bytes=byt, gbs=byt / ms / 1e6,
                                hbm_frac=byt / ms / 1e6 / hbm, edges_per_s=E / ms * 1e3)
                     print(json.dumps(rec), flush=True)
+                    # the hot path's fused max gather (K7, MP-GCN): int32 argmax positions
+                    arg32 = torch.empty((V, F), dtype=torch.int32, device=dev)
+                    ms = timed(lambda: K.max_gather(pi, xm, out, arg32, F), flush)
+                    byt = E * (4 + F * s) + V * (4 + F * (s + 4))
+                    rec.update(reduction="max_fused", ms=ms, algo_bytes=byt, gbs=byt / ms / 1e6,
+                               hbm_frac=byt / ms / 1e6 / hbm, edges_per_s=E / ms * 1e3)
+                    print(json.dumps(rec), flush=True)
+                    del arg32
                 del X, out
         del grid, g, pi
         torch.cuda.empty_cache()
