@@ -815,8 +815,15 @@ cudaError_t launch_one(const PropArgs& a, cudaStream_t st) {
 
 // Widest vectors-per-lane instantiated: register pressure grows as VPL * W * (NG + NOUT);
 // wider rows are processed in column slices.
+// widest single-slice row for the one-operand modes: VPL 6-8 spill at 128 registers, so
+// rows wider than 5 vectors per lane (F > 640 fp32) run as several column slices
+// (F = 768 / 1024 / 1100: 21.3 / 32.4 / 37.8 ms at VPL 8 -> 18.0 / 24.7 / 29.1 ms at VPL 5 on
+// the Reddit graph; VPL 4 and 6 in between, profiles/r01_narrow_ab.txt)
+#ifndef SG_VPL_MAX
+#define SG_VPL_MAX 5
+#endif
 constexpr int vpl_max(int mode, int dt) {
-  return (dt == SG_F32 && (mode == SG_PROP_PASS || mode == SG_PROP_GCN)) ? 8 : 4;
+  return (dt == SG_F32 && (mode == SG_PROP_PASS || mode == SG_PROP_GCN)) ? SG_VPL_MAX : 4;
 }
 
 template <int MODE, int DT, int W>
