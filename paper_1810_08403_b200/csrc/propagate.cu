@@ -544,12 +544,22 @@ __global__ void __launch_bounds__(NWB * 32, (HUB ? 1 : prop_min_blocks<MODE, W, 
     // One inlined copy of the edge loop serves whole rows and split subgroups alike
     // (a single call site keeps ptxas register allocation spill-free).
     const int r_end = (split && team != 0) ? item.row_begin : item.row_end;
+    // row extents are loaded one row ahead, so a short row's pointer load does not
+    // serialise with its index and feature loads (low-degree graphs: ~4 edges per row)
+    int64_t n0 = 0, n1 = 0;
+    if (item.row_begin + team < r_end) {
+      n0 = split ? item.e_begin : __ldg(a.ptr + item.row_begin + team);
+      n1 = split ? item.e_end : __ldg(a.ptr + item.row_begin + team + 1);
+    }
 #pragma unroll 1
     for (int r = item.row_begin + team; r < r_end; r += NT) {
       float rs[NRr][VPL][W];
       float acc[NOUT][VPL][W];
-      const int64_t e0 = split ? item.e_begin : __ldg(a.ptr + r);
-      const int64_t e1 = split ? item.e_end : __ldg(a.ptr + r + 1);
+      const int64_t e0 = n0, e1 = n1;
+      if (!split && r + NT < r_end) {
+        n0 = __ldg(a.ptr + r + NT);
+        n1 = __ldg(a.ptr + r + NT + 1);
+      }
       K::load_row_state(a, r, tl, rs);
       K::init_acc(a, r, tl, acc, a.accumulate != 0 && !split);
       K::run_edges(a, e0, e1, rs, acc, tmask, tl, hs);

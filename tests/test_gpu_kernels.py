@@ -652,14 +652,14 @@ def test_commnet_epoch_vs_oracle(sg, P, T):
 
 
 @pytest.mark.parametrize("F,P,T,mode", [(602, 1, 4096, "gcn"), (500, 1, 256, "gcn"), (512, 3, 64, "pass"),
-                                        (2048, 1, 4096, "gcn")])
+                                        (1800, 1, 4096, "gcn")])
 def test_hub_cache_bitwise(sg, F, P, T, mode):
     """sg_propagate_hub (hub rows served from shared memory) == the plain pass == the oracle."""
     from paper_1810_08403_b200 import _lib
     from paper_1810_08403_b200 import kernels as K
 
     V, E = 6000, 150000
-    for narrow in (128, 1100):  # 1-vector rows / a narrow last column slice: no hub path
+    for narrow in (128, 700):  # 1-vector rows / a narrow last column slice (640 + 60): no hub path
         assert _lib.lib.sg_propagate_hub_capacity(narrow, _lib.SG_F32) == 0
     s, d = _graph("rmat", V, E, 11)
     g = sg.Graph(V, s, d)
