@@ -57,12 +57,29 @@ __global__ void xent_rows_kernel(const float* Z, int64_t ldz, int relu_input, co
   }
 }
 
-// Deterministic mean: one block, fixed per-thread strided order, fixed tree.
-__global__ void xent_mean_kernel(const float* logp, int64_t n, int64_t n_total, float* loss) {
-  __shared__ double s[1024];
+// Deterministic mean in two launches: kXentParts blocks each sum a fixed contiguous range
+// (fixed per-thread strided order, fixed tree, fp64), then one block adds the partials in a
+// fixed tree.  kXentParts is a constant (not the SM count) so results do not depend on the GPU.
+constexpr int kXentParts = 148;
+
+__global__ void xent_partial_kernel(const float* logp, int64_t n, double* part) {
+  __shared__ double s[256];
+  const int64_t chunk = (n + kXentParts - 1) / kXentParts;
+  const int64_t b = (int64_t)blockIdx.x * chunk, e = min(n, b + chunk);
   double acc = 0.0;
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) acc += (double)logp[i];
+  for (int64_t i = b + threadIdx.x; i < e; i += blockDim.x) acc += (double)logp[i];
   s[threadIdx.x] = acc;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) s[threadIdx.x] += s[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = s[0];
+}
+
+__global__ void xent_mean_kernel(const double* part, int64_t n_total, float* loss) {
+  __shared__ double s[256];
+  s[threadIdx.x] = (int)threadIdx.x < kXentParts ? part[threadIdx.x] : 0.0;
   __syncthreads();
   for (int w = blockDim.x / 2; w > 0; w >>= 1) {
     if ((int)threadIdx.x < w) s[threadIdx.x] += s[threadIdx.x + w];
@@ -153,7 +170,9 @@ __global__ void convert_kernel(const S* X, int64_t ldx, D* Y, int64_t ldy, int64
 
 extern "C" {
 
-int64_t sg_xent_workspace_bytes(int64_t n) { return std::max<int64_t>(n, 1) * 4; }
+int64_t sg_xent_workspace_bytes(int64_t n) {
+  return (std::max<int64_t>(n, 1) * 4 + 255) / 256 * 256 + kXentParts * 8;
+}
 
 int sg_softmax_xent(const float* Z, int64_t ldz, int relu_input, const int64_t* labels, int64_t n,
                     int64_t C, int64_t n_total, float* loss, float* dZ, int64_t lddz,
@@ -166,9 +185,13 @@ int sg_softmax_xent(const float* Z, int64_t ldz, int relu_input, const int64_t* 
   xent_rows_kernel<<<grid_for(n * 32, 256), 256, 0, st>>>(Z, ldz, relu_input, labels, n, C, n_total,
                                                          dZ, lddz, logp, err_flag);
   SG_LAUNCH_CHECK("xent rows");
-  xent_mean_kernel<<<1, 1024, 0, st>>>(logp, n, n_total, loss);
+  double* part = reinterpret_cast<double*>(static_cast<char*>(workspace) +
+                                           (std::max<int64_t>(n, 1) * 4 + 255) / 256 * 256);
+  xent_partial_kernel<<<kXentParts, 256, 0, st>>>(logp, n, part);
+  SG_LAUNCH_CHECK("xent partial");
+  xent_mean_kernel<<<1, 256, 0, st>>>(part, n_total, loss);
   SG_LAUNCH_CHECK("xent mean");
-  sg::count_launch(2);
+  sg::count_launch(3);
   return SG_OK;
 }
 
