@@ -1,6 +1,4 @@
-timeout 900 python -m pytest tests -q -x -m gpu -k "propagate or model or ggcn or hub" 2>&1 | tail -2
-timeout 300 python tools/narrow_ab.py 16 128 602 2>&1 | grep -v Warn | tail -1
-timeout 900 python tools/sweep.py --quick 2>/dev/null | grep '"sum"' | python -c "
-import sys,json
-for l in sys.stdin:
-    d=json.loads(l); print(d['dtype'], d['F'], d['avg_degree'], round(d['ms'],3), round(d['hbm_frac'],2))"
+ncu --set full --clock-control none --import-source on -k regex:prop_kernel --launch-skip 2 --launch-count 1 -o /tmp/narrow python tools/narrow_point.py 16 4 > /tmp/n.log 2>&1
+tail -2 /tmp/n.log
+python tools/ncu_summary.py report /tmp/narrow.ncu-rep
+ncu -i /tmp/narrow.ncu-rep --page raw --csv --metrics l1tex__t_sector_hit_rate.pct,smsp__warps_eligible.avg.per_cycle_active,smsp__issue_active.avg.pct_of_peak_sustained_active,dram__throughput.avg.pct_of_peak_sustained_elapsed | tail -2
