@@ -251,7 +251,8 @@ class SAGAModel:
         X = torch.as_tensor(X)
         if tuple(X.shape[:1]) != (self.V,) or X.shape[1] < self.layers[0].F:
             raise ShapeError(f"features must be [V={self.V}, {self.layers[0].F}]")
-        self.X.copy_(X[:, : self.layers[0].F], non_blocking=True)
+        dst = self._xbufs[self._cur] if getattr(self, "_graphs", None) else self.X
+        dst.copy_(X[:, : self.layers[0].F], non_blocking=True)
 
     def load_labels(self, labels):
         self.labels.copy_(torch.as_tensor(np.asarray(labels, np.int64)), non_blocking=True)
@@ -259,32 +260,50 @@ class SAGAModel:
     def prefetch_inputs(self, X_host, labels_host):
         """Stage the NEXT step's features and labels (pinned host tensors) on a copy stream.
 
-        The H2D copy overlaps the current step's kernels; the next ``train_step`` makes
-        the compute stream wait for it and moves the staged inputs into place (a D2D
-        copy), so input transfer is pipelined with compute (double buffering)."""
+        The H2D copy overlaps the current step's kernels.  With two captured graphs
+        (``capture(double_buffer=True)``) the features land directly in the feature buffer
+        the next graph reads (the one the running step does not), so nothing is moved on
+        the device; otherwise the next step makes the compute stream wait for the copy and
+        moves the staged inputs into place (a D2D copy).  A host tensor laid out like the
+        device buffer (``[V, ld]``, 16-B padded rows) is copied as one contiguous block."""
+        F = self.layers[0].F
         if getattr(self, "_copy_stream", None) is None:
             self._copy_stream = torch.cuda.Stream(device=self.device)
-            self._stage_X = torch.empty((self.V, self.layers[0].F), dtype=torch.float32,
-                                        device=self.device)
             self._stage_y = torch.empty_like(self.labels)
+            self._stage_X = None if getattr(self, "_graphs", None) else torch.empty_like(self.X._base)[:, :F]
             self._staged = None
             self._consumed = None
         cs = self._copy_stream
-        if self._consumed is not None:
-            cs.wait_event(self._consumed)  # previous staging buffer already moved into place
+        graphs = getattr(self, "_graphs", None)
+        if graphs is not None:
+            tgt = 1 - self._cur
+            dst = self._xbufs[tgt]
+            if self._done[tgt] is not None:
+                cs.wait_event(self._done[tgt])  # the last step that read this buffer is done
+        else:
+            tgt, dst = None, self._stage_X
+            if self._consumed is not None:
+                cs.wait_event(self._consumed)  # previous staging buffer already moved into place
         with torch.cuda.stream(cs):
-            self._stage_X.copy_(X_host[:, : self.layers[0].F], non_blocking=True)
+            if X_host.is_contiguous() and tuple(X_host.shape) == tuple(dst._base.shape):
+                dst._base.copy_(X_host, non_blocking=True)
+            else:
+                dst.copy_(X_host[:, :F], non_blocking=True)
             self._stage_y.copy_(labels_host, non_blocking=True)
             ev = torch.cuda.Event()
             ev.record(cs)
         self._staged = ev
+        self._staged_tgt = tgt
 
     def _take_staged(self):
         if getattr(self, "_staged", None) is None:
             return
         cur = torch.cuda.current_stream(self.device)
         cur.wait_event(self._staged)
-        self.X.copy_(self._stage_X)
+        if self._staged_tgt is not None:
+            self._cur = self._staged_tgt          # the next graph reads the buffer just filled
+        else:
+            self.X.copy_(self._stage_X)
         self.labels.copy_(self._stage_y)
         ev = torch.cuda.Event()
         ev.record(cur)
@@ -581,8 +600,13 @@ class SAGAModel:
             return int(z["epoch"])
 
     # ------------------------------------------------------------------ CUDA graph
-    def capture(self, lr=0.01, warmup=1):
-        """Record one full training step (forward, backward, SGD) as a CUDA graph."""
+    def capture(self, lr=0.01, warmup=1, double_buffer=True):
+        """Record one full training step (forward, backward, SGD) as a CUDA graph.
+
+        ``double_buffer``: also record a second graph whose layer-1 input is a second
+        feature buffer, so ``prefetch_inputs`` can copy the next step's features straight
+        into the buffer the running step does not read (no device-side move); replays
+        alternate between the two (GCN / passthrough first layers)."""
         s = torch.cuda.Stream(device=self.device)
         s.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(s):
@@ -598,11 +622,34 @@ class SAGAModel:
         self.graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(self.graph):
             self.train_step(lr)
+        self._graphs = None
+        L0 = self.layers[0]
+        if double_buffer and L0.kind in ("gcn", "pass") and L0.hin is self.X:
+            X2 = torch.zeros_like(self.X._base)[:, : L0.F]
+            X2.copy_(self.X)
+            L0.hin = X2
+            try:
+                g2 = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g2):
+                    self.train_step(lr)
+            finally:
+                L0.hin = self.X
+            self._graphs = [self.graph, g2]
+            self._xbufs = [self.X, X2]
+            self._done = [None, None]
+            self._cur = 0
+            self._copy_stream = None  # re-created for the double-buffered layout
         return self.graph
 
     def replay(self):
         self._take_staged()
-        self.graph.replay()
+        if getattr(self, "_graphs", None) is None:
+            self.graph.replay()
+            return self.loss
+        self._graphs[self._cur].replay()
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(self.device))
+        self._done[self._cur] = ev
         return self.loss
 
     def check_status(self):
