@@ -192,6 +192,35 @@ class DistSAGA:
     def load_labels(self, y_local):
         self.labels.copy_(torch.as_tensor(np.asarray(y_local, np.int64)), non_blocking=True)
 
+    def prefetch_inputs(self, X_host, y_host):
+        """Stage the next step's local feature / label shard (pinned host) on a copy stream,
+        overlapping the running step; the next ``train_step`` waits for it and moves it into
+        place (one D2D copy of the shard)."""
+        if getattr(self, "_cs", None) is None:
+            self._cs = torch.cuda.Stream(device=self.c.device)
+            self._sx = torch.empty_like(self.h[0])
+            self._sy = torch.empty_like(self.labels)
+            self._used = None
+        if self._used is not None:
+            self._cs.wait_event(self._used)
+        with torch.cuda.stream(self._cs):
+            self._sx.copy_(torch.as_tensor(X_host)[:, : self.dims[0]], non_blocking=True)
+            self._sy.copy_(torch.as_tensor(y_host), non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(self._cs)
+        self._staged = ev
+
+    def _take_staged(self):
+        if getattr(self, "_staged", None) is None:
+            return
+        cur = torch.cuda.current_stream(self.c.device)
+        cur.wait_event(self._staged)
+        self.h[0].copy_(self._sx)
+        self.labels.copy_(self._sy)
+        self._used = torch.cuda.Event()
+        self._used.record(cur)
+        self._staged = None
+
     def weights(self):
         return [p.detach().cpu().numpy().copy() for p in self.params]
 
@@ -348,6 +377,7 @@ class DistSAGA:
         self._mark("sgd")
 
     def train_step(self, lr=0.01):
+        self._take_staged()
         self.forward()
         self.backward()
         self.sgd(lr)
@@ -447,14 +477,15 @@ def bench_main(a, cfg, metric, config, helpers):
     # and the loss read back; wall clock, max over ranks
     e2e = None
     if not a.no_e2e:
-        n_e2e = max(3, a.steps // 2)
+        n_e2e = max(5, a.steps)
         torch.cuda.synchronize()
         dist.barrier()
         t1 = time.perf_counter()
-        for _ in range(n_e2e):
-            model.load_features(X_host)
-            model.load_labels(y_host)
+        model.prefetch_inputs(X_host, y_host)
+        for k in range(n_e2e):
             model.train_step(a.lr)
+            if k + 1 < n_e2e:
+                model.prefetch_inputs(X_host, y_host)   # overlaps this step
             float(model.loss.item())
         te = torch.tensor([(time.perf_counter() - t1) / n_e2e], device=dev, dtype=torch.float64)
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
@@ -464,8 +495,8 @@ def bench_main(a, cfg, metric, config, helpers):
         t_e2e = float(te.item())
         e2e = {"value": E / t_e2e, "unit": "edges/s", "h2d_bytes_per_step": int(bi.item()),
                "d2h_bytes_per_step": 4 * world, "ms_per_step": t_e2e * 1e3,
-               "note": "wall clock, max over ranks: per-step H2D of every rank's feature/label "
-                       "shard, the step, loss D2H"}
+               "note": "wall clock, max over ranks: per step, H2D of every rank's feature/label "
+                       "shard (copy stream, overlapping the previous step), the step, loss D2H"}
     lt = torch.tensor([float(launches)], device=dev, dtype=torch.float64)
     dist.all_reduce(lt)
     shard_edges = _gather_ints(shard.local_edges, world, dev)
