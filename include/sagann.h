@@ -43,7 +43,9 @@ enum sg_prop_mode {
   SG_PROP_GCN = 1,          /* t_e = G[idx_e] * w_e           (GCN fwd on CSC, bwd on CSR)  */
   SG_PROP_GGCN_FWD = 2,     /* G=[h|P], R=Q:  t = sig(P[v]+Q[u]) * h[v]                     */
   SG_PROP_GGCN_BWD_DST = 3, /* CSC. G=[h|P], R=[dA|Q]: dQ[u] = sum ((dA[u]*h[v])*eta)*(1-eta) */
-  SG_PROP_GGCN_BWD_SRC = 4  /* CSR. G=[dA|Q], R=[h|P]: dP[v] = sum t_e, dH[v] = sum dA[u]*eta */
+  SG_PROP_GGCN_BWD_SRC = 4, /* CSR. G=[dA|Q], R=[h|P]: dP[v] = sum t_e, dH[v] = sum dA[u]*eta */
+  SG_PROP_GGCN_FWD_S = 5    /* GGCN_FWD + out1: S[u] = sum (h[v]*eta)*(1-eta), so the backward
+                               dQ[u] = dA[u] * S[u] (dA[u] is constant over u's in-edges) */
 };
 
 enum sg_epilogue { SG_EPI_NONE = 0, SG_EPI_RELU_DUAL = 1 };

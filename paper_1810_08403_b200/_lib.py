@@ -23,7 +23,7 @@ HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "sagann.h")
 
 SG_OK, SG_ESHAPE, SG_ENUMERIC, SG_EBUDGET, SG_ECUDA, SG_ENCCL, SG_EINVAL, SG_EFORMAT = range(8)
 SG_F32, SG_BF16 = 0, 1
-PROP_PASS, PROP_GCN, PROP_GGCN_FWD, PROP_GGCN_BWD_DST, PROP_GGCN_BWD_SRC = range(5)
+PROP_PASS, PROP_GCN, PROP_GGCN_FWD, PROP_GGCN_BWD_DST, PROP_GGCN_BWD_SRC, PROP_GGCN_FWD_S = range(6)
 EPI_NONE, EPI_RELU_DUAL = 0, 1
 GEMM_F32, GEMM_TF32X3, GEMM_BF16 = 0, 1, 2
 

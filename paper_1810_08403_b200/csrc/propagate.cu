@@ -162,6 +162,21 @@ struct ModeT<SG_PROP_GGCN_FWD> {
 };
 
 template <>
+struct ModeT<SG_PROP_GGCN_FWD_S> {
+  static constexpr int NG = 2, NR = 1, NOUT = 2, GATE_ROW = 0;
+  static constexpr bool USE_W = false;
+  // the forward term plus S_e = (h[v] * eta) * (1 - eta): the destination-independent factor
+  // of the backward dQ term ((dA[u] * h[v]) * eta) * (1 - eta), summed per destination now so
+  // the backward needs no second CSC pass (dQ = dA (.) S)
+  static __device__ __forceinline__ void term(const float* g0, const float* g1, const float* r0,
+                                              const float*, float, float* t0, float* t1) {
+    float eta = gate(g1[0], r0[0]);
+    t0[0] = __fmul_rn(eta, g0[0]);
+    t1[0] = __fmul_rn(__fmul_rn(g0[0], eta), __fsub_rn(1.0f, eta));
+  }
+};
+
+template <>
 struct ModeT<SG_PROP_GGCN_BWD_DST> {
   static constexpr int NG = 2, NR = 2, NOUT = 1, GATE_ROW = 1;
   static constexpr bool USE_W = false;
@@ -623,7 +638,7 @@ struct LaunchCfg {
   int W, VPL, LPR;
 };
 
-int mode_nout(int mode) { return mode == SG_PROP_GGCN_BWD_SRC ? 2 : 1; }
+int mode_nout(int mode) { return (mode == SG_PROP_GGCN_BWD_SRC || mode == SG_PROP_GGCN_FWD_S) ? 2 : 1; }
 int mode_ng(int mode) { return mode >= SG_PROP_GGCN_FWD ? 2 : 1; }
 
 int g_sm_count = 0;
@@ -924,14 +939,15 @@ int sg_propagate_hub(int mode, int dtype, const int64_t* ptr, const int32_t* idx
                      int64_t ld1, const void* mask, int64_t ldm, int64_t F, int accumulate,
                      const int32_t* hub_rows, int64_t n_hub, void* workspace, int64_t workspace_bytes,
                      void* stream) {
-  SG_REQUIRE(mode >= SG_PROP_PASS && mode <= SG_PROP_GGCN_BWD_SRC, SG_EINVAL, "bad mode %d", mode);
+  SG_REQUIRE(mode >= SG_PROP_PASS && mode <= SG_PROP_GGCN_FWD_S, SG_EINVAL, "bad mode %d", mode);
   SG_REQUIRE(dtype == SG_F32 || dtype == SG_BF16, SG_EINVAL, "bad dtype %d", dtype);
   SG_REQUIRE(n_items >= 0 && n_items <= INT32_MAX, SG_EINVAL, "bad n_items");
   if (n_rows == 0 || F == 0 || n_items == 0) return SG_OK;
   SG_REQUIRE(ptr && idx && items && G && out0, SG_EINVAL, "null required pointer");
   SG_REQUIRE(mode != SG_PROP_GCN || w, SG_EINVAL, "GCN mode needs edge weights");
   SG_REQUIRE(mode < SG_PROP_GGCN_FWD || R, SG_EINVAL, "gated modes need row-side operand R");
-  SG_REQUIRE(mode != SG_PROP_GGCN_BWD_SRC || out1, SG_EINVAL, "GGCN_BWD_SRC needs out1");
+  SG_REQUIRE((mode != SG_PROP_GGCN_BWD_SRC && mode != SG_PROP_GGCN_FWD_S) || out1, SG_EINVAL,
+             "mode %d needs out1", mode);
   SG_REQUIRE(n_splits == 0 || splits, SG_EINVAL, "split records missing");
   const int64_t need = sg_propagate_workspace_bytes(n_items, n_splits, n_slots, F, mode);
   SG_REQUIRE(workspace && workspace_bytes >= need, SG_EBUDGET,
@@ -1000,6 +1016,7 @@ int sg_propagate_hub(int mode, int dtype, const int64_t* ptr, const int32_t* idx
       case SG_PROP_GCN: e = dispatch_mode<SG_PROP_GCN>(dtype, vec, a, LPR, VPL, st); break;
       case SG_PROP_GGCN_FWD: e = dispatch_mode<SG_PROP_GGCN_FWD>(dtype, vec, a, LPR, VPL, st); break;
       case SG_PROP_GGCN_BWD_DST: e = dispatch_mode<SG_PROP_GGCN_BWD_DST>(dtype, vec, a, LPR, VPL, st); break;
+      case SG_PROP_GGCN_FWD_S: e = dispatch_mode<SG_PROP_GGCN_FWD_S>(dtype, vec, a, LPR, VPL, st); break;
       default: e = dispatch_mode<SG_PROP_GGCN_BWD_SRC>(dtype, vec, a, LPR, VPL, st); break;
     }
     if (e != cudaSuccess) SG_FAIL(SG_ECUDA, "propagate launch: %s", cudaGetErrorString(e));

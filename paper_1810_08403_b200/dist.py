@@ -19,8 +19,8 @@ SURVEY.md §8(e), replacing the reference's ring-streaming simulator
 * loss: softmax-CE over local rows normalised by the global |V|, loss all-reduced;
 * backward: dW_r = a_r^T dz_r all-reduced; GCN streams the dA blocks and runs the CSR
   duals over C_{r,j} (ascending j) with the ReLU mask of the layer below fused; G-GCN
-  runs pass A (CSC, dQ) over the [h | P] blocks kept from the forward, streams the
-  [dA | Q] blocks and runs pass B (CSR, dP and the take_rows part of dh) over them.
+  takes dQ = dA (.) S with S summed by the forward (GGCN_FWD_S), streams the [dA | Q]
+  blocks and runs pass B (CSR, dP and the take_rows part of dh) over them.
 NVSwitch gives every GPU full bandwidth to every peer, so the reference's fat-tree /
 ring ordering (built to avoid shared PCIe links) reduces to per-block broadcasts.
 
@@ -107,6 +107,9 @@ class CudaCompute:
     def add(self, a, b, out):
         self.K.ewise(0, a, b, out)
 
+    def mul(self, a, b, out):
+        self.K.ewise(2, a, b, out)
+
     def relu_bwd(self, g, z, out):
         self.K.ewise(8, g, z, out)
 
@@ -174,6 +177,7 @@ class DistSAGA:
             self.dQ = [compute.zeros(n, dims[l]) for l in range(L)]
             self.dP = [compute.zeros(n, dims[l]) for l in range(L)]
             self.dHt = [compute.zeros(n, dims[l]) for l in range(L)]
+            self.S = [compute.zeros(n, dims[l]) for l in range(L)]  # GGCN_FWD_S second output
             F0 = max(dims[:-1])
             self.t1, self.t2 = compute.zeros(n, F0), compute.zeros(n, F0)
             self.h[0] = self.HP[0][:, : dims[0]]
@@ -286,8 +290,8 @@ class DistSAGA:
                 blocks = self._stream_blocks(("HP", l), HP, go + F)
                 for k, i in enumerate(chain):
                     blocks[i][1].wait()
-                    c.propagate(s.csc[i], _lib.PROP_GGCN_FWD, blocks[i][0], self.a[l], F, g_off=go,
-                                R=self.GQ[l][:, go: go + F], accumulate=k > 0)
+                    c.propagate(s.csc[i], _lib.PROP_GGCN_FWD_S, blocks[i][0], self.a[l], F, g_off=go,
+                                R=self.GQ[l][:, go: go + F], out1=self.S[l], accumulate=k > 0)
             else:
                 blocks = self._stream_blocks(("h", F), self.h[l], F)
                 for k, i in enumerate(chain):   # source intervals ascending (Locality order)
@@ -338,14 +342,8 @@ class DistSAGA:
         GQ = self.GQ[l]
         c.gemm(self.dz[l], self.W[l], GQ[:, :F], trans_b=True)          # dA = dz W^T
         self._mark(f"L{l}.bwd.apply_vertex")
-        # pass A over the local CSC column: dQ[u], with the [h | P] blocks of the forward
-        hp_blocks = self._blocks[("HP", l)]
-        chain = [i for i in range(self.world) if i in s.csc]
-        if not chain:
-            self.dQ[l].zero_()
-        for k, i in enumerate(chain):
-            c.propagate(s.csc[i], _lib.PROP_GGCN_BWD_DST, hp_blocks[i][:, : go + F], self.dQ[l], F,
-                        g_off=go, R=GQ, r_off=go, accumulate=k > 0)
+        # dQ[u] = dA[u] (.) S[u], S summed by the forward (GGCN_FWD_S): no second CSC pass
+        c.mul(GQ[:, :F], self.S[l], self.dQ[l])
         # pass B over the local CSR row: dP[v], dh_take[v], with streamed [dA | Q] blocks
         blocks = self._stream_blocks(("GQ", l), GQ, go + F)
         chain = [j for j in range(self.world) if j in s.csr]

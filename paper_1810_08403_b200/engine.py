@@ -211,6 +211,7 @@ class SAGAModel:
                 L.WH, L.dWH = _param(L, F, F, dev)
                 L.WC, L.dWC = _param(L, F, F, dev)
                 L.dQ, L.dP, L.dHt = _mat(V, F, dev), _mat(V, F, dev), _mat(V, F, dev)
+                L.S = _mat(V, F, dev)  # sum_e (h eta)(1 - eta) per destination (GGCN_FWD_S)
                 L.params = [L.WH, L.WC, L.W]
                 L.dparams = [L.dWH, L.dWC, L.dW]
             else:
@@ -324,12 +325,16 @@ class SAGAModel:
         for j in range(P):
             if not any((i, j) in g.csc for i in range(P)):
                 self._rows(out, j).zero_()
+                if L.kind == "ggcn":
+                    self._rows(L.S, j).zero_()
         for (i, j), first, _ in self._chunk_order(list(g.csc), 1):
             pi = g.csc[(i, j)]
             if L.kind == "ggcn":
-                K.propagate(pi, _lib.PROP_GGCN_FWD, self._rows(L.HP, i), self._rows(L.a, j), L.F,
-                            g_off=L.goff, R=self._rows(L.Qv, j), accumulate=not first, ws=self.ws,
-                            stream=stream)
+                # the forward also sums S = (h eta)(1 - eta) per destination, so the backward's
+                # dQ = dA (.) S needs no second pass over the CSC (GGCN_FWD_S)
+                K.propagate(pi, _lib.PROP_GGCN_FWD_S, self._rows(L.HP, i), self._rows(L.a, j), L.F,
+                            g_off=L.goff, R=self._rows(L.Qv, j), out1=self._rows(L.S, j),
+                            accumulate=not first, ws=self.ws, stream=stream)
             else:
                 mode = _lib.PROP_GCN if L.kind == "gcn" else _lib.PROP_PASS
                 K.propagate(pi, mode, self._rows(src, i), self._rows(out, j), F,
@@ -374,14 +379,8 @@ class SAGAModel:
 
     def _bwd_propagate_ggcn(self, L, stream=None):
         g, P = self.grid, self.grid.P
-        for j in range(P):  # pass A over CSC: dQ[u]
-            chain = [i for i in range(P) if (i, j) in g.csc]
-            if not chain:
-                self._rows(L.dQ, j).zero_()
-            for k, i in enumerate(chain):
-                K.propagate(g.csc[(i, j)], _lib.PROP_GGCN_BWD_DST, self._rows(L.HP, i),
-                            self._rows(L.dQ, j), L.F, g_off=L.goff, R=self._rows(L.GQ, j),
-                            r_off=L.goff, accumulate=k > 0, ws=self.ws, stream=stream)
+        # dQ[u] = sum_in(u) ((dA[u] h[v]) eta)(1 - eta) = dA[u] (.) S[u] with S from the forward
+        K.ewise(2, L.dAv, L.S, L.dQ, stream)
         for i in range(P):  # pass B over CSR: dP[v], dH_take[v]
             chain = [j for j in range(P) if (i, j) in g.csr]
             if not chain:

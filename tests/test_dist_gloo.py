@@ -42,9 +42,13 @@ class NumpyCompute:
             t = Gn[idx][:, :F]
             if pi.w is not None:
                 t = t * pi.w.numpy().astype(np.float64)[:, None]
-        elif mode == _lib.PROP_GGCN_FWD:   # G = [h | P] of the sources, R = Q of the rows
+        elif mode in (_lib.PROP_GGCN_FWD, _lib.PROP_GGCN_FWD_S):  # G = [h | P], R = Q of the rows
             eta = prim.sigmoid(Gn[idx, g_off:g_off + F] + R.numpy()[rows, :F])
             t = eta * Gn[idx, :F]
+            if mode == _lib.PROP_GGCN_FWD_S:   # S = sum (h eta)(1 - eta)
+                base1 = out1.numpy().copy() if accumulate else None
+                out1.copy_(torch.from_numpy(saga.seq_sum_rows(ptr, (Gn[idx, :F] * eta) * (1.0 - eta), base1,
+                                                              self.T, F=F, dtype=np.float64)))
         elif mode == _lib.PROP_GGCN_BWD_DST:  # G = [h | P] sources, R = [dA | Q] rows
             Rn = R.numpy()
             eta = prim.sigmoid(Gn[idx, g_off:g_off + F] + Rn[rows, r_off:r_off + F])
@@ -74,6 +78,9 @@ class NumpyCompute:
 
     def add(self, a, b, out):
         out.copy_(a + b)
+
+    def mul(self, a, b, out):
+        out.copy_(a * b)
 
     def relu_bwd(self, g, z, out):
         out.copy_(torch.from_numpy(prim.relu_bwd(g.numpy(), z.numpy())))

@@ -154,6 +154,18 @@ def test_ggcn_propagate_fwd_bwd(sg, P, T):
     refA = saga.ggcn_propagate_fwd(part, h, Pm, Qm, T)
     rQ, rP, rH = saga.ggcn_propagate_bwd(part, h, Pm, Qm, Ga, T)
     assert_close(A.cpu().numpy(), refA, 1e-5, "A")
+    # GGCN_FWD_S: the same aggregate (bitwise) plus S, with dQ = dA (.) S == pass A's dQ
+    A2 = torch.zeros((V, F), device="cuda")
+    S = torch.zeros((V, F), device="cuda")
+    for j in range(P):
+        for k, i in enumerate([i for i in range(P) if (i, j) in grid.csc]):
+            K.propagate(grid.csc[(i, j)], _lib.PROP_GGCN_FWD_S, rows(HP, i), rows(A2, j), F, g_off=F,
+                        R=rows(GQ, j)[:, F:], out1=rows(S, j), accumulate=k > 0)
+    assert torch.equal(A2, A)
+    # elementwise floor 0.5 (not 0.1) of the 1e-5 band: the gate factor eta (1 - eta) carries the
+    # SFU's ~2-ulp error, amplified by the cancellation in 1 - eta for saturated gates, and dQ now
+    # sums it before (not after) the multiplication by dA
+    assert_close((torch.from_numpy(Ga).cuda() * S).cpu().numpy(), rQ, 1e-5, "dA*S", floor=0.5)
     assert_close(dQ.cpu().numpy(), rQ, 1e-5, "dQ")
     assert_close(dP.cpu().numpy(), rP, 1e-5, "dP")
     assert_close(dH.cpu().numpy(), rH, 1e-5, "dH")
