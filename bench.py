@@ -299,8 +299,10 @@ def run_ours(a, cfg):
     # ---- roofline of the dominant kernel: layer-1 fused gather (stage L0.fwd.propagate)
     peak, peak_src = measured_peaks()
     k_ms = stages.get("L0.fwd.propagate")
+    # G-GCN forward (GGCN_FWD_S): per edge index + [h | P] row; per destination the pointer,
+    # Q read, aggregate and S written
     algo = gcn_pass_bytes(V, E, F) if cfg["model"] == "gcn" else \
-        E * (4 + 2 * F * 4) + V * (4 + 2 * F * 4)
+        E * (4 + 2 * F * 4) + V * (4 + 3 * F * 4)
     achieved = algo / (k_ms / 1e3) / 1e9 if k_ms else None
     l2_ceiling = None  # measured L2->SM gather ceiling for 2.4-KB rows (tools/l2bw.cu)
     probe = os.path.join(ROOT, "profiles", "r01_l2_probe.txt")
@@ -395,7 +397,8 @@ def run_ours(a, cfg):
         "config": config_of(cfg, a, world),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                     "kernel": "L0.fwd.propagate (sg_propagate GCN, F=%d)" % F,
+                     "kernel": "L0.fwd.propagate (sg_propagate %s, F=%d)" % (
+                         "GCN" if cfg["model"] == "gcn" else "GGCN_FWD_S", F),
                      "algorithmic_bytes_per_launch": algo, "launch_ms": k_ms, "peak_source": peak_src,
                      "note": "frac > 1: the algorithmic bytes count one source row per edge, but "
                              "R-MAT's hot rows are re-served from L1/L2 (canonical CSC: sources "

@@ -389,7 +389,7 @@ def pass_bytes(model, nnz, rows, F, s=4):
     """SURVEY.md §8(d) algorithmic bytes of one forward gather pass over a chunk."""
     if model == "gcn":
         return nnz * (4 + 4 + F * s) + rows * (4 + F * s)
-    return nnz * (4 + 2 * F * s) + rows * (4 + 2 * F * s)
+    return nnz * (4 + 2 * F * s) + rows * (4 + 3 * F * s)
 
 
 def bench_main(a, cfg, metric, config, helpers):
