@@ -1,1 +1,2 @@
-for c in 0 -1 50 100; do SG_CARVEOUT=$c timeout 300 python tools/narrow_ab.py 128 602 2>&1 | grep env; done
+timeout 300 python tools/narrow_ab.py 16 128 602 2>&1 | grep env
+for d in 12 16; do SG_LIB_PATH=$PWD/paper_1810_08403_b200/libsagann_d$d.so timeout 300 python tools/narrow_ab.py 16 128 2>&1 | grep env; done
