@@ -25,7 +25,7 @@ __all__ = [
     "LayerProgram", "PassReport", "build_commnet", "build_gcn", "build_ggcn", "build_mpgcn", "evaluate_expr",
     "fuse_sag", "hoist_vertex_computation", "make_program", "matmul_rows", "optimize", "trace_udf",
     "validate_program", "vertex_form", "SAGAModel", "gcn_model", "ggcn_model", "mpgcn_model", "commnet_model", "run_train",
-    "StreamingGCN", "HostGrid", "GGNNModel", "ggnn_model", "build_ggnn",
+    "StreamingGCN", "StreamingGGCN", "HostGrid", "GGNNModel", "ggnn_model", "build_ggnn",
 ]
 
 
@@ -40,7 +40,7 @@ def __getattr__(name):
         from . import ggnn
 
         return getattr(ggnn, name)
-    if name in ("StreamingGCN", "HostGrid"):
+    if name in ("StreamingGCN", "StreamingGGCN", "HostGrid"):
         from . import stream
 
         return getattr(stream, name)

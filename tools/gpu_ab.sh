@@ -1,2 +1,3 @@
-timeout 300 python tools/narrow_ab.py 16 128 602 2>&1 | grep env
-for d in 12 16; do SG_LIB_PATH=$PWD/paper_1810_08403_b200/libsagann_d$d.so timeout 300 python tools/narrow_ab.py 16 128 2>&1 | grep env; done
+for p in 1 4; do timeout 900 python tools/stream_bench.py --parts $p --model gcn 2>&1 | tail -1; done
+for p in 1 4; do timeout 900 python tools/stream_bench.py --parts $p --model ggcn 2>&1 | tail -1; done
+timeout 900 python bench.py --config reddit --steps 3 --warmup 2 --no-cpu-baseline --no-e2e --no-reorder 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('resident gcn', d['ms_per_step'])"

@@ -1,6 +1,7 @@
-"""Out-of-core GCN epoch on the Reddit-shaped graph (host-resident features/activations/index).
+"""Out-of-core GCN / G-GCN epoch on the Reddit-shaped graph (host-resident features,
+activations and chunk index).
 
-    python tools/stream_bench.py [--parts 4] [--steps 3]
+    python tools/stream_bench.py [--parts 4] [--steps 3] [--model gcn|ggcn]
 
 Prints one JSON line: epoch ms (device events), H2D / D2H GB per epoch, device working set.
 """
@@ -22,12 +23,13 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--parts", type=int, default=4)
     ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--model", choices=["gcn", "ggcn"], default="gcn")
     a = ap.parse_args()
     V, E, dims = 232965, 114615892, [602, 128, 41]
     t0 = time.time()
     g = sg.rmat_graph(V, E, seed=0)
-    grid = sg.HostGrid(g, -(-V // a.parts))
-    m = sg.StreamingGCN(grid, dims)
+    grid = sg.HostGrid(g, -(-V // a.parts), gcn_weights=a.model == "gcn")
+    m = (sg.StreamingGCN if a.model == "gcn" else sg.StreamingGGCN)(grid, dims)
     m.load_features(torch.from_numpy(sg.synthetic_features(V, dims[0], seed=1)))
     m.load_labels(np.random.default_rng(3).integers(0, dims[-1], V))
     setup = time.time() - t0
@@ -42,7 +44,8 @@ def main():
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1))
     ms = sorted(ts)[len(ts) // 2]
-    print(json.dumps({"workload": "out-of-core 2-layer GCN epoch, Reddit-shaped", "parts": a.parts,
+    print(json.dumps({"workload": f"out-of-core 2-layer {a.model.upper()} epoch, Reddit-shaped",
+                      "parts": a.parts,
                       "epoch_ms": round(ms, 2), "edges_per_s": E / (ms / 1e3),
                       "h2d_gb": round(m.h2d_bytes / 1e9, 3), "d2h_gb": round(m.d2h_bytes / 1e9, 3),
                       "h2d_gbs": round(m.h2d_bytes / 1e6 / ms, 1),
