@@ -775,6 +775,33 @@ def test_streaming_ggcn_matches_resident(sg, P, T):
     assert st.h2d_bytes > 0 and st.d2h_bytes > 0
 
 
+def test_streaming_empty_columns_and_rows(sg):
+    """Chunk columns / rows without edges (destinations and sources with no edges at all):
+    both streaming executors still match the resident ones."""
+    V, P = 3000, 3
+    r = np.random.default_rng(5)
+    s = r.integers(0, 1000, 20000).astype(np.int32)        # sources only in interval 0
+    d = r.integers(0, 2000, 20000).astype(np.int32)        # destinations in intervals 0-1
+    g = sg.Graph(V, s, d)
+    X = rng.features(V, 24, seed=1)
+    lab = rng.labels(V, 4)
+    for model, Res, St in (("gcn", sg.gcn_model, sg.StreamingGCN), ("ggcn", sg.ggcn_model, sg.StreamingGGCN)):
+        res = Res(sg.ChunkGrid(g, 1000, gcn_weights=model == "gcn"), [24, 8, 4])
+        res.load_features(torch.from_numpy(X))
+        res.load_labels(lab)
+        st = St(sg.HostGrid(g, 1000, gcn_weights=model == "gcn"), [24, 8, 4], weights=res.weights())
+        st.load_features(torch.from_numpy(X))
+        st.load_labels(lab)
+        res.forward()
+        res.backward()
+        st.forward()
+        st.backward()
+        st.check_status()
+        assert abs(st.loss.item() - res.loss.item()) <= 1e-5 * res.loss.item(), model
+        for k, (a, b) in enumerate(zip(st.grads(), res.grads())):
+            assert_close(a, b, 1e-4, f"{model} grad {k}")
+
+
 def test_streaming_budget_error(sg):
     s, d = _graph("rmat", 2000, 20000, 3)
     g = sg.Graph(2000, s, d)
