@@ -88,7 +88,9 @@ int sg_host_reencode_balance(const int32_t* src, const int32_t* dst, int64_t E, 
                              int64_t num_intervals, int64_t* perm);
 /* partition_2d.  sg_host_partition_layout gives P and the length
  * of each pointer array (= P * (V + P)); sg_host_partition_2d fills the layout of
- * oracle/graph.py:Partition (chunk id c = i * P + j). */
+ * oracle/graph.py:Partition (chunk id c = i * P + j).  Canonical CSC: a destination's edges
+ * by local source, multi-edges in input order ("CSC sorted by local dest id");
+ * CSR stable over the CSC order. */
 int sg_host_partition_layout(int64_t V, int64_t interval_size, int64_t* P, int64_t* ptr_len);
 int sg_host_partition_2d(const int32_t* src, const int32_t* dst, int64_t E, int64_t V,
                          int64_t interval_size, int64_t* edge_off, int64_t* cptr_off,
@@ -122,7 +124,7 @@ int sg_host_read_matrix_bin(const char* path, int64_t rows, int64_t cols, double
 int sg_host_write_matrix_bin(const char* path, int64_t rows, int64_t cols, const double* data);
 int sg_host_scan_labels(const char* path, int64_t* n);
 int sg_host_read_labels(const char* path, int64_t n, int64_t* out);
-/* Order-sensitive 64-bit content hash (keys the on-disk partition cache). */
+/* Order-sensitive 64-bit content hash (keys the on-disk partition cache, SPEC.md:160). */
 uint64_t sg_host_hash64(const void* data, int64_t nbytes, uint64_t seed);
 
 /* ---------------------------------------------------------------- device: propagation
@@ -133,7 +135,7 @@ uint64_t sg_host_hash64(const void* data, int64_t nbytes, uint64_t seed);
  * :204-303) and SPEC stage ops fused_gather_chunk / backward_* (SPEC.md:419-436).
  *   G, ldg, g_off : gathered rows (second operand segment at column g_off)
  *   R, ldr, r_off : row-side rows (may be NULL for PASS / GCN)
- *   out0/out1     : outputs (out1 only for GGCN_BWD_SRC)
+ *   out0/out1     : outputs (out1 for GGCN_BWD_SRC: dH_take; for GGCN_FWD_S: S)
  *   mask, ldm     : optional ReLU-backward mask: out0 = acc * (mask > 0) (tensor.py:236)
  *   workspace     : >= sg_propagate_workspace_bytes(...) bytes of device memory
  */
