@@ -192,6 +192,23 @@ int sg_max_gather_bwd(const int64_t* ptr, const int32_t* idx, const int32_t* pos
                       const float* G, int64_t ldg, const int32_t* argpos, int64_t lda, float* out,
                       int64_t ldo, int64_t F, const float* mask, int64_t ldm, int64_t pos_base,
                       int accumulate, void* stream);
+/* Plan-driven variants of sg_max_gather / sg_max_gather_bwd for passes with split rows
+ * (R-MAT hubs): the pass's work plan (sg_host_plan) is pulled from an atomic queue and a
+ * heavy row's subgroups run in parallel.  The forward result is bit-identical to the
+ * sequential one (max / argmax are exact; partials are combined lowest position first); the
+ * backward sums a split row's subgroups in subgroup order (as sg_propagate).
+ * workspace >= sg_max_plan_workspace_bytes(n_splits, n_slots, F). */
+int64_t sg_max_plan_workspace_bytes(int64_t n_splits, int64_t n_slots, int64_t F);
+int sg_max_gather_plan(const int64_t* ptr, const int32_t* idx, const sg_item* items, int64_t n_items,
+                       const sg_split* splits, int64_t n_splits, int64_t n_slots, const float* Y, int64_t ldy,
+                       float* out, int64_t ldo, int32_t* argpos, int64_t lda, int64_t F, float empty_fill,
+                       int64_t pos_base, int accumulate, int finalize, void* workspace,
+                       int64_t workspace_bytes, void* stream);
+int sg_max_gather_bwd_plan(const int64_t* ptr, const int32_t* idx, const int32_t* pos, const sg_item* items,
+                           int64_t n_items, const sg_split* splits, int64_t n_splits, int64_t n_slots,
+                           const float* G, int64_t ldg, const int32_t* argpos, int64_t lda, float* out,
+                           int64_t ldo, int64_t F, const float* mask, int64_t ldm, int64_t pos_base,
+                           int accumulate, void* workspace, int64_t workspace_bytes, void* stream);
 /* Scatter (take_rows, tensor.py:424-436): out[k] = X[idx[k]] (int64 idx, bounds
  * checked on device: *err_flag set to 1 if any index is out of [0, n_src)). */
 int sg_take_rows(int dtype, const void* X, int64_t ldx, int64_t n_src, const int64_t* idx,

@@ -15,6 +15,13 @@
 namespace {
 using sg::VecIO;
 
+// source rows in flight per lane in the fused max gather and its backward: hub rows (R-MAT:
+// ~800K edges) are walked by one team, so the kernel time is that row's load-latency chain
+#ifndef SG_MAX_DEPTH
+#define SG_MAX_DEPTH 8
+#endif
+constexpr int kMaxDepth = SG_MAX_DEPTH;
+
 template <int DT, int W>
 __global__ void take_rows_kernel(const void* X, int64_t ldx, int64_t n_src, const int64_t* idx,
                                  int64_t n, void* out, int64_t ldo, int F, int32_t* err) {
@@ -207,10 +214,10 @@ __global__ void __launch_bounds__(256) maxgather_kernel(
         }
       }
       int64_t e = e0;
-      for (; e + 4 <= e1; e += 4) {
-        float v[4][W];
+      for (; e + kMaxDepth <= e1; e += kMaxDepth) {
+        float v[kMaxDepth][W];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < kMaxDepth; ++u) {
           const float* row = Y + (int64_t)__ldg(idx + e + u) * ldy + c0;
           if (W == 4) {
             const float4 q = __ldg(reinterpret_cast<const float4*>(row));
@@ -220,7 +227,7 @@ __global__ void __launch_bounds__(256) maxgather_kernel(
           }
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
+        for (int u = 0; u < kMaxDepth; ++u)
 #pragma unroll
           for (int k = 0; k < W; ++k)
             if (v[u][k] > best[k]) {  // strict '>' : the lowest position wins (tensor.py:467)
@@ -280,11 +287,11 @@ __global__ void __launch_bounds__(256) maxgather_bwd_kernel(
 #pragma unroll
       for (int k = 0; k < W; ++k) acc[k] = (accumulate && c0 + k < F) ? out[r * ldo + c0 + k] : 0.f;
       int64_t e = e0;
-      for (; e + 2 <= e1; e += 2) {  // 2 edges' rows in flight (each is a G and an arg read)
-        float g[2][W];
-        int32_t a[2][W], p[2];
+      for (; e + kMaxDepth <= e1; e += kMaxDepth) {  // kMaxDepth edges' rows in flight (G + arg)
+        float g[kMaxDepth][W];
+        int32_t a[kMaxDepth][W], p[kMaxDepth];
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < kMaxDepth; ++u) {
           const int64_t d = __ldg(idx + e + u);
           p[u] = (int32_t)(pos_base + __ldg(pos + e + u));
           if (W == 4) {
@@ -298,7 +305,7 @@ __global__ void __launch_bounds__(256) maxgather_bwd_kernel(
           }
         }
 #pragma unroll
-        for (int u = 0; u < 2; ++u)
+        for (int u = 0; u < kMaxDepth; ++u)
 #pragma unroll
           for (int k = 0; k < W; ++k) acc[k] = __fadd_rn(acc[k], a[u][k] == p[u] ? g[u][k] : 0.f);
       }
@@ -318,6 +325,249 @@ __global__ void __launch_bounds__(256) maxgather_bwd_kernel(
           if (mask) v = __fmul_rn(v, __ldg(mask + r * ldm + c0 + k) > 0.f ? 1.f : 0.f);
           out[r * ldo + c0 + k] = v;
         }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- plan-driven max gather
+// Hub-heavy passes (R-MAT: rows of ~10^5-10^6 edges) cannot be left to one team per row: the
+// kernel would last as long as the heaviest row.  These variants consume the pass's work plan
+// (sg_item / sg_split, as sg_propagate): warps pull items from an atomic queue; a split item
+// is one subgroup of <= T edges of a heavy row whose partial lands in the workspace, and the
+// last subgroup to finish combines the partials in subgroup order.
+//  * forward: max and argmax are exact, so the split result equals the sequential one bit for
+//    bit (partials are combined lowest position first with strict '>');
+//  * backward: a sum, so a split row follows the subgroup rule of every propagation pass
+//    (oracle/saga.py:seq_sum_rows).
+struct MaxPlan {
+  const int64_t* ptr;
+  const int32_t* idx;
+  const int32_t* pos;    // bwd: CSC position per CSR edge
+  const sg_item* items;
+  const sg_split* splits;
+  int32_t n_items;
+  int32_t* queue;
+  int32_t* counters;
+  float* pval;           // [n_slots][pld]
+  int32_t* parg;         // [n_slots][pld] (fwd)
+  int64_t pld;
+  const float* Y;        // fwd: gathered rows; bwd: dA rows
+  int64_t ldy;
+  float* out;
+  int64_t ldo;
+  int32_t* arg;          // fwd: out argmax; bwd: argmax of the destinations
+  int64_t lda;
+  const float* mask;
+  int64_t ldm;
+  int F;
+  float fill;
+  int64_t base;
+  int accumulate, finalize;
+};
+
+template <int W>
+__device__ __forceinline__ void ld_vec(const float* p, float (&v)[W]) {
+  if constexpr (W == 4) {
+    const float4 q = __ldg(reinterpret_cast<const float4*>(p));
+    v[0] = q.x; v[1 % W] = q.y; v[2 % W] = q.z; v[3 % W] = q.w;
+  } else {
+    v[0] = __ldg(p);
+  }
+}
+
+template <int W>
+__device__ __forceinline__ void ld_ivec(const int32_t* p, int32_t (&v)[W]) {
+  if constexpr (W == 4) {
+    const int4 q = __ldg(reinterpret_cast<const int4*>(p));
+    v[0] = q.x; v[1 % W] = q.y; v[2 % W] = q.z; v[3 % W] = q.w;
+  } else {
+    v[0] = __ldg(p);
+  }
+}
+
+template <int W>
+__global__ void __launch_bounds__(256) maxgather_plan_kernel(const MaxPlan a) {
+  const int lane = threadIdx.x & 31;
+  const int Fv = (a.F + W - 1) / W;
+  for (;;) {
+    int it = 0;
+    if (lane == 0) it = atomicAdd(a.queue, 1);
+    it = __shfl_sync(0xffffffffu, it, 0);
+    if (it >= a.n_items) break;
+    const sg_item item = a.items[it];
+    const bool split = item.split >= 0;
+    for (int r = item.row_begin; r < item.row_end; ++r) {
+      const int64_t e0 = split ? item.e_begin : __ldg(a.ptr + r);
+      const int64_t e1 = split ? item.e_end : __ldg(a.ptr + r + 1);
+      for (int cv = lane; cv < Fv; cv += 32) {
+        const int c0 = cv * W;
+        float best[W];
+        int32_t barg[W];
+#pragma unroll
+        for (int k = 0; k < W; ++k) {
+          best[k] = -INFINITY;
+          barg[k] = -1;
+          if (!split && a.accumulate && c0 + k < a.F) {
+            barg[k] = a.arg[r * a.lda + c0 + k];
+            if (barg[k] >= 0) best[k] = a.out[r * a.ldo + c0 + k];
+          }
+        }
+        int64_t e = e0;
+        for (; e + kMaxDepth <= e1; e += kMaxDepth) {
+          float v[kMaxDepth][W];
+#pragma unroll
+          for (int u = 0; u < kMaxDepth; ++u) ld_vec<W>(a.Y + (int64_t)__ldg(a.idx + e + u) * a.ldy + c0, v[u]);
+#pragma unroll
+          for (int u = 0; u < kMaxDepth; ++u)
+#pragma unroll
+            for (int k = 0; k < W; ++k)
+              if (v[u][k] > best[k]) {
+                best[k] = v[u][k];
+                barg[k] = (int32_t)(a.base + e + u);
+              }
+        }
+        for (; e < e1; ++e) {
+          float v[W];
+          ld_vec<W>(a.Y + (int64_t)__ldg(a.idx + e) * a.ldy + c0, v);
+#pragma unroll
+          for (int k = 0; k < W; ++k)
+            if (v[k] > best[k]) {
+              best[k] = v[k];
+              barg[k] = (int32_t)(a.base + e);
+            }
+        }
+        if (!split) {
+#pragma unroll
+          for (int k = 0; k < W; ++k)
+            if (c0 + k < a.F) {
+              a.out[r * a.ldo + c0 + k] = (a.finalize && barg[k] < 0) ? a.fill : best[k];
+              a.arg[r * a.lda + c0 + k] = barg[k];
+            }
+        } else {
+          const int64_t slot = a.splits[item.split].slot0 + item.sub;
+#pragma unroll
+          for (int k = 0; k < W; ++k)
+            if (c0 + k < a.F) {
+              __stcg(a.pval + slot * a.pld + c0 + k, best[k]);
+              __stcg(a.parg + slot * a.pld + c0 + k, barg[k]);
+            }
+        }
+      }
+    }
+    if (split) {
+      const sg_split sp = a.splits[item.split];
+      __threadfence();
+      __syncwarp();
+      int ticket = 0;
+      if (lane == 0) ticket = atomicAdd(a.counters + item.split, 1);
+      ticket = __shfl_sync(0xffffffffu, ticket, 0);
+      if (ticket == sp.n_sub - 1) {
+        __threadfence();
+        const int64_t r = sp.row;
+        for (int c = lane; c < a.F; c += 32) {
+          float best = -INFINITY;
+          int32_t barg = -1;
+          if (a.accumulate) {
+            barg = a.arg[r * a.lda + c];
+            if (barg >= 0) best = a.out[r * a.ldo + c];
+          }
+          for (int q = 0; q < sp.n_sub; ++q) {  // ascending positions: strict '>' keeps the first
+            const float v = __ldcg(a.pval + (sp.slot0 + q) * a.pld + c);
+            const int32_t g = __ldcg(a.parg + (sp.slot0 + q) * a.pld + c);
+            if (g >= 0 && v > best) {
+              best = v;
+              barg = g;
+            }
+          }
+          a.out[r * a.ldo + c] = (a.finalize && barg < 0) ? a.fill : best;
+          a.arg[r * a.lda + c] = barg;
+        }
+        if (lane == 0) a.counters[item.split] = 0;
+      }
+    }
+  }
+}
+
+template <int W>
+__global__ void __launch_bounds__(256) maxgather_bwd_plan_kernel(const MaxPlan a) {
+  const int lane = threadIdx.x & 31;
+  const int Fv = (a.F + W - 1) / W;
+  for (;;) {
+    int it = 0;
+    if (lane == 0) it = atomicAdd(a.queue, 1);
+    it = __shfl_sync(0xffffffffu, it, 0);
+    if (it >= a.n_items) break;
+    const sg_item item = a.items[it];
+    const bool split = item.split >= 0;
+    for (int r = item.row_begin; r < item.row_end; ++r) {
+      const int64_t e0 = split ? item.e_begin : __ldg(a.ptr + r);
+      const int64_t e1 = split ? item.e_end : __ldg(a.ptr + r + 1);
+      for (int cv = lane; cv < Fv; cv += 32) {
+        const int c0 = cv * W;
+        float acc[W];
+#pragma unroll
+        for (int k = 0; k < W; ++k)
+          acc[k] = (!split && a.accumulate && c0 + k < a.F) ? a.out[r * a.ldo + c0 + k] : 0.f;
+        int64_t e = e0;
+        for (; e + kMaxDepth <= e1; e += kMaxDepth) {
+          float g[kMaxDepth][W];
+          int32_t t[kMaxDepth][W], p[kMaxDepth];
+#pragma unroll
+          for (int u = 0; u < kMaxDepth; ++u) {
+            const int64_t d = __ldg(a.idx + e + u);
+            p[u] = (int32_t)(a.base + __ldg(a.pos + e + u));
+            ld_vec<W>(a.Y + d * a.ldy + c0, g[u]);
+            ld_ivec<W>(a.arg + d * a.lda + c0, t[u]);
+          }
+#pragma unroll
+          for (int u = 0; u < kMaxDepth; ++u)
+#pragma unroll
+            for (int k = 0; k < W; ++k) acc[k] = __fadd_rn(acc[k], t[u][k] == p[u] ? g[u][k] : 0.f);
+        }
+        for (; e < e1; ++e) {
+          const int64_t d = __ldg(a.idx + e);
+          const int32_t pp = (int32_t)(a.base + __ldg(a.pos + e));
+          float g[W];
+          int32_t t[W];
+          ld_vec<W>(a.Y + d * a.ldy + c0, g);
+          ld_ivec<W>(a.arg + d * a.lda + c0, t);
+#pragma unroll
+          for (int k = 0; k < W; ++k) acc[k] = __fadd_rn(acc[k], t[k] == pp ? g[k] : 0.f);
+        }
+        if (!split) {
+#pragma unroll
+          for (int k = 0; k < W; ++k)
+            if (c0 + k < a.F) {
+              float v = acc[k];
+              if (a.mask) v = __fmul_rn(v, __ldg(a.mask + r * a.ldm + c0 + k) > 0.f ? 1.f : 0.f);
+              a.out[r * a.ldo + c0 + k] = v;
+            }
+        } else {
+          const int64_t slot = a.splits[item.split].slot0 + item.sub;
+#pragma unroll
+          for (int k = 0; k < W; ++k)
+            if (c0 + k < a.F) __stcg(a.pval + slot * a.pld + c0 + k, acc[k]);
+        }
+      }
+    }
+    if (split) {
+      const sg_split sp = a.splits[item.split];
+      __threadfence();
+      __syncwarp();
+      int ticket = 0;
+      if (lane == 0) ticket = atomicAdd(a.counters + item.split, 1);
+      ticket = __shfl_sync(0xffffffffu, ticket, 0);
+      if (ticket == sp.n_sub - 1) {
+        __threadfence();
+        const int64_t r = sp.row;
+        for (int c = lane; c < a.F; c += 32) {
+          float v = a.accumulate ? a.out[r * a.ldo + c] : 0.f;
+          for (int q = 0; q < sp.n_sub; ++q) v = __fadd_rn(v, __ldcg(a.pval + (sp.slot0 + q) * a.pld + c));
+          if (a.mask) v = __fmul_rn(v, __ldg(a.mask + r * a.ldm + c) > 0.f ? 1.f : 0.f);
+          a.out[r * a.ldo + c] = v;
+        }
+        if (lane == 0) a.counters[item.split] = 0;
       }
     }
   }
@@ -401,6 +651,75 @@ int sg_max_gather_bwd(const int64_t* ptr, const int32_t* idx, const int32_t* pos
   if (e != cudaSuccess) SG_FAIL(SG_ECUDA, "max_gather_bwd launch: %s", cudaGetErrorString(e));
   sg::count_launch(1);
   return SG_OK;
+}
+
+int64_t sg_max_plan_workspace_bytes(int64_t n_splits, int64_t n_slots, int64_t F) {
+  const int64_t pld = (F + 3) / 4 * 4;
+  return 256 + (4 * std::max<int64_t>(n_splits, 1) + 255) / 256 * 256 + n_slots * pld * 8;
+}
+
+static int max_plan_launch(bool bwd, const int64_t* ptr, const int32_t* idx, const int32_t* pos,
+                           const sg_item* items, int64_t n_items, const sg_split* splits, int64_t n_splits,
+                           int64_t n_slots, const float* Y, int64_t ldy, float* out, int64_t ldo, int32_t* arg,
+                           int64_t lda, const float* mask, int64_t ldm, int64_t F, float fill, int64_t base,
+                           int accumulate, int finalize, void* ws, int64_t ws_bytes, void* stream) {
+  if (n_items == 0 || F == 0) return SG_OK;
+  SG_REQUIRE(ptr && idx && items && Y && out && arg && (!bwd || pos), SG_EINVAL, "max plan: null pointer");
+  SG_REQUIRE(n_splits == 0 || splits, SG_EINVAL, "max plan: split records missing");
+  SG_REQUIRE(ws && ws_bytes >= sg_max_plan_workspace_bytes(n_splits, n_slots, F), SG_EBUDGET,
+             "max plan workspace too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  char* w = static_cast<char*>(ws);
+  const int64_t cbytes = (4 * std::max<int64_t>(n_splits, 1) + 255) / 256 * 256;
+  const int64_t pld = (F + 3) / 4 * 4;
+  MaxPlan a;
+  a.ptr = ptr; a.idx = idx; a.pos = pos; a.items = items; a.splits = splits;
+  a.n_items = (int32_t)n_items;
+  a.queue = reinterpret_cast<int32_t*>(w);
+  a.counters = reinterpret_cast<int32_t*>(w + 256);
+  a.pval = reinterpret_cast<float*>(w + 256 + cbytes);
+  a.parg = reinterpret_cast<int32_t*>(w + 256 + cbytes + n_slots * pld * 4);
+  a.pld = pld;
+  a.Y = Y; a.ldy = ldy; a.out = out; a.ldo = ldo; a.arg = arg; a.lda = lda; a.mask = mask; a.ldm = ldm;
+  a.F = (int)F; a.fill = fill; a.base = base; a.accumulate = accumulate; a.finalize = finalize;
+  cudaError_t e = cudaMemsetAsync(w, 0, 256 + cbytes, st);
+  if (e != cudaSuccess) SG_FAIL(SG_ECUDA, "memset: %s", cudaGetErrorString(e));
+  const bool vec = (F % 4 == 0) && (ldy % 4 == 0) && (lda % 4 == 0) && aligned(Y, 16) && aligned(arg, 16);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n_items + 7) / 8, (int64_t)sms * 8));
+  if (bwd) {
+    if (vec) maxgather_bwd_plan_kernel<4><<<grid, 256, 0, st>>>(a);
+    else maxgather_bwd_plan_kernel<1><<<grid, 256, 0, st>>>(a);
+  } else {
+    if (vec) maxgather_plan_kernel<4><<<grid, 256, 0, st>>>(a);
+    else maxgather_plan_kernel<1><<<grid, 256, 0, st>>>(a);
+  }
+  e = cudaGetLastError();
+  if (e != cudaSuccess) SG_FAIL(SG_ECUDA, "max plan launch: %s", cudaGetErrorString(e));
+  sg::count_launch(1);
+  return SG_OK;
+}
+
+int sg_max_gather_plan(const int64_t* ptr, const int32_t* idx, const sg_item* items, int64_t n_items,
+                       const sg_split* splits, int64_t n_splits, int64_t n_slots, const float* Y, int64_t ldy,
+                       float* out, int64_t ldo, int32_t* argpos, int64_t lda, int64_t F, float empty_fill,
+                       int64_t pos_base, int accumulate, int finalize, void* workspace,
+                       int64_t workspace_bytes, void* stream) {
+  return max_plan_launch(false, ptr, idx, nullptr, items, n_items, splits, n_splits, n_slots, Y, ldy, out, ldo,
+                         argpos, lda, nullptr, 0, F, empty_fill, pos_base, accumulate, finalize, workspace,
+                         workspace_bytes, stream);
+}
+
+int sg_max_gather_bwd_plan(const int64_t* ptr, const int32_t* idx, const int32_t* pos, const sg_item* items,
+                           int64_t n_items, const sg_split* splits, int64_t n_splits, int64_t n_slots,
+                           const float* G, int64_t ldg, const int32_t* argpos, int64_t lda, float* out,
+                           int64_t ldo, int64_t F, const float* mask, int64_t ldm, int64_t pos_base,
+                           int accumulate, void* workspace, int64_t workspace_bytes, void* stream) {
+  return max_plan_launch(true, ptr, idx, pos, items, n_items, splits, n_splits, n_slots, G, ldg, out, ldo,
+                         const_cast<int32_t*>(argpos), lda, mask, ldm, F, 0.f, pos_base, accumulate, 0,
+                         workspace, workspace_bytes, stream);
 }
 
 int sg_take_rows(int dtype, const void* X, int64_t ldx, int64_t n_src, const int64_t* idx,

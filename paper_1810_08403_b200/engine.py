@@ -404,7 +404,7 @@ class SAGAModel:
         for (i, j), first, last in self._chunk_order(list(g.csc), 1):
             K.max_gather(g.csc[(i, j)], self._rows(Y, i), self._rows(L.a, j), self._rows(L.arg, j),
                          L.Aw, pos_base=g.edge_base[(i, j)], accumulate=not first, finalize=last,
-                         stream=stream)
+                         stream=stream, ws=self.ws)
 
     def _bwd_max(self, L, out, mask, stream=None):
         """dY[v] = sum over out-edges (destination intervals ascending, CSR order) of dA[dst]
@@ -417,7 +417,8 @@ class SAGAModel:
             K.max_gather_bwd(g.csr[(i, j)], g.csr_positions(i, j), self._rows(L.da, j),
                              self._rows(L.arg, j), self._rows(out, i), L.Aw,
                              mask=self._rows(mask, i) if (last and mask is not None) else None,
-                             pos_base=g.edge_base[(i, j)], accumulate=not first, stream=stream)
+                             pos_base=g.edge_base[(i, j)], accumulate=not first, stream=stream,
+                             ws=self.ws)
 
     def _gemm(self, A, B, C, **kw):
         K.gemm(A, B, C, prec=self.gemm_prec, ws=self.ws, **kw)

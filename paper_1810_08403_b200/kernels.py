@@ -115,16 +115,40 @@ def softmax_xent(Z, labels, loss, dZ, err, *, relu_input=True, n_total=0, ws=Non
                               stream_handle(stream)))
 
 
+def _max_ws(pi, F, ws, device):
+    nb = int(lib.sg_max_plan_workspace_bytes(pi.n_splits, pi.n_slots, F))
+    return ws.get(nb) if ws is not None else torch.empty(max(nb, 256), dtype=torch.uint8, device=device)
+
+
 def max_gather(pi, Y, out, arg, F, empty_fill=0.0, *, pos_base=0, accumulate=False, finalize=True,
-               stream=None):
-    """Fused Gather(max) over CSC pass index ``pi`` (argmax = pos_base + CSC position, int32)."""
+               stream=None, ws=None):
+    """Fused Gather(max) over CSC pass index ``pi`` (argmax = pos_base + CSC position, int32).
+    Passes with split rows (hubs) run the plan-driven kernel (bit-identical result)."""
+    if getattr(pi, "n_splits", 0) > 0:
+        buf = _max_ws(pi, F, ws, Y.device)
+        check(lib.sg_max_gather_plan(tptr(pi.ptr), tptr(pi.idx), tptr(pi.items), pi.n_items,
+                                     tptr(pi.splits), pi.n_splits, pi.n_slots, tptr(Y), ld(Y), tptr(out),
+                                     ld(out), tptr(arg), ld(arg), F, float(empty_fill), int(pos_base),
+                                     int(bool(accumulate)), int(bool(finalize)), tptr(buf), buf.numel(),
+                                     stream_handle(stream)))
+        return
     check(lib.sg_max_gather(tptr(pi.ptr), tptr(pi.idx), pi.n_rows, tptr(Y), ld(Y), tptr(out), ld(out),
                             tptr(arg), ld(arg), F, float(empty_fill), int(pos_base),
                             int(bool(accumulate)), int(bool(finalize)), stream_handle(stream)))
 
 
-def max_gather_bwd(pi, pos, G, arg, out, F, mask=None, *, pos_base=0, accumulate=False, stream=None):
-    """Backward of max_gather over CSR pass index ``pi`` (pos = CSC position per CSR edge)."""
+def max_gather_bwd(pi, pos, G, arg, out, F, mask=None, *, pos_base=0, accumulate=False, stream=None,
+                   ws=None):
+    """Backward of max_gather over CSR pass index ``pi`` (pos = CSC position per CSR edge).
+    Passes with split rows sum a heavy row's subgroups in subgroup order."""
+    if getattr(pi, "n_splits", 0) > 0:
+        buf = _max_ws(pi, F, ws, G.device)
+        check(lib.sg_max_gather_bwd_plan(tptr(pi.ptr), tptr(pi.idx), tptr(pos), tptr(pi.items), pi.n_items,
+                                         tptr(pi.splits), pi.n_splits, pi.n_slots, tptr(G), ld(G), tptr(arg),
+                                         ld(arg), tptr(out), ld(out), F, tptr(mask),
+                                         ld(mask) if mask is not None else 0, int(pos_base),
+                                         int(bool(accumulate)), tptr(buf), buf.numel(), stream_handle(stream)))
+        return
     check(lib.sg_max_gather_bwd(tptr(pi.ptr), tptr(pi.idx), tptr(pos), pi.n_rows, tptr(G), ld(G),
                                 tptr(arg), ld(arg), tptr(out), ld(out), F, tptr(mask),
                                 ld(mask) if mask is not None else 0, int(pos_base),

@@ -512,6 +512,29 @@ def _gpu_max_chunked(sg, grid, Y, G, M, F):
     return out, arg, dH, dHm
 
 
+def _max_bwd_ref(part, G, arg, T):
+    """Backward of the max gather in the executor's order: per source interval, destination
+    intervals ascending, each CSR row's routed gradients (G[dst] where the destination's argmax
+    is this edge's global position, else +0.0 -- tensor.py:473-482 then take_rows' backward)
+    summed with the subgroup rule of seq_sum_rows (rows > T edges)."""
+    V, F = G.shape
+    out = np.zeros((V, F), G.dtype)
+    for i in range(part.P):
+        acc = np.zeros((int(part.sizes[i]), F), G.dtype)
+        for j in range(part.P):
+            ch = part.chunk(i, j)
+            if ch["nnz"] == 0:
+                continue
+            csc_pos = {e: k for k, e in enumerate(ch["csc_eid"].tolist())}  # edge id -> CSC position
+            pos = int(part.edge_off[i * part.P + j]) + np.array([csc_pos[e] for e in ch["csr_eid"].tolist()],
+                                                               np.int64)
+            dst = part.begin(j) + ch["csr_idx"].astype(np.int64)
+            t = np.where(arg[dst] == pos[:, None], G[dst], np.float32(0.0)).astype(G.dtype)
+            acc = saga.seq_sum_rows(ch["csr_ptr"], t, acc, T)
+        out[part.begin(i): part.begin(i) + int(part.sizes[i])] = acc
+    return out
+
+
 @pytest.mark.parametrize("kind,V,E,F,P", [("rmat", 3000, 60000, 64, 1), ("rmat", 800, 20000, 7, 1),
                                           ("uniform", 2000, 30000, 602, 1), ("uniform", 60, 30, 9, 1),
                                           ("uniform", 50, 0, 16, 1), ("rmat", 3000, 60000, 64, 3),
@@ -532,7 +555,10 @@ def test_max_gather_fwd_bwd_bitwise(sg, kind, V, E, F, P):
     ref, ref_arg = prim.segment_max(prim.take_rows(Y, src), dst, V)
     assert np.array_equal(out.cpu().numpy(), ref)
     assert np.array_equal(arg.cpu().numpy().astype(np.int64), ref_arg)
-    ref_dh = prim.take_rows_bwd(prim.segment_max_bwd(G, ref_arg, len(src)), src, V)
+    ref_dh = _max_bwd_ref(og.partition_2d(s, d, V, size), G, ref_arg, grid.split_edges)
+    if int(np.diff(grid.part.csr_ptr).max(initial=0)) <= grid.split_edges:
+        # no split rows: the chunk chains are exactly take_rows' sequential backward
+        assert np.array_equal(ref_dh, prim.take_rows_bwd(prim.segment_max_bwd(G, ref_arg, len(src)), src, V))
     assert np.array_equal(dH.cpu().numpy(), ref_dh)
     assert np.array_equal(dHm.cpu().numpy(), prim.relu_bwd(ref_dh, M))
 
