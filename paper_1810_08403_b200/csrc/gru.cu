@@ -20,9 +20,9 @@
 
 namespace {
 
-int grid_for(int64_t work) {
-  int64_t g = (work + 255) / 256;
-  return (int)std::max<int64_t>(1, std::min<int64_t>(g, 148 * 16));
+// one 32 x 8 block per 8 rows (lanes over columns: coalesced, no index division), grid-stride
+int grid_rows(int64_t V) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>((V + 7) / 8, 148 * 16));
 }
 
 __device__ __forceinline__ float sigmoid_ref(float x) {
@@ -32,60 +32,56 @@ __device__ __forceinline__ float sigmoid_ref(float x) {
 __global__ void gru_gates_kernel(int64_t V, int64_t F, const float* G1, int64_t ld1,
                                  const float* G2, int64_t ld2, int64_t bs, const float* h,
                                  int64_t ldh, float* z, float* r, float* rh, int64_t ldo) {
-  const int64_t n = V * F;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t v = i / F, c = i - v * F;
-    const float zv = sigmoid_ref(__fadd_rn(G1[v * ld1 + c], G2[v * ld2 + c]));
-    const float rv = sigmoid_ref(__fadd_rn(G1[v * ld1 + bs + c], G2[v * ld2 + bs + c]));
-    z[v * ldo + c] = zv;
-    r[v * ldo + c] = rv;
-    rh[v * ldo + c] = __fmul_rn(rv, h[v * ldh + c]);
-  }
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.y + threadIdx.y; v < V;
+       v += (int64_t)gridDim.x * blockDim.y)
+    for (int64_t c = threadIdx.x; c < F; c += 32) {
+      const float zv = sigmoid_ref(__fadd_rn(G1[v * ld1 + c], G2[v * ld2 + c]));
+      const float rv = sigmoid_ref(__fadd_rn(G1[v * ld1 + bs + c], G2[v * ld2 + bs + c]));
+      z[v * ldo + c] = zv;
+      r[v * ldo + c] = rv;
+      rh[v * ldo + c] = __fmul_rn(rv, h[v * ldh + c]);
+    }
 }
 
 __global__ void gru_out_kernel(int64_t V, int64_t F, const float* G1, int64_t ld1, int64_t bs,
                                const float* G3, int64_t ld3, const float* z, const float* h,
                                int64_t ldh, float* c_out, float* hn, int64_t ldo, int64_t ldn) {
-  const int64_t n = V * F;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t v = i / F, k = i - v * F;
-    const float cv = tanhf(__fadd_rn(G1[v * ld1 + 2 * bs + k], G3[v * ld3 + k]));
-    const float zv = z[v * ldo + k], hv = h[v * ldh + k];
-    c_out[v * ldo + k] = cv;
-    hn[v * ldn + k] = __fadd_rn(__fmul_rn(__fsub_rn(1.0f, zv), hv), __fmul_rn(zv, cv));
-  }
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.y + threadIdx.y; v < V;
+       v += (int64_t)gridDim.x * blockDim.y)
+    for (int64_t k = threadIdx.x; k < F; k += 32) {
+      const float cv = tanhf(__fadd_rn(G1[v * ld1 + 2 * bs + k], G3[v * ld3 + k]));
+      const float zv = z[v * ldo + k], hv = h[v * ldh + k];
+      c_out[v * ldo + k] = cv;
+      hn[v * ldn + k] = __fadd_rn(__fmul_rn(__fsub_rn(1.0f, zv), hv), __fmul_rn(zv, cv));
+    }
 }
 
 __global__ void gru_bwd1_kernel(int64_t V, int64_t F, const float* g, int64_t ldg, const float* z,
                                 const float* c, int64_t ldo, const float* h, int64_t ldh, float* D3,
                                 int64_t ld3, int64_t bs, float* gh, int64_t ldgh) {
-  const int64_t n = V * F;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t v = i / F, k = i - v * F;
-    const float gv = g[v * ldg + k], zv = z[v * ldo + k], cv = c[v * ldo + k], hv = h[v * ldh + k];
-    const float gz = __fadd_rn(__fmul_rn(gv, cv), -__fmul_rn(gv, hv));
-    const float gc = __fmul_rn(gv, zv);
-    gh[v * ldgh + k] = __fmul_rn(gv, __fsub_rn(1.0f, zv));
-    D3[v * ld3 + 2 * bs + k] = __fmul_rn(gc, __fsub_rn(1.0f, __fmul_rn(cv, cv)));
-    D3[v * ld3 + k] = __fmul_rn(__fmul_rn(gz, zv), __fsub_rn(1.0f, zv));
-  }
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.y + threadIdx.y; v < V;
+       v += (int64_t)gridDim.x * blockDim.y)
+    for (int64_t k = threadIdx.x; k < F; k += 32) {
+      const float gv = g[v * ldg + k], zv = z[v * ldo + k], cv = c[v * ldo + k], hv = h[v * ldh + k];
+      const float gz = __fadd_rn(__fmul_rn(gv, cv), -__fmul_rn(gv, hv));
+      const float gc = __fmul_rn(gv, zv);
+      gh[v * ldgh + k] = __fmul_rn(gv, __fsub_rn(1.0f, zv));
+      D3[v * ld3 + 2 * bs + k] = __fmul_rn(gc, __fsub_rn(1.0f, __fmul_rn(cv, cv)));
+      D3[v * ld3 + k] = __fmul_rn(__fmul_rn(gz, zv), __fsub_rn(1.0f, zv));
+    }
 }
 
 __global__ void gru_bwd2_kernel(int64_t V, int64_t F, const float* grh, int64_t ldr,
                                 const float* r, int64_t ldo, const float* h, int64_t ldh,
                                 float* gh, int64_t ldgh, float* D3, int64_t ld3, int64_t bs) {
-  const int64_t n = V * F;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t v = i / F, k = i - v * F;
-    const float g = grh[v * ldr + k], rv = r[v * ldo + k];
-    const float gr = __fmul_rn(g, h[v * ldh + k]);
-    gh[v * ldgh + k] = __fadd_rn(gh[v * ldgh + k], __fmul_rn(g, rv));
-    D3[v * ld3 + bs + k] = __fmul_rn(__fmul_rn(gr, rv), __fsub_rn(1.0f, rv));
-  }
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.y + threadIdx.y; v < V;
+       v += (int64_t)gridDim.x * blockDim.y)
+    for (int64_t k = threadIdx.x; k < F; k += 32) {
+      const float g = grh[v * ldr + k], rv = r[v * ldo + k];
+      const float gr = __fmul_rn(g, h[v * ldh + k]);
+      gh[v * ldgh + k] = __fadd_rn(gh[v * ldgh + k], __fmul_rn(g, rv));
+      D3[v * ld3 + bs + k] = __fmul_rn(__fmul_rn(gr, rv), __fsub_rn(1.0f, rv));
+    }
 }
 
 }  // namespace
@@ -98,7 +94,7 @@ int sg_gru_gates(int64_t V, int64_t F, const float* G1, int64_t ld1, const float
   SG_REQUIRE(V >= 0 && F >= 0 && bs >= F, SG_ESHAPE, "gru_gates: bad extents");
   if (V * F == 0) return SG_OK;
   SG_REQUIRE(G1 && G2 && h && z && r && rh, SG_EINVAL, "gru_gates: null pointer");
-  gru_gates_kernel<<<grid_for(V * F), 256, 0, (cudaStream_t)stream>>>(V, F, G1, ld1, G2, ld2, bs, h,
+  gru_gates_kernel<<<grid_rows(V), dim3(32, 8), 0, (cudaStream_t)stream>>>(V, F, G1, ld1, G2, ld2, bs, h,
                                                                       ldh, z, r, rh, ldo);
   sg::count_launch();
   cudaError_t e = cudaGetLastError();
@@ -112,7 +108,7 @@ int sg_gru_out(int64_t V, int64_t F, const float* G1, int64_t ld1, int64_t bs, c
   SG_REQUIRE(V >= 0 && F >= 0 && bs >= F, SG_ESHAPE, "gru_out: bad extents");
   if (V * F == 0) return SG_OK;
   SG_REQUIRE(G1 && G3 && z && h && c && hn, SG_EINVAL, "gru_out: null pointer");
-  gru_out_kernel<<<grid_for(V * F), 256, 0, (cudaStream_t)stream>>>(V, F, G1, ld1, bs, G3, ld3, z, h,
+  gru_out_kernel<<<grid_rows(V), dim3(32, 8), 0, (cudaStream_t)stream>>>(V, F, G1, ld1, bs, G3, ld3, z, h,
                                                                     ldh, c, hn, ldo, ldn);
   sg::count_launch();
   cudaError_t e = cudaGetLastError();
@@ -126,7 +122,7 @@ int sg_gru_bwd1(int64_t V, int64_t F, const float* g, int64_t ldg, const float* 
   SG_REQUIRE(V >= 0 && F >= 0 && bs >= F, SG_ESHAPE, "gru_bwd1: bad extents");
   if (V * F == 0) return SG_OK;
   SG_REQUIRE(g && z && c && h && D3 && gh, SG_EINVAL, "gru_bwd1: null pointer");
-  gru_bwd1_kernel<<<grid_for(V * F), 256, 0, (cudaStream_t)stream>>>(V, F, g, ldg, z, c, ldo, h, ldh,
+  gru_bwd1_kernel<<<grid_rows(V), dim3(32, 8), 0, (cudaStream_t)stream>>>(V, F, g, ldg, z, c, ldo, h, ldh,
                                                                      D3, ld3, bs, gh, ldgh);
   sg::count_launch();
   cudaError_t e = cudaGetLastError();
@@ -140,7 +136,7 @@ int sg_gru_bwd2(int64_t V, int64_t F, const float* grh, int64_t ldr, const float
   SG_REQUIRE(V >= 0 && F >= 0 && bs >= F, SG_ESHAPE, "gru_bwd2: bad extents");
   if (V * F == 0) return SG_OK;
   SG_REQUIRE(grh && r && h && gh && D3, SG_EINVAL, "gru_bwd2: null pointer");
-  gru_bwd2_kernel<<<grid_for(V * F), 256, 0, (cudaStream_t)stream>>>(V, F, grh, ldr, r, ldo, h, ldh, gh,
+  gru_bwd2_kernel<<<grid_rows(V), dim3(32, 8), 0, (cudaStream_t)stream>>>(V, F, grh, ldr, r, ldo, h, ldh, gh,
                                                                      ldgh, D3, ld3, bs);
   sg::count_launch();
   cudaError_t e = cudaGetLastError();
