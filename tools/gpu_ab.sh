@@ -1,2 +1,2 @@
-timeout 900 python -m pytest tests/test_gpu_kernels.py -q -x -k "max or mpgcn" 2>&1 | grep -E "^E  |passed|failed" | head -8
-timeout 600 python tools/mp_time.py 2>&1 | tail -1
+timeout 300 python tools/gemm_bench.py 2>&1 | tail -5
+for kb in 64 100; do echo "== smem $kb KB"; SG_LIB_PATH=$PWD/paper_1810_08403_b200/libsagann_g$kb.so timeout 300 python tools/gemm_bench.py 2>&1 | tail -5; done
