@@ -204,6 +204,13 @@ int sg_max_gather_plan(const int64_t* ptr, const int32_t* idx, const sg_item* it
                        float* out, int64_t ldo, int32_t* argpos, int64_t lda, int64_t F, float empty_fill,
                        int64_t pos_base, int accumulate, int finalize, void* workspace,
                        int64_t workspace_bytes, void* stream);
+/* segment_max (tensor.py:453-484) over a segment index with split segments, fp32: as
+ * sg_segment_max (argmax = the gathered row idx[e], int64) but plan-driven like
+ * sg_max_gather_plan (bit-identical to the sequential result). */
+int sg_segment_max_plan(const int64_t* ptr, const int32_t* idx, const sg_item* items, int64_t n_items,
+                        const sg_split* splits, int64_t n_splits, int64_t n_slots, const float* X, int64_t ldx,
+                        float* out, int64_t ldo, int64_t* argmax, int64_t lda, int64_t F, float empty_fill,
+                        void* workspace, int64_t workspace_bytes, void* stream);
 int sg_max_gather_bwd_plan(const int64_t* ptr, const int32_t* idx, const int32_t* pos, const sg_item* items,
                            int64_t n_items, const sg_split* splits, int64_t n_splits, int64_t n_slots,
                            const float* G, int64_t ldg, const int32_t* argpos, int64_t lda, float* out,

@@ -88,6 +88,8 @@ _SIGS = {
     "sg_max_plan_workspace_bytes": (_i64, [_i64, _i64, _i64]),
     "sg_max_gather_plan": (_i32, [_p, _p, _p, _i64, _p, _i64, _i64, _p, _i64, _p, _i64, _p, _i64, _i64,
                                   _f32, _i64, _i32, _i32, _p, _i64, _p]),
+    "sg_segment_max_plan": (_i32, [_p, _p, _p, _i64, _p, _i64, _i64, _p, _i64, _p, _i64, _p, _i64, _i64,
+                                   _f32, _p, _i64, _p]),
     "sg_max_gather_bwd_plan": (_i32, [_p, _p, _p, _p, _i64, _p, _i64, _i64, _p, _i64, _p, _i64, _p, _i64,
                                       _i64, _p, _i64, _i64, _i32, _p, _i64, _p]),
     "sg_gru_gates": (_i32, [_i64, _i64, _p, _i64, _p, _i64, _i64, _p, _i64, _p, _p, _p, _i64, _p]),

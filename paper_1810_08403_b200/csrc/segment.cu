@@ -357,6 +357,7 @@ struct MaxPlan {
   float* out;
   int64_t ldo;
   int32_t* arg;          // fwd: out argmax; bwd: argmax of the destinations
+  int64_t* arg64;        // fwd (segment_max primitive): argmax written as the gathered row idx[pos]
   int64_t lda;
   const float* mask;
   int64_t ldm;
@@ -442,7 +443,10 @@ __global__ void __launch_bounds__(256) maxgather_plan_kernel(const MaxPlan a) {
           for (int k = 0; k < W; ++k)
             if (c0 + k < a.F) {
               a.out[r * a.ldo + c0 + k] = (a.finalize && barg[k] < 0) ? a.fill : best[k];
-              a.arg[r * a.lda + c0 + k] = barg[k];
+              if (a.arg64)
+                a.arg64[r * a.lda + c0 + k] = barg[k] >= 0 ? (int64_t)__ldg(a.idx + barg[k]) : -1;
+              else
+                a.arg[r * a.lda + c0 + k] = barg[k];
             }
         } else {
           const int64_t slot = a.splits[item.split].slot0 + item.sub;
@@ -481,7 +485,10 @@ __global__ void __launch_bounds__(256) maxgather_plan_kernel(const MaxPlan a) {
             }
           }
           a.out[r * a.ldo + c] = (a.finalize && barg < 0) ? a.fill : best;
-          a.arg[r * a.lda + c] = barg;
+          if (a.arg64)
+            a.arg64[r * a.lda + c] = barg >= 0 ? (int64_t)__ldg(a.idx + barg) : -1;
+          else
+            a.arg[r * a.lda + c] = barg;
         }
         if (lane == 0) a.counters[item.split] = 0;
       }
@@ -662,9 +669,12 @@ static int max_plan_launch(bool bwd, const int64_t* ptr, const int32_t* idx, con
                            const sg_item* items, int64_t n_items, const sg_split* splits, int64_t n_splits,
                            int64_t n_slots, const float* Y, int64_t ldy, float* out, int64_t ldo, int32_t* arg,
                            int64_t lda, const float* mask, int64_t ldm, int64_t F, float fill, int64_t base,
-                           int accumulate, int finalize, void* ws, int64_t ws_bytes, void* stream) {
+                           int accumulate, int finalize, void* ws, int64_t ws_bytes, void* stream,
+                           int64_t* arg64 = nullptr) {
   if (n_items == 0 || F == 0) return SG_OK;
-  SG_REQUIRE(ptr && idx && items && Y && out && arg && (!bwd || pos), SG_EINVAL, "max plan: null pointer");
+  SG_REQUIRE(ptr && idx && items && Y && out && (arg || arg64) && (!bwd || pos), SG_EINVAL,
+             "max plan: null pointer");
+  SG_REQUIRE(!arg64 || (!bwd && !accumulate), SG_EINVAL, "max plan: int64 argmax is forward-only");
   SG_REQUIRE(n_splits == 0 || splits, SG_EINVAL, "max plan: split records missing");
   SG_REQUIRE(ws && ws_bytes >= sg_max_plan_workspace_bytes(n_splits, n_slots, F), SG_EBUDGET,
              "max plan workspace too small");
@@ -680,11 +690,13 @@ static int max_plan_launch(bool bwd, const int64_t* ptr, const int32_t* idx, con
   a.pval = reinterpret_cast<float*>(w + 256 + cbytes);
   a.parg = reinterpret_cast<int32_t*>(w + 256 + cbytes + n_slots * pld * 4);
   a.pld = pld;
-  a.Y = Y; a.ldy = ldy; a.out = out; a.ldo = ldo; a.arg = arg; a.lda = lda; a.mask = mask; a.ldm = ldm;
+  a.Y = Y; a.ldy = ldy; a.out = out; a.ldo = ldo; a.arg = arg; a.arg64 = arg64; a.lda = lda;
+  a.mask = mask; a.ldm = ldm;
   a.F = (int)F; a.fill = fill; a.base = base; a.accumulate = accumulate; a.finalize = finalize;
   cudaError_t e = cudaMemsetAsync(w, 0, 256 + cbytes, st);
   if (e != cudaSuccess) SG_FAIL(SG_ECUDA, "memset: %s", cudaGetErrorString(e));
-  const bool vec = (F % 4 == 0) && (ldy % 4 == 0) && (lda % 4 == 0) && aligned(Y, 16) && aligned(arg, 16);
+  const bool vec = (F % 4 == 0) && (ldy % 4 == 0) && (lda % 4 == 0) && aligned(Y, 16) &&
+                   (arg64 || aligned(arg, 16));
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -710,6 +722,15 @@ int sg_max_gather_plan(const int64_t* ptr, const int32_t* idx, const sg_item* it
   return max_plan_launch(false, ptr, idx, nullptr, items, n_items, splits, n_splits, n_slots, Y, ldy, out, ldo,
                          argpos, lda, nullptr, 0, F, empty_fill, pos_base, accumulate, finalize, workspace,
                          workspace_bytes, stream);
+}
+
+int sg_segment_max_plan(const int64_t* ptr, const int32_t* idx, const sg_item* items, int64_t n_items,
+                        const sg_split* splits, int64_t n_splits, int64_t n_slots, const float* X, int64_t ldx,
+                        float* out, int64_t ldo, int64_t* argmax, int64_t lda, int64_t F, float empty_fill,
+                        void* workspace, int64_t workspace_bytes, void* stream) {
+  return max_plan_launch(false, ptr, idx, nullptr, items, n_items, splits, n_splits, n_slots, X, ldx, out, ldo,
+                         nullptr, lda, nullptr, 0, F, empty_fill, 0, 0, 1, workspace, workspace_bytes, stream,
+                         argmax);
 }
 
 int sg_max_gather_bwd_plan(const int64_t* ptr, const int32_t* idx, const int32_t* pos, const sg_item* items,

@@ -10,7 +10,7 @@ reference              here                            kernel
 =====================  ==============================  ================================
 take_rows  :424-436    take_rows                       sg_take_rows / sort + PASS gather
 segment_sum :439-450   segment_sum                     sg_segment_sort + sg_propagate(PASS)
-segment_max :453-484   segment_max                     sg_segment_max / _bwd
+segment_max :453-484   segment_max                     sg_segment_max (/ _plan) / _bwd
 mul/add/... :204-303   mul, add, sub, div, maximum...  sg_ewise
 matmul     :306-319    matmul                          sg_gemm
 softmax_cross_entropy  softmax_cross_entropy           sg_softmax_xent
@@ -138,10 +138,20 @@ class _SegmentMax(torch.autograd.Function):
         F = a2.shape[1]
         out = torch.empty((num_segments, F), dtype=a.dtype, device=a.device)
         arg = torch.empty((num_segments, F), dtype=torch.int64, device=a.device)
-        _lib.check(_lib.lib.sg_segment_max(K.dtype_code(a2), pi.ptr.data_ptr(), pi.idx.data_ptr(),
-                                           num_segments, a2.data_ptr(), a2.stride(0), out.data_ptr(),
-                                           F, arg.data_ptr(), F, F, float(empty_fill),
-                                           _lib.stream_handle()))
+        if pi.n_splits > 0 and a2.dtype == torch.float32:
+            # segments with more than T rows (hubs): plan-driven, bit-identical result
+            nb = int(_lib.lib.sg_max_plan_workspace_bytes(pi.n_splits, pi.n_slots, F))
+            ws = torch.empty(max(nb, 256), dtype=torch.uint8, device=a.device)
+            _lib.check(_lib.lib.sg_segment_max_plan(
+                pi.ptr.data_ptr(), pi.idx.data_ptr(), pi.items.data_ptr(), pi.n_items,
+                pi.splits.data_ptr(), pi.n_splits, pi.n_slots, a2.data_ptr(), a2.stride(0),
+                out.data_ptr(), F, arg.data_ptr(), F, F, float(empty_fill), ws.data_ptr(), ws.numel(),
+                _lib.stream_handle()))
+        else:
+            _lib.check(_lib.lib.sg_segment_max(K.dtype_code(a2), pi.ptr.data_ptr(), pi.idx.data_ptr(),
+                                               num_segments, a2.data_ptr(), a2.stride(0), out.data_ptr(),
+                                               F, arg.data_ptr(), F, F, float(empty_fill),
+                                               _lib.stream_handle()))
         ctx.save_for_backward(arg)
         ctx.shape, ctx.n = a.shape, a.shape[0]
         ctx.mark_non_differentiable(arg)

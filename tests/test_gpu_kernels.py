@@ -259,6 +259,25 @@ def test_primitives_vs_oracle(sg):
     assert ops.sigmoid(_dev(np.zeros(1, np.float32))).item() == 0.5
 
 
+def test_segment_max_primitive_hub_segments(sg):
+    """ops.segment_max with segments far longer than the split threshold (the plan-driven
+    kernel): values and argmax bitwise vs the reference's segment_max, gradient routed alike."""
+    from paper_1810_08403_b200 import ops
+
+    r = np.random.default_rng(7)
+    n, S, F = 30000, 5, 12
+    seg = np.where(r.random(n) < 0.8, 2, r.integers(0, S, n)).astype(np.int64)   # segment 2: ~24K rows
+    x = r.uniform(-1, 1, (n, F)).astype(np.float32)
+    x[::5] = x[::5].round(1)                                                      # ties: lowest row wins
+    xt = _dev(x).requires_grad_(True)
+    m = ops.segment_max(xt, seg, S + 1)                                           # segment S stays empty
+    ref, ref_arg = prim.segment_max(x, seg, S + 1)
+    assert np.array_equal(m.detach().cpu().numpy(), ref)
+    m.sum().backward()
+    assert np.array_equal(xt.grad.cpu().numpy(),
+                          prim.segment_max_bwd(np.ones((S + 1, F), np.float32), ref_arg, n))
+
+
 def test_softmax_xent_vs_oracle(sg):
     from paper_1810_08403_b200 import ops
 
