@@ -200,15 +200,21 @@ class DistSAGA:
         """Stage the next step's local feature / label shard (pinned host) on a copy stream,
         overlapping the running step; the next ``train_step`` waits for it and moves it into
         place (one D2D copy of the shard)."""
+        h0 = self.h[0]
+        base = h0._base if h0._base is not None else h0
         if getattr(self, "_cs", None) is None:
             self._cs = torch.cuda.Stream(device=self.c.device)
-            self._sx = torch.empty_like(self.h[0])
+            self._sx = torch.empty_like(base)     # the padded device layout: contiguous copies
             self._sy = torch.empty_like(self.labels)
             self._used = None
         if self._used is not None:
             self._cs.wait_event(self._used)
+        X_host = torch.as_tensor(X_host)
         with torch.cuda.stream(self._cs):
-            self._sx.copy_(torch.as_tensor(X_host)[:, : self.dims[0]], non_blocking=True)
+            if X_host.is_contiguous() and tuple(X_host.shape) == tuple(self._sx.shape):
+                self._sx.copy_(X_host, non_blocking=True)
+            else:
+                self._sx[:, : self.dims[0]].copy_(X_host[:, : self.dims[0]], non_blocking=True)
             self._sy.copy_(torch.as_tensor(y_host), non_blocking=True)
             ev = torch.cuda.Event()
             ev.record(self._cs)
@@ -219,7 +225,11 @@ class DistSAGA:
             return
         cur = torch.cuda.current_stream(self.c.device)
         cur.wait_event(self._staged)
-        self.h[0].copy_(self._sx)
+        h0 = self.h[0]
+        if h0._base is not None and h0._base.shape == self._sx.shape and h0.data_ptr() == h0._base.data_ptr():
+            h0._base.copy_(self._sx)              # one contiguous device copy
+        else:
+            h0.copy_(self._sx[:, : self.dims[0]])
         self.labels.copy_(self._sy)
         self._used = torch.cuda.Event()
         self._used.record(cur)
@@ -417,7 +427,10 @@ def bench_main(a, cfg, metric, config, helpers):
     model = DistSAGA(shard, [F, H, C], comp, model=cfg["model"])
     X_all = G.synthetic_features(V, F, seed=1)
     y_all = np.random.default_rng(3).integers(0, C, V)
-    X_host = torch.from_numpy(np.ascontiguousarray(X_all[shard.vertices])).pin_memory()
+    Fp = (F + 3) // 4 * 4                   # host shard in the padded device row layout
+    Xs = np.zeros((shard.rows, Fp), np.float32)
+    Xs[:, :F] = X_all[shard.vertices]
+    X_host = torch.from_numpy(Xs).pin_memory()
     y_host = torch.from_numpy(np.ascontiguousarray(y_all[shard.vertices])).pin_memory()
     del X_all, y_all
     model.load_features(X_host)
