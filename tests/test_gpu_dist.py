@@ -1,7 +1,7 @@
 """Multi-GPU engine with the REAL product backend (libsagann kernels) on one GPU.
 
 NCCL refuses two ranks on one device, so these tests run the sharded engine of
-paper_1810_08403_b200.dist with world_size 2 over gloo (which moves CUDA tensors through
+paper_1810_08403_b200.dist with world_size 2, 4 and 8 over gloo (which moves CUDA tensors through
 host memory) with both ranks on cuda:0 and ``CudaCompute`` doing every gather, GEMM and
 loss.  The result must equal the single-GPU chunked executor with P = world on the same
 re-encoded graph: layer-1 aggregates bitwise (same kernels, same chunk order), the rest
@@ -63,15 +63,18 @@ def _worker(rank, world, port, case, outdir):
     dist.destroy_process_group()
 
 
-CASES = [("gcn", 3000, 60000, 37, 16, 5, "rmat", 4096), ("gcn", 2500, 40000, 130, 24, 7, "uniform", 64),
-         ("ggcn", 2000, 30000, 32, 16, 5, "rmat", 128)]
+CASES = [("gcn", 3000, 60000, 37, 16, 5, "rmat", 4096, 2), ("gcn", 2500, 40000, 130, 24, 7, "uniform", 64, 2),
+         ("ggcn", 2000, 30000, 32, 16, 5, "rmat", 128, 2),
+         # the bench's rank counts: 8 (and 4) processes sharing one B200 over gloo
+         ("gcn", 4000, 80000, 40, 16, 5, "rmat", 256, 8), ("ggcn", 3000, 50000, 24, 16, 5, "rmat", 512, 4)]
 
 
 @pytest.mark.parametrize("case", CASES)
-def test_dist_world2_cuda_matches_single_gpu_chunked(case):
+def test_dist_cuda_matches_single_gpu_chunked(case):
     import paper_1810_08403_b200 as sg
 
-    world = 2
+    world = case[-1]
+    case = case[:-1]
     with tempfile.TemporaryDirectory() as outdir:
         mp.start_processes(_worker, args=(world, _free_port(), case, outdir), nprocs=world,
                            join=True, start_method="spawn")
@@ -103,4 +106,6 @@ def test_dist_world2_cuda_matches_single_gpu_chunked(case):
         assert_close(res[r]["z1"], z1[b: b + n], rel=1e-5, what="z1")
         assert abs(float(res[r]["loss"][0]) - m.loss.item()) <= 1e-5 * m.loss.item()
         for k, gw in enumerate(grads):
-            assert_close(res[r][f"g{k}"], gw, rel=1e-5, what=f"grad {k}")
+            # dW = sum over ranks of per-rank partials (all-reduce) vs one GEMM over all rows: the
+            # project's 1e-4 parity band (cancelling entries differ in the last bits at 8 ranks)
+            assert_close(res[r][f"g{k}"], gw, rel=1e-4, what=f"grad {k}")
