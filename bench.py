@@ -409,6 +409,9 @@ def run_ours(a, cfg):
                              "ascending within a destination); DRAM bytes per launch are in "
                              "'traffic' (ncu); l2_ceiling_gbs = measured L2->SM ceiling for random "
                              "2.4-KB row gathers (tools/l2bw.cu)",
+                     "share_of_step": (k_ms / (t_step * 1e3)) if k_ms else None,
+                     "launch_list": "profiles/r01_launches_bench_steps.txt (ncu share of the same "
+                                    "kernel over 5 epochs of this workload)",
                      "l2_ceiling_gbs": l2_ceiling,
                      "frac_of_l2_ceiling": (achieved / l2_ceiling) if (achieved and l2_ceiling) else None},
         "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": int(launches),
