@@ -429,6 +429,9 @@ def run_ours(a, cfg):
 def main():
     a = parse()
     cfg = CONFIGS[a.config]
+    if a.gpus != dist_env()[2]:
+        raise SystemExit(f"--gpus {a.gpus} but WORLD_SIZE={dist_env()[2]}: launch N > 1 ranks with "
+                         f"python -m torch.distributed.run --nproc-per-node {a.gpus} bench.py --gpus {a.gpus}")
     if a.impl == "reference":
         return run_reference(a, cfg)
     return run_ours(a, cfg)
