@@ -257,9 +257,9 @@ int sg_sgd(float* W, const float* dW, int64_t n, float lr, void* stream);
 int sg_check_finite(int dtype, const void* X, int64_t rows, int64_t cols, int64_t ld,
                     int32_t* flag, void* stream);
 /* Elementwise ops used by unfused ApplyEdge programs (tensor.py:204-303):
- * op 0 add, 1 sub, 2 mul, 3 div, 4 max, 5 sigmoid, 6 tanh, 7 relu, 8 relu-backward,
- * 9 sigmoid-backward (a * b * (1 - b) with b = y, tensor.py:232)
- * (a * (b > 0), tensor.py:236); b is broadcast
+ * op 0 add, 1 sub, 2 mul, 3 div, 4 max, 5 sigmoid, 6 tanh, 7 relu,
+ * 8 relu-backward (a * (b > 0), tensor.py:236),
+ * 9 sigmoid-backward (a * b * (1 - b) with b = y, tensor.py:232); b is broadcast
  * per row when b_cols == 1 (the "b_row" kind, tensor.py:184-185), along the
  * leading axis when b_rows == 1 ("b_lead"). */
 int sg_ewise(int op, int64_t rows, int64_t cols, const float* a, int64_t lda, const float* b,

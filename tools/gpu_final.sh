@@ -1,4 +1,4 @@
-timeout 900 python -m pytest tests -q -m gpu 2>&1 | tail -1 > gpurun_out/final_pytest.txt
+timeout 1800 python -m pytest tests -q -m gpu 2>&1 | tail -15 > gpurun_out/final_pytest.txt
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/final_smoke.txt 2>&1
 timeout 900 python bench.py > gpurun_out/final_bench.json 2> gpurun_out/final_bench.err
 timeout 900 python bench.py --impl reference > gpurun_out/final_bench_ref.json 2> gpurun_out/final_bench_ref.err
