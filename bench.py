@@ -23,6 +23,13 @@ import subprocess
 import sys
 import time
 
+# torchrun sets OMP_NUM_THREADS=1 in every rank; the reference arm runs on rank 0 alone with every
+# host thread, so undo that before numpy loads OpenBLAS
+_argv = " ".join(sys.argv[1:]).replace("=", " ")
+if "--impl reference" in _argv and "LOCAL_RANK" in os.environ:
+    for _k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS"):
+        os.environ[_k] = str(len(os.sched_getaffinity(0)))
+
 import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
@@ -170,7 +177,8 @@ def config_of(cfg, a, world):
             "layers": 2, "split_edges": a.split_edges,
             "interval_size": cfg["V"] if (world == 1 and a.engine != "dist") else -(-cfg["V"] // world),
             "parallelism": ("single GPU" if world == 1 and a.engine != "dist" else
-                            f"dest-interval sharding x{world} (reencode_balance, NCCL block broadcasts)"),
+                            f"dest-interval sharding x{world} (reencode_balance, "
+                            f"{os.environ.get('SG_DIST_BACKEND', 'nccl').upper()} block broadcasts)"),
             "l2": "256 MiB L2 flush between timed steps; inputs (X, edge index) > L2"}
 
 

@@ -413,9 +413,17 @@ def bench_main(a, cfg, metric, config, helpers):
 
     rank, local = int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
+    # SG_DIST_BACKEND=gloo is a test hook: N ranks sharing the visible GPU(s) (NCCL refuses two
+    # ranks on one device), so the multi-rank bench logic runs on a one-GPU box
+    backend = os.environ.get("SG_DIST_BACKEND", "nccl")
+    if backend != "nccl":
+        local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    dist.init_process_group("nccl", device_id=dev)
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=dev)
+    else:
+        dist.init_process_group(backend)
     V, E, F, H, C = cfg["V"], cfg["E"], cfg["F"], cfg["H"], cfg["C"]
     t0 = time.perf_counter()
     g = (G.rmat_graph if cfg["graph"] == "rmat" else G.uniform_graph)(V, E, seed=0)
@@ -523,6 +531,7 @@ def bench_main(a, cfg, metric, config, helpers):
                              "algorithmic_bytes_per_launch": float(tb.item()), "launch_ms": k_ms,
                              "peak_source": peak_src + f" x {world} GPUs"},
                 "e2e": e2e, "cpu_baseline": None, "gpu_launches": int(lt.item()),
+                "backend": backend,
                 "clocks": clk, "stages_ms": {k: round(v, 4) for k, v in stages_max.items()},
                 "shard_edges": [int(x) for x in shard_edges],
                 "setup_s": round(t_setup, 2),
