@@ -1,2 +1,5 @@
-timeout 600 python -m pytest tests/test_gpu_dist.py -q -x 2>&1 | tail -1
-for c in reddit blogcatalog10; do timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29511 bench.py --engine dist --config $c --steps 5 --warmup 3 --no-cpu-baseline > /tmp/d.txt 2>&1; tail -1 /tmp/d.txt | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['config']['workload'][:30], d['ms_per_step'], d['e2e']['ms_per_step'], d['gpu_launches'])"; done
+P=$PWD/paper_1810_08403_b200
+for i in 1 2; do
+for n in "" _aba _abb _abc; do
+echo "lib$n $(SG_LIB_PATH=$P/libsagann$n.so timeout 600 python tools/narrow_ab.py 128 41 2>&1 | tail -1)"
+done; done
