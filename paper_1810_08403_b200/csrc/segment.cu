@@ -18,7 +18,7 @@ using sg::VecIO;
 // source rows in flight per lane in the fused max gather and its backward: hub rows (R-MAT:
 // ~800K edges) are walked by one team, so the kernel time is that row's load-latency chain
 #ifndef SG_MAX_DEPTH
-#define SG_MAX_DEPTH 8
+#define SG_MAX_DEPTH 12
 #endif
 constexpr int kMaxDepth = SG_MAX_DEPTH;
 
