@@ -373,6 +373,9 @@ struct Prop {
       // the index load latency no longer serialises with the row loads.
       constexpr int WIN = LPR > DEPTH ? LPR : DEPTH;
       constexpr int WPL = WIN / LPR;
+      // every window slot is loaded by some team lane (a DEPTH of 6 with 4-lane teams would
+      // leave slots 4-5 unloaded), and a multi-slot window is exactly one step
+      static_assert(WIN % LPR == 0 && (WPL == 1 || WIN == DEPTH), "DEPTH must be a multiple of LPR");
       int src_next[WPL];
       float w_next[WPL];
       int n_next = (int)min((int64_t)WIN, e1 - e0);
@@ -805,8 +808,11 @@ cudaError_t launch_one(const PropArgs& a, cudaStream_t st) {
 #ifndef SG_DEPTH_WIDE
 #define SG_DEPTH_WIDE 2
 #endif
+#ifndef SG_DEPTH_MID
+#define SG_DEPTH_MID 8
+#endif
   constexpr int DEPTH = (VPL * NG) == 1 ? SG_DEPTH1
-                                        : ((VPL * NG) <= 4 ? 8 / (VPL * NG) : (NG > 1 ? 1 : SG_DEPTH_WIDE));
+                                        : ((VPL * NG) <= 4 ? SG_DEPTH_MID / (VPL * NG) : (NG > 1 ? 1 : SG_DEPTH_WIDE));
   if constexpr (LPR == 32 && VPL >= 2 && NG == 1 && W > 1) {
     if (tma_enabled() && a.n_hub == 0) return launch_tma<MODE, DT, VPL>(a, st);
   }
