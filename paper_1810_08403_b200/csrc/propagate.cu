@@ -811,8 +811,15 @@ cudaError_t launch_one(const PropArgs& a, cudaStream_t st) {
 #ifndef SG_DEPTH_MID
 #define SG_DEPTH_MID 8
 #endif
+  // single-operand rows of 2-4 vectors per lane: ~4 vectors per lane in flight measured faster
+  // than ~8 (F = 384: 9.1 -> 7.8-8.0 ms per Reddit pass); two-operand rows (G-GCN) keep ~8
+#ifndef SG_DEPTH_MID1
+#define SG_DEPTH_MID1 4
+#endif
+  constexpr int DEPTH_MID = NG == 1 ? (SG_DEPTH_MID1 / VPL > 0 ? SG_DEPTH_MID1 / VPL : 1)
+                                    : SG_DEPTH_MID / (VPL * NG);
   constexpr int DEPTH = (VPL * NG) == 1 ? SG_DEPTH1
-                                        : ((VPL * NG) <= 4 ? SG_DEPTH_MID / (VPL * NG) : (NG > 1 ? 1 : SG_DEPTH_WIDE));
+                                        : ((VPL * NG) <= 4 ? DEPTH_MID : (NG > 1 ? 1 : SG_DEPTH_WIDE));
   if constexpr (LPR == 32 && VPL >= 2 && NG == 1 && W > 1) {
     if (tma_enabled() && a.n_hub == 0) return launch_tma<MODE, DT, VPL>(a, st);
   }
