@@ -509,9 +509,15 @@ struct Prop {
 #ifndef SG_VPL1_BLOCKS
 #define SG_VPL1_BLOCKS 2
 #endif
+#ifndef SG_WIDE_BLOCKS
+#define SG_WIDE_BLOCKS 3
+#endif
 template <int MODE, int W, int VPL, int DEPTH>
 constexpr int prop_min_blocks() {
   if (VPL == 1 && ModeT<MODE>::NG == 1 && SG_VPL1_BLOCKS != 2) return SG_VPL1_BLOCKS;
+  // wide single-operand rows: one row in flight per warp at 3 blocks/SM (85 regs, no spill)
+  // beat two rows at 2 blocks/SM (F = 602 CSC pass 14.2-14.5 -> 13.1 ms)
+  if (VPL >= 5 && ModeT<MODE>::NG == 1 && SG_WIDE_BLOCKS > 0) return SG_WIDE_BLOCKS;
   // per in-flight edge: raw vectors + 64-bit row pointer + shuffled (src, w)
   constexpr int regs = DEPTH * (ModeT<MODE>::NG * VPL * 4 + 4) +
                        (ModeT<MODE>::NOUT + ModeT<MODE>::NR) * VPL * W + 40;
@@ -806,7 +812,7 @@ cudaError_t launch_one(const PropArgs& a, cudaStream_t st) {
 #define SG_DEPTH1 8
 #endif
 #ifndef SG_DEPTH_WIDE
-#define SG_DEPTH_WIDE 2
+#define SG_DEPTH_WIDE 1
 #endif
 #ifndef SG_DEPTH_MID
 #define SG_DEPTH_MID 8
