@@ -44,48 +44,6 @@ int64_t hub_smem_bytes() {
   return v;
 }
 
-// Thread-block-cluster hub cache: the hub rows are spread round-robin over the shared memory
-// of the CS CTAs of a cluster (slot k lives in CTA k % CS at row k / CS) and read through
-// DSMEM (ld.shared::cluster), so a cluster holds CS x the rows one CTA can.  Opt-in A/B knob
-// SG_HUB_CLUSTER = 1 | 2 | 4 | 8 | 16, default 1: on the Reddit L0 pass it measured SLOWER
-// (CSC 17.5 / 18.0 / 19.0 / 20.5 / 23.0 ms for CS = 1 / 2 / 4 / 8 / 16, profiles/r01_hub_cluster_ab.txt):
-// DSMEM (~20 B/clk/SM, served from the owner's shared-memory port) is slower than the L2 path
-// it replaces for 2.4-KB rows, and clusters leave SMs idle.
-int hub_cluster() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("SG_HUB_CLUSTER");
-    v = e ? atoi(e) : 1;
-    if (v != 1 && v != 2 && v != 4 && v != 8 && v != 16) v = 1;
-  }
-  return v;
-}
-
-__device__ __forceinline__ uint32_t cluster_rank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-
-// 16 bytes of CTA `rank`'s shared memory at the address `local` has in this CTA
-template <typename Raw>
-__device__ __forceinline__ Raw ld_dsmem(uint32_t local, uint32_t rank) {
-  uint32_t remote, x, y, z, w;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local), "r"(rank));
-  asm volatile("ld.shared::cluster.v4.b32 {%0, %1, %2, %3}, [%4];"
-               : "=r"(x), "=r"(y), "=r"(z), "=r"(w)
-               : "r"(remote)
-               : "memory");
-  Raw out;
-  uint32_t* o = reinterpret_cast<uint32_t*>(&out);
-  o[0] = x; o[1] = y; o[2] = z; o[3] = w;
-  return out;
-}
-
 // ------------------------------------------------------------------ modes
 template <int MODE>
 struct ModeT;
@@ -233,7 +191,7 @@ struct PropArgs {
   int32_t n_hub;
 };
 
-template <int MODE, int DT, int W, int VPL, int LPR, int DEPTH, bool HUB = false, int CS = 1>
+template <int MODE, int DT, int W, int VPL, int LPR, int DEPTH, bool HUB = false>
 struct Prop {
   using M = ModeT<MODE>;
   using IO = VecIO<DT, W>;
@@ -241,35 +199,33 @@ struct Prop {
 
   using Elem = typename IO::Elem;
   using Raw = typename IO::Raw;
+  // run-length reuse of multi-edges (see step): single-operand rows of >= 2 vectors per lane.
+  // One-vector rows (F <= 128 fp32) keep one load per edge: there the run bookkeeping cost
+  // more than the loads it saved (Reddit F = 128 passes 3.6 -> 4.5 ms).
+  static constexpr bool kRuns = NG == 1 && VPL >= 2;
 
   // Load the lane's slice of DEPTH gathered rows (raw 16-byte vectors in flight), then add
   // their terms in edge order.  FULL: all DEPTH edges valid (no per-edge predicates).
   // `gl` is G advanced to this lane's first column; only the last vector needs a bound check.
-  template <bool FULL>
+  // RUNS: entry d stands for a run of cnt[d] consecutive edges with the same (source, weight)
+  // (multi-edges: R-MAT repeats 31% of the Reddit-shaped edges), so one row load serves the
+  // whole run and its term is added cnt[d] times -- the same sequence of IEEE adds as one
+  // load per edge, i.e. bitwise identical.
+  template <bool FULL, bool RUNS>
   static __device__ __forceinline__ void step(const PropArgs& a, const Elem* gl, const Raw* hl,
                                               bool last_ok, const int (&s)[DEPTH],
-                                              const float (&wv)[DEPTH], int n,
+                                              const float (&wv)[DEPTH], const int (&cnt)[DEPTH], int n,
                                               const float (&rs)[NR > 0 ? NR : 1][VPL][W],
                                               float (&acc)[NOUT][VPL][W]) {
     Raw g[DEPTH][NG][VPL];
 #pragma unroll
     for (int d = 0; d < DEPTH; ++d) {
       if (HUB && (FULL || d < n) && s[d] < 0) {
-        // hub row: served from shared memory (same bits as the HBM row) -- this CTA's copy,
-        // or with CS > 1 the owning cluster CTA's, through DSMEM
-        const int slot = s[d] & 0x7fffffff;
-        if constexpr (CS == 1) {
-          const Raw* hrow = hl + slot * a.Fv;
+        // hub row: served from this CTA's shared memory (same bits as the HBM row)
+        const Raw* hrow = hl + (s[d] & 0x7fffffff) * a.Fv;
 #pragma unroll
-          for (int v = 0; v < VPL; ++v)
-            if (v < VPL - 1 || last_ok) g[d][0][v] = hrow[v * LPR];
-        } else {
-          const uint32_t local = (uint32_t)__cvta_generic_to_shared(hl) +
-                                 (uint32_t)((slot / CS) * a.Fv) * 16u;
-#pragma unroll
-          for (int v = 0; v < VPL; ++v)
-            if (v < VPL - 1 || last_ok) g[d][0][v] = ld_dsmem<Raw>(local + v * LPR * 16u, slot % CS);
-        }
+        for (int v = 0; v < VPL; ++v)
+          if (v < VPL - 1 || last_ok) g[d][0][v] = hrow[v * LPR];
       } else if (FULL || d < n) {
         // 32x32->64 IMAD.WIDE row address; column offsets are immediates
         const Elem* row = gl + (uint64_t)(uint32_t)s[d] * (uint32_t)a.ldg;
@@ -286,28 +242,34 @@ struct Prop {
 #pragma unroll
     for (int d = 0; d < DEPTH; ++d) {
       if (FULL || d < n) {
+        // a run's terms are recomputed from the raw vectors still in registers (cheaper in
+        // registers than keeping the fp32 terms of a whole row live)
+        const int reps = RUNS ? cnt[d] : 1;
+#pragma unroll 1
+        for (int c = 0; c < reps; ++c) {
 #pragma unroll
-        for (int v = 0; v < VPL; ++v) {
-          float x0[W], x1[W];
-          IO::unpack(g[d][0][v], x0);
-          IO::unpack(g[d][NG - 1][v], x1);
-          if constexpr (W % 2 == 0) {
+          for (int v = 0; v < VPL; ++v) {
+            float x0[W], x1[W];
+            IO::unpack(g[d][0][v], x0);
+            IO::unpack(g[d][NG - 1][v], x1);
+            if constexpr (W % 2 == 0) {
 #pragma unroll
-            for (int k = 0; k < W; k += 2) {
-              float t0a, t1a = 0.f, t0b, t1b = 0.f;
-              M::term(&x0[k], &x1[k], &rs[0][v][k], &rs[NR > 1 ? 1 : 0][v][k], wv[d], &t0a, &t1a);
-              M::term(&x0[k + 1], &x1[k + 1], &rs[0][v][k + 1], &rs[NR > 1 ? 1 : 0][v][k + 1], wv[d],
-                      &t0b, &t1b);
-              add2_rn(acc[0][v][k], acc[0][v][k + 1], t0a, t0b);
-              if (NOUT > 1) add2_rn(acc[NOUT - 1][v][k], acc[NOUT - 1][v][k + 1], t1a, t1b);
-            }
-          } else {
+              for (int k = 0; k < W; k += 2) {
+                float t0a, t1a = 0.f, t0b, t1b = 0.f;
+                M::term(&x0[k], &x1[k], &rs[0][v][k], &rs[NR > 1 ? 1 : 0][v][k], wv[d], &t0a, &t1a);
+                M::term(&x0[k + 1], &x1[k + 1], &rs[0][v][k + 1], &rs[NR > 1 ? 1 : 0][v][k + 1], wv[d],
+                        &t0b, &t1b);
+                add2_rn(acc[0][v][k], acc[0][v][k + 1], t0a, t0b);
+                if (NOUT > 1) add2_rn(acc[NOUT - 1][v][k], acc[NOUT - 1][v][k + 1], t1a, t1b);
+              }
+            } else {
 #pragma unroll
-            for (int k = 0; k < W; ++k) {
-              float t0, t1 = 0.f;
-              M::term(&x0[k], &x1[k], &rs[0][v][k], &rs[NR > 1 ? 1 : 0][v][k], wv[d], &t0, &t1);
-              acc[0][v][k] = __fadd_rn(acc[0][v][k], t0);
-              if (NOUT > 1) acc[NOUT - 1][v][k] = __fadd_rn(acc[NOUT - 1][v][k], t1);
+              for (int k = 0; k < W; ++k) {
+                float t0, t1 = 0.f;
+                M::term(&x0[k], &x1[k], &rs[0][v][k], &rs[NR > 1 ? 1 : 0][v][k], wv[d], &t0, &t1);
+                acc[0][v][k] = __fadd_rn(acc[0][v][k], t0);
+                if (NOUT > 1) acc[NOUT - 1][v][k] = __fadd_rn(acc[NOUT - 1][v][k], t1);
+              }
             }
           }
         }
@@ -324,8 +286,10 @@ struct Prop {
     const Raw* hl = hs + tl;
     const bool last_ok = (VPL - 1) * LPR + tl < a.Fv;
     if constexpr (LPR == 32) {
-      // warp-wide index window: 32 (src, w) pairs loaded coalesced, broadcast by shuffle;
-      // the next window is prefetched while this one is consumed.
+      // warp-wide index window: 32 (src, w) pairs loaded coalesced, run-length encoded by
+      // ballot (a lane heads a run unless it repeats the previous lane's (src, w)), the run
+      // heads broadcast by shuffle DEPTH at a time; the next window is prefetched while this
+      // one is consumed.  A run split by a window boundary is just two runs.
       int n_next = (int)min((int64_t)32, e1 - e0);
       int src_next = 0;
       float w_next = 0.f;
@@ -343,27 +307,55 @@ struct Prop {
           src_next = __ldcs(a.idx + eb + 32 + tl);
           if (M::USE_W) w_next = __ldcs(a.w + eb + 32 + tl);
         }
-        int d0 = 0;
-        #pragma unroll 1
-        for (; d0 + DEPTH <= n; d0 += DEPTH) {
-          int s[DEPTH];
-          float wv[DEPTH];
+        if constexpr (kRuns) {
+          const int prev_src = __shfl_up_sync(0xffffffffu, my_src, 1);
+          const float prev_w = __shfl_up_sync(0xffffffffu, my_w, 1);
+          const bool head = tl < n && (tl == 0 || prev_src != my_src ||
+                                       (M::USE_W && __float_as_int(prev_w) != __float_as_int(my_w)));
+          unsigned heads = __ballot_sync(0xffffffffu, head);
+          const unsigned later = heads & (0xfffffffeu << tl);  // heads after this lane
+          const int my_cnt = (later ? __ffs(later) - 1 : n) - tl;
+          int nu = __popc(heads);
+          #pragma unroll 1
+          for (; nu > 0; nu -= DEPTH) {
+            int s[DEPTH], cnt[DEPTH];
+            float wv[DEPTH];
 #pragma unroll
-          for (int d = 0; d < DEPTH; ++d) {
-            s[d] = __shfl_sync(0xffffffffu, my_src, d0 + d);
-            wv[d] = M::USE_W ? __shfl_sync(0xffffffffu, my_w, d0 + d) : 0.f;
+            for (int d = 0; d < DEPTH; ++d) {
+              const int hl_d = heads ? __ffs(heads) - 1 : 0;
+              heads &= heads - 1u;
+              s[d] = __shfl_sync(0xffffffffu, my_src, hl_d);
+              wv[d] = M::USE_W ? __shfl_sync(0xffffffffu, my_w, hl_d) : 0.f;
+              cnt[d] = __shfl_sync(0xffffffffu, my_cnt, hl_d);
+            }
+            if (nu >= DEPTH)
+              step<true, true>(a, gl, hl, last_ok, s, wv, cnt, DEPTH, rs, acc);
+            else
+              step<false, true>(a, gl, hl, last_ok, s, wv, cnt, nu, rs, acc);
           }
-          step<true>(a, gl, hl, last_ok, s, wv, DEPTH, rs, acc);
-        }
-        if (d0 < n) {
-          int s[DEPTH];
-          float wv[DEPTH];
+        } else {
+          int d0 = 0;
+          #pragma unroll 1
+          for (; d0 + DEPTH <= n; d0 += DEPTH) {
+            int s[DEPTH];
+            float wv[DEPTH];
 #pragma unroll
-          for (int d = 0; d < DEPTH; ++d) {
-            s[d] = __shfl_sync(0xffffffffu, my_src, (d0 + d) & 31);
-            wv[d] = M::USE_W ? __shfl_sync(0xffffffffu, my_w, (d0 + d) & 31) : 0.f;
+            for (int d = 0; d < DEPTH; ++d) {
+              s[d] = __shfl_sync(0xffffffffu, my_src, d0 + d);
+              wv[d] = M::USE_W ? __shfl_sync(0xffffffffu, my_w, d0 + d) : 0.f;
+            }
+            step<true, false>(a, gl, hl, last_ok, s, wv, s, DEPTH, rs, acc);
           }
-          step<false>(a, gl, hl, last_ok, s, wv, n - d0, rs, acc);
+          if (d0 < n) {
+            int s[DEPTH];
+            float wv[DEPTH];
+#pragma unroll
+            for (int d = 0; d < DEPTH; ++d) {
+              s[d] = __shfl_sync(0xffffffffu, my_src, (d0 + d) & 31);
+              wv[d] = M::USE_W ? __shfl_sync(0xffffffffu, my_w, (d0 + d) & 31) : 0.f;
+            }
+            step<false, false>(a, gl, hl, last_ok, s, wv, s, n - d0, rs, acc);
+          }
         }
       }
     } else {
@@ -414,9 +406,9 @@ struct Prop {
             wv[d] = M::USE_W ? __shfl_sync(tmask, my_w[d / LPR], d % LPR, LPR) : 0.f;
           }
           if (n == DEPTH)
-            step<true>(a, gl, hl, last_ok, s, wv, DEPTH, rs, acc);
+            step<true, false>(a, gl, hl, last_ok, s, wv, s, DEPTH, rs, acc);
           else
-            step<false>(a, gl, hl, last_ok, s, wv, n, rs, acc);
+            step<false, false>(a, gl, hl, last_ok, s, wv, s, n, rs, acc);
         } else {
           int d0 = 0;
           #pragma unroll 1
@@ -428,7 +420,7 @@ struct Prop {
               s[d] = __shfl_sync(tmask, my_src[0], d0 + d, LPR);
               wv[d] = M::USE_W ? __shfl_sync(tmask, my_w[0], d0 + d, LPR) : 0.f;
             }
-            step<true>(a, gl, hl, last_ok, s, wv, DEPTH, rs, acc);
+            step<true, false>(a, gl, hl, last_ok, s, wv, s, DEPTH, rs, acc);
           }
           if (d0 < n) {
             int s[DEPTH];
@@ -438,7 +430,7 @@ struct Prop {
               s[d] = __shfl_sync(tmask, my_src[0], (d0 + d) & (LPR - 1), LPR);
               wv[d] = M::USE_W ? __shfl_sync(tmask, my_w[0], (d0 + d) & (LPR - 1), LPR) : 0.f;
             }
-            step<false>(a, gl, hl, last_ok, s, wv, n - d0, rs, acc);
+            step<false, false>(a, gl, hl, last_ok, s, wv, s, n - d0, rs, acc);
           }
         }
       }
@@ -527,29 +519,22 @@ constexpr int prop_min_blocks() {
 // HUB: the block first copies the pass's hub rows (most-referenced source rows, listed in
 // a.hub_rows; their edges carry idx = slot | 0x80000000) into shared memory, so those
 // gathers are served on-chip instead of through L2.  One block of NWB warps per SM.
-template <int MODE, int DT, int W, int VPL, int LPR, int DEPTH, bool HUB = false, int NWB = kWarpsPerBlock,
-          int CS = 1>
+template <int MODE, int DT, int W, int VPL, int LPR, int DEPTH, bool HUB = false, int NWB = kWarpsPerBlock>
 __global__ void __launch_bounds__(NWB * 32, (HUB ? 1 : prop_min_blocks<MODE, W, VPL, DEPTH>()))
     prop_kernel(const PropArgs a) {
-  using K = Prop<MODE, DT, W, VPL, LPR, DEPTH, HUB, CS>;
+  using K = Prop<MODE, DT, W, VPL, LPR, DEPTH, HUB>;
   using Raw = typename K::Raw;
   extern __shared__ __align__(16) unsigned char prop_smem[];
   const Raw* hs = reinterpret_cast<const Raw*>(prop_smem);
   if constexpr (HUB) {
-    // this CTA's hub rows: slots rank, rank + CS, rank + 2 CS, ... (all of them for CS = 1)
     Raw* hw = reinterpret_cast<Raw*>(prop_smem);
-    const int rank = CS > 1 ? (int)cluster_rank() : 0;
-    const int mine = (a.n_hub - rank + CS - 1) / CS;
-    const int total = mine * a.Fv;
+    const int total = a.n_hub * a.Fv;
     for (int i = threadIdx.x; i < total; i += blockDim.x) {
       const int r = i / a.Fv, c = i - r * a.Fv;
       hw[i] = K::IO::ld_raw(static_cast<const typename K::Elem*>(a.G) +
-                            (int64_t)__ldg(a.hub_rows + r * CS + rank) * a.ldg + (int64_t)c * W);
+                            (int64_t)__ldg(a.hub_rows + r) * a.ldg + (int64_t)c * W);
     }
-    if constexpr (CS > 1)
-      cluster_sync_all();  // every CTA's rows visible cluster-wide before any DSMEM read
-    else
-      __syncthreads();
+    __syncthreads();
   }
   constexpr int NOUT = K::NOUT;
   constexpr int NRr = K::NR > 0 ? K::NR : 1;
@@ -638,8 +623,6 @@ __global__ void __launch_bounds__(NWB * 32, (HUB ? 1 : prop_min_blocks<MODE, W, 
       }
     }
   }
-  if constexpr (HUB && CS > 1)
-    cluster_sync_all();  // no CTA leaves while a peer may still read its shared memory
 }
 
 // ------------------------------------------------------------------ dispatch
@@ -662,140 +645,19 @@ int sm_count() {
   return g_sm_count;
 }
 
-#include "propagate_tma.cuh"
-
-// TMA ring path for wide single-operand rows (opt-in with SG_PROP_TMA=1; see propagate_tma.cuh).
-bool tma_enabled() {
-  static int on = -1;
-  if (on < 0) {
-    const char* e = getenv("SG_PROP_TMA");
-    on = (e && e[0] == '1') ? 1 : 0;  // opt-in until it beats the register path
-  }
-  return on == 1;
-}
-
-template <int MODE, int DT, int VPL>
-cudaError_t launch_tma(const PropArgs& a, cudaStream_t st) {
-  constexpr int W = DT == SG_F32 ? 4 : 8;
-  (void)W;
-  const uint32_t slot_bytes = (uint32_t)a.Fv * 16u;
-  const int budget = 110 * 1024;  // per block; two 8-warp blocks per SM
-  int S = (int)((budget - 1024) / ((int64_t)kTmaWarps * slot_bytes));
-  S = std::max(2, std::min(S, 16));
-  const size_t smem = (size_t)((kTmaWarps * S * 8 + 127) / 128 * 128) + (size_t)kTmaWarps * S * slot_bytes;
-  auto kern = prop_tma_kernel<MODE, DT, VPL>;
-  static int configured = 0;
-  if (!configured) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    configured = 1;
-  }
-  int blocks_per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, kTmaWarps * 32, smem);
-  if (blocks_per_sm <= 0) blocks_per_sm = 1;
-  int64_t want = ((int64_t)a.n_items + kTmaWarps - 1) / kTmaWarps;
-  int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)blocks_per_sm * sm_count()));
-  kern<<<grid, kTmaWarps * 32, smem, st>>>(a, S, slot_bytes);
-  sg::count_launch();
-  return cudaGetLastError();
-}
-
-#include "propagate_async.cuh"
-
-// cp.async ring path for wide single-operand rows: opt-in (SG_PROP_ASYNC=1).  Measured
-// slower than the register path on the Reddit-shaped pass (20.1 vs 17.1 ms): that pass
-// is bound by L2 throughput (~72% of peak), not by per-warp loads in flight.
-// SG_PROP_TEAM2=1: rows of 17..32 vectors (F 65..128 fp32) as half-warp teams (A/B knob).
-// SG_PROP_TEAM_MAXV: widest row (in 16-B vectors) still given to a lane team of < 32 lanes;
-// wider rows take one warp per row (A/B knob, default 16).
-int team_max_vectors() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("SG_PROP_TEAM_MAXV");
-    v = e ? atoi(e) : 16;
-  }
-  return v;
-}
-
-bool team_rows() {
-  static int on = -1;
-  if (on < 0) {
-    const char* e = getenv("SG_PROP_TEAM2");
-    on = (e && e[0] == '1') ? 1 : 0;
-  }
-  return on == 1;
-}
-
-// SG_PROP_ASYNC: 0 off (default), 1 all widths, 2 one-vector rows only (F <= 128 fp32).
-bool async_enabled(int vpl) {
-  static int mode = -1;
-  if (mode < 0) {
-    const char* e = getenv("SG_PROP_ASYNC");
-    mode = (e && (e[0] == '1' || e[0] == '2')) ? e[0] - '0' : 0;
-  }
-  return mode == 1 || (mode == 2 && vpl == 1);
-}
-
-template <int MODE, int DT, int VPL>
-cudaError_t launch_async(const PropArgs& a, cudaStream_t st) {
-  // ring depth S: as many rows in flight as ~100 KB of shared memory per 8-warp block
-  // allows while keeping two blocks (16 warps) per SM
-  constexpr int S = VPL == 1 ? 16 : (VPL <= 3 ? 8 : (VPL == 4 ? 6 : 4));
-  const size_t smem = (size_t)kAsyncWarps * S * VPL * 512;
-  auto kern = prop_async_kernel<MODE, DT, VPL, S>;
-  static int blocks_per_sm = 0;
-  if (!blocks_per_sm) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, kAsyncWarps * 32, smem);
-    if (blocks_per_sm <= 0) blocks_per_sm = 1;
-  }
-  int64_t want = ((int64_t)a.n_items + kAsyncWarps - 1) / kAsyncWarps;
-  int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)blocks_per_sm * sm_count()));
-  kern<<<grid, kAsyncWarps * 32, smem, st>>>(a);
-  sg::count_launch();
-  return cudaGetLastError();
-}
-
-// hub-cache kernel: one block per SM holding (its share of) the hub rows; CS > 1 launches
-// clusters of CS blocks sharing the rows through DSMEM
-template <int MODE, int DT, int W, int VPL, int LPR, int DEPTH, int NWB, int CS>
+// hub-cache kernel: one block per SM holding the hub rows
+template <int MODE, int DT, int W, int VPL, int LPR, int DEPTH, int NWB>
 cudaError_t launch_hub(const PropArgs& a, cudaStream_t st) {
-  auto hk = prop_kernel<MODE, DT, W, VPL, LPR, DEPTH, true, NWB, CS>;
-  const int per_cta = (a.n_hub + CS - 1) / CS;
-  const size_t smem = (size_t)per_cta * a.Fv * 16;
+  auto hk = prop_kernel<MODE, DT, W, VPL, LPR, DEPTH, true, NWB>;
+  const size_t smem = (size_t)a.n_hub * a.Fv * 16;
   static int hub_cfg = 0;
   if (!hub_cfg) {
     cudaFuncSetAttribute(hk, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    if (CS > 8) cudaFuncSetAttribute(hk, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     hub_cfg = 1;
   }
   int64_t want = ((int64_t)a.n_items + NWB - 1) / NWB;
-  if constexpr (CS == 1) {
-    int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, sm_count()));
-    hk<<<grid, NWB * 32, smem, st>>>(a);
-  } else {
-    cudaLaunchConfig_t cfg = {};
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = CS;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.blockDim = dim3(NWB * 32);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    static int max_clusters = 0;
-    if (!max_clusters) {
-      cfg.gridDim = dim3(CS * ((sm_count() + CS - 1) / CS));
-      if (cudaOccupancyMaxActiveClusters(&max_clusters, hk, &cfg) != cudaSuccess || max_clusters <= 0)
-        max_clusters = sm_count() / CS;
-      if (max_clusters <= 0) max_clusters = 1;
-    }
-    const int64_t clusters = std::max<int64_t>(1, std::min<int64_t>((want + CS - 1) / CS, max_clusters));
-    cfg.gridDim = dim3((unsigned)(clusters * CS));
-    cudaError_t e = cudaLaunchKernelEx(&cfg, hk, a);
-    if (e != cudaSuccess) return e;
-  }
+  int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, sm_count()));
+  hk<<<grid, NWB * 32, smem, st>>>(a);
   sg::count_launch();
   return cudaGetLastError();
 }
@@ -803,10 +665,6 @@ cudaError_t launch_hub(const PropArgs& a, cudaStream_t st) {
 template <int MODE, int DT, int W, int VPL, int LPR>
 cudaError_t launch_one(const PropArgs& a, cudaStream_t st) {
   constexpr int NG = ModeT<MODE>::NG;
-  // (the opt-in ring paths read raw indices: never with a hub-encoded index)
-  if constexpr (LPR == 32 && NG == 1 && W > 1) {
-    if (async_enabled(VPL) && !tma_enabled() && a.n_hub == 0) return launch_async<MODE, DT, VPL>(a, st);
-  }
   // rows in flight per warp: ~8 vectors per lane (DEPTH 3 at VPL 5 spills and runs 50% slower)
 #ifndef SG_DEPTH1
 #define SG_DEPTH1 8
@@ -826,21 +684,12 @@ cudaError_t launch_one(const PropArgs& a, cudaStream_t st) {
                                     : SG_DEPTH_MID / (VPL * NG);
   constexpr int DEPTH = (VPL * NG) == 1 ? SG_DEPTH1
                                         : ((VPL * NG) <= 4 ? DEPTH_MID : (NG > 1 ? 1 : SG_DEPTH_WIDE));
-  if constexpr (LPR == 32 && VPL >= 2 && NG == 1 && W > 1) {
-    if (tma_enabled() && a.n_hub == 0) return launch_tma<MODE, DT, VPL>(a, st);
-  }
   if constexpr (LPR == 32 && NG == 1 && W > 1 && VPL >= kHubMinVpl) {
     if (a.n_hub > 0) {
       // hub-cache kernel: one block per SM holding the hub rows, as many warps as the
       // register budget allowed the default kernel (2-3 blocks of 8 warps)
       constexpr int NWB = kWarpsPerBlock * prop_min_blocks<MODE, W, VPL, DEPTH>();
-      switch (hub_cluster()) {
-        case 2: return launch_hub<MODE, DT, W, VPL, LPR, DEPTH, NWB, 2>(a, st);
-        case 4: return launch_hub<MODE, DT, W, VPL, LPR, DEPTH, NWB, 4>(a, st);
-        case 8: return launch_hub<MODE, DT, W, VPL, LPR, DEPTH, NWB, 8>(a, st);
-        case 16: return launch_hub<MODE, DT, W, VPL, LPR, DEPTH, NWB, 16>(a, st);
-        default: return launch_hub<MODE, DT, W, VPL, LPR, DEPTH, NWB, 1>(a, st);
-      }
+      return launch_hub<MODE, DT, W, VPL, LPR, DEPTH, NWB>(a, st);
     }
   }
   auto kern = prop_kernel<MODE, DT, W, VPL, LPR, DEPTH>;
@@ -948,7 +797,7 @@ int64_t sg_propagate_hub_capacity(int64_t F, int dtype) {
   // every column slice must be wide enough for the hub kernel (the index is encoded)
   const int64_t last_cols = F % max_cols == 0 ? std::min(F, max_cols) : F % max_cols;
   if (last_cols <= (int64_t)32 * (kHubMinVpl - 1) * VW) return 0;
-  return std::min<int64_t>((hub_smem_bytes() / row_bytes) * hub_cluster(), INT32_MAX);
+  return std::min<int64_t>(hub_smem_bytes() / row_bytes, INT32_MAX);
 }
 
 int sg_propagate_hub(int mode, int dtype, const int64_t* ptr, const int32_t* idx, const float* w,
@@ -1000,13 +849,10 @@ int sg_propagate_hub(int mode, int dtype, const int64_t* ptr, const int32_t* idx
     // team 0 works on split items and heavy packed rows leave teams idle: one warp per row
     // measured 17% faster there (tools/narrow_ab.py), so teams are not used.
     const bool hub_heavy = n_slots * 2 >= n_items;
-    if (Fv <= team_max_vectors() && Fv <= 16 && !hub_heavy) {
+    if (Fv <= 16 && !hub_heavy) {
       LPR = 2;
       while (LPR < Fv) LPR *= 2;
       VPL = 1;
-    } else if (Fv <= 32 && team_rows()) {
-      LPR = 16;  // half-warp teams: two destination rows per warp, 2 vectors per lane
-      VPL = 2;
     }
     PropArgs a;
     a.ptr = ptr; a.idx = idx; a.w = w; a.items = items; a.splits = splits;
