@@ -26,4 +26,10 @@ void count_launch(int n = 1);
     if (!(cond)) SG_FAIL(code, __VA_ARGS__); \
   } while (0)
 
+#ifdef __CUDACC__
+// ReLU with numpy's np.maximum(x, 0) semantics (tensor.py:207): NaN propagates (fmaxf
+// would map NaN to 0 and hide it from the strict non-finite check).
+__device__ __forceinline__ float relu_np(float v) { return (v >= 0.f || v != v) ? v : 0.f; }
+#endif
+
 }  // namespace sg

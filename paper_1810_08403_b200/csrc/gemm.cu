@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(NTHR) sgemm_kernel(const GemmArgs p) {
         p.partial[((int64_t)blockIdx.z * p.M + m) * p.N + n] = v;
       } else {
         p.C[m * p.ldc + n] = v;
-        if (p.epilogue == SG_EPI_RELU_DUAL) p.D[m * p.ldd + n] = fmaxf(v, 0.f);
+        if (p.epilogue == SG_EPI_RELU_DUAL) p.D[m * p.ldd + n] = sg::relu_np(v);
       }
     }
   }
@@ -142,7 +142,7 @@ __global__ void splitk_reduce_kernel(const float* partial, int splits, int64_t M
     for (int z = 0; z < splits; ++z) s += partial[(int64_t)z * total + t];  // fixed order
     const int64_t m = t / N, n = t % N;
     C[m * ldc + n] = s;
-    if (epilogue == SG_EPI_RELU_DUAL) D[m * ldd + n] = fmaxf(s, 0.f);
+    if (epilogue == SG_EPI_RELU_DUAL) D[m * ldd + n] = sg::relu_np(s);
   }
 }
 

@@ -272,11 +272,11 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tf32x3_kernel(const TcArgs p
           if (relu) {
             if (p.vec_d && col + 3 < p.N) {
               *reinterpret_cast<float4*>(p.D + row * p.ldd + col) =
-                  make_float4(fmaxf(v[j], 0.f), fmaxf(v[j + 1], 0.f), fmaxf(v[j + 2], 0.f), fmaxf(v[j + 3], 0.f));
+                  make_float4(sg::relu_np(v[j]), sg::relu_np(v[j + 1]), sg::relu_np(v[j + 2]), sg::relu_np(v[j + 3]));
             } else {
 #pragma unroll
               for (int q = 0; q < 4; ++q)
-                if (col + q < p.N) p.D[row * p.ldd + col + q] = fmaxf(v[j + q], 0.f);
+                if (col + q < p.N) p.D[row * p.ldd + col + q] = sg::relu_np(v[j + q]);
             }
           }
         }
@@ -322,7 +322,7 @@ __global__ void tc_splitk_reduce(const float* partial, int splits, int64_t M, in
     for (int z = 0; z < splits; ++z) s += partial[(int64_t)z * total + t];  // fixed order
     const int64_t m = t / N, n = t % N;
     C[m * ldc + n] = s;
-    if (epilogue == SG_EPI_RELU_DUAL) D[m * ldd + n] = fmaxf(s, 0.f);
+    if (epilogue == SG_EPI_RELU_DUAL) D[m * ldd + n] = sg::relu_np(s);
   }
 }
 

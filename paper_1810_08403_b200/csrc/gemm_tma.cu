@@ -232,11 +232,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (relu) {
             if (p.vec_d && col + 3 < p.N) {
               *reinterpret_cast<float4*>(p.D + row * p.ldd + col) =
-                  make_float4(fmaxf(v[j], 0.f), fmaxf(v[j + 1], 0.f), fmaxf(v[j + 2], 0.f), fmaxf(v[j + 3], 0.f));
+                  make_float4(sg::relu_np(v[j]), sg::relu_np(v[j + 1]), sg::relu_np(v[j + 2]), sg::relu_np(v[j + 3]));
             } else {
 #pragma unroll
               for (int q = 0; q < 4; ++q)
-                if (col + q < p.N) p.D[row * p.ldd + col + q] = fmaxf(v[j + q], 0.f);
+                if (col + q < p.N) p.D[row * p.ldd + col + q] = sg::relu_np(v[j + q]);
             }
           }
         }

@@ -31,7 +31,7 @@ __global__ void xent_rows_kernel(const float* Z, int64_t ldz, int relu_input, co
     float zmax = -INFINITY;
     for (int64_t c = lane; c < C; c += 32) {
       float v = z[c];
-      if (relu_input) v = fmaxf(v, 0.f);
+      if (relu_input) v = sg::relu_np(v);
       zmax = fmaxf(zmax, v);
     }
 #pragma unroll
@@ -39,7 +39,7 @@ __global__ void xent_rows_kernel(const float* Z, int64_t ldz, int relu_input, co
     float denom = 0.f;
     for (int64_t c = lane; c < C; c += 32) {
       float v = z[c];
-      if (relu_input) v = fmaxf(v, 0.f);
+      if (relu_input) v = sg::relu_np(v);
       denom += expf(v - zmax);
     }
 #pragma unroll
@@ -47,7 +47,7 @@ __global__ void xent_rows_kernel(const float* Z, int64_t ldz, int relu_input, co
     const float logd = logf(denom);
     for (int64_t c = lane; c < C; c += 32) {
       const float zc = z[c];
-      const float v = relu_input ? fmaxf(zc, 0.f) : zc;
+      const float v = relu_input ? sg::relu_np(zc) : zc;
       const float p = expf(v - zmax) / denom;
       float g = (p - (c == l ? 1.f : 0.f)) * inv_n;     // g * (p - onehot) / n, g = 1
       if (relu_input) g = g * (zc > 0.f ? 1.f : 0.f);   // relu bwd (tensor.py:236)
@@ -131,7 +131,7 @@ __global__ void ewise_kernel(int op, int64_t rows, int64_t cols, const float* a,
       case 4: y = x >= w ? x : w; break;
       case 5: y = __fdiv_rn(1.0f, __fadd_rn(1.0f, expf(-x))); break;
       case 6: y = tanhf(x); break;
-      case 7: y = fmaxf(x, 0.f); break;
+      case 7: y = sg::relu_np(x); break;
       case 8: y = __fmul_rn(x, w > 0.f ? 1.f : 0.f); break;  // relu bwd: g * (z > 0)
       default: y = __fmul_rn(__fmul_rn(x, w), __fsub_rn(1.0f, w)); break;  // sigmoid bwd g*y*(1-y)
     }

@@ -51,6 +51,40 @@ class _Layer:
     pass
 
 
+def lower_programs(programs, reorder=False):
+    """hoist + fuse + validate each LayerProgram and pick its kernel lowering (host only,
+    no device work): fused gather kind (gcn / pass / ggcn / max / max_pool) and
+    ApplyVertex form.  Raises ProgramError for programs the executor cannot run
+    exactly as written (instead of running a different model)."""
+    layers = []
+    for p in programs:
+        q, reports = prog.optimize(p, reorder=reorder)
+        diags = prog.validate_program(q)
+        if diags:
+            raise ProgramError("; ".join(diags))
+        if q.fused is None or q.fused.kind not in ("gcn", "pass", "ggcn", "max", "max_pool"):
+            raise ProgramError(f"layer ApplyEdge {p.apply_edge!r} has no fused kernel "
+                               f"({reports[-1].blocker or (q.fused and q.fused.kind)})")
+        form = prog.vertex_form(q)
+        if form is None or form[0] not in ("w", "hc"):
+            raise ProgramError("ApplyVertex must be ReLU(W accum) or ReLU(W_H vertex + "
+                               "W_C accum) for the fused executor"
+                               + (" (GRU ApplyVertex: use ggnn.GGNNModel)"
+                                  if form is not None else ""))
+        if form[0] == "hc" and q.fused.kind not in ("gcn", "pass"):
+            raise ProgramError("ReLU(W_H vertex + W_C accum) is lowered for sum gathers only")
+        L = _Layer()
+        L.prog, L.kind, L.F, L.O = q, q.fused.kind, q.f_in, q.f_out
+        L.vform, L.wname = form[0], form[1:]
+        L.gate = q.fused.params
+        # reorder_linear_gather: Y = h W per vertex, then propagate Y (width O)
+        L.reorder = bool(getattr(q, "reorder", False))
+        # accumulator width: the pooled width for MP-GCN, else the input width
+        L.Aw = q.params[L.gate[0]][1] if L.kind == "max_pool" else q.f_in
+        layers.append(L)
+    return layers
+
+
 class SAGAModel:
     """An L-layer SAGA-NN model bound to a ChunkGrid and executed by libsagann kernels.
 
@@ -69,33 +103,9 @@ class SAGAModel:
         self.V = grid.V
         self.gemm_prec = gemm_prec
         self.ws = K.Workspace(self.device)
-        self.layers = []
-        dims = []
         self.reorder = bool(reorder)
-        for p in programs:
-            q, reports = prog.optimize(p, reorder=self.reorder)
-            diags = prog.validate_program(q)
-            if diags:
-                raise ProgramError("; ".join(diags))
-            if q.fused is None or q.fused.kind not in ("gcn", "pass", "ggcn", "max", "max_pool"):
-                raise ProgramError(f"layer ApplyEdge {p.apply_edge!r} has no fused kernel "
-                                   f"({reports[-1].blocker or (q.fused and q.fused.kind)})")
-            form = prog.vertex_form(q)
-            if form is None:
-                raise ProgramError("ApplyVertex must be ReLU(W accum) or ReLU(W_H vertex + "
-                                   "W_C accum) for the fused executor")
-            if form[0] == "hc" and q.fused.kind not in ("gcn", "pass"):
-                raise ProgramError("ReLU(W_H vertex + W_C accum) is lowered for sum gathers only")
-            L = _Layer()
-            L.prog, L.kind, L.F, L.O = q, q.fused.kind, q.f_in, q.f_out
-            L.vform, L.wname = form[0], form[1:]
-            L.gate = q.fused.params
-            # reorder_linear_gather: Y = h W per vertex, then propagate Y (width O)
-            L.reorder = bool(getattr(q, "reorder", False))
-            # accumulator width: the pooled width for MP-GCN, else the input width
-            L.Aw = q.params[L.gate[0]][1] if L.kind == "max_pool" else q.f_in
-            self.layers.append(L)
-            dims.append((q.f_in, q.f_out))
+        self.layers = lower_programs(programs, self.reorder)
+        dims = [(L.F, L.O) for L in self.layers]
         for a, b in zip(dims, dims[1:]):
             if a[1] != b[0]:
                 raise ShapeError(f"layer widths do not chain: {a} -> {b}")
@@ -283,8 +293,10 @@ class SAGAModel:
                 cs.wait_event(self._done[tgt])  # the last step that read this buffer is done
         else:
             tgt, dst = None, self._stage_X
-            if self._consumed is not None:
-                cs.wait_event(self._consumed)  # previous staging buffer already moved into place
+        if self._consumed is not None:
+            # the previous staged labels (single _stage_y buffer, both modes) and features
+            # (single-graph mode) have been moved into place
+            cs.wait_event(self._consumed)
         with torch.cuda.stream(cs):
             if X_host.is_contiguous() and tuple(X_host.shape) == tuple(dst._base.shape):
                 dst._base.copy_(X_host, non_blocking=True)

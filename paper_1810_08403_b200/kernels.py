@@ -11,6 +11,7 @@ import torch
 
 from . import _lib
 from ._lib import check, lib, stream_handle, tptr
+from .errors import ShapeError
 
 _DT = {torch.float32: _lib.SG_F32, torch.bfloat16: _lib.SG_BF16}
 
@@ -94,7 +95,6 @@ def gemm(A, B, C, *, trans_a=False, trans_b=False, relu_out=None, prec=_lib.GEMM
     N = B.shape[0] if trans_b else B.shape[1]
     Kb = B.shape[1] if trans_b else B.shape[0]
     if K != Kb:
-        from .errors import ShapeError
 
         raise ShapeError(f"matmul inner extents differ: {K} vs {Kb}")
     wsb = int(lib.sg_gemm_workspace_bytes(M, N, K, prec))
@@ -120,10 +120,18 @@ def _max_ws(pi, F, ws, device):
     return ws.get(nb) if ws is not None else torch.empty(max(nb, 256), dtype=torch.uint8, device=device)
 
 
+def _check_pos_range(pi, pos_base):
+    """Max-gather positions are int32 with -1 = empty (segment.cu): refuse a pass whose
+    global positions pos_base .. pos_base + nnz would wrap (graphs with >= 2^31 edges)."""
+    if int(pos_base) < 0 or int(pos_base) + int(getattr(pi, "nnz", 0)) > 2**31 - 1:
+        raise ShapeError(f"max gather positions {pos_base} + {getattr(pi, 'nnz', 0)} exceed int32")
+
+
 def max_gather(pi, Y, out, arg, F, empty_fill=0.0, *, pos_base=0, accumulate=False, finalize=True,
                stream=None, ws=None):
     """Fused Gather(max) over CSC pass index ``pi`` (argmax = pos_base + CSC position, int32).
     Passes with split rows (hubs) run the plan-driven kernel (bit-identical result)."""
+    _check_pos_range(pi, pos_base)
     if getattr(pi, "n_splits", 0) > 0:
         buf = _max_ws(pi, F, ws, Y.device)
         check(lib.sg_max_gather_plan(tptr(pi.ptr), tptr(pi.idx), tptr(pi.items), pi.n_items,
@@ -141,6 +149,7 @@ def max_gather_bwd(pi, pos, G, arg, out, F, mask=None, *, pos_base=0, accumulate
                    ws=None):
     """Backward of max_gather over CSR pass index ``pi`` (pos = CSC position per CSR edge).
     Passes with split rows sum a heavy row's subgroups in subgroup order."""
+    _check_pos_range(pi, pos_base)
     if getattr(pi, "n_splits", 0) > 0:
         buf = _max_ws(pi, F, ws, G.device)
         check(lib.sg_max_gather_bwd_plan(tptr(pi.ptr), tptr(pi.idx), tptr(pos), tptr(pi.items), pi.n_items,

@@ -367,8 +367,13 @@ def fuse_sag(p):
                     if t.op == "pre":
                         sides[p.precompute[t.name][0]] = p.precompute[t.name][1]
                 src_e, dst_e = sides.get("src"), sides.get("dest")
-                if src_e is not None and dst_e is not None and _is(src_e, "matmul") and \
-                        _is(dst_e, "matmul") and x.op == "pre" and y.op == "pre" and \
+                # both hoisted sides must be the bare per-vertex matmul `vertex @ param`:
+                # the kernel computes P = h W_H and Q = h W_C and nothing else
+                def bare(t):
+                    return t is not None and _is(t, "matmul") and \
+                        _is(t.args[0], "input", "vertex") and t.args[1].op == "param"
+
+                if bare(src_e) and bare(dst_e) and x.op == "pre" and y.op == "pre" and \
                         p.precompute[x.name][0] == "src":
                     kind = "ggcn"
                     params = (src_e.args[1].name, dst_e.args[1].name)

@@ -118,3 +118,33 @@ def test_ggnn_program_typed_hoist_and_gru():
     with pytest.raises(ProgramError):   # the family is selected by edge.data only
         prog.make_program(lambda e, p: prog.typed_matmul(e.src, e.dest, p.A), lambda v, a, p: a, "sum",
                           {"A": (2, 4, 4)}, 4, 4)
+
+
+def test_ggcn_fusion_requires_bare_vertex_matmuls():
+    """a gate over non-bare hoisted sides (relu(src) @ W_H, (dest*dest) @ W_C)
+    must not fuse as G-GCN (the kernel computes P = h W_H, Q = h W_C only)."""
+    p = sg.make_program(
+        lambda e, p: P.sigmoid(P.relu(e.src) @ p.W_H + (e.dest * e.dest) @ p.W_C) * e.src,
+        lambda v, acc, p: P.relu(acc @ p.W), "sum",
+        {"W_H": (4, 4), "W_C": (4, 4), "W": (4, 3)}, 4, 3)
+    q, _ = sg.optimize(p)
+    assert q.fused is None or q.fused.kind != "ggcn"
+    from paper_1810_08403_b200.engine import lower_programs
+    with pytest.raises(ProgramError):
+        lower_programs([p])
+    # the real G-GCN still fuses
+    assert lower_programs([sg.build_ggcn(4, 3)])[0].kind == "ggcn"
+
+
+def test_gru_apply_vertex_rejected_by_fused_executor():
+    """ApplyEdge = e.src with a GRU ApplyVertex must raise, not run ReLU(accum W)."""
+    from paper_1810_08403_b200.engine import lower_programs
+    f = 4
+    names = ["Wz", "Uz", "Wr", "Ur", "Wh", "Uh"]
+    p = sg.make_program(lambda e, p: e.src,
+                        lambda v, acc, p: P.gru(v, acc, *[getattr(p, n) for n in names]),
+                        "sum", {n: (f, f) for n in names}, f, f)
+    with pytest.raises(ProgramError, match="GRU"):
+        lower_programs([p])
+    assert [L.kind for L in lower_programs([sg.build_gcn(4, 3), sg.build_commnet(3, 3)])] == \
+        ["gcn", "pass"]
