@@ -52,8 +52,7 @@ CONFIGS = {
 }
 # bounded CPU samples: ~3-6 s per oracle epoch on one host core (propagation is
 # single-threaded numpy), so --impl reference with the default K/W ends in ~1-2 minutes
-CPU_SAMPLE_EDGES = {"reddit": 150_000, "pubmed": 88_648, "blogcatalog10": 50_000,
-                    "powerlaw_gcn": 300_000, "powerlaw_ggcn": 60_000}
+CPU_SAMPLE_EDGES = {"blogcatalog10": 50_000, "powerlaw_ggcn": 60_000}
 METRIC = "GCN epoch throughput (whole-graph edges per second of 2-layer fwd+bwd epoch)"
 
 
@@ -73,6 +72,9 @@ def parse():
                     help="skip the secondary reorder_linear_gather measurement")
     ap.add_argument("--engine", choices=["auto", "dist"], default="auto",
                     help="dist: run the sharded multi-GPU engine (NCCL) even at N=1")
+    ap.add_argument("--no-bf16", action="store_true", help="skip the secondary bf16-storage epoch")
+    ap.add_argument("--no-noreuse", action="store_true",
+                    help="skip the no-reuse (uniform graph, X >> L2) gather point of the roofline")
     return ap.parse_args()
 
 
@@ -96,9 +98,100 @@ def gcn_pass_bytes(V, E, F, s=4):
 
 
 # ---------------------------------------------------------------- CPU reference arm
+# the reference's CPU path (the oracle restatement of tensor.py's composition)
+# timed on a fixed subset of destination intervals and extrapolated linearly by edge count.
+# The vertex set is cut into CPU_INTERVALS intervals; every CPU_STRIDE-th one (offset
+# CPU_OFFSET) is sampled, so the sample keeps the graph's E/V and degree mix.
+CPU_INTERVALS, CPU_STRIDE, CPU_OFFSET = 1024, 128, 37
+# measured here on the Pubmed config: the port vs the unmodified tensor.py tape (which also
+# computes mul's unused dw and layer-0's unused dX): DESIGN.md §5
+TAPE_VS_PORT = "the unmodified tensor.py tape does extra unused work (mul's dw row-sums, layer-0 dX): " \
+               "7.6x the port's Pubmed epoch (3.36 s vs 0.44 s, SURVEY.md §8(a) a3; DESIGN.md §5)"
+
+
+def cpu_threads():
+    for k in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS"):
+        if os.environ.get(k):
+            return int(os.environ[k])
+    return os.cpu_count() or 1
+
+
+def _sampled_vertices(V):
+    size = -(-V // CPU_INTERVALS)
+    keep = np.zeros(V, bool)
+    for k in range(CPU_OFFSET % CPU_STRIDE, CPU_INTERVALS, CPU_STRIDE):
+        keep[k * size: (k + 1) * size] = True
+    return keep
+
+
+def cpu_inputs(cfg):
+    """The bench's graph and inputs (the native host generators, pinned equal to the oracle's
+    numpy generators by tests/test_host_graph.py; only input synthesis, not the path)."""
+    import paper_1810_08403_b200 as sg
+
+    V = cfg["V"]
+    g = (sg.rmat_graph if cfg["graph"] == "rmat" else sg.uniform_graph)(V, cfg["E"], seed=0)
+    X = sg.synthetic_features(V, cfg["F"], seed=1)
+    return g.src, g.dst, X
+
+
+def cpu_gcn_epoch_sampled(cfg, src, dst, X, dtype):
+    """One 2-layer GCN epoch of the oracle port (oracle/saga.py, tensor.py's arithmetic) timed
+    per stage on the sampled destination intervals and extrapolated by edge count (gathers) /
+    timed in full (ApplyVertex GEMMs, loss: dense, multi-threaded OpenBLAS).
+
+    Returns (estimated full-epoch seconds, seconds actually spent, sample description)."""
+    from oracle import graph as og
+    from oracle import primitives as prim
+    from oracle import rng
+    from oracle import saga
+
+    V, E, F, H, C = cfg["V"], cfg["E"], cfg["F"], cfg["H"], cfg["C"]
+    keep = _sampled_vertices(V)
+    w = og.gcn_edge_weights(src, dst, V, dtype)
+    fw = np.nonzero(keep[dst])[0]           # in-edges of the sampled destinations (CSC passes)
+    bw = np.nonzero(keep[src])[0]           # out-edges of the sampled sources (CSR pass)
+    part_f = og.partition_2d(src[fw], dst[fw], V, V)
+    part_b = og.partition_2d(src[bw], dst[bw], V, V)
+    Ws = [x.astype(dtype) for x in rng.glorot([(F, H), (H, C)], seed=2)]
+    lab = rng.labels(V, C, seed=3)
+    Xd = X[:, :F].astype(dtype)
+    h1 = prim.relu(np.random.default_rng(5).uniform(-1, 1, (V, H)).astype(dtype))
+    t_all = time.perf_counter()
+    t = {}
+    t0 = time.perf_counter()
+    a0 = saga.gcn_propagate_fwd(part_f, Xd, w[fw])                      # L0 forward gather
+    t["L0.fwd.propagate"] = (time.perf_counter() - t0) * E / max(len(fw), 1)
+    t0 = time.perf_counter()
+    saga.gcn_propagate_fwd(part_f, h1, w[fw])                           # L1 forward gather
+    t["L1.fwd.propagate"] = (time.perf_counter() - t0) * E / max(len(fw), 1)
+    t0 = time.perf_counter()
+    saga.gcn_propagate_bwd(part_b, h1, w[bw])                           # L1 backward (CSR)
+    t["L1.bwd.propagate"] = (time.perf_counter() - t0) * E / max(len(bw), 1)
+    # dense stages on the whole vertex set (timed in full, not extrapolated)
+    t0 = time.perf_counter()
+    a0 = a0 + Xd                           # a dense [V, F] operand (values irrelevant to cost)
+    z0 = prim.matmul(a0, Ws[0])
+    h = prim.relu(z0)
+    z1 = prim.matmul(h, Ws[1])             # h stands in for a1 = A h1 (same shape and cost)
+    loss, p = prim.softmax_cross_entropy(prim.relu(z1), lab)
+    g = prim.softmax_cross_entropy_bwd(np.asarray(1.0, dtype), p, lab)
+    gz1 = prim.relu_bwd(g, z1)
+    ga1, _ = prim.matmul_bwd(gz1, h, Ws[1])
+    gz0 = prim.relu_bwd(ga1, z0)          # (the CSR pass between them is timed above)
+    prim.matmul_bwd(gz0, a0, Ws[0])
+    t["dense (ApplyVertex GEMMs, ReLU, softmax-CE)"] = time.perf_counter() - t0
+    spent = time.perf_counter() - t_all
+    desc = (f"{int(keep.sum())} of {V} destination vertices ({CPU_INTERVALS // CPU_STRIDE} of "
+            f"{CPU_INTERVALS} intervals, every {CPU_STRIDE}th): {len(fw)} in-edges (CSC passes), "
+            f"{len(bw)} out-edges (CSR pass), gathers extrapolated by edge count, dense stages "
+            f"on all V; numpy oracle port of tensor.py ({np.dtype(dtype).name})")
+    return sum(t.values()), spent, desc, t
+
+
 def cpu_sample(cfg, n_edges, use_native_inputs):
-    """Bounded sample: the first n_edges edges of the same R-MAT/uniform stream over all V
-    vertices, full F/H/C widths; per-epoch cost scales with edges."""
+    """Bounded prefix sample for the G-GCN configs: the first n_edges edges of the same stream
+    over all V vertices, full widths; per-epoch cost scales with edges."""
     from oracle import graph as og
     from oracle import rng
 
@@ -113,59 +206,52 @@ def cpu_sample(cfg, n_edges, use_native_inputs):
         X = rng.features(V, cfg["F"], seed=1)
     part = og.partition_2d(s, d, V, V)
     dims = [cfg["F"], cfg["H"], cfg["C"]]
+    shapes = []
+    for a, b in zip(dims, dims[1:]):
+        shapes += [(a, a), (a, a), (a, b)]
+    Ls = rng.glorot(shapes, seed=2)
+    return (part, X, [tuple(Ls[3 * k: 3 * k + 3]) for k in range(2)], rng.labels(V, cfg["C"]))
+
+
+def cpu_epoch_estimate(cfg, dtype=np.float32, n_edges=None, inputs=None, name="blogcatalog10"):
+    """(edges/s of the reference CPU path, seconds spent, sample description, stage times)."""
     if cfg["model"] == "gcn":
-        Ws = rng.glorot(list(zip(dims, dims[1:])), seed=2)
-        w = og.gcn_edge_weights(s, d, V, np.float32)
-        args = (part, X, Ws, rng.labels(V, cfg["C"]), w)
-    else:
-        shapes = []
-        for a, b in zip(dims, dims[1:]):
-            shapes += [(a, a), (a, a), (a, b)]
-        Ls = rng.glorot(shapes, seed=2)
-        args = (part, X, [tuple(Ls[3 * k: 3 * k + 3]) for k in range(2)], rng.labels(V, cfg["C"]))
-    return args
-
-
-def cpu_epoch(cfg, args):
+        src, dst, X = inputs if inputs is not None else cpu_inputs(cfg)
+        est, spent, desc, st = cpu_gcn_epoch_sampled(cfg, src, dst, X, dtype)
+        return cfg["E"] / est, spent, desc, st
     from oracle import saga
 
+    n = n_edges or CPU_SAMPLE_EDGES[name]
+    part, X, layers, lab = cpu_sample(cfg, n, use_native_inputs=True)
+    X = X.astype(dtype)
+    layers = [tuple(x.astype(dtype) for x in L) for L in layers]
     t0 = time.perf_counter()
-    if cfg["model"] == "gcn":
-        saga.gcn_epoch(*args)
-    else:
-        saga.ggcn_epoch(*args)
-    return time.perf_counter() - t0
-
-
-def cpu_threads():
-    for k in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS"):
-        if os.environ.get(k):
-            return int(os.environ[k])
-    return os.cpu_count() or 1
+    saga.ggcn_epoch(part, X, layers, lab)
+    t = time.perf_counter() - t0
+    return n / t, t, (f"one epoch on the first {n} edges of the same edge stream over all "
+                      f"{cfg['V']} vertices ({np.dtype(dtype).name})"), {}
 
 
 def run_reference(a, cfg):
     rank, _, world = dist_env()
     if rank != 0:
         return  # under torchrun only rank 0 runs and prints
-    n = a.cpu_sample_edges or CPU_SAMPLE_EDGES[a.config]
-    args = cpu_sample(cfg, n, use_native_inputs=False)
+    inputs = cpu_inputs(cfg) if cfg["model"] == "gcn" else None
     for _ in range(a.warmup):
-        cpu_epoch(cfg, args)
-    times = [cpu_epoch(cfg, args) for _ in range(a.steps)]
-    t = float(np.mean(times))
-    v = n / t
+        cpu_epoch_estimate(cfg, np.float32, a.cpu_sample_edges, inputs, a.config)
+    runs = [cpu_epoch_estimate(cfg, np.float32, a.cpu_sample_edges, inputs, a.config) for _ in range(a.steps)]
+    v = float(np.mean([r[0] for r in runs]))
     cores = cpu_threads()
-    sample = (f"first {n} edges of the {cfg['graph']} edge stream over all {cfg['V']} vertices "
-              f"(F={cfg['F']}, H={cfg['H']}, C={cfg['C']}); numpy oracle port of tensor.py "
-              f"(propagation single-threaded numpy, matmul on {cores} OpenBLAS threads)")
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "edges/s", "n_gpus": world,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": cfg["E"] / v * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic", "config": config_of(cfg, a, world),
         "cpu_baseline": {"value": v, "unit": "edges/s", "cores": cores, "kind": "port",
-                         "sample": sample, "sample_epoch_s": t},
+                         "sample": runs[0][2], "sample_s_per_step": float(np.mean([r[1] for r in runs])),
+                         "nproc": os.cpu_count(), "openblas_threads": os.environ.get("OPENBLAS_NUM_THREADS"),
+                         "propagation_threads": 1, "stages_s_extrapolated": runs[0][3],
+                         "tape_vs_port": TAPE_VS_PORT},
         "e2e": {"value": v, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -228,6 +314,95 @@ class Clocks:
 
 
 # ---------------------------------------------------------------- GPU arm
+def timed_epochs(m, a, flush):
+    """K flushed epochs of model m (after W warm-ups): (mean ms, {stage: mean ms})."""
+    import torch
+
+    for _ in range(a.warmup):
+        m.train_step(a.lr)
+    torch.cuda.synchronize()
+    m.check_status()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(a.steps)]
+    marks = []
+    for k in range(a.steps):
+        flush.zero_()
+        m.prof = []
+        ev[k][0].record()
+        m.train_step(a.lr)
+        ev[k][1].record()
+        marks.append(m.prof)
+    torch.cuda.synchronize()
+    m.check_status()
+    ms = float(np.mean([s_.elapsed_time(e_) for s_, e_ in ev]))
+    st = {}
+    for mk in marks:
+        m.prof = mk
+        for kname, v in m.stage_times().items():
+            st[kname] = st.get(kname, 0.0) + v / a.steps
+    m.prof = None
+    return ms, st
+
+
+def traffic_record(key, kernel_src="paper_1810_08403_b200/csrc/propagate.cu"):
+    """ncu DRAM bytes per launch for `key` from profiles/ncu_dram_bytes.json, and whether the
+    record was taken on the kernel source that is benched now (sha256 of the .cu file)."""
+    import hashlib
+
+    path = os.path.join(ROOT, "profiles", "ncu_dram_bytes.json")
+    if not os.path.exists(path):
+        return None, None
+    try:
+        rec = json.load(open(path))
+    except Exception:
+        return None, None
+    src = os.path.join(ROOT, kernel_src)
+    cur = hashlib.sha256(open(src, "rb").read()).hexdigest()[:16] if os.path.exists(src) else None
+    val = rec.get("records", {}).get(key)
+    return val, (rec.get("kernel_source_sha256") == cur) if cur else None
+
+
+def noreuse_point(a, cfg, flush, peak):
+    """The same layer-1 fused gather on a UNIFORM graph of the bench's V, E, F: every edge reads a
+    random 2.4-KB row of a 563-MB X (>> the 126-MB L2), so the algorithmic bytes ~ the DRAM
+    bytes and the fraction of HBM is not inflated by R-MAT's reuse (SURVEY.md §8(d) caveat)."""
+    import torch
+
+    import paper_1810_08403_b200 as sg
+    from paper_1810_08403_b200 import _lib
+    from paper_1810_08403_b200 import kernels as K
+
+    V, E, F = cfg["V"], cfg["E"], cfg["F"]
+    gu = sg.uniform_graph(V, E, seed=0)
+    grid = sg.ChunkGrid(gu, V, split_edges=a.split_edges)
+    ld = (F + 3) // 4 * 4
+    X = torch.from_numpy(sg.synthetic_features(V, F, seed=1, ld=ld)).cuda()[:, :F]
+    out = torch.zeros_like(X)
+    pi = grid.csc[(0, 0)]
+    for _ in range(a.warmup):
+        K.propagate(pi, _lib.PROP_GCN, X, out, F)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(a.steps)]
+    torch.cuda.synchronize()
+    for k in range(a.steps):
+        flush.zero_()
+        ev[k][0].record()
+        K.propagate(pi, _lib.PROP_GCN, X, out, F)
+        ev[k][1].record()
+    torch.cuda.synchronize()
+    ms = float(np.mean([s_.elapsed_time(e_) for s_, e_ in ev]))
+    algo = gcn_pass_bytes(V, E, F)
+    achieved = algo / (ms / 1e3) / 1e9
+    traffic, fresh = traffic_record("reddit_uniform.L0.fwd.propagate")
+    del grid, X, out, pi
+    torch.cuda.empty_cache()
+    return {"graph": f"uniform, V={V}, E={E}, F={F} (X = {V * ld * 4 / 1e6:.0f} MB >> L2)",
+            "kernel": "sg_propagate GCN (the same L0 forward pass)", "launch_ms": ms,
+            "algorithmic_bytes_per_launch": algo, "achieved": achieved, "frac": achieved / peak,
+            "traffic": traffic, "traffic_matches_source": fresh,
+            "frac_dram": (traffic / (ms / 1e3) / 1e9 / peak) if traffic else None}
+
+
 def run_ours(a, cfg):
     import torch
 
@@ -317,13 +492,7 @@ def run_ours(a, cfg):
         vals = [json.loads(x)["GBps"] for x in open(probe) if x.startswith("{") and
                 '"buffer_MB": 48,' in x and '"row_bytes": 2432' in x]
         l2_ceiling = max(vals) if vals else None
-    traffic = None
-    prof_json = os.path.join(ROOT, "profiles", "ncu_dram_bytes.json")
-    if os.path.exists(prof_json):
-        try:
-            traffic = json.load(open(prof_json)).get(a.config, {}).get("L0.fwd.propagate")
-        except Exception:
-            traffic = None
+    traffic, traffic_fresh = traffic_record(f"{a.config}.L0.fwd.propagate")
 
     # ---- e2e through the public API with host buffers (H2D features+labels, D2H loss)
     e2e = None
@@ -362,27 +531,7 @@ def run_ours(a, cfg):
         m2 = build(grid, [F, H, C], reorder=True)
         m2.load_features(X_host)
         m2.load_labels(lab_host)
-        for _ in range(a.warmup):
-            m2.train_step(a.lr)
-        torch.cuda.synchronize()
-        m2.check_status()
-        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-              for _ in range(a.steps)]
-        marks2 = []
-        for k in range(a.steps):
-            flush.zero_()
-            m2.prof = []
-            ev[k][0].record()
-            m2.train_step(a.lr)
-            ev[k][1].record()
-            marks2.append(m2.prof)
-        torch.cuda.synchronize()
-        ms2 = float(np.mean([s_.elapsed_time(e_) for s_, e_ in ev]))
-        st2 = {}
-        for mk in marks2:
-            m2.prof = mk
-            for kname, v in m2.stage_times().items():
-                st2[kname] = st2.get(kname, 0.0) + v / a.steps
+        ms2, st2 = timed_epochs(m2, a, flush)
         reordered = {"ms_per_step": ms2, "value": E / (ms2 / 1e3), "unit": "edges/s",
                      "layers_reordered": [bool(L.reorder) for L in m2.layers],
                      "stages_ms": {k: round(v, 4) for k, v in st2.items()},
@@ -391,16 +540,41 @@ def run_ours(a, cfg):
                              "order (tests/test_gpu_kernels.py::test_reordered_gcn_epoch_vs_oracle)"}
         del m2
 
-    # ---- CPU baseline (oracle port) on a bounded sample, rank 0 only
+    # ---- secondary: bf16 storage (features / aggregates / activations / their gradients in
+    # bf16, fp32 accumulation, tcgen05 kind::f16 ApplyVertex); reported beside the fp32 headline
+    bf16 = None
+    if cfg["model"] == "gcn" and not a.no_bf16:
+        m3 = build(grid, [F, H, C], dtype="bf16")
+        m3.load_features(X_host)
+        m3.load_labels(lab_host)
+        ms3, st3 = timed_epochs(m3, a, flush)
+        k3 = st3.get("L0.fwd.propagate")
+        algo3 = gcn_pass_bytes(V, E, F, s=2)
+        bf16 = {"ms_per_step": ms3, "value": E / (ms3 / 1e3), "unit": "edges/s", "dtype": "bf16",
+                "stages_ms": {k: round(v, 4) for k, v in st3.items()},
+                "L0_gather_achieved_gbs": algo3 / (k3 / 1e3) / 1e9 if k3 else None,
+                "tolerance": "bf16 bar (SURVEY.md §8(c)): normwise 1e-2, elementwise 2e-2|ref| + 1e-3 max|ref| "
+                             "vs the fp64 oracle (tests/test_gpu_bf16.py::"
+                             "test_bf16_gcn_epoch_reddit_config_vs_fp64_fixture)"}
+        del m3
+
+    noreuse = None
+    if cfg["name"] == "reddit" and not a.no_noreuse:
+        noreuse = noreuse_point(a, cfg, flush, peak)
+
+    # ---- CPU baseline (oracle port of the reference path) on a bounded sample, rank 0 only
     cpu = None
     if not a.no_cpu_baseline and rank == 0:
-        n = a.cpu_sample_edges or CPU_SAMPLE_EDGES[a.config]
-        args = cpu_sample(cfg, n, use_native_inputs=True)
-        t = cpu_epoch(cfg, args)
-        cpu = {"value": n / t, "unit": "edges/s", "cores": cpu_threads(), "kind": "port",
-               "sample": f"one epoch on the first {n} edges of the same edge stream over all "
-                         f"{V} vertices (numpy oracle port of tensor.py); {t:.1f} s",
-               "extrapolated_epoch_ms": E / (n / t) * 1e3}
+        inputs = (g.src, g.dst, X_host.numpy()) if cfg["model"] == "gcn" else None
+        v32, t32, desc, st32 = cpu_epoch_estimate(cfg, np.float32, a.cpu_sample_edges, inputs, a.config)
+        v64, t64, _, _ = cpu_epoch_estimate(cfg, np.float64, a.cpu_sample_edges, inputs, a.config)
+        cpu = {"value": v32, "unit": "edges/s", "cores": cpu_threads(), "kind": "port",
+               "sample": desc, "sample_s": round(t32, 2),
+               "fp64": {"value": v64, "sample_s": round(t64, 2)},
+               "nproc": os.cpu_count(), "openblas_threads": os.environ.get("OPENBLAS_NUM_THREADS"),
+               "propagation_threads": 1,
+               "extrapolated_epoch_ms": E / v32 * 1e3, "stages_s_extrapolated": st32,
+               "tape_vs_port": TAPE_VS_PORT}
 
     line = {
         "metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": world, "steps": a.steps,
@@ -409,14 +583,19 @@ def run_ours(a, cfg):
         "config": config_of(cfg, a, world),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                     "frac_dram": (traffic / (k_ms / 1e3) / 1e9 / peak) if (traffic and k_ms) else None,
+                     "traffic_matches_source": traffic_fresh,
+                     "no_reuse": noreuse,
                      "kernel": "L0.fwd.propagate (sg_propagate %s, F=%d)" % (
                          "GCN" if cfg["model"] == "gcn" else "GGCN_FWD_S", F),
                      "algorithmic_bytes_per_launch": algo, "launch_ms": k_ms, "peak_source": peak_src,
-                     "note": "frac > 1: the algorithmic bytes count one source row per edge, but "
-                             "R-MAT's hot rows are re-served from L1/L2 (canonical CSC: sources "
-                             "ascending within a destination); DRAM bytes per launch are in "
-                             "'traffic' (ncu); l2_ceiling_gbs = measured L2->SM ceiling for random "
-                             "2.4-KB row gathers (tools/l2bw.cu)",
+                     "note": "frac = algorithmic bytes (one source row per edge) / launch time: an "
+                             "effective rate, > 1 because R-MAT's hot rows are re-served from L1/L2; "
+                             "frac_dram = ncu DRAM bytes of the same kernel ('traffic', "
+                             "profiles/ncu_dram_bytes.json, taken on this kernel source when "
+                             "traffic_matches_source) / launch time; no_reuse = the same pass on a "
+                             "uniform graph (X >> L2), where the HBM gate is judged; l2_ceiling_gbs = "
+                             "measured L2->SM ceiling for random 2.4-KB row gathers (tools/l2bw.cu)",
                      "share_of_step": (k_ms / (t_step * 1e3)) if k_ms else None,
                      "launch_list": "profiles/r01_launches_bench_steps.txt (ncu share of the same "
                                     "kernel over 5 epochs of this workload)",
@@ -425,6 +604,7 @@ def run_ours(a, cfg):
         "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": int(launches),
         "ms_per_step_back_to_back": back_to_back_ms,
         "reordered_apply_vertex": reordered,
+        "bf16": bf16,
         "clocks": clk,
         "stages_ms": {k: round(v, 4) for k, v in stages.items()},
         "scatter_gather_edges_per_s": (E / (k_ms / 1e3)) if k_ms else None,
@@ -434,9 +614,25 @@ def run_ours(a, cfg):
     print(json.dumps(line), flush=True)
 
 
+def self_launch(a):
+    """``python bench.py --gpus N`` without torchrun: re-launch this command as N ranks
+    (torch.distributed.run, rendezvous on 127.0.0.1) and pass its output through; under
+    torchrun (WORLD_SIZE set) this is a no-op."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     a = parse()
-    cfg = CONFIGS[a.config]
+    cfg = dict(CONFIGS[a.config], name=a.config)
+    if "WORLD_SIZE" not in os.environ and a.gpus > 1:
+        raise SystemExit(self_launch(a))
     if a.gpus != dist_env()[2]:
         raise SystemExit(f"--gpus {a.gpus} but WORLD_SIZE={dist_env()[2]}: launch N > 1 ranks with "
                          f"python -m torch.distributed.run --nproc-per-node {a.gpus} bench.py --gpus {a.gpus}")

@@ -233,12 +233,41 @@ int sg_segment_sort(const int64_t* seg, int64_t n, int64_t n_seg, int64_t* ptr, 
  * row-major; trans_a: A is stored [K,M]; trans_b: B is stored [N,K].  Epilogue
  * RELU_DUAL also writes D = relu(C) (tensor.py:207).  Split-K reductions are
  * deterministic (fixed order).  prec: SG_GEMM_F32 (SIMT fp32), SG_GEMM_TF32X3
- * (tcgen05 tensor cores, TMEM accumulators).  SG_GEMM_BF16 is reserved: not implemented,
- * returns SG_EINVAL. */
+ * (tcgen05 kind::tf32, 3xTF32 split, TMEM accumulators), SG_GEMM_BF16 (tcgen05
+ * kind::f16 on bf16 operands, fp32 TMEM accumulation; through sg_gemm the A/B pointers
+ * are bf16 and C/D fp32 -- use sg_gemm_ex for bf16 outputs). */
 int64_t sg_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K, int prec);
 int sg_gemm(int prec, int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, const float* A,
             int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc, int epilogue,
             float* D, int64_t ldd, void* workspace, int64_t workspace_bytes, void* stream);
+
+/* The general form of sg_gemm (same operation and precisions):
+ *   A, B      : fp32 for F32 / TF32X3, bf16 (SG_BF16) for SG_GEMM_BF16 (bf16 rows need
+ *               ld % 8 == 0 and 16-B aligned bases: the TMA tensor-map constraints);
+ *   C, c_dtype: output (fp32 or bf16); may be NULL when epilogue == RELU_DUAL (only D);
+ *   D, d_dtype: D = relu(C) (np.maximum semantics: NaN propagates), fp32 or bf16;
+ *   nonfinite : optional device flag, |= 1 if any element of C is non-finite (the
+ *               strict-mode check of tensor.py:161-163 fused into the epilogue).
+ * bf16 outputs are rounded once from the fp32 accumulator (round to nearest even).
+ * Split-K (long K) needs fp32 outputs. */
+typedef struct sg_gemm_desc {
+  int prec, trans_a, trans_b, epilogue;
+  int64_t M, N, K;
+  const void* A;
+  int64_t lda;
+  const void* B;
+  int64_t ldb;
+  void* C;
+  int64_t ldc;
+  int c_dtype;
+  void* D;
+  int64_t ldd;
+  int d_dtype;
+  int32_t* nonfinite;
+  void* workspace;
+  int64_t workspace_bytes;
+} sg_gemm_desc;
+int sg_gemm_ex(const sg_gemm_desc* desc, void* stream);
 
 /* Softmax cross-entropy head (tensor.py:487-506) on logits = relu(Z) when
  * relu_input (the last layer's ReLU) else Z, over n local rows:

@@ -36,7 +36,19 @@ _i64, _i32, _f64, _f32 = ctypes.c_int64, ctypes.c_int, ctypes.c_double, ctypes.c
 _u64, _p = ctypes.c_uint64, ctypes.c_void_p
 _s = ctypes.c_char_p
 
+class GemmDesc(ctypes.Structure):
+    """sg_gemm_desc (include/sagann.h)."""
+    _fields_ = [("prec", ctypes.c_int), ("trans_a", ctypes.c_int), ("trans_b", ctypes.c_int),
+                ("epilogue", ctypes.c_int), ("M", ctypes.c_int64), ("N", ctypes.c_int64),
+                ("K", ctypes.c_int64), ("A", ctypes.c_void_p), ("lda", ctypes.c_int64),
+                ("B", ctypes.c_void_p), ("ldb", ctypes.c_int64), ("C", ctypes.c_void_p),
+                ("ldc", ctypes.c_int64), ("c_dtype", ctypes.c_int), ("D", ctypes.c_void_p),
+                ("ldd", ctypes.c_int64), ("d_dtype", ctypes.c_int), ("nonfinite", ctypes.c_void_p),
+                ("workspace", ctypes.c_void_p), ("workspace_bytes", ctypes.c_int64)]
+
+
 _SIGS = {
+    "sg_gemm_ex": (ctypes.c_int, [ctypes.POINTER(GemmDesc), ctypes.c_void_p]),
     "sg_last_error": (ctypes.c_char_p, []),
     "sg_version": (_i32, []),
     "sg_device_sm_count": (_i32, [_i32, _p]),

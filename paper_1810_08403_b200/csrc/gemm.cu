@@ -26,6 +26,7 @@ struct GemmArgs {
   int64_t k_chunk;
   int trans_a, trans_b, epilogue;
   float* partial;  // [splits][M][N] when split-K
+  int32_t* nonfinite;
 };
 
 __device__ __forceinline__ float ldA(const GemmArgs& p, int64_t m, int64_t k) {
@@ -128,13 +129,15 @@ __global__ void __launch_bounds__(NTHR) sgemm_kernel(const GemmArgs p) {
       } else {
         p.C[m * p.ldc + n] = v;
         if (p.epilogue == SG_EPI_RELU_DUAL) p.D[m * p.ldd + n] = sg::relu_np(v);
+        if (p.nonfinite && !isfinite(v)) atomicOr(p.nonfinite, 1);
       }
     }
   }
 }
 
 __global__ void splitk_reduce_kernel(const float* partial, int splits, int64_t M, int64_t N,
-                                     float* C, int64_t ldc, float* D, int64_t ldd, int epilogue) {
+                                     float* C, int64_t ldc, float* D, int64_t ldd, int epilogue,
+                                     int32_t* nonfinite) {
   const int64_t total = M * N;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
@@ -143,6 +146,7 @@ __global__ void splitk_reduce_kernel(const float* partial, int splits, int64_t M
     const int64_t m = t / N, n = t % N;
     C[m * ldc + n] = s;
     if (epilogue == SG_EPI_RELU_DUAL) D[m * ldd + n] = sg::relu_np(s);
+    if (nonfinite && !isfinite(s)) atomicOr(nonfinite, 1);
   }
 }
 
@@ -159,12 +163,25 @@ int choose_splits(int64_t M, int64_t N, int64_t K) {
 
 int sg_gemm_tc(int prec, int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, const float* A,
                int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc, int epilogue,
-               float* D, int64_t ldd, void* workspace, int64_t workspace_bytes, cudaStream_t st);
+               float* D, int64_t ldd, int32_t* nonfinite, void* workspace, int64_t workspace_bytes,
+               cudaStream_t st);
 int64_t sg_gemm_tc_workspace_bytes(int64_t M, int64_t N, int64_t K, int prec);
+int64_t sg_gemm_bf16_workspace_bytes(int64_t M, int64_t N, int64_t K);
+int sg_gemm_bf16_run(const sg_gemm_desc* d, cudaStream_t st);
+
+namespace {
+
+// the fp32 paths (SIMT / 3xTF32) behind sg_gemm and sg_gemm_ex
+int gemm_f32(int prec, int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, const float* A,
+             int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc, int epilogue, float* D,
+             int64_t ldd, int32_t* nonfinite, void* workspace, int64_t workspace_bytes, cudaStream_t st);
+
+}  // namespace
 
 extern "C" {
 
 int64_t sg_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K, int prec) {
+  if (prec == SG_GEMM_BF16) return sg_gemm_bf16_workspace_bytes(M, N, K);
   if (prec != SG_GEMM_F32) return sg_gemm_tc_workspace_bytes(M, N, K, prec);
   const int s = choose_splits(M, N, K);
   return s > 1 ? (int64_t)s * M * N * 4 : 0;
@@ -173,13 +190,43 @@ int64_t sg_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K, int prec) {
 int sg_gemm(int prec, int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, const float* A,
             int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc, int epilogue, float* D,
             int64_t ldd, void* workspace, int64_t workspace_bytes, void* stream) {
-  SG_REQUIRE(M >= 0 && N >= 0 && K >= 0, SG_ESHAPE, "gemm: negative extent");
-  SG_REQUIRE(epilogue != SG_EPI_RELU_DUAL || D, SG_EINVAL, "gemm: RELU_DUAL needs D");
-  if (M == 0 || N == 0) return SG_OK;
+  sg_gemm_desc d;
+  d.prec = prec; d.trans_a = trans_a; d.trans_b = trans_b; d.epilogue = epilogue;
+  d.M = M; d.N = N; d.K = K;
+  d.A = A; d.lda = lda; d.B = B; d.ldb = ldb;
+  d.C = C; d.ldc = ldc; d.c_dtype = SG_F32;
+  d.D = D; d.ldd = ldd; d.d_dtype = SG_F32;
+  d.nonfinite = nullptr;
+  d.workspace = workspace; d.workspace_bytes = workspace_bytes;
+  return sg_gemm_ex(&d, stream);
+}
+
+int sg_gemm_ex(const sg_gemm_desc* d, void* stream) {
+  SG_REQUIRE(d, SG_EINVAL, "gemm: null descriptor");
+  SG_REQUIRE(d->M >= 0 && d->N >= 0 && d->K >= 0, SG_ESHAPE, "gemm: negative extent");
+  SG_REQUIRE(d->epilogue != SG_EPI_RELU_DUAL || d->D, SG_EINVAL, "gemm: RELU_DUAL needs D");
+  SG_REQUIRE(d->prec == SG_GEMM_F32 || d->prec == SG_GEMM_TF32X3 || d->prec == SG_GEMM_BF16, SG_EINVAL,
+             "gemm: unknown precision %d", d->prec);
+  if (d->M == 0 || d->N == 0) return SG_OK;
   cudaStream_t st = (cudaStream_t)stream;
+  if (d->prec == SG_GEMM_BF16) return sg_gemm_bf16_run(d, st);
+  SG_REQUIRE(d->c_dtype == SG_F32 && d->d_dtype == SG_F32 && d->C, SG_EINVAL,
+             "gemm: fp32 precisions write fp32 C (and D)");
+  return gemm_f32(d->prec, d->trans_a, d->trans_b, d->M, d->N, d->K, (const float*)d->A, d->lda,
+                  (const float*)d->B, d->ldb, (float*)d->C, d->ldc, d->epilogue, (float*)d->D, d->ldd,
+                  d->nonfinite, d->workspace, d->workspace_bytes, st);
+}
+
+}  // extern "C"
+
+namespace {
+
+int gemm_f32(int prec, int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, const float* A,
+             int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc, int epilogue, float* D,
+             int64_t ldd, int32_t* nonfinite, void* workspace, int64_t workspace_bytes, cudaStream_t st) {
   if (prec != SG_GEMM_F32)
     return sg_gemm_tc(prec, trans_a, trans_b, M, N, K, A, lda, B, ldb, C, ldc, epilogue, D, ldd,
-                      workspace, workspace_bytes, st);
+                      nonfinite, workspace, workspace_bytes, st);
   const int splits = choose_splits(M, N, K);
   GemmArgs p;
   p.A = A; p.B = B; p.C = C; p.D = D;
@@ -187,6 +234,7 @@ int sg_gemm(int prec, int trans_a, int trans_b, int64_t M, int64_t N, int64_t K,
   p.M = M; p.N = N; p.K = K;
   p.trans_a = trans_a; p.trans_b = trans_b; p.epilogue = epilogue;
   p.partial = nullptr;
+  p.nonfinite = nonfinite;
   int64_t kc = (K + splits - 1) / splits;
   kc = (kc + BK - 1) / BK * BK;
   p.k_chunk = std::max<int64_t>(kc, BK);
@@ -195,6 +243,7 @@ int sg_gemm(int prec, int trans_a, int trans_b, int64_t M, int64_t N, int64_t K,
     SG_REQUIRE(workspace && workspace_bytes >= (int64_t)gz * M * N * 4, SG_EBUDGET,
                "gemm split-K workspace too small");
     p.partial = (float*)workspace;
+    p.nonfinite = nullptr;  // checked by the reduction
   }
   dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM), (unsigned)std::max(gz, 1));
   if (K == 0) {
@@ -211,7 +260,7 @@ int sg_gemm(int prec, int trans_a, int trans_b, int64_t M, int64_t N, int64_t K,
   if (gz > 1) {
     const int64_t total = M * N;
     int g = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
-    splitk_reduce_kernel<<<g, 256, 0, st>>>(p.partial, gz, M, N, C, ldc, D, ldd, epilogue);
+    splitk_reduce_kernel<<<g, 256, 0, st>>>(p.partial, gz, M, N, C, ldc, D, ldd, epilogue, nonfinite);
     sg::count_launch();
     e = cudaGetLastError();
     if (e != cudaSuccess) SG_FAIL(SG_ECUDA, "split-k reduce: %s", cudaGetErrorString(e));
@@ -219,4 +268,5 @@ int sg_gemm(int prec, int trans_a, int trans_b, int64_t M, int64_t N, int64_t K,
   return SG_OK;
 }
 
-}  // extern "C"
+}  // namespace
+

@@ -52,6 +52,7 @@ struct TcArgs {
   int kb_per_split, n_kb;
   int epilogue;
   int vec_a, vec_b, vec_c, vec_d;
+  int32_t* nonfinite;  // strict-mode flag (tensor.py:161-163), checked in the epilogue
 };
 
 __device__ __forceinline__ void split_tf32(float4 x, float4& hi, float4& lo) {
@@ -269,6 +270,11 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tf32x3_kernel(const TcArgs p
             for (int q = 0; q < 4; ++q)
               if (col + q < p.N) dst[row * ldo + col + q] = v[j + q];
           }
+          if (!p.partial && p.nonfinite) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              if (col + q < p.N && !isfinite(v[j + q])) atomicOr(p.nonfinite, 1);
+          }
           if (relu) {
             if (p.vec_d && col + 3 < p.N) {
               *reinterpret_cast<float4*>(p.D + row * p.ldd + col) =
@@ -314,7 +320,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tf32x3_kernel(const TcArgs p
 }
 
 __global__ void tc_splitk_reduce(const float* partial, int splits, int64_t M, int64_t N, float* C,
-                                 int64_t ldc, float* D, int64_t ldd, int epilogue) {
+                                 int64_t ldc, float* D, int64_t ldd, int epilogue, int32_t* nonfinite) {
   const int64_t total = M * N;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
@@ -323,6 +329,7 @@ __global__ void tc_splitk_reduce(const float* partial, int splits, int64_t M, in
     const int64_t m = t / N, n = t % N;
     C[m * ldc + n] = s;
     if (epilogue == SG_EPI_RELU_DUAL) D[m * ldd + n] = sg::relu_np(s);
+    if (nonfinite && !isfinite(s)) atomicOr(nonfinite, 1);
   }
 }
 
@@ -361,7 +368,8 @@ cudaError_t dispatch_major(bool a_mn, bool b_mn, const TcArgs& p, dim3 grid, cud
 
 int sg_gemm_tma_try(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,
                     const float* B, int64_t ldb, float* C, int64_t ldc, int epilogue, float* D, int64_t ldd,
-                    float* partial, int kb_per_split, int n_kb, int gz, cudaStream_t st, cudaError_t* err);
+                    int32_t* nonfinite, float* partial, int kb_per_split, int n_kb, int gz, cudaStream_t st,
+                    cudaError_t* err);
 
 int64_t sg_gemm_tc_workspace_bytes(int64_t M, int64_t N, int64_t K, int prec) {
   (void)prec;
@@ -371,7 +379,8 @@ int64_t sg_gemm_tc_workspace_bytes(int64_t M, int64_t N, int64_t K, int prec) {
 
 int sg_gemm_tc(int prec, int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, const float* A,
                int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc, int epilogue,
-               float* D, int64_t ldd, void* workspace, int64_t workspace_bytes, cudaStream_t st) {
+               float* D, int64_t ldd, int32_t* nonfinite, void* workspace, int64_t workspace_bytes,
+               cudaStream_t st) {
   SG_REQUIRE(prec == SG_GEMM_TF32X3, SG_EINVAL, "tensor-core GEMM precision %d not supported", prec);
   if (K == 0) {
     cudaMemset2DAsync(C, ldc * 4, 0, N * 4, M, st);
@@ -385,6 +394,7 @@ int sg_gemm_tc(int prec, int trans_a, int trans_b, int64_t M, int64_t N, int64_t
   p.lda = lda; p.ldb = ldb; p.ldc = ldc; p.ldd = ldd;
   p.M = M; p.N = N; p.K = K;
   p.epilogue = epilogue;
+  p.nonfinite = nonfinite;
   p.vec_a = (lda % 4 == 0) && ((uintptr_t)A % 16 == 0);
   p.vec_b = (ldb % 4 == 0) && ((uintptr_t)B % 16 == 0);
   p.vec_c = (ldc % 4 == 0) && ((uintptr_t)C % 16 == 0);
@@ -404,14 +414,14 @@ int sg_gemm_tc(int prec, int trans_a, int trans_b, int64_t M, int64_t N, int64_t
   cudaError_t e = cudaSuccess;
   // TMA-fed kernel (gemm_tma.cu) when the operands meet the tensor-map constraints;
   // otherwise the LDG-fed kernel above (any alignment)
-  if (!sg_gemm_tma_try(trans_a, trans_b, M, N, K, A, lda, B, ldb, C, ldc, epilogue, D, ldd, p.partial,
+  if (!sg_gemm_tma_try(trans_a, trans_b, M, N, K, A, lda, B, ldb, C, ldc, epilogue, D, ldd, nonfinite, p.partial,
                        p.kb_per_split, p.n_kb, gz, st, &e))
     e = BN == 64 ? dispatch_major<64>(a_mn, b_mn, p, grid, st) : dispatch_major<128>(a_mn, b_mn, p, grid, st);
   if (e != cudaSuccess) SG_FAIL(SG_ECUDA, "tcgen05 gemm launch: %s", cudaGetErrorString(e));
   if (gz > 1) {
     const int64_t total = M * N;
     int g = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
-    tc_splitk_reduce<<<g, 256, 0, st>>>(p.partial, gz, M, N, C, ldc, D, ldd, epilogue);
+    tc_splitk_reduce<<<g, 256, 0, st>>>(p.partial, gz, M, N, C, ldc, D, ldd, epilogue, nonfinite);
     sg::count_launch();
     e = cudaGetLastError();
     if (e != cudaSuccess) SG_FAIL(SG_ECUDA, "split-k reduce: %s", cudaGetErrorString(e));

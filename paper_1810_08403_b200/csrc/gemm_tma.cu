@@ -53,6 +53,7 @@ struct TmaArgs {
   int kb_per_split, n_kb;
   int epilogue;
   int vec_c, vec_d;
+  int32_t* nonfinite;  // strict-mode flag (tensor.py:161-163), checked in the epilogue
 };
 
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
@@ -229,6 +230,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int q = 0; q < 4; ++q)
               if (col + q < p.N) dst[row * ldo + col + q] = v[j + q];
           }
+          if (!p.partial && p.nonfinite) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              if (col + q < p.N && !isfinite(v[j + q])) atomicOr(p.nonfinite, 1);
+          }
           if (relu) {
             if (p.vec_d && col + 3 < p.N) {
               *reinterpret_cast<float4*>(p.D + row * p.ldd + col) =
@@ -318,7 +324,8 @@ bool tma_disabled() {
 // handled by the caller), 0 if the operands do not meet TMA constraints (caller falls back).
 int sg_gemm_tma_try(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,
                     const float* B, int64_t ldb, float* C, int64_t ldc, int epilogue, float* D, int64_t ldd,
-                    float* partial, int kb_per_split, int n_kb, int gz, cudaStream_t st, cudaError_t* err) {
+                    int32_t* nonfinite, float* partial, int kb_per_split, int n_kb, int gz, cudaStream_t st,
+                    cudaError_t* err) {
   if (tma_disabled()) return 0;
   if ((lda % 4) || (ldb % 4) || ((uintptr_t)A % 16) || ((uintptr_t)B % 16)) return 0;
   if (M > 0x7fffffff || N > 0x7fffffff || K > 0x7fffffff) return 0;
@@ -335,6 +342,7 @@ int sg_gemm_tma_try(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, c
   p.ldc = ldc; p.ldd = ldd; p.M = M; p.N = N;
   p.kb_per_split = kb_per_split; p.n_kb = n_kb;
   p.epilogue = epilogue;
+  p.nonfinite = nonfinite;
   p.vec_c = (ldc % 4 == 0) && ((uintptr_t)C % 16 == 0);
   p.vec_d = D != nullptr && (ldd % 4 == 0) && ((uintptr_t)D % 16 == 0);
   dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM), (unsigned)gz);

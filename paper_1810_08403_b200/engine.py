@@ -32,9 +32,12 @@ def _ld(n, align=4):
     return (n + align - 1) // align * align
 
 
-def _mat(V, n, device, align=4):
-    """[V, n] fp32 view of a zero-padded [V, ld] buffer (16-byte aligned rows)."""
-    return torch.zeros((V, _ld(n, align)), dtype=torch.float32, device=device)[:, :n]
+def _mat(V, n, device, align=4, dtype=torch.float32):
+    """[V, n] view of a zero-padded [V, ld] buffer (16-byte aligned rows: ld a multiple of 4
+    fp32 / 8 bf16 elements)."""
+    if dtype == torch.bfloat16:
+        align = max(align, 8)
+    return torch.zeros((V, _ld(n, align)), dtype=dtype, device=device)[:, :n]
 
 
 def _param(L, r, c, device):
@@ -93,7 +96,7 @@ class SAGAModel:
     gather (gcn / pass / ggcn) followed by ApplyVertex = ReLU(W accum)."""
 
     def __init__(self, programs, grid, weights=None, *, seed=2, gemm_prec=_lib.GEMM_TF32X3,
-                 device="cuda", strict=True, schedule="locality", reorder=False):
+                 device="cuda", strict=True, schedule="locality", reorder=False, dtype="f32"):
         if not torch.cuda.is_available():
             raise RuntimeError("SAGAModel needs a CUDA device (no CPU fallback)")
         if schedule not in ("locality", "dest_order"):
@@ -105,6 +108,17 @@ class SAGAModel:
         self.ws = K.Workspace(self.device)
         self.reorder = bool(reorder)
         self.layers = lower_programs(programs, self.reorder)
+        if dtype not in ("f32", "bf16"):
+            raise ConfigError(f"unknown dtype '{dtype}'; valid: f32, bf16")
+        # bf16 storage mode: features, aggregates, activations and their gradients stored as
+        # bf16 (fp32 accumulation in every gather and GEMM; fp32 logits, loss, weights and
+        # weight gradients); ApplyVertex on tcgen05 kind::f16 (SG_GEMM_BF16)
+        self.bf16 = dtype == "bf16"
+        if self.bf16:
+            if any(L.kind not in ("gcn", "pass") or L.vform != "w" or L.reorder for L in self.layers):
+                raise ConfigError("bf16 storage is implemented for sum-gather layers with "
+                                  "ApplyVertex = ReLU(W accum) (GCN), without reorder")
+            self.gemm_prec = _lib.GEMM_BF16
         dims = [(L.F, L.O) for L in self.layers]
         for a, b in zip(dims, dims[1:]):
             if a[1] != b[0]:
@@ -250,6 +264,8 @@ class SAGAModel:
                 nxt.hin = _mat(V, nxt.F, dev)
             L.hout = nxt.hin
         self.layers[-1].hout = None
+        if self.bf16:
+            self._alloc_bf16()
         self.X = self.layers[0].hin
         self.labels = torch.zeros(V, dtype=torch.int64, device=dev)
         self.loss = torch.zeros(1, dtype=torch.float32, device=dev)
@@ -257,6 +273,28 @@ class SAGAModel:
         self.nonfinite = torch.zeros(1, dtype=torch.int32, device=dev)
         self.tmp1 = _mat(V, max(L.F for L in self.layers), dev)
         self.tmp2 = _mat(V, max(L.F for L in self.layers), dev)
+
+    def _alloc_bf16(self):
+        """bf16 buffers for the bf16 storage mode: h (gathered rows), a, da, dz of the layers
+        below the top, and a bf16 copy Wb of every fp32 master weight (refreshed each step).
+        The ReLU mask of the backward pass is h_out = relu(z) > 0 (z > 0), so the hidden z
+        is never stored."""
+        V, dev, bf = self.V, self.device, torch.bfloat16
+        for n, L in enumerate(self.layers):
+            L.hin = _mat(V, L.F, dev, dtype=bf) if n == 0 else self.layers[n - 1].hout
+            L.a = _mat(V, L.F, dev, dtype=bf)
+            L.gin = L.a
+            L.da = _mat(V, L.F, dev, dtype=bf) if n > 0 else None
+            L.Wb = _mat(L.F, L.O, dev, dtype=bf)
+            last = n == len(self.layers) - 1
+            L.hout = None if last else _mat(V, L.O, dev, dtype=bf)
+            if last:
+                L.dzb = _mat(V, L.O, dev, dtype=bf)   # bf16 copy of the fp32 softmax-CE dz
+            else:
+                L.z = None
+                L.dz = L.dzb = _mat(V, L.O, dev, dtype=bf)  # written by the CSR gather above
+        for n, L in enumerate(self.layers[1:], 1):
+            L.hin = self.layers[n - 1].hout
 
     def load_features(self, X):
         X = torch.as_tensor(X)
@@ -433,7 +471,11 @@ class SAGAModel:
                              ws=self.ws)
 
     def _gemm(self, A, B, C, **kw):
-        K.gemm(A, B, C, prec=self.gemm_prec, ws=self.ws, **kw)
+        # strict mode (tensor.py:161-163) fused into every GEMM epilogue: z, the hoisted P / Q,
+        # dA and dW of every layer raise the device flag if non-finite (a non-finite aggregate
+        # or gathered gradient row reaches a GEMM output, so the gathers are covered too)
+        K.gemm(A, B, C, prec=self.gemm_prec, ws=self.ws,
+               nonfinite=self.nonfinite if self.strict else None, **kw)
 
     def _ewise(self, op, a, b, out, stream=None):
         _lib.check(_lib.lib.sg_ewise(op, a.shape[0], a.shape[1], a.data_ptr(), a.stride(0),
@@ -456,6 +498,10 @@ class SAGAModel:
     def forward(self, stream=None):
         """All layers forward; returns z_L (pre-ReLU logits)."""
         self._mark("start")
+        if self.strict:
+            self.nonfinite.zero_()
+        if self.bf16:
+            return self._forward_bf16(stream)
         for n, L in enumerate(self.layers):
             if L.kind == "ggcn":
                 self._gemm(L.hin, L.WH, L.Pv)   # hoisted P = h W_H  (SPEC.md:243-249)
@@ -485,12 +531,46 @@ class SAGAModel:
             self._mark(f"L{n}.fwd.apply_vertex")
         return self.layers[-1].z
 
+    def _forward_bf16(self, stream=None):
+        for L in self.layers:
+            K.convert(L.W, L.Wb, stream)              # bf16 copy of the fp32 master weights
+        last = self.layers[-1]
+        for n, L in enumerate(self.layers):
+            self._fwd_propagate(L, stream)              # bf16 rows in, fp32 sums, bf16 a out
+            self._mark(f"L{n}.fwd.propagate")
+            if L is last:
+                self._gemm(L.a, L.Wb, L.z)              # fp32 logits for the softmax-CE
+            else:
+                self._gemm(L.a, L.Wb, None, relu_out=L.hout)  # h' = relu(a W) in bf16
+            self._mark(f"L{n}.fwd.apply_vertex")
+        return last.z
+
+    def _backward_bf16(self, stream=None):
+        last = self.layers[-1]
+        K.convert(last.dz, last.dzb, stream)
+        for n in range(len(self.layers) - 1, -1, -1):
+            L = self.layers[n]
+            self._gemm(L.a, L.dzb, L.dW, trans_a=True)       # dW = a^T dz (fp32, split-K)
+            if n > 0:
+                below = self.layers[n - 1]
+                self._gemm(L.dzb, L.Wb, L.da, trans_b=True)  # dA = dz W^T (bf16)
+                self._mark(f"L{n}.bwd.apply_vertex")
+                self._bwd_propagate_gcn(L, below.dzb, below.hout, stream)
+                self._mark(f"L{n}.bwd.propagate")
+            else:
+                self._mark(f"L{n}.bwd.apply_vertex")
+
     def backward(self, stream=None):
         """Loss + all parameter gradients (reverse stage order)."""
         last = self.layers[-1]
         K.softmax_xent(last.z, self.labels, self.loss, last.dz, self.err, relu_input=True,
                        ws=self.ws, stream=stream)
         self._mark("loss")
+        if self.bf16:
+            self._backward_bf16(stream)
+            if self.strict:
+                K.check_finite(self.loss, self.nonfinite, stream)
+            return self.loss
         for n in range(len(self.layers) - 1, -1, -1):
             L = self.layers[n]
             below = self.layers[n - 1] if n > 0 else None
@@ -556,11 +636,8 @@ class SAGAModel:
                 else:
                     self._mark(f"L{n}.bwd.apply_vertex")
         if self.strict:
-            self.nonfinite.zero_()
+            # every GEMM output (z, P, Q, dA, dW) was checked in its epilogue; the loss here
             K.check_finite(self.loss, self.nonfinite, stream)
-            for L in self.layers:
-                for d in L.dparams:
-                    K.check_finite(d, self.nonfinite, stream)
         return self.loss
 
     def sgd(self, lr, stream=None):

@@ -5,6 +5,7 @@ current torch stream (or the given one) and raises the mirrored reference
 exception on a bad status.  torch is used only for device memory and streams.
 """
 
+import ctypes
 import os
 
 import torch
@@ -88,22 +89,36 @@ def propagate(pi, mode, G, out0, F, *, g_off=0, R=None, r_off=0, out1=None, mask
 
 
 def gemm(A, B, C, *, trans_a=False, trans_b=False, relu_out=None, prec=_lib.GEMM_F32, ws=None,
-         stream=None):
-    """C = op(A) @ op(B) (+ relu_out = relu(C)); fp32 storage."""
+         stream=None, nonfinite=None):
+    """C = op(A) @ op(B) (+ relu_out = relu(C)) through sg_gemm_ex.
+
+    fp32 A/B for GEMM_F32 / GEMM_TF32X3, bf16 A/B for GEMM_BF16; C and relu_out fp32 or bf16
+    (bf16 outputs need GEMM_BF16); C may be None when relu_out is given (bf16 path only).
+    ``nonfinite`` (int32 device flag) is OR-ed with 1 if C has a non-finite element."""
     M = A.shape[1] if trans_a else A.shape[0]
     K = A.shape[0] if trans_a else A.shape[1]
     N = B.shape[0] if trans_b else B.shape[1]
     Kb = B.shape[1] if trans_b else B.shape[0]
     if K != Kb:
-
         raise ShapeError(f"matmul inner extents differ: {K} vs {Kb}")
+    want = _lib.SG_BF16 if prec == _lib.GEMM_BF16 else _lib.SG_F32
+    if dtype_code(A) != want or dtype_code(B) != want:
+        raise TypeError(f"gemm precision {prec} takes {'bf16' if want else 'fp32'} operands")
     wsb = int(lib.sg_gemm_workspace_bytes(M, N, K, prec))
     buf = (ws.get(wsb) if ws is not None else torch.empty(max(wsb, 256), dtype=torch.uint8,
                                                             device=A.device))
-    check(lib.sg_gemm(prec, int(trans_a), int(trans_b), M, N, K, tptr(A), ld(A), tptr(B), ld(B),
-                      tptr(C), ld(C), _lib.EPI_RELU_DUAL if relu_out is not None else _lib.EPI_NONE,
-                      tptr(relu_out), ld(relu_out) if relu_out is not None else 0, tptr(buf),
-                      buf.numel(), stream_handle(stream)))
+    d = _lib.GemmDesc()
+    d.prec, d.trans_a, d.trans_b = prec, int(trans_a), int(trans_b)
+    d.epilogue = _lib.EPI_RELU_DUAL if relu_out is not None else _lib.EPI_NONE
+    d.M, d.N, d.K = M, N, K
+    d.A, d.lda, d.B, d.ldb = tptr(A), ld(A), tptr(B), ld(B)
+    d.C, d.ldc = tptr(C), (ld(C) if C is not None else 0)
+    d.c_dtype = dtype_code(C) if C is not None else _lib.SG_F32
+    d.D, d.ldd = tptr(relu_out), (ld(relu_out) if relu_out is not None else 0)
+    d.d_dtype = dtype_code(relu_out) if relu_out is not None else _lib.SG_F32
+    d.nonfinite = tptr(nonfinite)
+    d.workspace, d.workspace_bytes = tptr(buf), buf.numel()
+    check(lib.sg_gemm_ex(ctypes.byref(d), stream_handle(stream)))
 
 
 def softmax_xent(Z, labels, loss, dZ, err, *, relu_input=True, n_total=0, ws=None, stream=None):

@@ -36,18 +36,32 @@ def load_golden(name):
         return {k: z[k] for k in z.files}
 
 
-def assert_close(got, ref, rel=1e-4, what="", floor=0.1):
-    """Parity criterion (build decision): normwise rel <= rel AND
-    elementwise |d| <= rel*|ref| + 0.1*rel*max|ref|.
+def needed_floor(got, ref, rel=1e-4):
+    """The smallest ``floor`` with which ``got`` passes the elementwise test against ``ref``."""
+    got = np.asarray(got, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    scale = float(np.abs(ref).max()) if ref.size else 0.0
+    if scale == 0.0:
+        return 0.0
+    return float(np.max((np.abs(got - ref) - rel * np.abs(ref)) / (rel * scale), initial=0.0))
 
-    The absolute floor (1e-5 of the tensor's scale at rel = 1e-4) covers entries
-    that are sums of many cancelling terms (gradients), where any fp32 reduction
-    order -- SIMT fp32 or 3xTF32 tensor-core -- leaves ~sqrt(K) ulp of the term
-    magnitudes.  ``floor`` scales that absolute term (deep chains -- GG-NN's GRU + typed
-    gather + K = V weight-gradient GEMMs -- pass 0.5)."""
+
+def assert_close(got, ref, rel=1e-4, what="", floor=0.01, ref32=None):
+    """Parity criterion: normwise rel <= rel AND
+    elementwise |d| <= rel*|ref| + floor*rel*max|ref|; the default floor 0.01 is the
+    SURVEY's 1e-6 * max|ref| at rel = 1e-4.
+
+    The absolute term covers entries that are sums of many cancelling terms, where any fp32
+    reduction order leaves ~sqrt(K) ulp of the term magnitudes.  When the reference's own fp32
+    result ``ref32`` is given (``ref`` being its fp64 result), the floor is widened to twice
+    what the reference itself needs on this tensor: the GPU must be no further from fp64 than
+    2x the reference's own fp32 run.  Tests that pass a larger ``floor`` say why at the call
+    site (DESIGN.md §2 lists them)."""
     got = np.asarray(got, dtype=np.float64)
     ref = np.asarray(ref, dtype=np.float64)
     assert got.shape == ref.shape, (what, got.shape, ref.shape)
+    if ref32 is not None:
+        floor = max(floor, 2.0 * needed_floor(ref32, ref, rel))
     d = np.abs(got - ref)
     nref = np.linalg.norm(ref)
     scale = float(np.abs(ref).max()) if ref.size else 0.0
@@ -57,4 +71,4 @@ def assert_close(got, ref, rel=1e-4, what="", floor=0.1):
     bad = d > rel * np.abs(ref) + floor * rel * scale + 1e-30
     assert not bad.any(), (
         f"{what}: {int(bad.sum())} elements out of tolerance; max abs err {d.max():.3e}, "
-        f"max |ref| {scale:.3e}")
+        f"max |ref| {scale:.3e}; needed floor {needed_floor(got, ref, rel):.4f} > {floor:.4f}")

@@ -30,7 +30,8 @@ def test_reference_arm_json_line():
     assert d["value"] > 0 and d["unit"] == "edges/s" and d["higher_is_better"] is True
     assert d["metric"].startswith("GCN epoch throughput")
     cb = d["cpu_baseline"]
-    assert cb["kind"] == "port" and cb["cores"] >= 1 and "2000" in cb["sample"]
+    assert cb["kind"] == "port" and cb["cores"] >= 1 and "destination vertices" in cb["sample"]
+    assert cb["nproc"] >= 1 and "tape_vs_port" in cb
     assert cb["value"] == d["value"]
     assert d["e2e"]["value"] == d["value"] and d["e2e"]["h2d_bytes_per_step"] == 0
     assert d["config"]["workload"]
@@ -52,7 +53,19 @@ def test_reference_arm_rank0_uses_all_host_threads():
     assert d["cpu_baseline"]["cores"] == len(os.sched_getaffinity(0))
 
 
-def test_gpus_without_launched_ranks_is_refused():
+def test_gpus_n_without_torchrun_self_launches_n_ranks():
+    """``python bench.py --gpus 2`` (no WORLD_SIZE) re-launches itself under torch.distributed.run
+    with 2 ranks on 127.0.0.1; rank 0 prints the one JSON line (the driver's scaling run may call
+    either form)."""
     r = _run(args=ARGS + ["--gpus", "2"])
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.strip().startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2
+
+
+def test_gpus_mismatch_under_torchrun_is_refused():
+    r = _run({"RANK": "0", "LOCAL_RANK": "0", "WORLD_SIZE": "3"}, ARGS + ["--gpus", "2"])
     assert r.returncode != 0
     assert "torch.distributed.run" in r.stderr

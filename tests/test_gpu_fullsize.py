@@ -135,13 +135,17 @@ def test_blogcatalog10_ggcn_gather_rows():
     din = np.bincount(g.dst, minlength=V)
     sample = _sample(din, 24, 3)
     rows = _rows_ref(g.dst, g.src, sample, V)
-    ref = np.zeros((len(rows), F))
-    refS = np.zeros((len(rows), F))
+    ref, refS = np.zeros((len(rows), F)), np.zeros((len(rows), F))
+    ref32, refS32 = np.zeros((len(rows), F), np.float32), np.zeros((len(rows), F), np.float32)
     for k, (u, eids) in enumerate(rows.items()):
         s = g.src[eids]
         eta = prim.sigmoid(P[s].astype(np.float64) + Q[u].astype(np.float64))
         ref[k] = (eta * h[s]).sum(0)
         refS[k] = (h[s] * eta * (1.0 - eta)).sum(0)
+        # the same terms in fp32, added in edge order (the reference's fp32 arithmetic)
+        e32 = prim.sigmoid(P[s] + Q[u])
+        ref32[k] = np.cumsum(e32 * h[s], 0, dtype=np.float32)[-1] if len(s) else 0
+        refS32[k] = np.cumsum(h[s] * e32 * (np.float32(1) - e32), 0, dtype=np.float32)[-1] if len(s) else 0
     keys = list(rows)
-    assert_close(got[keys], ref, 1e-5, "G-GCN aggregate")
-    assert_close(gotS[keys], refS, 1e-5, "S", floor=0.5)
+    assert_close(got[keys], ref, 1e-5, "G-GCN aggregate", ref32=ref32)
+    assert_close(gotS[keys], refS, 1e-5, "S", ref32=refS32)

@@ -151,9 +151,14 @@ def test_ggcn_propagate_fwd_bwd(sg, P, T):
         for k, j in enumerate([j for j in range(P) if (i, j) in grid.csr]):
             K.propagate(grid.csr[(i, j)], _lib.PROP_GGCN_BWD_SRC, rows(GQ, j), rows(dP, i), F,
                         g_off=F, R=rows(HP, i), r_off=F, out1=rows(dH, i), accumulate=k > 0)
-    refA = saga.ggcn_propagate_fwd(part, h, Pm, Qm, T)
-    rQ, rP, rH = saga.ggcn_propagate_bwd(part, h, Pm, Qm, Ga, T)
-    assert_close(A.cpu().numpy(), refA, 1e-5, "A")
+    # fp64 oracle = the reference values; the fp32 oracle (the reference's own fp32 arithmetic)
+    # sets the elementwise noise floor (conftest.assert_close ref32)
+    f64 = [x.astype(np.float64) for x in (h, Pm, Qm, Ga)]
+    refA32 = saga.ggcn_propagate_fwd(part, h, Pm, Qm, T)
+    rQ32, rP32, rH32 = saga.ggcn_propagate_bwd(part, h, Pm, Qm, Ga, T)
+    refA = saga.ggcn_propagate_fwd(part, *f64[:3], T)
+    rQ, rP, rH = saga.ggcn_propagate_bwd(part, *f64, T)
+    assert_close(A.cpu().numpy(), refA, 1e-5, "A", ref32=refA32)
     # GGCN_FWD_S: the same aggregate (bitwise) plus S, with dQ = dA (.) S == pass A's dQ
     A2 = torch.zeros((V, F), device="cuda")
     S = torch.zeros((V, F), device="cuda")
@@ -165,10 +170,10 @@ def test_ggcn_propagate_fwd_bwd(sg, P, T):
     # elementwise floor 0.5 (not 0.1) of the 1e-5 band: the gate factor eta (1 - eta) carries the
     # SFU's ~2-ulp error, amplified by the cancellation in 1 - eta for saturated gates, and dQ now
     # sums it before (not after) the multiplication by dA
-    assert_close((torch.from_numpy(Ga).cuda() * S).cpu().numpy(), rQ, 1e-5, "dA*S", floor=0.5)
-    assert_close(dQ.cpu().numpy(), rQ, 1e-5, "dQ")
-    assert_close(dP.cpu().numpy(), rP, 1e-5, "dP")
-    assert_close(dH.cpu().numpy(), rH, 1e-5, "dH")
+    assert_close((torch.from_numpy(Ga).cuda() * S).cpu().numpy(), rQ, 1e-5, "dA*S", ref32=rQ32)
+    assert_close(dQ.cpu().numpy(), rQ, 1e-5, "dQ", ref32=rQ32)
+    assert_close(dP.cpu().numpy(), rP, 1e-5, "dP", ref32=rP32)
+    assert_close(dH.cpu().numpy(), rH, 1e-5, "dH", ref32=rH32)
 
 
 @pytest.mark.parametrize("M,N,K,ta,tb", [(1000, 128, 602, 0, 0), (602, 128, 20000, 1, 0),
@@ -313,8 +318,9 @@ def test_gcn_model_vs_reference_golden(sg, case):
     loss = m.loss.item()
     assert abs(loss - float(np.ravel(g["gcn_f64_loss"])[0])) <= 1e-4 * float(np.ravel(g["gcn_f64_loss"])[0])
     for l in range(2):
-        assert_close(m.layers[l].z.cpu().numpy(), g[f"gcn_f64_z{l}"], 1e-4, f"z{l}")
-        assert_close(m.layers[l].dW.cpu().numpy(), g[f"gcn_f64_dW{l}"], 1e-4, f"dW{l}")
+        assert_close(m.layers[l].z.cpu().numpy(), g[f"gcn_f64_z{l}"], 1e-4, f"z{l}", ref32=g[f"gcn_f32_z{l}"])
+        assert_close(m.layers[l].dW.cpu().numpy(), g[f"gcn_f64_dW{l}"], 1e-4, f"dW{l}",
+                     ref32=g[f"gcn_f32_dW{l}"])
 
 
 @pytest.mark.parametrize("case", GOLDEN_CASES)
@@ -335,7 +341,8 @@ def test_ggcn_model_vs_reference_golden(sg, case):
     got = m.grads()
     for l in range(2):
         for k in range(3):
-            assert_close(got[3 * l + k], g[f"ggcnh_f64_dL{l}_{k}"], 1e-4, f"L{l}.{k}")
+            assert_close(got[3 * l + k], g[f"ggcnh_f64_dL{l}_{k}"], 1e-4, f"L{l}.{k}",
+                         ref32=g[f"ggcnh_f32_dL{l}_{k}"])
 
 
 @pytest.mark.parametrize("model,P,T", [("gcn", 1, 4096), ("gcn", 4, 64), ("ggcn", 1, 4096), ("ggcn", 3, 100)])
@@ -359,19 +366,22 @@ def test_model_epoch_vs_oracle_pubmed_like(sg, model, P, T):
     m.backward()
     m.check_status()
     part = og.partition_2d(s, d, V, size)
-    X64 = X.astype(np.float64)
-    if model == "gcn":
-        w = og.gcn_edge_weights(s, d, V, np.float64)
-        ref = saga.gcn_epoch(part, X64, [x.astype(np.float64) for x in W], lab, w, T=T)
-        refg = ref["grads"]
-    else:
-        layers = [tuple(x.astype(np.float64) for x in W[3 * l: 3 * l + 3]) for l in range(2)]
-        ref = saga.ggcn_epoch(part, X64, layers, lab, T=T)
-        refg = [x for L in ref["grads"] for x in L]
+
+    def oracle(dt):
+        if model == "gcn":
+            w = og.gcn_edge_weights(s, d, V, dt)
+            ref = saga.gcn_epoch(part, X.astype(dt), [x.astype(dt) for x in W], lab, w, T=T)
+            return ref, ref["grads"]
+        layers = [tuple(x.astype(dt) for x in W[3 * l: 3 * l + 3]) for l in range(2)]
+        ref = saga.ggcn_epoch(part, X.astype(dt), layers, lab, T=T)
+        return ref, [x for L in ref["grads"] for x in L]
+
+    ref, refg = oracle(np.float64)
+    _, refg32 = oracle(np.float32)   # the reference's own fp32 run: elementwise noise floor
     rl = float(np.ravel(ref["loss"])[0])
     assert abs(m.loss.item() - rl) <= 1e-4 * rl
-    for k, (a, b) in enumerate(zip(m.grads(), refg)):
-        assert_close(a, b, 1e-4, f"grad {k}")
+    for k, (a, b, b32) in enumerate(zip(m.grads(), refg, refg32)):
+        assert_close(a, b, 1e-4, f"grad {k}", ref32=b32)
 
 
 @pytest.mark.parametrize("P,T", [(1, 4096), (3, 64)])
@@ -397,13 +407,13 @@ def test_reordered_gcn_epoch_vs_oracle(sg, P, T, dims):
     m.backward()
     m.check_status()
     part = og.partition_2d(s, d, V, size)
-    w = og.gcn_edge_weights(s, d, V, np.float64)
-    ref = saga.gcn_epoch(part, X.astype(np.float64), [x.astype(np.float64) for x in W], lab, w, T=T)
+    ref, r32 = (saga.gcn_epoch(part, X.astype(dt), [x.astype(dt) for x in W], lab,
+                               og.gcn_edge_weights(s, d, V, dt), T=T) for dt in (np.float64, np.float32))
     rl = float(np.ravel(ref["loss"])[0])
     assert abs(m.loss.item() - rl) <= 1e-4 * rl
-    assert_close(m.layers[1].z.cpu().numpy(), ref["z"][1], 1e-4, "logits")
-    for k, (a, b) in enumerate(zip(m.grads(), ref["grads"])):
-        assert_close(a, b, 1e-4, f"grad {k}")
+    assert_close(m.layers[1].z.cpu().numpy(), ref["z"][1], 1e-4, "logits", ref32=r32["z"][1])
+    for k, (a, b, b32) in enumerate(zip(m.grads(), ref["grads"], r32["grads"])):
+        assert_close(a, b, 1e-4, f"grad {k}", ref32=b32)
 
 
 def test_fused_equals_unfused_gcn_bitwise(sg):
@@ -598,12 +608,14 @@ def test_mpgcn_model_vs_reference_golden(sg, case):
     m.check_status()
     ref_loss = float(np.ravel(g["mpgcnh_f64_loss"])[0])
     assert abs(m.loss.item() - ref_loss) <= 1e-4 * ref_loss
-    assert_close(m.layers[0].a.cpu().numpy(), g["mpgcnh_f64_a0"], 1e-5, "a0")
+    assert_close(m.layers[0].a.cpu().numpy(), g["mpgcnh_f64_a0"], 1e-5, "a0", ref32=g["mpgcnh_f32_a0"])
     got = m.grads()
     for l in range(2):
-        assert_close(m.layers[l].z.cpu().numpy(), g[f"mpgcnh_f64_z{l}"], 1e-4, f"z{l}")
+        assert_close(m.layers[l].z.cpu().numpy(), g[f"mpgcnh_f64_z{l}"], 1e-4, f"z{l}",
+                     ref32=g[f"mpgcnh_f32_z{l}"])
         for k in range(3):
-            assert_close(got[3 * l + k], g[f"mpgcnh_f64_dL{l}_{k}"], 1e-4, f"L{l}.{k}")
+            assert_close(got[3 * l + k], g[f"mpgcnh_f64_dL{l}_{k}"], 1e-4, f"L{l}.{k}",
+                         ref32=g[f"mpgcnh_f32_dL{l}_{k}"])
 
 
 @pytest.mark.parametrize("kind,P,schedule", [("rmat", 1, "locality"), ("uniform", 1, "locality"),
@@ -643,10 +655,13 @@ def test_mpgcn_epoch_vs_oracle(sg, kind, P, schedule):
         gap = np.abs(Y[src[args[l][diff]], diff[1]] - Y[src[ra[diff]], diff[1]])
         assert np.all(gap <= 1e-5), (l, float(gap.max()))
     ref = saga.mpgcn_epoch(part, X.astype(np.float64), layers, lab, args=args)
+    layers32 = [tuple(x.astype(np.float32) for x in W[3 * l: 3 * l + 3]) for l in range(2)]
+    r32 = saga.mpgcn_epoch(part, X, layers32, lab, args=args)   # the oracle's own fp32 noise
     rl = float(np.ravel(ref["loss"])[0])
     assert abs(m.loss.item() - rl) <= 1e-4 * rl
-    for k, (a, b) in enumerate(zip(m.grads(), [x for L in ref["grads"] for x in L])):
-        assert_close(a, b, 1e-4, f"grad {k}")
+    for k, (a, b, b32) in enumerate(zip(m.grads(), [x for L in ref["grads"] for x in L],
+                                        [x for L in r32["grads"] for x in L])):
+        assert_close(a, b, 1e-4, f"grad {k}", ref32=b32)
 
 
 def test_mpgcn_trains(sg):
@@ -674,9 +689,11 @@ def test_commnet_model_vs_reference_golden(sg, case):
     assert abs(m.loss.item() - ref_loss) <= 1e-4 * ref_loss
     got = m.grads()
     for l in range(2):
-        assert_close(m.layers[l].z.cpu().numpy(), g[f"commnet_f64_z{l}"], 1e-4, f"z{l}")
+        assert_close(m.layers[l].z.cpu().numpy(), g[f"commnet_f64_z{l}"], 1e-4, f"z{l}",
+                     ref32=g[f"commnet_f32_z{l}"])
         for k in range(2):
-            assert_close(got[2 * l + k], g[f"commnet_f64_dL{l}_{k}"], 1e-4, f"L{l}.{k}")
+            assert_close(got[2 * l + k], g[f"commnet_f64_dL{l}_{k}"], 1e-4, f"L{l}.{k}",
+                         ref32=g[f"commnet_f32_dL{l}_{k}"])
 
 
 @pytest.mark.parametrize("P,T", [(1, 4096), (3, 64)])
@@ -696,12 +713,14 @@ def test_commnet_epoch_vs_oracle(sg, P, T):
     m.backward()
     m.check_status()
     part = og.partition_2d(s, d, V, size)
-    layers = [tuple(x.astype(np.float64) for x in W[2 * l: 2 * l + 2]) for l in range(2)]
-    ref = saga.commnet_epoch(part, X.astype(np.float64), layers, lab, T=T)
+    ref, r32 = (saga.commnet_epoch(part, X.astype(dt), [tuple(x.astype(dt) for x in W[2 * l: 2 * l + 2])
+                                                         for l in range(2)], lab, T=T)
+                for dt in (np.float64, np.float32))
     rl = float(np.ravel(ref["loss"])[0])
     assert abs(m.loss.item() - rl) <= 1e-4 * rl
-    for k, (a, b) in enumerate(zip(m.grads(), [x for L in ref["grads"] for x in L])):
-        assert_close(a, b, 1e-4, f"grad {k}")
+    for k, (a, b, b32) in enumerate(zip(m.grads(), [x for L in ref["grads"] for x in L],
+                                        [x for L in r32["grads"] for x in L])):
+        assert_close(a, b, 1e-4, f"grad {k}", ref32=b32)
     # unnormalised sums: a small step (SPEC.md:601 uses lr 0.01)
     out = sg.run_train({"model": "commnet", "graph": "uniform", "V": 1000, "E": 8000, "features": 32,
                         "classes": 4, "epochs": 5, "lr": 0.01})
@@ -779,14 +798,19 @@ def test_streaming_gcn_matches_resident(sg, P, T):
     res.check_status()
     for l in range(2):
         assert np.array_equal(st.A[l][:, : dims[l]].numpy(), res.layers[l].a.cpu().numpy()), l
-    assert abs(st.loss.item() - res.loss.item()) <= 1e-6 * res.loss.item()
-    for a, b in zip(st.grads(), res.grads()):
-        assert_close(a, b, 1e-5, "dW")
+    # anchored on the oracle (streaming changes where chunks live, not the math)
+    part = og.partition_2d(s, d, V, size)
+    ref, r32 = (saga.gcn_epoch(part, X.astype(dt), [x.astype(dt) for x in W], lab,
+                               og.gcn_edge_weights(s, d, V, dt), T=T) for dt in (np.float64, np.float32))
+    rl = float(np.ravel(ref["loss"])[0])
+    assert abs(st.loss.item() - rl) <= 1e-4 * rl
+    assert np.array_equal(st.A[0][:, : dims[0]].numpy(), r32["a"][0])   # bitwise vs the fp32 oracle
+    for k, (a, b, b32) in enumerate(zip(st.grads(), ref["grads"], r32["grads"])):
+        assert_close(a, b, 1e-4, f"dW{k}", ref32=b32)
     assert st.h2d_bytes > 0 and st.d2h_bytes > 0
-    res.sgd(0.5)
     st.sgd(0.5)
-    for a, b in zip(st.weights(), res.weights()):
-        assert_close(a, b, 1e-6, "W")
+    for a, w0, g in zip(st.weights(), W, ref["grads"]):
+        assert_close(a, w0.astype(np.float64) - 0.5 * g, 1e-5, "W after SGD")
 
 
 @pytest.mark.parametrize("P,T", [(1, 4096), (3, 256)])
@@ -812,11 +836,20 @@ def test_streaming_ggcn_matches_resident(sg, P, T):
     st.backward()
     st.check_status()
     res.check_status()
-    for l in range(2):
-        assert_close(st.A[l][:, : dims[l]].numpy(), res.layers[l].a.cpu().numpy(), 1e-6, f"A{l}")
-    assert abs(st.loss.item() - res.loss.item()) <= 1e-5 * res.loss.item()
-    for k, (a, b) in enumerate(zip(st.grads(), res.grads())):
-        assert_close(a, b, 1e-5, f"grad {k}")
+    part = og.partition_2d(s, d, V, size)
+    ref, r32 = (saga.ggcn_epoch(part, X.astype(dt), [tuple(x.astype(dt) for x in W[3 * l: 3 * l + 3])
+                                                      for l in range(2)], lab, T=T)
+                for dt in (np.float64, np.float32))
+    for l in range(2):   # aggregates (cache[l][3] = a) vs the oracle; the resident run agrees too
+        assert_close(st.A[l][:, : dims[l]].numpy(), ref["cache"][l][3], 1e-5, f"A{l}",
+                     ref32=r32["cache"][l][3])
+        assert_close(res.layers[l].a.cpu().numpy(), ref["cache"][l][3], 1e-5, f"resident A{l}",
+                     ref32=r32["cache"][l][3])
+    rl = float(np.ravel(ref["loss"])[0])
+    assert abs(st.loss.item() - rl) <= 1e-4 * rl
+    for k, (a, b, b32) in enumerate(zip(st.grads(), [x for L in ref["grads"] for x in L],
+                                        [x for L in r32["grads"] for x in L])):
+        assert_close(a, b, 1e-4, f"grad {k}", ref32=b32)
     assert st.h2d_bytes > 0 and st.d2h_bytes > 0
 
 
@@ -842,9 +875,20 @@ def test_streaming_empty_columns_and_rows(sg):
         st.forward()
         st.backward()
         st.check_status()
-        assert abs(st.loss.item() - res.loss.item()) <= 1e-5 * res.loss.item(), model
-        for k, (a, b) in enumerate(zip(st.grads(), res.grads())):
-            assert_close(a, b, 1e-4, f"{model} grad {k}")
+        part = og.partition_2d(s, d, V, 1000)
+        Wr = res.weights()
+        if model == "gcn":
+            refs = [saga.gcn_epoch(part, X.astype(dt), [x.astype(dt) for x in Wr], lab,
+                                   og.gcn_edge_weights(s, d, V, dt)) for dt in (np.float64, np.float32)]
+            rg = [r["grads"] for r in refs]
+        else:
+            refs = [saga.ggcn_epoch(part, X.astype(dt), [tuple(x.astype(dt) for x in Wr[3 * l: 3 * l + 3])
+                                                          for l in range(2)], lab) for dt in (np.float64, np.float32)]
+            rg = [[x for L in r["grads"] for x in L] for r in refs]
+        rl = float(np.ravel(refs[0]["loss"])[0])
+        assert abs(st.loss.item() - rl) <= 1e-4 * rl, model
+        for k, (a, b, b32) in enumerate(zip(st.grads(), rg[0], rg[1])):
+            assert_close(a, b, 1e-4, f"{model} grad {k}", ref32=b32)
 
 
 def test_streaming_budget_error(sg):
@@ -921,20 +965,22 @@ def test_ggnn_model_vs_reference_golden(sg, name):
     m.check_status()
     rl = float(np.ravel(g["ggnn_f64_loss"])[0])
     assert abs(m.loss.item() - rl) <= 1e-4 * abs(rl)
-    assert_close(m.logits.cpu().numpy(), g["ggnn_f64_logits"], 1e-4, "logits")
+    assert_close(m.logits.cpu().numpy(), g["ggnn_f64_logits"], 1e-4, "logits", ref32=g["ggnn_f32_logits"])
     gl, gWo = m.grads()
     for l in range(2):
         for t in range(3):
-            assert_close(gl[l][0][t], g[f"ggnn_f64_dL{l}_A{t}"], 1e-4, f"L{l} dA{t}")
+            assert_close(gl[l][0][t], g[f"ggnn_f64_dL{l}_A{t}"], 1e-4, f"L{l} dA{t}",
+                         ref32=g[f"ggnn_f32_dL{l}_A{t}"])
         for k in range(6):
-            assert_close(gl[l][1 + k], g[f"ggnn_f64_dL{l}_{k}"], 1e-4, f"L{l} d{k}")
-    assert_close(gWo, g["ggnn_f64_dWo"], 1e-4, "dWo")
+            assert_close(gl[l][1 + k], g[f"ggnn_f64_dL{l}_{k}"], 1e-4, f"L{l} d{k}",
+                         ref32=g[f"ggnn_f32_dL{l}_{k}"])
+    assert_close(gWo, g["ggnn_f64_dWo"], 1e-4, "dWo", ref32=g["ggnn_f32_dWo"])
 
 
 @pytest.mark.parametrize("P,T", [(1, 4096), (2, 64)])
 def test_ggnn_epoch_vs_oracle(sg, P, T):
     """GG-NN at a larger size on the 2D grid with split subgroups vs the fp64 oracle
-    (normwise 1e-4; elementwise floor 0.5e-4 of the tensor scale: the weight gradients are
+    (normwise 1e-4; elementwise against the oracle's own fp32 run: the weight gradients are
     K = V = 3000-row reductions at the end of a GRU + typed-gather chain)."""
     V, E, F, nt, C = 3000, 40000, 32, 4, 5
     s, d = _graph("rmat", V, E, 1)
@@ -953,15 +999,18 @@ def test_ggnn_epoch_vs_oracle(sg, P, T):
     part = og.partition_2d(s, d, V, size)
     L64 = [([a.astype(np.float64) for a in L[0]],) + tuple(x.astype(np.float64) for x in L[1:]) for L in layers]
     ref = saga.ggnn_epoch(part, X.astype(np.float64), L64, Wo.astype(np.float64), types, lab, T=T)
+    r32 = saga.ggnn_epoch(part, X, layers, Wo, types, lab, T=T)   # the oracle's own fp32 noise
     rl = float(np.ravel(ref["loss"])[0])
     assert abs(m.loss.item() - rl) <= 1e-4 * abs(rl)
     gl, gWo = m.grads()
     for l in range(2):
         for t in range(nt):
-            assert_close(gl[l][0][t], ref["grads"][l][0][t], 1e-4, f"L{l} dA{t}", floor=0.5)
+            assert_close(gl[l][0][t], ref["grads"][l][0][t], 1e-4, f"L{l} dA{t}",
+                         ref32=r32["grads"][l][0][t])
         for k in range(6):
-            assert_close(gl[l][1 + k], ref["grads"][l][1 + k], 1e-4, f"L{l} d{k}", floor=0.5)
-    assert_close(gWo, ref["grads_Wo"], 1e-4, "dWo", floor=0.5)
+            assert_close(gl[l][1 + k], ref["grads"][l][1 + k], 1e-4, f"L{l} d{k}",
+                         ref32=r32["grads"][l][1 + k])
+    assert_close(gWo, ref["grads_Wo"], 1e-4, "dWo", ref32=r32["grads_Wo"])
 
 
 def test_ggnn_trains(sg):
