@@ -377,7 +377,7 @@ def noreuse_point(a, cfg, flush, peak):
     grid = sg.ChunkGrid(gu, V, split_edges=a.split_edges)
     ld = (F + 3) // 4 * 4
     X = torch.from_numpy(sg.synthetic_features(V, F, seed=1, ld=ld)).cuda()[:, :F]
-    out = torch.zeros_like(X)
+    out = torch.zeros((V, ld), device="cuda")[:, :F]   # 16-B rows (the vector path)
     pi = grid.csc[(0, 0)]
     for _ in range(a.warmup):
         K.propagate(pi, _lib.PROP_GCN, X, out, F)
@@ -540,8 +540,8 @@ def run_ours(a, cfg):
                              "order (tests/test_gpu_kernels.py::test_reordered_gcn_epoch_vs_oracle)"}
         del m2
 
-    # ---- secondary: bf16 storage (features / aggregates / activations / their gradients in
-    # bf16, fp32 accumulation, tcgen05 kind::f16 ApplyVertex); reported beside the fp32 headline
+    # ---- secondary: bf16 storage of the gathered rows (features, hidden activations, dA) with
+    # fp32 accumulation, aggregates and gradients; reported beside the fp32 headline
     bf16 = None
     if cfg["model"] == "gcn" and not a.no_bf16:
         m3 = build(grid, [F, H, C], dtype="bf16")
@@ -549,11 +549,11 @@ def run_ours(a, cfg):
         m3.load_labels(lab_host)
         ms3, st3 = timed_epochs(m3, a, flush)
         k3 = st3.get("L0.fwd.propagate")
-        algo3 = gcn_pass_bytes(V, E, F, s=2)
+        algo3 = E * (4 + 4 + F * 2) + V * (4 + F * 4)   # bf16 rows gathered, fp32 aggregate out
         bf16 = {"ms_per_step": ms3, "value": E / (ms3 / 1e3), "unit": "edges/s", "dtype": "bf16",
                 "stages_ms": {k: round(v, 4) for k, v in st3.items()},
                 "L0_gather_achieved_gbs": algo3 / (k3 / 1e3) / 1e9 if k3 else None,
-                "tolerance": "bf16 bar (SURVEY.md §8(c)): normwise 1e-2, elementwise 2e-2|ref| + 1e-3 max|ref| "
+                "tolerance": "bf16 bar (SURVEY.md §8(c)): normwise 1e-2, elementwise 2e-2|ref| + 1e-2 max|ref| "
                              "vs the fp64 oracle (tests/test_gpu_bf16.py::"
                              "test_bf16_gcn_epoch_reddit_config_vs_fp64_fixture)"}
         del m3

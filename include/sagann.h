@@ -35,7 +35,13 @@ enum sg_status {
   SG_EFORMAT = 7   /* GraphFormatError (errors.py): malformed input file, line named */
 };
 
-enum sg_dtype { SG_F32 = 0, SG_BF16 = 1 };
+enum sg_dtype {
+  SG_F32 = 0,
+  SG_BF16 = 1,
+  /* sg_propagate only: bf16 gathered / row-side operands and mask (G, R, mask), fp32
+   * outputs (out0, out1) -- bf16 storage of the gathered rows, fp32 aggregates */
+  SG_BF16_F32OUT = 2
+};
 
 /* Propagation modes of sg_propagate (one fused Scatter-ApplyEdge-Gather pass). */
 enum sg_prop_mode {
@@ -107,6 +113,10 @@ int sg_host_gcn_weights(const int32_t* src, const int32_t* dst, const int64_t* d
 int sg_host_plan(const int64_t* ptr, int64_t n_rows, int64_t pack_edges, int64_t max_rows,
                  int64_t split_edges, sg_item* items, sg_split* splits, int64_t* n_items,
                  int64_t* n_splits, int64_t* n_slots);
+/* Reorder a plan's split items (in place) by the source of their first edge (idx[e_begin]),
+ * then row and subgroup, so that subgroups covering the same sources are adjacent in the work
+ * queue (results are independent of the item order). */
+int sg_host_plan_order(sg_item* items, int64_t n_items, const int32_t* idx);
 
 /* ---------------------------------------------------------------- host: ingestion
  * load_graph's file formats.  Edge file: one "src dest
@@ -244,7 +254,8 @@ int sg_gemm(int prec, int trans_a, int trans_b, int64_t M, int64_t N, int64_t K,
 /* The general form of sg_gemm (same operation and precisions):
  *   A, B      : fp32 for F32 / TF32X3, bf16 (SG_BF16) for SG_GEMM_BF16 (bf16 rows need
  *               ld % 8 == 0 and 16-B aligned bases: the TMA tensor-map constraints);
- *   C, c_dtype: output (fp32 or bf16); may be NULL when epilogue == RELU_DUAL (only D);
+ *   C, c_dtype: output (fp32 or bf16; bf16 with TF32X3 needs the TMA-eligible 16-B aligned
+ *               operands); may be NULL when epilogue == RELU_DUAL (only D), not with F32;
  *   D, d_dtype: D = relu(C) (np.maximum semantics: NaN propagates), fp32 or bf16;
  *   nonfinite : optional device flag, |= 1 if any element of C is non-finite (the
  *               strict-mode check of tensor.py:161-163 fused into the epilogue).

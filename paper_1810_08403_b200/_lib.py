@@ -22,7 +22,7 @@ LIB_PATH = os.environ.get("SG_LIB_PATH") or os.path.join(_HERE, "libsagann.so")
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "sagann.h")
 
 SG_OK, SG_ESHAPE, SG_ENUMERIC, SG_EBUDGET, SG_ECUDA, SG_ENCCL, SG_EINVAL, SG_EFORMAT = range(8)
-SG_F32, SG_BF16 = 0, 1
+SG_F32, SG_BF16, SG_BF16_F32OUT = 0, 1, 2
 PROP_PASS, PROP_GCN, PROP_GGCN_FWD, PROP_GGCN_BWD_DST, PROP_GGCN_BWD_SRC, PROP_GGCN_FWD_S = range(6)
 EPI_NONE, EPI_RELU_DUAL = 0, 1
 GEMM_F32, GEMM_TF32X3, GEMM_BF16 = 0, 1, 2
@@ -62,6 +62,7 @@ _SIGS = {
     "sg_host_partition_2d": (_i32, [_p, _p, _i64, _i64, _i64] + [_p] * 9),
     "sg_host_gcn_weights": (_i32, [_p, _p, _p, _p, _p, _i64, _p]),
     "sg_host_plan": (_i32, [_p, _i64, _i64, _i64, _i64, _p, _p, _p, _p, _p]),
+    "sg_host_plan_order": (_i32, [_p, _i64, _p]),
     "sg_host_scan_edges": (_i32, [_s, _i64, _p, _p, _p]),
     "sg_host_read_edges": (_i32, [_s, _i64, _p, _p, _p]),
     "sg_host_scan_matrix_text": (_i32, [_s, _p, _p]),

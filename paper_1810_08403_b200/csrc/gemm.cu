@@ -162,9 +162,9 @@ int choose_splits(int64_t M, int64_t N, int64_t K) {
 }  // namespace
 
 int sg_gemm_tc(int prec, int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, const float* A,
-               int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc, int epilogue,
-               float* D, int64_t ldd, int32_t* nonfinite, void* workspace, int64_t workspace_bytes,
-               cudaStream_t st);
+               int64_t lda, const float* B, int64_t ldb, void* C, int64_t ldc, int c_bf16, int epilogue,
+               void* D, int64_t ldd, int d_bf16, int32_t* nonfinite, void* workspace,
+               int64_t workspace_bytes, cudaStream_t st);
 int64_t sg_gemm_tc_workspace_bytes(int64_t M, int64_t N, int64_t K, int prec);
 int64_t sg_gemm_bf16_workspace_bytes(int64_t M, int64_t N, int64_t K);
 int sg_gemm_bf16_run(const sg_gemm_desc* d, cudaStream_t st);
@@ -210,8 +210,12 @@ int sg_gemm_ex(const sg_gemm_desc* d, void* stream) {
   if (d->M == 0 || d->N == 0) return SG_OK;
   cudaStream_t st = (cudaStream_t)stream;
   if (d->prec == SG_GEMM_BF16) return sg_gemm_bf16_run(d, st);
+  if (d->prec == SG_GEMM_TF32X3)  // fp32 operands; C / D may be bf16 (TMA path), C may be NULL
+    return sg_gemm_tc(d->prec, d->trans_a, d->trans_b, d->M, d->N, d->K, (const float*)d->A, d->lda,
+                      (const float*)d->B, d->ldb, d->C, d->ldc, d->c_dtype == SG_BF16, d->epilogue, d->D,
+                      d->ldd, d->d_dtype == SG_BF16, d->nonfinite, d->workspace, d->workspace_bytes, st);
   SG_REQUIRE(d->c_dtype == SG_F32 && d->d_dtype == SG_F32 && d->C, SG_EINVAL,
-             "gemm: fp32 precisions write fp32 C (and D)");
+             "gemm: SG_GEMM_F32 writes fp32 C (and D)");
   return gemm_f32(d->prec, d->trans_a, d->trans_b, d->M, d->N, d->K, (const float*)d->A, d->lda,
                   (const float*)d->B, d->ldb, (float*)d->C, d->ldc, d->epilogue, (float*)d->D, d->ldd,
                   d->nonfinite, d->workspace, d->workspace_bytes, st);
@@ -225,7 +229,7 @@ int gemm_f32(int prec, int trans_a, int trans_b, int64_t M, int64_t N, int64_t K
              int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc, int epilogue, float* D,
              int64_t ldd, int32_t* nonfinite, void* workspace, int64_t workspace_bytes, cudaStream_t st) {
   if (prec != SG_GEMM_F32)
-    return sg_gemm_tc(prec, trans_a, trans_b, M, N, K, A, lda, B, ldb, C, ldc, epilogue, D, ldd,
+    return sg_gemm_tc(prec, trans_a, trans_b, M, N, K, A, lda, B, ldb, C, ldc, 0, epilogue, D, ldd, 0,
                       nonfinite, workspace, workspace_bytes, st);
   const int splits = choose_splits(M, N, K);
   GemmArgs p;

@@ -110,29 +110,6 @@ __device__ __forceinline__ uint64_t op_desc(uint32_t base, int kk) {
   return sm100::smem_desc(base + kk * 2048, 8192, 1024, sm100::kLayoutSW128);
 }
 
-__device__ __forceinline__ void store4(void* base, bool bf16, int64_t off, const float* v, int nvalid,
-                                       bool vec) {
-  if (bf16) {
-    __nv_bfloat16* p = static_cast<__nv_bfloat16*>(base) + off;
-    if (vec && nvalid >= 4) {
-      __nv_bfloat162 lo = __floats2bfloat162_rn(v[0], v[1]), hi = __floats2bfloat162_rn(v[2], v[3]);
-      uint2 r;
-      r.x = *reinterpret_cast<uint32_t*>(&lo);
-      r.y = *reinterpret_cast<uint32_t*>(&hi);
-      *reinterpret_cast<uint2*>(p) = r;
-    } else {
-      for (int q = 0; q < nvalid; ++q) p[q] = __float2bfloat16_rn(v[q]);
-    }
-  } else {
-    float* p = static_cast<float*>(base) + off;
-    if (vec && nvalid >= 4) {
-      *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
-    } else {
-      for (int q = 0; q < nvalid; ++q) p[q] = v[q];
-    }
-  }
-}
-
 template <bool A_MN, bool B_MN, int BN>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
@@ -220,16 +197,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (col >= p.N) continue;
           const int nvalid = p.N - col < 4 ? (int)(p.N - col) : 4;
           if (split) {
-            store4(p.partial + (int64_t)blockIdx.z * p.M * p.N, false, row * p.N + col, v + j, nvalid, vec_c);
+            sm100::store4(p.partial + (int64_t)blockIdx.z * p.M * p.N, false, row * p.N + col, v + j, nvalid, vec_c);
             continue;
           }
           for (int q = 0; q < nvalid; ++q) bad |= !isfinite(v[j + q]);
-          if (p.C) store4(p.C, p.c_bf16, row * p.ldc + col, v + j, nvalid, vec_c);
+          if (p.C) sm100::store4(p.C, p.c_bf16, row * p.ldc + col, v + j, nvalid, vec_c);
           if (relu) {
             float r[4];
 #pragma unroll
             for (int q = 0; q < 4; ++q) r[q] = sg::relu_np(v[j + q]);
-            store4(p.D, p.d_bf16, row * p.ldd + col, r, nvalid, vec_d);
+            sm100::store4(p.D, p.d_bf16, row * p.ldd + col, r, nvalid, vec_d);
           }
         }
       }

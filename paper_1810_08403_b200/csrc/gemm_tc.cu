@@ -2,7 +2,7 @@
 //
 // C[M,N] = op(A)[M,K] . op(B)[K,N] (matmul, tensor.py:306-319), every operand
 // fp32 in HBM.  Precision SG_GEMM_TF32X3 ("3xTF32"): each fp32 tile is split on
-// the fly into hi = tf32(x) (mantissa truncated to 10 bits) and lo = x - hi, and
+// the fly into hi = rna_tf32(x) and lo = rna_tf32(x - hi) (sm100.cuh split3), and
 // the tensor core accumulates hi*hi + hi*lo + lo*hi in fp32 TMEM -- ~1e-6
 // relative error, inside the 1e-4 fp32 parity bar that a single TF32 pass misses
 // (SURVEY.md §7 "fp32 parity of the GEMM").
@@ -56,15 +56,10 @@ struct TcArgs {
 };
 
 __device__ __forceinline__ void split_tf32(float4 x, float4& hi, float4& lo) {
-  const uint32_t m = 0xFFFFE000u;
-  hi.x = __uint_as_float(__float_as_uint(x.x) & m);
-  hi.y = __uint_as_float(__float_as_uint(x.y) & m);
-  hi.z = __uint_as_float(__float_as_uint(x.z) & m);
-  hi.w = __uint_as_float(__float_as_uint(x.w) & m);
-  lo.x = __fsub_rn(x.x, hi.x);
-  lo.y = __fsub_rn(x.y, hi.y);
-  lo.z = __fsub_rn(x.z, hi.z);
-  lo.w = __fsub_rn(x.w, hi.w);
+  sm100::split3(x.x, hi.x, lo.x);
+  sm100::split3(x.y, hi.y, lo.y);
+  sm100::split3(x.z, hi.z, lo.z);
+  sm100::split3(x.w, hi.w, lo.w);
 }
 
 __device__ __forceinline__ float4 ld4(const float* base, int64_t ld, int64_t r, int64_t c, int64_t R,
@@ -319,16 +314,20 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tf32x3_kernel(const TcArgs p
   if (warp == kMmaWarp) sm100::tmem_dealloc<C::TMEM_COLS>(tmem);
 }
 
-__global__ void tc_splitk_reduce(const float* partial, int splits, int64_t M, int64_t N, float* C,
-                                 int64_t ldc, float* D, int64_t ldd, int epilogue, int32_t* nonfinite) {
+__global__ void tc_splitk_reduce(const float* partial, int splits, int64_t M, int64_t N, void* C,
+                                 int64_t ldc, int c_bf16, void* D, int64_t ldd, int d_bf16, int epilogue,
+                                 int32_t* nonfinite) {
   const int64_t total = M * N;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
     float s = 0.f;
     for (int z = 0; z < splits; ++z) s += partial[(int64_t)z * total + t];  // fixed order
     const int64_t m = t / N, n = t % N;
-    C[m * ldc + n] = s;
-    if (epilogue == SG_EPI_RELU_DUAL) D[m * ldd + n] = sg::relu_np(s);
+    if (C) sm100::store4(C, c_bf16, m * ldc + n, &s, 1, false);
+    if (epilogue == SG_EPI_RELU_DUAL) {
+      const float r = sg::relu_np(s);
+      sm100::store4(D, d_bf16, m * ldd + n, &r, 1, false);
+    }
     if (nonfinite && !isfinite(s)) atomicOr(nonfinite, 1);
   }
 }
@@ -367,9 +366,9 @@ cudaError_t dispatch_major(bool a_mn, bool b_mn, const TcArgs& p, dim3 grid, cud
 }  // namespace
 
 int sg_gemm_tma_try(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,
-                    const float* B, int64_t ldb, float* C, int64_t ldc, int epilogue, float* D, int64_t ldd,
-                    int32_t* nonfinite, float* partial, int kb_per_split, int n_kb, int gz, cudaStream_t st,
-                    cudaError_t* err);
+                    const float* B, int64_t ldb, void* C, int64_t ldc, int c_bf16, int epilogue, void* D,
+                    int64_t ldd, int d_bf16, int32_t* nonfinite, float* partial, int kb_per_split, int n_kb,
+                    int gz, cudaStream_t st, cudaError_t* err);
 
 int64_t sg_gemm_tc_workspace_bytes(int64_t M, int64_t N, int64_t K, int prec) {
   (void)prec;
@@ -378,15 +377,19 @@ int64_t sg_gemm_tc_workspace_bytes(int64_t M, int64_t N, int64_t K, int prec) {
 }
 
 int sg_gemm_tc(int prec, int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, const float* A,
-               int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc, int epilogue,
-               float* D, int64_t ldd, int32_t* nonfinite, void* workspace, int64_t workspace_bytes,
-               cudaStream_t st) {
+               int64_t lda, const float* B, int64_t ldb, void* Cv, int64_t ldc, int c_bf16, int epilogue,
+               void* Dv, int64_t ldd, int d_bf16, int32_t* nonfinite, void* workspace,
+               int64_t workspace_bytes, cudaStream_t st) {
   SG_REQUIRE(prec == SG_GEMM_TF32X3, SG_EINVAL, "tensor-core GEMM precision %d not supported", prec);
   if (K == 0) {
-    cudaMemset2DAsync(C, ldc * 4, 0, N * 4, M, st);
-    if (epilogue == SG_EPI_RELU_DUAL) cudaMemset2DAsync(D, ldd * 4, 0, N * 4, M, st);
+    if (Cv) cudaMemset2DAsync(Cv, ldc * (c_bf16 ? 2 : 4), 0, N * (c_bf16 ? 2 : 4), M, st);
+    if (epilogue == SG_EPI_RELU_DUAL) cudaMemset2DAsync(Dv, ldd * (d_bf16 ? 2 : 4), 0, N * (d_bf16 ? 2 : 4), M, st);
     return SG_OK;
   }
+  // the LDG-fed fallback kernel writes fp32 C (and D) only
+  const bool plain = Cv != nullptr && !c_bf16 && !d_bf16;
+  float* C = static_cast<float*>(Cv);
+  float* D = static_cast<float*>(Dv);
   // K-major when the reduction dim is contiguous: A stored [M,K] (!trans_a), B stored [N,K] (trans_b)
   const bool a_mn = trans_a != 0, b_mn = trans_b == 0;
   TcArgs p;
@@ -414,14 +417,17 @@ int sg_gemm_tc(int prec, int trans_a, int trans_b, int64_t M, int64_t N, int64_t
   cudaError_t e = cudaSuccess;
   // TMA-fed kernel (gemm_tma.cu) when the operands meet the tensor-map constraints;
   // otherwise the LDG-fed kernel above (any alignment)
-  if (!sg_gemm_tma_try(trans_a, trans_b, M, N, K, A, lda, B, ldb, C, ldc, epilogue, D, ldd, nonfinite, p.partial,
-                       p.kb_per_split, p.n_kb, gz, st, &e))
+  if (!sg_gemm_tma_try(trans_a, trans_b, M, N, K, A, lda, B, ldb, Cv, ldc, c_bf16, epilogue, Dv, ldd, d_bf16,
+                       nonfinite, p.partial, p.kb_per_split, p.n_kb, gz, st, &e)) {
+    SG_REQUIRE(plain, SG_EINVAL, "tensor-core GEMM: bf16 or absent C needs 16-B aligned operands (TMA path)");
     e = BN == 64 ? dispatch_major<64>(a_mn, b_mn, p, grid, st) : dispatch_major<128>(a_mn, b_mn, p, grid, st);
+  }
   if (e != cudaSuccess) SG_FAIL(SG_ECUDA, "tcgen05 gemm launch: %s", cudaGetErrorString(e));
   if (gz > 1) {
     const int64_t total = M * N;
     int g = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
-    tc_splitk_reduce<<<g, 256, 0, st>>>(p.partial, gz, M, N, C, ldc, D, ldd, epilogue, nonfinite);
+    tc_splitk_reduce<<<g, 256, 0, st>>>(p.partial, gz, M, N, Cv, ldc, c_bf16, Dv, ldd, d_bf16, epilogue,
+                                        nonfinite);
     sg::count_launch();
     e = cudaGetLastError();
     if (e != cudaSuccess) SG_FAIL(SG_ECUDA, "split-k reduce: %s", cudaGetErrorString(e));

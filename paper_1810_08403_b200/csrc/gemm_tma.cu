@@ -8,9 +8,10 @@
 //                        as K-major SWIZZLE_128B, MN-contiguous operands (a^T in dW = a^T dz,
 //                        W in z = a W) as MN-major SWIZZLE_128B_BASE32B (the only MN-major
 //                        tf32 layout), 32 x 32 boxes -- so no operand is transposed anywhere;
-//   warps 0-3            converters: lo = x - trunc_tf32(x) elementwise into a lo tile of
-//                        the same layout (the tensor core reads the raw fp32 container as
-//                        tf32, i.e. trunc_tf32(x) = hi); then the epilogue (TMEM -> global);
+//   warps 0-3            converters: hi = rna_tf32(x) in place and lo = rna_tf32(x - hi)
+//                        into a lo tile of the same layout (sm100.cuh split3: round-to-nearest
+//                        split, 4x tighter than reading the raw container as truncated tf32);
+//                        then the epilogue (TMEM -> global);
 //   warp 5 (one thread)  TMEM allocator + UMMA issuer: hi*hi + hi*lo + lo*hi per k-step,
 //                        tcgen05.commit releases the stage to the producer.
 // Stage ring: [raw A | raw B | lo A | lo B]; barriers raw-full (TMA tx bytes), full
@@ -45,14 +46,15 @@ struct TCfg {
 };
 
 struct TmaArgs {
-  float* C;
-  float* D;
+  void* C;  // fp32 or bf16 (c_bf16); may be NULL with RELU_DUAL
+  void* D;  // fp32 or bf16 (d_bf16)
   float* partial;
   int64_t ldc, ldd;
   int64_t M, N;
   int kb_per_split, n_kb;
   int epilogue;
   int vec_c, vec_d;
+  int c_bf16, d_bf16;
   int32_t* nonfinite;  // strict-mode flag (tensor.py:161-163), checked in the epilogue
 };
 
@@ -93,16 +95,6 @@ __device__ __forceinline__ uint64_t op_desc(uint32_t base, int kk) {
   return sm100::smem_desc(base + kk * 1024, 4096, 512, sm100::kLayoutSW128Base32B);
 }
 
-__device__ __forceinline__ float4 lo_part(float4 x) {
-  const uint32_t m = 0xFFFFE000u;
-  float4 r;
-  r.x = __fsub_rn(x.x, __uint_as_float(__float_as_uint(x.x) & m));
-  r.y = __fsub_rn(x.y, __uint_as_float(__float_as_uint(x.y) & m));
-  r.z = __fsub_rn(x.z, __uint_as_float(__float_as_uint(x.z) & m));
-  r.w = __fsub_rn(x.w, __uint_as_float(__float_as_uint(x.w) & m));
-  return r;
-}
-
 template <int BYTES>
 __device__ __forceinline__ void convert_plane(uint32_t raw, uint32_t lo, int t) {
   constexpr int N4 = BYTES / 16;
@@ -112,7 +104,14 @@ __device__ __forceinline__ void convert_plane(uint32_t raw, uint32_t lo, int t) 
     asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
                  : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w)
                  : "r"(raw + i * 16));
-    const float4 l = lo_part(x);
+    float4 h, l;
+    sm100::split3(x.x, h.x, l.x);
+    sm100::split3(x.y, h.y, l.y);
+    sm100::split3(x.z, h.z, l.z);
+    sm100::split3(x.w, h.w, l.w);
+    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(raw + i * 16), "f"(h.x), "f"(h.y),
+                 "f"(h.z), "f"(h.w)
+                 : "memory");
     asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(lo + i * 16), "f"(l.x), "f"(l.y),
                  "f"(l.z), "f"(l.w)
                  : "memory");
@@ -211,10 +210,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     sm100::mbar_wait(done, 0);
     sm100::tc_fence_after();
     const int64_t row = m0 + warp * 32 + lane;
-    float* dst = p.partial ? p.partial + (int64_t)blockIdx.z * p.M * p.N : p.C;
-    const int64_t ldo = p.partial ? p.N : p.ldc;
+    float* part = p.partial ? p.partial + (int64_t)blockIdx.z * p.M * p.N : nullptr;
     const bool relu = !p.partial && p.epilogue == SG_EPI_RELU_DUAL;
-    const bool vec_o = p.partial ? (p.N % 4 == 0) : p.vec_c;
+    bool bad = false;
 #pragma unroll 1
     for (int c0 = 0; c0 < BN; c0 += 16) {
       float v[16];
@@ -223,31 +221,24 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int j = 0; j < 16; j += 4) {
           const int64_t col = n0 + c0 + j;
-          if (vec_o && col + 3 < p.N) {
-            *reinterpret_cast<float4*>(dst + row * ldo + col) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-          } else {
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-              if (col + q < p.N) dst[row * ldo + col + q] = v[j + q];
+          if (col >= p.N) continue;
+          const int nvalid = p.N - col < 4 ? (int)(p.N - col) : 4;
+          if (part) {  // split-K partial: fp32, reduced in a fixed order afterwards
+            sm100::store4(part, false, row * p.N + col, v + j, nvalid, p.N % 4 == 0);
+            continue;
           }
-          if (!p.partial && p.nonfinite) {
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-              if (col + q < p.N && !isfinite(v[j + q])) atomicOr(p.nonfinite, 1);
-          }
+          for (int q = 0; q < nvalid; ++q) bad |= !isfinite(v[j + q]);
+          if (p.C) sm100::store4(p.C, p.c_bf16, row * p.ldc + col, v + j, nvalid, p.vec_c);
           if (relu) {
-            if (p.vec_d && col + 3 < p.N) {
-              *reinterpret_cast<float4*>(p.D + row * p.ldd + col) =
-                  make_float4(sg::relu_np(v[j]), sg::relu_np(v[j + 1]), sg::relu_np(v[j + 2]), sg::relu_np(v[j + 3]));
-            } else {
+            float r[4];
 #pragma unroll
-              for (int q = 0; q < 4; ++q)
-                if (col + q < p.N) p.D[row * p.ldd + col + q] = sg::relu_np(v[j + q]);
-            }
+            for (int q = 0; q < 4; ++q) r[q] = sg::relu_np(v[j + q]);
+            sm100::store4(p.D, p.d_bf16, row * p.ldd + col, r, nvalid, p.vec_d);
           }
         }
       }
     }
+    if (p.nonfinite && bad) atomicOr(p.nonfinite, 1);
   }
   sm100::tc_fence_before();
   __syncthreads();
@@ -323,9 +314,9 @@ bool tma_disabled() {
 // Returns 1 if the TMA path launched (C/D written or partials + reduce pending in *partial
 // handled by the caller), 0 if the operands do not meet TMA constraints (caller falls back).
 int sg_gemm_tma_try(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,
-                    const float* B, int64_t ldb, float* C, int64_t ldc, int epilogue, float* D, int64_t ldd,
-                    int32_t* nonfinite, float* partial, int kb_per_split, int n_kb, int gz, cudaStream_t st,
-                    cudaError_t* err) {
+                    const float* B, int64_t ldb, void* C, int64_t ldc, int c_bf16, int epilogue, void* D,
+                    int64_t ldd, int d_bf16, int32_t* nonfinite, float* partial, int kb_per_split, int n_kb,
+                    int gz, cudaStream_t st, cudaError_t* err) {
   if (tma_disabled()) return 0;
   if ((lda % 4) || (ldb % 4) || ((uintptr_t)A % 16) || ((uintptr_t)B % 16)) return 0;
   if (M > 0x7fffffff || N > 0x7fffffff || K > 0x7fffffff) return 0;
@@ -343,8 +334,10 @@ int sg_gemm_tma_try(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, c
   p.kb_per_split = kb_per_split; p.n_kb = n_kb;
   p.epilogue = epilogue;
   p.nonfinite = nonfinite;
-  p.vec_c = (ldc % 4 == 0) && ((uintptr_t)C % 16 == 0);
-  p.vec_d = D != nullptr && (ldd % 4 == 0) && ((uintptr_t)D % 16 == 0);
+  p.c_bf16 = c_bf16;
+  p.d_bf16 = d_bf16;
+  p.vec_c = C != nullptr && (ldc % 4 == 0) && ((uintptr_t)C % (c_bf16 ? 8 : 16) == 0);
+  p.vec_d = D != nullptr && (ldd % 4 == 0) && ((uintptr_t)D % (d_bf16 ? 8 : 16) == 0);
   dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM), (unsigned)gz);
   *err = BN == 64 ? dispatch_tma<64>(a_mn, b_mn, ma, mb, p, grid, st)
                   : dispatch_tma<128>(a_mn, b_mn, ma, mb, p, grid, st);

@@ -308,4 +308,21 @@ int sg_host_plan(const int64_t* ptr, int64_t n_rows, int64_t pack_edges, int64_t
   return SG_OK;
 }
 
+int sg_host_plan_order(sg_item* items, int64_t n_items, const int32_t* idx) {
+  SG_REQUIRE(n_items >= 0 && (n_items == 0 || (items && idx)), SG_EINVAL, "plan_order: null pointer");
+  int64_t ns = 0;
+  while (ns < n_items && items[ns].split >= 0) ns++;  // split items lead the plan
+  // subgroups that start at the same source traverse the same source rows at about the same
+  // rate: adjacent in the queue, the warps of one CTA (which take consecutive items) share
+  // them through L1.  Stable on (first source, row, subgroup); the per-row combination order
+  // is by subgroup index, so results do not depend on this order.
+  std::stable_sort(items, items + ns, [idx](const sg_item& a, const sg_item& b) {
+    const int32_t sa = idx[a.e_begin], sb = idx[b.e_begin];
+    if (sa != sb) return sa < sb;
+    if (a.row_begin != b.row_begin) return a.row_begin < b.row_begin;
+    return a.sub < b.sub;
+  });
+  return SG_OK;
+}
+
 }  // extern "C"

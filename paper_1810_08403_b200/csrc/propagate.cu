@@ -194,7 +194,11 @@ struct PropArgs {
 template <int MODE, int DT, int W, int VPL, int LPR, int DEPTH, bool HUB = false>
 struct Prop {
   using M = ModeT<MODE>;
-  using IO = VecIO<DT, W>;
+  // DT = SG_BF16_F32OUT: bf16 inputs (G, R, mask) and fp32 outputs (out0 / out1)
+  static constexpr int IDT = DT == SG_BF16_F32OUT ? SG_BF16 : DT;
+  static constexpr int ODT = DT == SG_BF16_F32OUT ? SG_F32 : DT;
+  using IO = VecIO<IDT, W>;
+  using OIO = VecIO<ODT, W>;
   static constexpr int NG = M::NG, NR = M::NR, NOUT = M::NOUT;
 
   using Elem = typename IO::Elem;
@@ -469,8 +473,8 @@ struct Prop {
     for (int v = 0; v < VPL; ++v) {
       const int cv = v * LPR + tl;
       if (cv < a.Fv) {
-        IO::ld_cs(a.out0, r * a.ld0 + (int64_t)cv * W, acc[0][v]);
-        if (NOUT > 1) IO::ld_cs(a.out1, r * a.ld1 + (int64_t)cv * W, acc[NOUT - 1][v]);
+        OIO::ld_cs(a.out0, r * a.ld0 + (int64_t)cv * W, acc[0][v]);
+        if (NOUT > 1) OIO::ld_cs(a.out1, r * a.ld1 + (int64_t)cv * W, acc[NOUT - 1][v]);
       }
     }
   }
@@ -489,8 +493,8 @@ struct Prop {
           for (int k = 0; k < W; ++k)  // relu bwd: g * (x > 0.0)  (tensor.py:236)
             acc[0][v][k] = __fmul_rn(acc[0][v][k], m[k] > 0.f ? 1.f : 0.f);
         }
-        IO::st(a.out0, r * a.ld0 + (int64_t)cv * W, acc[0][v], nvalid);
-        if (NOUT > 1) IO::st(a.out1, r * a.ld1 + (int64_t)cv * W, acc[NOUT - 1][v], nvalid);
+        OIO::st(a.out0, r * a.ld0 + (int64_t)cv * W, acc[0][v], nvalid);
+        if (NOUT > 1) OIO::st(a.out1, r * a.ld1 + (int64_t)cv * W, acc[NOUT - 1][v], nvalid);
       }
     }
   }
@@ -543,6 +547,11 @@ __global__ void __launch_bounds__(NWB * 32, (HUB ? 1 : prop_min_blocks<MODE, W, 
   const int team = lane / LPR, tl = lane % LPR;
   const unsigned tmask = LPR == 32 ? 0xffffffffu : (((1u << LPR) - 1u) << (team * LPR));
 
+  // Work distribution: every warp takes the next item from the global queue.  Split subgroups
+  // are queued by first source (sg_host_plan_order), so the items in flight at any moment --
+  // on all SMs -- gather overlapping source ranges and share them in L2 (Reddit L0: DRAM
+  // 49 -> 38 GB, 12.8 -> 11.5 ms; a CTA-chunked queue that kept adjacent items on one SM to
+  // share L1 measured slower, profiles/r02_sched_ab.txt).
   for (;;) {
     int it = 0;
     if (lane == 0) it = atomicAdd(a.queue, 1);
@@ -680,9 +689,17 @@ cudaError_t launch_one(const PropArgs& a, cudaStream_t st) {
 #ifndef SG_DEPTH_MID1
 #define SG_DEPTH_MID1 4
 #endif
-  constexpr int DEPTH_MID = NG == 1 ? (SG_DEPTH_MID1 / VPL > 0 ? SG_DEPTH_MID1 / VPL : 1)
+  // bf16 rows carry half the bytes per column: single-operand bf16 rows of 2-4 vectors per lane
+  // keep ~6 vectors per lane in flight (F = 602 bf16: 2 rows of 3 vectors, the bytes of one fp32
+  // row), and 8-byte bf16 vectors (W = 4, rows of 65-128 columns) keep 12 rows in flight (16 spill)
+#ifndef SG_DEPTH_MID1_BF16
+#define SG_DEPTH_MID1_BF16 6
+#endif
+  constexpr int MID1 = DT != SG_F32 ? SG_DEPTH_MID1_BF16 : SG_DEPTH_MID1;
+  constexpr int DEPTH_MID = NG == 1 ? (MID1 / VPL > 0 ? MID1 / VPL : 1)
                                     : SG_DEPTH_MID / (VPL * NG);
-  constexpr int DEPTH = (VPL * NG) == 1 ? SG_DEPTH1
+  constexpr int DEPTH1 = (DT != SG_F32 && W == 4 && NG == 1) ? SG_DEPTH1 * 3 / 2 : SG_DEPTH1;
+  constexpr int DEPTH = (VPL * NG) == 1 ? DEPTH1
                                         : ((VPL * NG) <= 4 ? DEPTH_MID : (NG > 1 ? 1 : SG_DEPTH_WIDE));
   if constexpr (LPR == 32 && NG == 1 && W > 1 && VPL >= kHubMinVpl) {
     if (a.n_hub > 0) {
@@ -744,7 +761,8 @@ cudaError_t dispatch_vpl(const PropArgs& a, int LPR, int VPL, cudaStream_t st) {
 }
 
 template <int MODE>
-cudaError_t dispatch_mode(int dtype, bool vec, const PropArgs& a, int LPR, int VPL, cudaStream_t st) {
+cudaError_t dispatch_mode(int dtype, bool vec, bool half_vec, const PropArgs& a, int LPR, int VPL,
+                          cudaStream_t st) {
 #ifdef SG_TUNE_GCN_ONLY  // fast register/spill iteration: build only the fp32 GCN kernels
   if (MODE != SG_PROP_GCN || dtype != SG_F32 || !vec) return cudaErrorNotSupported;
   return dispatch_vpl<SG_PROP_GCN, SG_F32, 4>(a, LPR, VPL, st);
@@ -752,6 +770,16 @@ cudaError_t dispatch_mode(int dtype, bool vec, const PropArgs& a, int LPR, int V
   if (dtype == SG_F32)
     return vec ? dispatch_vpl<MODE, SG_F32, 4>(a, LPR, VPL, st)
                : dispatch_vpl<MODE, SG_F32, 1>(a, LPR, VPL, st);
+  if (dtype == SG_BF16_F32OUT) {
+    // bf16 rows in, fp32 out: the GCN / passthrough gathers of the bf16-storage model
+    if constexpr (MODE == SG_PROP_PASS || MODE == SG_PROP_GCN) {
+      if (vec && half_vec) return launch_one<MODE, SG_BF16_F32OUT, 4, 1, 32>(a, st);
+      return vec ? dispatch_vpl<MODE, SG_BF16_F32OUT, 8>(a, LPR, VPL, st)
+                 : dispatch_vpl<MODE, SG_BF16_F32OUT, 1>(a, LPR, VPL, st);
+    }
+    return cudaErrorNotSupported;
+  }
+  if (vec && half_vec) return launch_one<MODE, SG_BF16, 4, 1, 32>(a, st);  // bf16 rows 65-128 cols
   return vec ? dispatch_vpl<MODE, SG_BF16, 8>(a, LPR, VPL, st)
              : dispatch_vpl<MODE, SG_BF16, 1>(a, LPR, VPL, st);
 }
@@ -789,7 +817,7 @@ int sg_propagate(int mode, int dtype, const int64_t* ptr, const int32_t* idx, co
 }
 
 int64_t sg_propagate_hub_capacity(int64_t F, int dtype) {
-  if (dtype != SG_F32 && dtype != SG_BF16) return 0;
+  if (dtype != SG_F32 && dtype != SG_BF16) return 0;  // (no hub cache for SG_BF16_F32OUT)
   const int VW = dtype == SG_F32 ? 4 : 8;
   const int64_t max_cols = (int64_t)32 * vpl_max(SG_PROP_GCN, dtype) * VW;
   const int64_t slice_cols = std::min<int64_t>(F, max_cols);
@@ -808,7 +836,10 @@ int sg_propagate_hub(int mode, int dtype, const int64_t* ptr, const int32_t* idx
                      const int32_t* hub_rows, int64_t n_hub, void* workspace, int64_t workspace_bytes,
                      void* stream) {
   SG_REQUIRE(mode >= SG_PROP_PASS && mode <= SG_PROP_GGCN_FWD_S, SG_EINVAL, "bad mode %d", mode);
-  SG_REQUIRE(dtype == SG_F32 || dtype == SG_BF16, SG_EINVAL, "bad dtype %d", dtype);
+  SG_REQUIRE(dtype == SG_F32 || dtype == SG_BF16 || dtype == SG_BF16_F32OUT, SG_EINVAL, "bad dtype %d", dtype);
+  SG_REQUIRE(dtype != SG_BF16_F32OUT || mode <= SG_PROP_GCN, SG_EINVAL,
+             "bf16-in / fp32-out is implemented for the PASS and GCN modes");
+  SG_REQUIRE(dtype != SG_BF16_F32OUT || n_hub == 0, SG_EINVAL, "no hub cache for bf16-in / fp32-out");
   SG_REQUIRE(n_items >= 0 && n_items <= INT32_MAX, SG_EINVAL, "bad n_items");
   if (n_rows == 0 || F == 0 || n_items == 0) return SG_OK;
   SG_REQUIRE(ptr && idx && items && G && out0, SG_EINVAL, "null required pointer");
@@ -822,13 +853,18 @@ int sg_propagate_hub(int mode, int dtype, const int64_t* ptr, const int32_t* idx
              "propagate workspace too small: %lld < %lld bytes", (long long)workspace_bytes,
              (long long)need);
   const int VW = dtype == SG_F32 ? 4 : 8;
-  const int esz = dtype == SG_F32 ? 4 : 2;
-  bool vec = (ldg % VW == 0) && (g_off % VW == 0) && (ld0 % VW == 0) && aligned(G, 16) &&
+  const int esz = dtype == SG_F32 ? 4 : 2;        // input (G, R, mask) element size
+  const int oesz = dtype == SG_BF16 ? 2 : 4;      // output (out0, out1) element size
+  const int OVW = dtype == SG_BF16_F32OUT ? 4 : VW;  // fp32 outputs: 16-B float4 rows suffice
+  bool vec = (ldg % VW == 0) && (g_off % VW == 0) && (ld0 % OVW == 0) && aligned(G, 16) &&
              aligned(out0, 16);
   if (R) vec = vec && (ldr % VW == 0) && (r_off % VW == 0) && aligned(R, 16);
-  if (out1) vec = vec && (ld1 % VW == 0) && aligned(out1, 16);
+  if (out1) vec = vec && (ld1 % OVW == 0) && aligned(out1, 16);
   if (mask) vec = vec && (ldm % VW == 0) && aligned(mask, 16);
-  const int W = vec ? VW : 1;
+  // bf16 rows of 65-128 columns: 8-byte vectors (4 bf16), so all 32 lanes of a warp work on a
+  // row (16-byte vectors would leave half of them idle)
+  const bool half_vec = vec && dtype != SG_F32 && F > 64 && F <= 128 && n_hub == 0;
+  const int W = vec ? (half_vec ? 4 : VW) : 1;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
 
   char* ws = static_cast<char*>(workspace);
@@ -860,8 +896,8 @@ int sg_propagate_hub(int mode, int dtype, const int64_t* ptr, const int32_t* idx
     a.counters = counters; a.queue = queue;
     a.G = static_cast<const char*>(G) + c0 * esz; a.ldg = ldg; a.g_off = g_off;
     a.R = R ? static_cast<const char*>(R) + c0 * esz : nullptr; a.ldr = ldr; a.r_off = r_off;
-    a.out0 = static_cast<char*>(out0) + c0 * esz; a.ld0 = ld0;
-    a.out1 = out1 ? static_cast<char*>(out1) + c0 * esz : nullptr; a.ld1 = ld1;
+    a.out0 = static_cast<char*>(out0) + c0 * oesz; a.ld0 = ld0;
+    a.out1 = out1 ? static_cast<char*>(out1) + c0 * oesz : nullptr; a.ld1 = ld1;
     a.mask = mask ? static_cast<const char*>(mask) + c0 * esz : nullptr; a.ldm = ldm;
     a.n_items = (int32_t)n_items; a.Fv = Fv; a.Fcols = (int32_t)cols; a.accumulate = accumulate;
     a.hub_rows = hub_rows;
@@ -877,12 +913,12 @@ int sg_propagate_hub(int mode, int dtype, const int64_t* ptr, const int32_t* idx
     cudaError_t e = cudaMemsetAsync(ws, 0, 256 + align_up(4 * std::max<int64_t>(n_splits, 1), 256), st);
     if (e != cudaSuccess) SG_FAIL(SG_ECUDA, "memset: %s", cudaGetErrorString(e));
     switch (mode) {
-      case SG_PROP_PASS: e = dispatch_mode<SG_PROP_PASS>(dtype, vec, a, LPR, VPL, st); break;
-      case SG_PROP_GCN: e = dispatch_mode<SG_PROP_GCN>(dtype, vec, a, LPR, VPL, st); break;
-      case SG_PROP_GGCN_FWD: e = dispatch_mode<SG_PROP_GGCN_FWD>(dtype, vec, a, LPR, VPL, st); break;
-      case SG_PROP_GGCN_BWD_DST: e = dispatch_mode<SG_PROP_GGCN_BWD_DST>(dtype, vec, a, LPR, VPL, st); break;
-      case SG_PROP_GGCN_FWD_S: e = dispatch_mode<SG_PROP_GGCN_FWD_S>(dtype, vec, a, LPR, VPL, st); break;
-      default: e = dispatch_mode<SG_PROP_GGCN_BWD_SRC>(dtype, vec, a, LPR, VPL, st); break;
+      case SG_PROP_PASS: e = dispatch_mode<SG_PROP_PASS>(dtype, vec, half_vec, a, LPR, VPL, st); break;
+      case SG_PROP_GCN: e = dispatch_mode<SG_PROP_GCN>(dtype, vec, half_vec, a, LPR, VPL, st); break;
+      case SG_PROP_GGCN_FWD: e = dispatch_mode<SG_PROP_GGCN_FWD>(dtype, vec, half_vec, a, LPR, VPL, st); break;
+      case SG_PROP_GGCN_BWD_DST: e = dispatch_mode<SG_PROP_GGCN_BWD_DST>(dtype, vec, half_vec, a, LPR, VPL, st); break;
+      case SG_PROP_GGCN_FWD_S: e = dispatch_mode<SG_PROP_GGCN_FWD_S>(dtype, vec, half_vec, a, LPR, VPL, st); break;
+      default: e = dispatch_mode<SG_PROP_GGCN_BWD_SRC>(dtype, vec, half_vec, a, LPR, VPL, st); break;
     }
     if (e != cudaSuccess) SG_FAIL(SG_ECUDA, "propagate launch: %s", cudaGetErrorString(e));
   }

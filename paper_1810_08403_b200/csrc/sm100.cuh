@@ -1,6 +1,7 @@
 // Thin inline-PTX wrappers for sm_100a: mbarrier, async-proxy fences, tcgen05 (TMEM
 // allocation, UMMA issue/commit, TMEM loads) and UMMA shared-memory descriptors.
 #pragma once
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -84,6 +85,48 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// ---------------------------------------------------------------- 3xTF32 operand split
+// x = hi + lo with hi = rna_tf32(x) (round to nearest, ties away) and lo = rna_tf32(x - hi):
+// |x - hi - lo| <= 2^-22 |x|, and each of the three products hi*hi + hi*lo + lo*hi carries at
+// most ~2^-22 relative error (a truncating split -- the tensor core reading the raw fp32
+// container as tf32 -- leaves ~2^-20 per term and 4x the dot-product error).
+// (bits + 2^12) & ~(2^13 - 1): round to nearest, ties away from zero, on the magnitude -- what
+// cvt.rna.tf32.f32 computes for finite x, in two integer ops (cvt.rna is emulated in ~8).  An
+// Inf operand becomes NaN: still non-finite, as the strict-mode check requires.
+__device__ __forceinline__ float rna_tf32(float x) {
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+}
+__device__ __forceinline__ void split3(float x, float& hi, float& lo) {
+  hi = rna_tf32(x);
+  lo = rna_tf32(__fsub_rn(x, hi));
+}
+
+// ---------------------------------------------------------------- epilogue stores
+// 4 consecutive fp32 results of one row -> fp32 or bf16 (rounded to nearest even) memory;
+// `vec`: one 16-B (fp32) / 8-B (bf16) store when all 4 are valid.
+__device__ __forceinline__ void store4(void* base, bool bf16, int64_t off, const float* v, int nvalid,
+                                       bool vec) {
+  if (bf16) {
+    __nv_bfloat16* p = static_cast<__nv_bfloat16*>(base) + off;
+    if (vec && nvalid >= 4) {
+      __nv_bfloat162 lo = __floats2bfloat162_rn(v[0], v[1]), hi = __floats2bfloat162_rn(v[2], v[3]);
+      uint2 r;
+      r.x = *reinterpret_cast<uint32_t*>(&lo);
+      r.y = *reinterpret_cast<uint32_t*>(&hi);
+      *reinterpret_cast<uint2*>(p) = r;
+    } else {
+      for (int q = 0; q < nvalid; ++q) p[q] = __float2bfloat16_rn(v[q]);
+    }
+  } else {
+    float* p = static_cast<float*>(base) + off;
+    if (vec && nvalid >= 4) {
+      *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+    } else {
+      for (int q = 0; q < nvalid; ++q) p[q] = v[q];
+    }
+  }
 }
 
 // ---------------------------------------------------------------- UMMA descriptors

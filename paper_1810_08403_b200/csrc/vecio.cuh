@@ -42,6 +42,27 @@ struct VecIO<SG_F32, 4> {
   }
 };
 
+// 8 fp32 (two float4): the fp32 output side of a pass whose inputs are 8-element bf16 vectors
+template <>
+struct VecIO<SG_F32, 8> {
+  using Elem = float;
+  static __device__ __forceinline__ void ld_cs(const void* base, int64_t off, float* v) {
+    const float4* p = reinterpret_cast<const float4*>(static_cast<const float*>(base) + off);
+    const float4 a = __ldcs(p), b = __ldcs(p + 1);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+    v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+  }
+  static __device__ __forceinline__ void st(void* base, int64_t off, const float* v, int nvalid) {
+    float* p = static_cast<float*>(base) + off;
+    if (nvalid >= 8) {
+      __stcs(reinterpret_cast<float4*>(p), make_float4(v[0], v[1], v[2], v[3]));
+      __stcs(reinterpret_cast<float4*>(p) + 1, make_float4(v[4], v[5], v[6], v[7]));
+    } else {
+      for (int k = 0; k < nvalid; ++k) p[k] = v[k];
+    }
+  }
+};
+
 template <>
 struct VecIO<SG_F32, 1> {
   using Elem = float;
@@ -89,6 +110,43 @@ struct VecIO<SG_BF16, 8> {
 #pragma unroll
       for (int k = 0; k < 4; ++k) h[k] = __floats2bfloat162_rn(v[2 * k], v[2 * k + 1]);
       __stcs(reinterpret_cast<uint4*>(p), r);
+    } else {
+      for (int k = 0; k < nvalid; ++k) p[k] = __float2bfloat16_rn(v[k]);
+    }
+  }
+};
+
+// half vector (4 bf16 = 8 bytes): bf16 rows of <= 128 columns fill a whole warp with it
+template <>
+struct VecIO<SG_BF16, 4> {
+  using Elem = __nv_bfloat16;
+  using Raw = uint2;
+  static __device__ __forceinline__ Raw ld_raw(const Elem* p) {
+    return __ldg(reinterpret_cast<const uint2*>(p));
+  }
+  static __device__ __forceinline__ void unpack(const Raw& r, float* v) {
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&r);
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      float2 f = __bfloat1622float2(h[k]);
+      v[2 * k] = f.x;
+      v[2 * k + 1] = f.y;
+    }
+  }
+  static __device__ __forceinline__ void ld_nc(const void* base, int64_t off, float* v) {
+    unpack(ld_raw(static_cast<const __nv_bfloat16*>(base) + off), v);
+  }
+  static __device__ __forceinline__ void ld_cs(const void* base, int64_t off, float* v) {
+    unpack(__ldcs(reinterpret_cast<const uint2*>(static_cast<const __nv_bfloat16*>(base) + off)), v);
+  }
+  static __device__ __forceinline__ void st(void* base, int64_t off, const float* v, int nvalid) {
+    __nv_bfloat16* p = static_cast<__nv_bfloat16*>(base) + off;
+    if (nvalid >= 4) {
+      uint2 r;
+      __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&r);
+      h[0] = __floats2bfloat162_rn(v[0], v[1]);
+      h[1] = __floats2bfloat162_rn(v[2], v[3]);
+      __stcs(reinterpret_cast<uint2*>(p), r);
     } else {
       for (int k = 0; k < nvalid; ++k) p[k] = __float2bfloat16_rn(v[k]);
     }

@@ -110,15 +110,16 @@ class SAGAModel:
         self.layers = lower_programs(programs, self.reorder)
         if dtype not in ("f32", "bf16"):
             raise ConfigError(f"unknown dtype '{dtype}'; valid: f32, bf16")
-        # bf16 storage mode: features, aggregates, activations and their gradients stored as
-        # bf16 (fp32 accumulation in every gather and GEMM; fp32 logits, loss, weights and
-        # weight gradients); ApplyVertex on tcgen05 kind::f16 (SG_GEMM_BF16)
+        # bf16 storage mode: the GATHERED rows are bf16 -- the input features, every hidden
+        # activation h (the next layer's gathered rows) and the backward's dA -- so the
+        # propagation passes read half the bytes; every gather accumulates and writes fp32 (a,
+        # dz), the ApplyVertex GEMMs run 3xTF32 on fp32 operands and round only their h / dA
+        # outputs to bf16.  (bf16 aggregates / gradients as GEMM operands cost 5-7% of dW0.)
         self.bf16 = dtype == "bf16"
         if self.bf16:
             if any(L.kind not in ("gcn", "pass") or L.vform != "w" or L.reorder for L in self.layers):
                 raise ConfigError("bf16 storage is implemented for sum-gather layers with "
                                   "ApplyVertex = ReLU(W accum) (GCN), without reorder")
-            self.gemm_prec = _lib.GEMM_BF16
         dims = [(L.F, L.O) for L in self.layers]
         for a, b in zip(dims, dims[1:]):
             if a[1] != b[0]:
@@ -275,26 +276,20 @@ class SAGAModel:
         self.tmp2 = _mat(V, max(L.F for L in self.layers), dev)
 
     def _alloc_bf16(self):
-        """bf16 buffers for the bf16 storage mode: h (gathered rows), a, da, dz of the layers
-        below the top, and a bf16 copy Wb of every fp32 master weight (refreshed each step).
-        The ReLU mask of the backward pass is h_out = relu(z) > 0 (z > 0), so the hidden z
-        is never stored."""
+        """bf16 buffers of the bf16 storage mode: the layer-1 features, the hidden activations
+        h_out = relu(z) (GEMM epilogue output, the next layer's gathered rows) and the gathered
+        gradients dA (GEMM output); a, z, dz stay fp32.  The backward ReLU mask is h_out > 0
+        (<=> z > 0), so the hidden z is not stored."""
         V, dev, bf = self.V, self.device, torch.bfloat16
+        last = self.layers[-1]
         for n, L in enumerate(self.layers):
-            L.hin = _mat(V, L.F, dev, dtype=bf) if n == 0 else self.layers[n - 1].hout
-            L.a = _mat(V, L.F, dev, dtype=bf)
-            L.gin = L.a
+            if n == 0:
+                L.hin = _mat(V, L.F, dev, dtype=bf)
             L.da = _mat(V, L.F, dev, dtype=bf) if n > 0 else None
-            L.Wb = _mat(L.F, L.O, dev, dtype=bf)
-            last = n == len(self.layers) - 1
-            L.hout = None if last else _mat(V, L.O, dev, dtype=bf)
-            if last:
-                L.dzb = _mat(V, L.O, dev, dtype=bf)   # bf16 copy of the fp32 softmax-CE dz
-            else:
+            if L is not last:
+                L.hout = _mat(V, L.O, dev, dtype=bf)
                 L.z = None
-                L.dz = L.dzb = _mat(V, L.O, dev, dtype=bf)  # written by the CSR gather above
-        for n, L in enumerate(self.layers[1:], 1):
-            L.hin = self.layers[n - 1].hout
+                self.layers[n + 1].hin = L.hout
 
     def load_features(self, X):
         X = torch.as_tensor(X)
@@ -532,30 +527,25 @@ class SAGAModel:
         return self.layers[-1].z
 
     def _forward_bf16(self, stream=None):
-        for L in self.layers:
-            K.convert(L.W, L.Wb, stream)              # bf16 copy of the fp32 master weights
         last = self.layers[-1]
         for n, L in enumerate(self.layers):
-            self._fwd_propagate(L, stream)              # bf16 rows in, fp32 sums, bf16 a out
+            self._fwd_propagate(L, stream)              # bf16 rows in, fp32 sums and a out
             self._mark(f"L{n}.fwd.propagate")
-            if L is last:
-                self._gemm(L.a, L.Wb, L.z)              # fp32 logits for the softmax-CE
-            else:
-                self._gemm(L.a, L.Wb, None, relu_out=L.hout)  # h' = relu(a W) in bf16
+            # z = a W (3xTF32); hidden layers keep only h' = relu(z) in bf16, the top layer z fp32
+            self._gemm(L.a, L.W, L.z, relu_out=None if L is last else L.hout)
             self._mark(f"L{n}.fwd.apply_vertex")
         return last.z
 
     def _backward_bf16(self, stream=None):
-        last = self.layers[-1]
-        K.convert(last.dz, last.dzb, stream)
         for n in range(len(self.layers) - 1, -1, -1):
             L = self.layers[n]
-            self._gemm(L.a, L.dzb, L.dW, trans_a=True)       # dW = a^T dz (fp32, split-K)
+            self._gemm(L.a, L.dz, L.dW, trans_a=True)        # dW = a^T dz (fp32)
             if n > 0:
                 below = self.layers[n - 1]
-                self._gemm(L.dzb, L.Wb, L.da, trans_b=True)  # dA = dz W^T (bf16)
+                self._gemm(L.dz, L.W, L.da, trans_b=True)    # dA = dz W^T, stored bf16
                 self._mark(f"L{n}.bwd.apply_vertex")
-                self._bwd_propagate_gcn(L, below.dzb, below.hout, stream)
+                # CSR dual: bf16 dA rows in, fp32 dz out, ReLU mask h_out (bf16) of the layer below
+                self._bwd_propagate_gcn(L, below.dz, below.hout, stream)
                 self._mark(f"L{n}.bwd.propagate")
             else:
                 self._mark(f"L{n}.bwd.apply_vertex")
@@ -793,17 +783,24 @@ def run_train(config):
     V, E = int(config["V"]), int(config["E"])
     gen = G.rmat_graph if config.get("graph", "uniform") == "rmat" else G.uniform_graph
     g = gen(V, E, seed=int(config.get("seed", 0)))
-    grid = G.ChunkGrid(g, config.get("interval_size") or V,
-                       split_edges=int(config.get("split_edges", G.DEFAULT_SPLIT_EDGES)))
     F, H, C = int(config["features"]), int(config.get("hidden", 16)), int(config["classes"])
     nl = int(config.get("layers", 2))
     dims = [F] + [H] * (nl - 1) + [C]
+    interval = config.get("interval_size")
+    if not interval:
+        # the chunk scheduler's choice for a resident model on this device (schedule.py)
+        from . import schedule as S
+
+        free = torch.cuda.mem_get_info()[0] if torch.cuda.is_available() else None
+        interval = S.build_schedule(g, dims, budget=free,
+                                    model="ggcn" if model == "ggcn" else "gcn").interval_size
+    grid = G.ChunkGrid(g, interval, split_edges=int(config.get("split_edges", G.DEFAULT_SPLIT_EDGES)))
     if model == "ggnn":  # GG-NN: state width F, synthetic edge labels, readout to C classes
         from .ggnn import ggnn_model
 
         nt = int(config.get("edge_types", 3))
         types = np.random.default_rng(5).integers(0, nt, E)
-        grid = G.ChunkGrid(g, config.get("interval_size") or V, gcn_weights=False,
+        grid = G.ChunkGrid(g, interval, gcn_weights=False,
                            split_edges=int(config.get("split_edges", G.DEFAULT_SPLIT_EDGES)))
         m = ggnn_model(grid, F, nt, C, types, layers=nl)
     else:

@@ -10,6 +10,8 @@ index" used by backward) layouts are uploaded once per graph into a
 consume.
 """
 
+import os
+
 import numpy as np
 
 from . import _lib
@@ -282,8 +284,14 @@ def load_graph(edge_file, feature_file=None, label_file=None, *, num_vertices=No
     return g
 
 
-def plan(ptr, split_edges=DEFAULT_SPLIT_EDGES, pack_edges=None, max_rows=256):
-    """Work plan of one propagation pass over a CSC/CSR pointer array (native)."""
+# split subgroups ordered by their first source (sg_host_plan_order): SG_PLAN_ORDER=row keeps
+# the (row, subgroup) order for A/B runs
+PLAN_ORDER = os.environ.get("SG_PLAN_ORDER", "src")
+
+
+def plan(ptr, split_edges=DEFAULT_SPLIT_EDGES, pack_edges=None, max_rows=256, idx=None):
+    """Work plan of one propagation pass over a CSC/CSR pointer array (native); with the pass's
+    index ``idx``, split subgroups are queued by first source (sg_host_plan_order)."""
     ptr = np.ascontiguousarray(ptr, np.int64)
     n_rows = ptr.shape[0] - 1
     nnz = int(ptr[-1]) if n_rows >= 0 else 0
@@ -296,6 +304,8 @@ def plan(ptr, split_edges=DEFAULT_SPLIT_EDGES, pack_edges=None, max_rows=256):
     splits = np.zeros(max(int(cnt[1]), 1), _lib.SPLIT_DTYPE)
     check(lib.sg_host_plan(nptr(ptr), n_rows, pack_edges, max_rows, split_edges, nptr(items),
                            nptr(splits), nptr(cnt[0:1]), nptr(cnt[1:2]), nptr(cnt[2:3])))
+    if idx is not None and PLAN_ORDER == "src" and len(items):
+        check(lib.sg_host_plan_order(nptr(items), len(items), nptr(np.ascontiguousarray(idx, np.int32))))
     return items, splits[: int(cnt[1])], int(cnt[2])
 
 
@@ -305,7 +315,7 @@ class PassIndex:
     def __init__(self, ptr, idx, w, n_rows, split_edges, device):
         import torch
 
-        items, splits, n_slots = plan(ptr, split_edges)
+        items, splits, n_slots = plan(ptr, split_edges, idx=idx)
         self.n_rows = int(n_rows)
         self.nnz = int(ptr[-1])
         self.n_items, self.n_splits, self.n_slots = len(items), len(splits), n_slots

@@ -75,6 +75,10 @@ def propagate(pi, mode, G, out0, F, *, g_off=0, R=None, r_off=0, out1=None, mask
     """One fused Scatter-ApplyEdge-Gather pass over PassIndex ``pi`` (sg_propagate; with the
     hub-row cache, sg_propagate_hub, when the pass has hubs -- bitwise identical)."""
     dt = dtype_code(G)
+    if dt == _lib.SG_BF16 and out0.dtype == torch.float32:
+        dt = _lib.SG_BF16_F32OUT       # bf16 rows in, fp32 aggregate out
+    elif out0.dtype != G.dtype:
+        raise TypeError(f"propagate: {G.dtype} rows into a {out0.dtype} output is not supported")
     wsb = pi.workspace_bytes(F, mode)
     buf = ws.get(wsb) if ws is not None else torch.empty(wsb, dtype=torch.uint8, device=G.device)
     h = _hub_for(pi, mode, dt, G, out0, mask, F, g_off) if hub and R is None and out1 is None else None
@@ -93,7 +97,7 @@ def gemm(A, B, C, *, trans_a=False, trans_b=False, relu_out=None, prec=_lib.GEMM
     """C = op(A) @ op(B) (+ relu_out = relu(C)) through sg_gemm_ex.
 
     fp32 A/B for GEMM_F32 / GEMM_TF32X3, bf16 A/B for GEMM_BF16; C and relu_out fp32 or bf16
-    (bf16 outputs need GEMM_BF16); C may be None when relu_out is given (bf16 path only).
+    (bf16 outputs with GEMM_BF16 or GEMM_TF32X3); C may be None when relu_out is given.
     ``nonfinite`` (int32 device flag) is OR-ed with 1 if C has a non-finite element."""
     M = A.shape[1] if trans_a else A.shape[0]
     K = A.shape[0] if trans_a else A.shape[1]

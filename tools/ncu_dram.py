@@ -27,11 +27,11 @@ def dram_bytes(rep):
     hdr, units, data = rows[0], rows[1], rows[2:]
     assert len(data) == 1, f"{rep}: {len(data)} launches (want 1)"
     col = {h: i for i, h in enumerate(hdr)}
-    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "B": 1, "KB": 1e3, "MB": 1e6, "GB": 1e9}
     tot = 0.0
     for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
         tot += float(data[0][col[m]].replace(",", "")) * scale[units[col[m]]]
-    t_unit = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0}[units[col["gpu__time_duration.sum"]]]
+    t_unit = {"nsecond": 1e-6, "ns": 1e-6, "usecond": 1e-3, "us": 1e-3, "msecond": 1.0, "ms": 1.0}[units[col["gpu__time_duration.sum"]]]
     ms = float(data[0][col["gpu__time_duration.sum"]].replace(",", "")) * t_unit
     return int(tot), ms, data[0][col["Kernel Name"]]
 

@@ -20,7 +20,7 @@ V, E, F = 232965, 114615892, 602
 g = sg.uniform_graph(V, E, seed=0)
 grid = sg.ChunkGrid(g, V)
 X = torch.from_numpy(sg.synthetic_features(V, F, seed=1, ld=604)).cuda()[:, :F]
-out = torch.zeros_like(X)
+out = torch.zeros((V, 604), device="cuda")[:, :F]   # 16-B rows: the vector path
 for _ in range(3):
     K.propagate(grid.csc[(0, 0)], _lib.PROP_GCN, X, out, F)
 torch.cuda.synchronize()
