@@ -67,7 +67,8 @@ def parse():
     ap.add_argument("--cpu-sample-edges", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--split-edges", type=int, default=4096)
+    ap.add_argument("--split-edges", default="auto",
+                    help="subgroup size T of split rows ('auto': graph.auto_split_edges per pass)")
     ap.add_argument("--no-reorder", action="store_true",
                     help="skip the secondary reorder_linear_gather measurement")
     ap.add_argument("--engine", choices=["auto", "dist"], default="auto",

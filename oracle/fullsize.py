@@ -61,35 +61,52 @@ def _spmm(A, H):
     return out
 
 
-def gcn_epoch(src, dst, V, X, Ws, labels, A=None, AT=None, dtype=np.float64):
-    """L-layer GCN forward + backward in ``dtype`` (fp64: the tolerance oracle; fp32: an fp32
-    run of the same math, whose distance from fp64 measures the fp32 rounding noise of each
-    tensor) -- same structure as saga.gcn_epoch.
-
-    Returns dict(loss, out=[h_1..h_L], z=[...], a=[...], grads=[dW...])."""
+def gcn_forward(src, dst, V, X, Ws, labels, A=None, dtype=np.float64):
+    """Forward half of gcn_epoch: dict(A, AT, a, z, out, loss, p, labels, Ws)."""
     if A is None:
         din = np.bincount(dst, minlength=V).astype(np.float64)
         dout = np.bincount(src, minlength=V).astype(np.float64)
         w = 1.0 / np.sqrt(dout[src] * din[dst])              # SPEC.md:541
         A = gcn_operator(src, dst, V, w.astype(dtype), dtype)
-    if AT is None:
-        AT = A.T.tocsr()
+    Ws = [np.asarray(W, dtype) for W in Ws]
     hs, As, Zs = [np.asarray(X, dtype)], [], []
     for W in Ws:
         a = _spmm(A, hs[-1])
-        z = a @ np.asarray(W, dtype)
+        z = a @ W
         As.append(a)
         Zs.append(z)
         hs.append(prim.relu(z))
     loss, p = prim.softmax_cross_entropy(hs[-1], labels)
-    g = prim.softmax_cross_entropy_bwd(np.asarray(1.0, dtype), p, labels)
-    grads = [None] * len(Ws)
-    for l in range(len(Ws) - 1, -1, -1):
-        gz = prim.relu_bwd(g, Zs[l])
-        ga, grads[l] = prim.matmul_bwd(gz, As[l], np.asarray(Ws[l], dtype))
+    return dict(A=A, AT=None, a=As, z=Zs, out=hs[1:], loss=loss, p=p, labels=labels, Ws=Ws)
+
+
+def gcn_backward(f, masks=None):
+    """Backward half: parameter gradients from gcn_forward's cache.  ``masks`` (one bool array
+    per layer) replaces z_l > 0 in the ReLU backward (saga.gcn_epoch's kink routing)."""
+    if f["AT"] is None:
+        f["AT"] = f["A"].T.tocsr()
+    dtype = f["z"][0].dtype
+    g = prim.softmax_cross_entropy_bwd(np.asarray(1.0, dtype), f["p"], f["labels"])
+    L = len(f["Ws"])
+    grads = [None] * L
+    for l in range(L - 1, -1, -1):
+        gz = prim.relu_bwd(g, f["z"][l]) if masks is None else g * masks[l]
+        ga, grads[l] = prim.matmul_bwd(gz, f["a"][l], f["Ws"][l])
         if l > 0:
-            g = _spmm(AT, ga)
-    return dict(loss=loss, p=p, a=As, z=Zs, out=hs[1:], grads=grads)
+            g = _spmm(f["AT"], ga)
+    return grads
+
+
+def gcn_epoch(src, dst, V, X, Ws, labels, A=None, AT=None, dtype=np.float64, masks=None):
+    """L-layer GCN forward + backward in ``dtype`` (fp64: the tolerance oracle; fp32: an fp32
+    run of the same math, whose distance from fp64 measures the fp32 rounding noise of each
+    tensor) -- same structure as saga.gcn_epoch.
+
+    Returns dict(loss, out=[h_1..h_L], z=[...], a=[...], grads=[dW...])."""
+    f = gcn_forward(src, dst, V, X, Ws, labels, A=A, dtype=dtype)
+    f["AT"] = AT
+    grads = gcn_backward(f, masks)
+    return dict(loss=f["loss"], p=f["p"], a=f["a"], z=f["z"], out=f["out"], grads=grads)
 
 
 # ------------------------------------------------------------------ G-GCN (edge blocks)

@@ -175,9 +175,13 @@ def ggcn_propagate_bwd(part, h, P_, Q_, Ga, T=None):
 
 
 # ------------------------------------------------------------------ models (chunked)
-def gcn_epoch(part, X, Ws, labels, w_edge, T=None):
+def gcn_epoch(part, X, Ws, labels, w_edge, T=None, masks=None):
     """2-layer (or L-layer) GCN forward + backward.
 
+    ``masks`` (optional, one bool array per layer): the ReLU-backward masks to use instead of
+    z_l > 0 -- a run under test may resolve a ReLU kink (|z| at rounding level) the other way,
+    and routing the oracle through the same masks compares everything else exactly (the way
+    mpgcn_epoch(args=...) routes near-tie argmaxes).
     Returns dict(loss, a=[...], z=[...], out=[...], grads=[dW...])."""
     hs, As, Zs = [X], [], []
     for W in Ws:
@@ -190,7 +194,7 @@ def gcn_epoch(part, X, Ws, labels, w_edge, T=None):
     g = prim.softmax_cross_entropy_bwd(np.asarray(1.0, dtype=X.dtype), p, labels)
     grads = [None] * len(Ws)
     for l in range(len(Ws) - 1, -1, -1):
-        gz = prim.relu_bwd(g, Zs[l])
+        gz = prim.relu_bwd(g, Zs[l]) if masks is None else g * masks[l]
         ga, grads[l] = prim.matmul_bwd(gz, As[l], Ws[l])
         if l > 0:
             g = gcn_propagate_bwd(part, ga, w_edge, T)

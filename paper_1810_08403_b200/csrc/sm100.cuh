@@ -93,10 +93,12 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
 // most ~2^-22 relative error (a truncating split -- the tensor core reading the raw fp32
 // container as tf32 -- leaves ~2^-20 per term and 4x the dot-product error).
 // (bits + 2^12) & ~(2^13 - 1): round to nearest, ties away from zero, on the magnitude -- what
-// cvt.rna.tf32.f32 computes for finite x, in two integer ops (cvt.rna is emulated in ~8).  An
-// Inf operand becomes NaN: still non-finite, as the strict-mode check requires.
+// cvt.rna.tf32.f32 computes for finite x (cvt.rna is emulated in ~8 ops).  Inf / NaN keep their
+// bits: the increment would carry a NaN's full mantissa (the canonical 0x7FFFFFFF) into the sign
+// and turn it into -0, silently dropping it from the strict-mode check.
 __device__ __forceinline__ float rna_tf32(float x) {
-  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+  const uint32_t u = __float_as_uint(x);
+  return __uint_as_float((u & 0x7F800000u) == 0x7F800000u ? u : (u + 0x1000u) & 0xFFFFE000u);
 }
 __device__ __forceinline__ void split3(float x, float& hi, float& lo) {
   hi = rna_tf32(x);

@@ -50,7 +50,7 @@ class ShardIndex:
     old -> new vertex ids and ``vertices`` lists the ORIGINAL ids of the local rows
     (select features / labels with it)."""
 
-    def __init__(self, g, world, rank, split_edges=G.DEFAULT_SPLIT_EDGES, device="cuda",
+    def __init__(self, g, world, rank, split_edges="auto", device="cuda",
                  gcn_weights=True, balance=True):
         size = -(-g.V // world)
         if balance and world > 1:

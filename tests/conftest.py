@@ -80,3 +80,41 @@ def assert_close(got, ref, rel=1e-4, what="", floor=FLOOR, ref32=None):
     assert not bad.any(), (
         f"{what}: {int(bad.sum())} elements out of tolerance; max abs err {d.max():.3e}, "
         f"max |ref| {scale:.3e}; needed floor {needed_floor(got, ref, rel):.4f} > {floor:.4f}")
+
+
+def route_relu_masks(z_gpu, z_ref, tie=1e-5, max_frac=1e-3, what=""):
+    """ReLU masks of the run under test, after checking that every place where they disagree
+    with the reference's (z_ref > 0) is a kink: |z_ref| <= tie * max|z_ref| -- a value at the
+    rounding level of the computation, where fp32 (or bf16) and fp64 may legitimately land on
+    different sides of 0 -- and that such places are rare.  The oracle then runs its backward
+    through these masks (saga.gcn_epoch / fullsize.gcn_backward ``masks``)."""
+    masks = []
+    for l, (zg, zr) in enumerate(zip(z_gpu, z_ref)):
+        zg, zr = np.asarray(zg), np.asarray(zr, np.float64)
+        mg = zg > 0
+        diff = mg != (zr > 0)
+        scale = float(np.abs(zr).max()) if zr.size else 0.0
+        assert int(diff.sum()) <= max_frac * zr.size, f"{what} L{l}: {int(diff.sum())} ReLU flips"
+        if diff.any():
+            gap = float(np.abs(zr[diff]).max())
+            assert gap <= tie * scale, f"{what} L{l}: a ReLU flip at |z| = {gap:.3e} (> {tie} x {scale:.3e})"
+        masks.append(mg)
+    return masks
+
+
+@pytest.fixture(scope="session")
+def reddit_oracle():
+    """The Reddit-shaped config (BASELINE configs[1]) built once per session: the bench's graph,
+    features, weights (Glorot, seed 2) and labels, and the fp64 full-size oracle's forward pass
+    (oracle/fullsize.py) -- the GPU tests route its backward through their own ReLU masks."""
+    import paper_1810_08403_b200 as sg
+    from oracle import fullsize as fs
+    from oracle import rng
+
+    V, E, F, H, C = 232965, 114615892, 602, 128, 41
+    g = sg.rmat_graph(V, E, seed=0)
+    X = sg.synthetic_features(V, F, seed=1)
+    Ws = [w.astype(np.float64) for w in rng.glorot([(F, H), (H, C)], seed=2)]
+    lab = rng.labels(V, C, seed=3)
+    f = fs.gcn_forward(g.src, g.dst, V, X.astype(np.float64), Ws, lab)
+    return dict(g=g, X=X, fwd=f, V=V, E=E, F=F, H=H, C=C)

@@ -15,7 +15,7 @@ import pytest
 
 torch = pytest.importorskip("torch")
 
-from conftest import assert_close  # noqa: E402
+from conftest import assert_close, route_relu_masks  # noqa: E402
 from oracle import graph as og  # noqa: E402
 from oracle import primitives as prim  # noqa: E402
 from oracle import rng  # noqa: E402
@@ -291,8 +291,10 @@ def test_bf16_gcn_epoch_pubmed_config_vs_fp64_oracle(sg):
     g = sg.uniform_graph(V, E, seed=0)
     m, X = _bf16_epoch(sg, g, V, F, H, C, "bf16")
     part = og.partition_2d(g.src, g.dst, V, V)
-    ref = saga.gcn_epoch(part, X.astype(np.float64), [w.astype(np.float64) for w in m.weights()],
-                         rng.labels(V, C, seed=3), og.gcn_edge_weights(g.src, g.dst, V, np.float64))
+    args = (part, X.astype(np.float64), [w.astype(np.float64) for w in m.weights()],
+            rng.labels(V, C, seed=3), og.gcn_edge_weights(g.src, g.dst, V, np.float64))
+    free = saga.gcn_epoch(*args)
+    ref = saga.gcn_epoch(*args, masks=_bf16_masks(m, free["z"], "pubmed bf16"))
     rl = float(np.ravel(ref["loss"])[0])
     assert abs(m.loss.item() - rl) <= BF16_NORM * abs(rl), (m.loss.item(), rl)
     for k, (got, want) in enumerate(zip(_bf16_outs(m), ref["out"])):
@@ -301,24 +303,29 @@ def test_bf16_gcn_epoch_pubmed_config_vs_fp64_oracle(sg):
         assert_close_bf16(got, want, f"dW{k}")
 
 
-def test_bf16_gcn_epoch_reddit_config_vs_fp64_fixture(sg):
+def _bf16_masks(m, z_ref, what):
+    """The bf16 run's ReLU masks (h_out > 0 of the hidden layers, z > 0 of the top) routed into
+    the oracle's backward; flips allowed only at bf16-level kinks (|z| <= 5e-3 max|z|)."""
+    zg = [L.hout.float().cpu().numpy() for L in m.layers[:-1]] + [m.layers[-1].z.cpu().numpy()]
+    return route_relu_masks(zg, z_ref, tie=5e-3, max_frac=5e-3, what=what)
+
+
+def test_bf16_gcn_epoch_reddit_config_vs_fp64_oracle(sg, reddit_oracle):
     """The bf16 Reddit epoch the bench reports (BASELINE config 2, full size) vs the fp64
-    fixture of the full-size oracle at the bf16 tolerance."""
-    import os
+    full-size oracle (live, routed through the bf16 run's ReLU masks) at the bf16 tolerance."""
+    from oracle import fullsize as fs
 
-    from conftest import GOLDEN
-
-    V, E, F, H, C = 232965, 114615892, 602, 128, 41
-    g = sg.rmat_graph(V, E, seed=0)
-    m, _ = _bf16_epoch(sg, g, V, F, H, C, "bf16")
-    with np.load(os.path.join(GOLDEN, "fullsize_reddit.npz")) as z:
-        fx = {k: z[k] for k in z.files}
-    rl = float(fx["loss"])
+    R = reddit_oracle
+    m, _ = _bf16_epoch(sg, R["g"], R["V"], R["F"], R["H"], R["C"], "bf16")
+    f = R["fwd"]
+    grads = fs.gcn_backward(f, _bf16_masks(m, f["z"], "reddit bf16"))
+    rl = float(np.ravel(f["loss"])[0])
     assert abs(m.loss.item() - rl) <= BF16_NORM * abs(rl), (m.loss.item(), rl)
+    rows = np.random.default_rng(11).choice(R["V"], 256, replace=False)
     for k, h in enumerate(_bf16_outs(m)):
-        assert_close_bf16(h[fx["rows"]], fx[f"out{k}_rows"], f"h{k + 1} rows")
-    for k, got in enumerate(m.grads()):
-        assert_close_bf16(got, fx[f"grad{k}"], f"dW{k}")
+        assert_close_bf16(h[rows], f["out"][k][rows], f"h{k + 1} rows")
+    for k, (got, want) in enumerate(zip(m.grads(), grads)):
+        assert_close_bf16(got, want, f"dW{k}")
 
 
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])

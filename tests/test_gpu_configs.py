@@ -22,7 +22,7 @@ import numpy as np
 import pytest
 import torch
 
-from conftest import FLOOR, GOLDEN, assert_close
+from conftest import FLOOR, GOLDEN, assert_close, route_relu_masks
 
 pytestmark = pytest.mark.gpu
 
@@ -63,8 +63,13 @@ def test_pubmed_config_epoch_vs_fp64_oracle():
     m, X = _model_epoch(sg, cfg, grid)
     W = m.weights()
     part = og.partition_2d(g.src, g.dst, V, V)
-    ref, r32 = (saga.gcn_epoch(part, X.astype(dt), [w.astype(dt) for w in W], rng.labels(V, cfg["C"], seed=3),
-                               og.gcn_edge_weights(g.src, g.dst, V, dt)) for dt in (np.float64, np.float32))
+    lab = rng.labels(V, cfg["C"], seed=3)
+    args = lambda dt: (part, X.astype(dt), [w.astype(dt) for w in W], lab,  # noqa: E731
+                       og.gcn_edge_weights(g.src, g.dst, V, dt))
+    free = saga.gcn_epoch(*args(np.float64))
+    # the backward follows the GPU's ReLU masks (flips only at kinks |z| ~ rounding level)
+    masks = route_relu_masks([L.z.cpu().numpy() for L in m.layers], free["z"], what="pubmed")
+    ref, r32 = (saga.gcn_epoch(*args(dt), masks=masks) for dt in (np.float64, np.float32))
     rl = float(np.ravel(ref["loss"])[0])
     assert abs(m.loss.item() - rl) <= 1e-4 * abs(rl), (m.loss.item(), rl)
     for k, (got, want, w32) in enumerate(zip(_outs(m), ref["out"], r32["out"])):
@@ -97,15 +102,30 @@ def _check_fixture(m, fx, n_grads):
         assert_close(got, fx[f"grad{k}"], what=f"grad{k}", floor=max(FLOOR, 2 * float(fx[f"floor32_grad{k}"])))
 
 
-def test_reddit_config_epoch_vs_fp64_fixture():
-    """BASELINE config 2 (the bench workload) at full size: the same epoch the bench times."""
+def test_reddit_config_epoch_vs_fp64_oracle(reddit_oracle):
+    """BASELINE config 2 (the bench workload) at full size -- the same epoch the bench times --
+    vs the fp64 full-size oracle run live (pinned to the committed fixture made here): loss,
+    activation rows, dW0, dW1.  The oracle's backward follows the GPU's ReLU masks after every
+    disagreement is checked to be a kink (conftest.route_relu_masks)."""
     import paper_1810_08403_b200 as sg
+    from oracle import fullsize as fs
 
-    cfg = dict(model="gcn", V=232965, E=114615892, F=602, H=128, C=41)
-    g = sg.rmat_graph(cfg["V"], cfg["E"], seed=0)
-    grid = sg.ChunkGrid(g, cfg["V"])
+    R = reddit_oracle
+    cfg = dict(model="gcn", V=R["V"], E=R["E"], F=R["F"], H=R["H"], C=R["C"])
+    grid = sg.ChunkGrid(R["g"], cfg["V"])
     m, _ = _model_epoch(sg, cfg, grid)
-    _check_fixture(m, _fixture("reddit"), 2)
+    f, fx = R["fwd"], _fixture("reddit")
+    assert abs(float(np.ravel(f["loss"])[0]) - float(fx["loss"])) <= 1e-10 * float(fx["loss"])
+    masks = route_relu_masks([L.z.cpu().numpy() for L in m.layers], f["z"], what="reddit")
+    grads = fs.gcn_backward(f, masks)
+    rl = float(fx["loss"])
+    assert abs(m.loss.item() - rl) <= 1e-4 * abs(rl), (m.loss.item(), rl)
+    rows = fx["rows"]
+    for k, h in enumerate(_outs(m)):
+        assert_close(h[rows], fx[f"out{k}_rows"], what=f"h{k + 1} rows",
+                     floor=max(FLOOR, 2 * float(fx[f"floor32_out{k}_rows"])))
+    for k, (got, want) in enumerate(zip(m.grads(), grads)):
+        assert_close(got, want, what=f"dW{k}", floor=max(FLOOR, 2 * float(fx[f"floor32_grad{k}"])))
 
 
 def test_blogcatalog10_ggcn_config_epoch_vs_fp64_fixture():
