@@ -319,11 +319,26 @@ int sg_check_finite(int dtype, const void* X, int64_t rows, int64_t cols, int64_
 /* Elementwise ops used by unfused ApplyEdge programs (tensor.py:204-303):
  * op 0 add, 1 sub, 2 mul, 3 div, 4 max, 5 sigmoid, 6 tanh, 7 relu,
  * 8 relu-backward (a * (b > 0), tensor.py:236),
- * 9 sigmoid-backward (a * b * (1 - b) with b = y, tensor.py:232); b is broadcast
+ * 9 sigmoid-backward (a * b * (1 - b) with b = y, tensor.py:232),
+ * 10 tanh-backward (a * (1 - b * b) with b = y, tensor.py:234); b is broadcast
  * per row when b_cols == 1 (the "b_row" kind, tensor.py:184-185), along the
  * leading axis when b_rows == 1 ("b_lead"). */
 int sg_ewise(int op, int64_t rows, int64_t cols, const float* a, int64_t lda, const float* b,
              int64_t b_rows, int64_t b_cols, int64_t ldb, float* out, int64_t ldo, void* stream);
+/* Backward of binary op 0-4 (the bwd closure of _binary, tensor.py:255-265): given the
+ * upstream gradient g and the forward operands a (full [rows, cols]) and b (broadcast as in
+ * sg_ewise), writes both full-shape partials ga, gb (add: g, g; sub: g, -g; mul: g*b, g*a;
+ * div: g/b, -g*a/(b*b); max: g*(a>=b), g*!(a>=b) -- ties route to a).  The caller reduces
+ * a broadcast side back to its shape with sg_reduce_sum (_reduce_to, tensor.py:191-201). */
+int sg_ewise_bwd(int op, int64_t rows, int64_t cols, const float* g, int64_t ldg, const float* a,
+                 int64_t lda, const float* b, int64_t b_rows, int64_t b_cols, int64_t ldb, float* ga,
+                 int64_t ldga, float* gb, int64_t ldgb, void* stream);
+/* _reduce_to's sums (tensor.py:197-201): axis 1 -> out[rows] = row sums (row-scalar side),
+ * axis 0 -> out[cols] = column sums over the broadcast leading axis (fixed-order partials in
+ * the caller-owned workspace of sg_reduce_workspace_bytes(cols) bytes).  Deterministic. */
+int64_t sg_reduce_workspace_bytes(int64_t cols);
+int sg_reduce_sum(int axis, const float* X, int64_t ld, int64_t rows, int64_t cols, float* out,
+                  void* workspace, int64_t workspace_bytes, void* stream);
 /* GG-NN ApplyVertex = GRU(vertex, accum) (Li et al. form,
  * no biases), the element-wise stages around the ApplyVertex GEMMs.  G1 = a [Wz|Wr|Wh],
  * G2 = h [Uz|Ur], G3 = (r*h) Uh, gate blocks at column stride bs (>= F); z/r/rh/c share ldo.

@@ -26,6 +26,7 @@ __all__ = [
     "fuse_sag", "hoist_vertex_computation", "make_program", "matmul_rows", "optimize", "trace_udf",
     "validate_program", "vertex_form", "SAGAModel", "gcn_model", "ggcn_model", "mpgcn_model", "commnet_model", "run_train",
     "StreamingGCN", "StreamingGGCN", "HostGrid", "GGNNModel", "ggnn_model", "build_ggnn",
+    "UnfusedSAGAModel", "unfused_model",
 ]
 
 
@@ -40,6 +41,10 @@ def __getattr__(name):
         from . import ggnn
 
         return getattr(ggnn, name)
+    if name in ("UnfusedSAGAModel", "unfused_model"):
+        from . import stages
+
+        return getattr(stages, name)
     if name in ("StreamingGCN", "StreamingGGCN", "HostGrid"):
         from . import stream
 

@@ -103,6 +103,10 @@ _SIGS = {
     "sg_sgd": (_i32, [_p, _p, _i64, _f32, _p]),
     "sg_check_finite": (_i32, [_i32, _p, _i64, _i64, _i64, _p, _p]),
     "sg_ewise": (_i32, [_i32, _i64, _i64, _p, _i64, _p, _i64, _i64, _i64, _p, _i64, _p]),
+    "sg_ewise_bwd": (_i32, [_i32, _i64, _i64, _p, _i64, _p, _i64, _p, _i64, _i64, _i64, _p, _i64, _p,
+                            _i64, _p]),
+    "sg_reduce_workspace_bytes": (_i64, [_i64]),
+    "sg_reduce_sum": (_i32, [_i32, _p, _i64, _i64, _i64, _p, _p, _i64, _p]),
     "sg_max_plan_workspace_bytes": (_i64, [_i64, _i64, _i64]),
     "sg_max_gather_plan": (_i32, [_p, _p, _p, _i64, _p, _i64, _i64, _p, _i64, _p, _i64, _p, _i64, _i64,
                                   _f32, _i64, _i32, _i32, _p, _i64, _p]),

@@ -133,9 +133,84 @@ __global__ void ewise_kernel(int op, int64_t rows, int64_t cols, const float* a,
       case 6: y = tanhf(x); break;
       case 7: y = sg::relu_np(x); break;
       case 8: y = __fmul_rn(x, w > 0.f ? 1.f : 0.f); break;  // relu bwd: g * (z > 0)
-      default: y = __fmul_rn(__fmul_rn(x, w), __fsub_rn(1.0f, w)); break;  // sigmoid bwd g*y*(1-y)
+      case 9: y = __fmul_rn(__fmul_rn(x, w), __fsub_rn(1.0f, w)); break;  // sigmoid bwd g*y*(1-y)
+      default: y = __fmul_rn(x, __fsub_rn(1.0f, __fmul_rn(w, w))); break;  // tanh bwd g*(1-y*y)
     }
     out[r * ldo + c] = y;
+  }
+}
+
+// Backward of the binary ops (tensor.py:255-265), both partials in one pass over the full
+// [rows, cols] shape: x is a (already expanded by the caller), w is b with its broadcast.  The
+// reductions of _reduce_to (tensor.py:191-201) run afterwards in reduce_*_kernel.
+__global__ void ewise_bwd_kernel(int op, int64_t rows, int64_t cols, const float* g, int64_t ldg,
+                                 const float* a, int64_t lda, const float* b, int64_t b_rows,
+                                 int64_t b_cols, int64_t ldb, float* ga, int64_t ldga, float* gb,
+                                 int64_t ldgb) {
+  const int64_t total = rows * cols;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = t / cols, c = t % cols;
+    const float gv = g[r * ldg + c];
+    const float x = a[r * lda + c];
+    const float w = b[(b_rows == 1 ? 0 : r) * ldb + (b_cols == 1 ? 0 : c)];
+    float u, v;
+    switch (op) {
+      case 0: u = gv; v = gv; break;                                   // add
+      case 1: u = gv; v = -gv; break;                                  // sub
+      case 2: u = __fmul_rn(gv, w); v = __fmul_rn(gv, x); break;       // mul
+      case 3:                                                          // div: g/w, -g*x/(w*w)
+        u = __fdiv_rn(gv, w);
+        v = __fdiv_rn(__fmul_rn(-gv, x), __fmul_rn(w, w));
+        break;
+      default: {                                                       // max: ties -> a
+        const bool m = x >= w;
+        u = __fmul_rn(gv, m ? 1.f : 0.f);
+        v = __fmul_rn(gv, m ? 0.f : 1.f);
+      }
+    }
+    ga[r * ldga + c] = u;
+    gb[r * ldgb + c] = v;
+  }
+}
+
+// out[r] = sum_c X[r, c] (the "row-scalar side" of _reduce_to, tensor.py:201): one warp per
+// row, lanes stride the columns, fixed shuffle tree -- deterministic.
+__global__ void reduce_cols_kernel(const float* X, int64_t ld, int64_t rows, int64_t cols, float* out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = warp; r < rows; r += nwarps) {
+    float acc = 0.f;
+    for (int64_t c = lane; c < cols; c += 32) acc = __fadd_rn(acc, X[r * ld + c]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc = __fadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o));
+    if (lane == 0) out[r] = acc;
+  }
+}
+
+// Leading-axis reduction (tensor.py:197-198, g.sum over the broadcast rows) in two fixed-order
+// passes: kRedParts row ranges -> partial[kRedParts, cols], then the partials in order.
+constexpr int kRedParts = 148;
+
+__global__ void reduce_rows_partial_kernel(const float* X, int64_t ld, int64_t rows, int64_t cols,
+                                           float* part) {
+  const int64_t chunk = (rows + kRedParts - 1) / kRedParts;
+  const int64_t r0 = (int64_t)blockIdx.y * chunk, r1 = min(rows, r0 + chunk);
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < cols;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    float acc = 0.f;
+    for (int64_t r = r0; r < r1; ++r) acc = __fadd_rn(acc, X[r * ld + c]);
+    part[(int64_t)blockIdx.y * cols + c] = acc;
+  }
+}
+
+__global__ void reduce_rows_final_kernel(const float* part, int64_t cols, float* out) {
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < cols;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    float acc = 0.f;
+    for (int p = 0; p < kRedParts; ++p) acc = __fadd_rn(acc, part[(int64_t)p * cols + c]);
+    out[c] = acc;
   }
 }
 
@@ -219,13 +294,52 @@ int sg_check_finite(int dtype, const void* X, int64_t rows, int64_t cols, int64_
 
 int sg_ewise(int op, int64_t rows, int64_t cols, const float* a, int64_t lda, const float* b,
              int64_t b_rows, int64_t b_cols, int64_t ldb, float* out, int64_t ldo, void* stream) {
-  SG_REQUIRE(op >= 0 && op <= 9, SG_EINVAL, "ewise: unknown op %d", op);
+  SG_REQUIRE(op >= 0 && op <= 10, SG_EINVAL, "ewise: unknown op %d", op);
   SG_REQUIRE((op > 4 && op < 8) || b, SG_EINVAL, "ewise: binary op needs b");
   if (rows == 0 || cols == 0) return SG_OK;
   ewise_kernel<<<grid_for(rows * cols, 256), 256, 0, (cudaStream_t)stream>>>(
       op, rows, cols, a, lda, b, b_rows, b_cols, ldb, out, ldo);
   SG_LAUNCH_CHECK("ewise");
   sg::count_launch(1);
+  return SG_OK;
+}
+
+int sg_ewise_bwd(int op, int64_t rows, int64_t cols, const float* g, int64_t ldg, const float* a,
+                 int64_t lda, const float* b, int64_t b_rows, int64_t b_cols, int64_t ldb, float* ga,
+                 int64_t ldga, float* gb, int64_t ldgb, void* stream) {
+  SG_REQUIRE(op >= 0 && op <= 4, SG_EINVAL, "ewise_bwd: unknown binary op %d", op);
+  SG_REQUIRE(g && a && b && ga && gb, SG_EINVAL, "ewise_bwd: null operand");
+  if (rows == 0 || cols == 0) return SG_OK;
+  ewise_bwd_kernel<<<grid_for(rows * cols, 256), 256, 0, (cudaStream_t)stream>>>(
+      op, rows, cols, g, ldg, a, lda, b, b_rows, b_cols, ldb, ga, ldga, gb, ldgb);
+  SG_LAUNCH_CHECK("ewise_bwd");
+  sg::count_launch(1);
+  return SG_OK;
+}
+
+int64_t sg_reduce_workspace_bytes(int64_t cols) { return (int64_t)kRedParts * std::max<int64_t>(cols, 1) * 4; }
+
+int sg_reduce_sum(int axis, const float* X, int64_t ld, int64_t rows, int64_t cols, float* out,
+                  void* workspace, int64_t workspace_bytes, void* stream) {
+  SG_REQUIRE(axis == 0 || axis == 1, SG_EINVAL, "reduce_sum: axis must be 0 or 1");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (axis == 1) {
+    if (rows == 0) return SG_OK;
+    if (cols == 0) return cudaMemsetAsync(out, 0, rows * 4, st) == cudaSuccess ? SG_OK : SG_ECUDA;
+    reduce_cols_kernel<<<grid_for(rows * 32, 256), 256, 0, st>>>(X, ld, rows, cols, out);
+    SG_LAUNCH_CHECK("reduce_sum cols");
+    sg::count_launch(1);
+    return SG_OK;
+  }
+  if (cols == 0) return SG_OK;
+  SG_REQUIRE(workspace_bytes >= sg_reduce_workspace_bytes(cols), SG_EBUDGET, "reduce workspace too small");
+  float* part = (float*)workspace;
+  dim3 g1((unsigned)std::min<int64_t>((cols + 127) / 128, 64), kRedParts);
+  reduce_rows_partial_kernel<<<g1, 128, 0, st>>>(X, ld, rows, cols, part);
+  SG_LAUNCH_CHECK("reduce_sum rows partial");
+  reduce_rows_final_kernel<<<grid_for(cols, 128), 128, 0, st>>>(part, cols, out);
+  SG_LAUNCH_CHECK("reduce_sum rows final");
+  sg::count_launch(2);
   return SG_OK;
 }
 

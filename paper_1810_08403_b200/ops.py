@@ -219,13 +219,37 @@ def _ewise_raw(op, a, b=None):
 
 
 def _reduce_to(g, shape, kind, side):
-    """tensor.py:191-201."""
+    """tensor.py:191-201, on the device (sg_reduce_sum: fixed-order sums, no torch reduction)."""
     if kind == "equal" or (kind == "b_lead" and side == "a") or (kind == "a_lead" and side == "b") \
             or (kind == "b_row" and side == "a") or (kind == "a_row" and side == "b"):
         return g
+    g2 = _as2d(g).contiguous()
     if kind in ("a_lead", "b_lead"):
-        return g.sum(dim=tuple(range(g.dim() - len(shape))))
-    return g.sum(dim=1, keepdim=True)
+        n = 1
+        for d in shape:
+            n *= d
+        g2 = g2.reshape(-1, n)
+        out = torch.empty(n, dtype=g.dtype, device=g.device)
+        ws = torch.empty(int(_lib.lib.sg_reduce_workspace_bytes(n)), dtype=torch.uint8, device=g.device)
+        _lib.check(_lib.lib.sg_reduce_sum(0, g2.data_ptr(), g2.stride(0), g2.shape[0], n, out.data_ptr(),
+                                          ws.data_ptr(), ws.numel(), _lib.stream_handle()))
+        return out.reshape(shape)
+    out = torch.empty((g2.shape[0], 1), dtype=g.dtype, device=g.device)
+    _lib.check(_lib.lib.sg_reduce_sum(1, g2.data_ptr(), g2.stride(0), g2.shape[0], g2.shape[1],
+                                      out.data_ptr(), None, 0, _lib.stream_handle()))
+    return out
+
+
+def _b_view(b, a_shape):
+    """(tensor, b_rows, b_cols, ldb) of operand b broadcast against a [rows, cols] view of a."""
+    b2 = b.contiguous()
+    if tuple(b2.shape) == tuple(a_shape):
+        b2 = _as2d(b2)
+        return b2, b2.shape[0], b2.shape[1], b2.stride(0)
+    if b2.dim() == 2 and b2.shape[1] == 1:             # b_row
+        return b2, b2.shape[0], 1, b2.stride(0)
+    b2 = b2.reshape(1, -1)                             # b_lead
+    return b2, 1, b2.shape[1], b2.shape[1]
 
 
 class _Binary(torch.autograd.Function):
@@ -239,25 +263,31 @@ class _Binary(torch.autograd.Function):
         else:
             y = _ewise_raw(op, a, b)
         ctx.op, ctx.kind = op, kind
+        ctx.a_shape, ctx.b_shape = tuple(a.shape), tuple(b.shape)
         ctx.save_for_backward(a, b)
         return y
 
     @staticmethod
     def backward(ctx, g):
+        # both partials in one sg_ewise_bwd pass (tensor.py:255-265), then _reduce_to
         a, b = ctx.saved_tensors
         op, kind = ctx.op, ctx.kind
-        if op == "add":
-            ga, gb = g, g
-        elif op == "sub":
-            ga, gb = g, -g
-        elif op == "mul":
-            ga, gb = g * b, g * a
-        elif op == "div":
-            ga, gb = g / b, -g * a / (b * b)
+        if kind in ("a_lead", "a_row"):
+            a = a.expand(b.shape)
+            ae, be = a.contiguous(), b
         else:
-            mask = a >= b
-            ga, gb = g * mask, g * ~mask
-        return None, _reduce_to(ga, a.shape, kind, "a"), _reduce_to(gb, b.shape, kind, "b")
+            ae, be = a, b
+        a2 = _as2d(ae).contiguous()
+        g2 = _as2d(g).contiguous()
+        b2, br, bc, ldb = _b_view(be, ae.shape)
+        ga = torch.empty_like(a2)
+        gb = torch.empty_like(a2)
+        _lib.check(_lib.lib.sg_ewise_bwd(_OPS[op], a2.shape[0], a2.shape[1], g2.data_ptr(), g2.stride(0),
+                                         a2.data_ptr(), a2.stride(0), b2.data_ptr(), br, bc, ldb,
+                                         ga.data_ptr(), ga.stride(0), gb.data_ptr(), gb.stride(0),
+                                         _lib.stream_handle()))
+        ga, gb = ga.reshape(ae.shape), gb.reshape(ae.shape)
+        return None, _reduce_to(ga, ctx.a_shape, kind, "a"), _reduce_to(gb, ctx.b_shape, kind, "b")
 
 
 class _Unary(torch.autograd.Function):
@@ -270,12 +300,17 @@ class _Unary(torch.autograd.Function):
 
     @staticmethod
     def backward(ctx, g):
+        # tensor.py:231-236 on the device: sigmoid g*y*(1-y) (op 9), tanh g*(1-y*y) (op 10),
+        # relu g*(x>0) (op 8, gradient 0 at 0)
         a, y = ctx.saved_tensors
-        if ctx.op == "sigmoid":
-            return None, g * y * (1.0 - y)
-        if ctx.op == "tanh":
-            return None, g * (1.0 - y * y)
-        return None, g * (a > 0.0)  # relu: gradient at 0 is 0 (tensor.py:236)
+        code, other = {"sigmoid": (9, y), "tanh": (10, y), "relu": (8, a)}[ctx.op]
+        g2 = _as2d(g).contiguous()
+        o2 = _as2d(other).contiguous()
+        out = torch.empty_like(g2)
+        _lib.check(_lib.lib.sg_ewise(code, g2.shape[0], g2.shape[1], g2.data_ptr(), g2.stride(0),
+                                     o2.data_ptr(), o2.shape[0], o2.shape[1], o2.stride(0),
+                                     out.data_ptr(), out.stride(0), _lib.stream_handle()))
+        return None, out.reshape(g.shape)
 
 
 def _binary(op, a, b):
@@ -336,7 +371,7 @@ class _Matmul(torch.autograd.Function):
     @staticmethod
     def forward(ctx, a, b):
         out = torch.empty((a.shape[0], b.shape[1]), dtype=torch.float32, device=a.device)
-        K.gemm(a.contiguous(), b.contiguous(), out)
+        K.gemm(a.contiguous(), b.contiguous(), out, prec=_lib.GEMM_TF32X3)
         ctx.save_for_backward(a, b)
         return out
 
@@ -346,8 +381,9 @@ class _Matmul(torch.autograd.Function):
         g = g.contiguous()
         ga = torch.empty_like(a)
         gb = torch.empty_like(b)
-        K.gemm(g, b.contiguous(), ga, trans_b=True)   # g @ w.T  (tensor.py:317)
-        K.gemm(a.contiguous(), g, gb, trans_a=True)   # x.T @ g
+        # tcgen05 3xTF32 (fp32-parity error bound), like the forward
+        K.gemm(g, b.contiguous(), ga, trans_b=True, prec=_lib.GEMM_TF32X3)   # g @ w.T  (tensor.py:317)
+        K.gemm(a.contiguous(), g, gb, trans_a=True, prec=_lib.GEMM_TF32X3)   # x.T @ g
         return ga, gb
 
 
