@@ -113,16 +113,6 @@ int sg_host_gcn_weights(const int32_t* src, const int32_t* dst, const int64_t* d
 int sg_host_plan(const int64_t* ptr, int64_t n_rows, int64_t pack_edges, int64_t max_rows,
                  int64_t split_edges, sg_item* items, sg_split* splits, int64_t* n_items,
                  int64_t* n_splits, int64_t* n_slots);
-/* Run-length encoding of a pass index: consecutive edges of a row with the same (idx, w) --
- * multi-edges -- become one entry with a count (<= 65535), never crossing a split_edges subgroup
- * boundary of the row.  rptr[n_rows + 1] counts entries; call with ridx == NULL to size. */
-int sg_host_rle(const int64_t* ptr, const int32_t* idx, const float* w, int64_t n_rows, int64_t split_edges,
-                int64_t* rptr, int32_t* ridx, float* rw, uint16_t* rcnt, int64_t* n_entries);
-/* sg_host_plan's plan (same split decisions and slots, from the edge ptr) with its item ranges
- * expressed in entries of the run-length encoded index (rptr, rcnt). */
-int sg_host_plan_rle(const int64_t* ptr, const int64_t* rptr, const uint16_t* rcnt, int64_t n_rows,
-                     int64_t pack_edges, int64_t max_rows, int64_t split_edges, sg_item* items,
-                     sg_split* splits, int64_t* n_items, int64_t* n_splits, int64_t* n_slots);
 /* Reorder a plan's split items (in place) by the source of their first edge (idx[e_begin]),
  * then row and subgroup, so that subgroups covering the same sources are adjacent in the work
  * queue (results are independent of the item order). */
@@ -167,16 +157,6 @@ int sg_propagate(int mode, int dtype, const int64_t* ptr, const int32_t* idx, co
                  const void* R, int64_t ldr, int64_t r_off, void* out0, int64_t ld0, void* out1,
                  int64_t ld1, const void* mask, int64_t ldm, int64_t F, int accumulate,
                  void* workspace, int64_t workspace_bytes, void* stream);
-
-/* sg_propagate over a run-length encoded index (sg_host_rle / sg_host_plan_rle): ptr, idx, w
- * and the plan count entries, and entry e's term is added cnt[e] times in place -- the same
- * sequence of IEEE adds as the edge-level pass (bitwise identical), one row load per entry. */
-int sg_propagate_rle(int mode, int dtype, const int64_t* ptr, const int32_t* idx, const float* w,
-                     const uint16_t* cnt, int64_t n_rows, const sg_item* items, int64_t n_items,
-                     const sg_split* splits, int64_t n_splits, int64_t n_slots, const void* G, int64_t ldg,
-                     int64_t g_off, const void* R, int64_t ldr, int64_t r_off, void* out0, int64_t ld0,
-                     void* out1, int64_t ld1, const void* mask, int64_t ldm, int64_t F, int accumulate,
-                     void* workspace, int64_t workspace_bytes, void* stream);
 
 /* sg_propagate with a hub-row cache (GCN / PASS modes, rows wider than 16 vectors).
  * The n_hub most referenced gathered rows (hub_rows[0..n_hub), int32 row ids of G) are

@@ -309,78 +309,6 @@ int sg_host_plan(const int64_t* ptr, int64_t n_rows, int64_t pack_edges, int64_t
   return SG_OK;
 }
 
-int sg_host_rle(const int64_t* ptr, const int32_t* idx, const float* w, int64_t n_rows, int64_t split_edges,
-                int64_t* rptr, int32_t* ridx, float* rw, uint16_t* rcnt, int64_t* n_entries) {
-  SG_REQUIRE(ptr && idx && rptr && n_entries && split_edges >= 1, SG_EINVAL, "rle: null pointer");
-  // per row: count entries (two passes, rows in parallel), then fill
-  std::vector<int64_t> cnt(n_rows + 1, 0);
-  auto breaks = [&](int64_t r, int64_t e) {  // does edge e start a new entry of row r?
-    if (e == ptr[r] || (e - ptr[r]) % split_edges == 0) return true;  // row start / subgroup start
-    if (idx[e] != idx[e - 1]) return true;
-    return w && std::memcmp(&w[e], &w[e - 1], sizeof(float)) != 0;
-  };
-#pragma omp parallel for schedule(dynamic, 1024)
-  for (int64_t r = 0; r < n_rows; ++r) {
-    int64_t c = 0, run = 0;
-    for (int64_t e = ptr[r]; e < ptr[r + 1]; ++e) {
-      if (breaks(r, e) || run == 65535) {
-        c++;
-        run = 0;
-      }
-      run++;
-    }
-    cnt[r + 1] = c;
-  }
-  rptr[0] = 0;
-  for (int64_t r = 0; r < n_rows; ++r) rptr[r + 1] = rptr[r] + cnt[r + 1];
-  *n_entries = rptr[n_rows];
-  if (!ridx) return SG_OK;
-#pragma omp parallel for schedule(dynamic, 1024)
-  for (int64_t r = 0; r < n_rows; ++r) {
-    int64_t k = rptr[r] - 1, run = 0;
-    for (int64_t e = ptr[r]; e < ptr[r + 1]; ++e) {
-      if (breaks(r, e) || run == 65535) {
-        k++;
-        ridx[k] = idx[e];
-        if (rw) rw[k] = w[e];
-        run = 0;
-      }
-      run++;
-      rcnt[k] = (uint16_t)run;
-    }
-  }
-  return SG_OK;
-}
-
-int sg_host_plan_rle(const int64_t* ptr, const int64_t* rptr, const uint16_t* rcnt, int64_t n_rows,
-                     int64_t pack_edges, int64_t max_rows, int64_t split_edges, sg_item* items,
-                     sg_split* splits, int64_t* n_items, int64_t* n_splits, int64_t* n_slots) {
-  // the edge-level plan (same split decisions, subgroup count and slots), then its edge offsets
-  // rewritten as entry offsets: a split subgroup starts at an entry boundary by construction
-  int rc = sg_host_plan(ptr, n_rows, pack_edges, max_rows, split_edges, items, splits, n_items, n_splits,
-                        n_slots);
-  if (rc != SG_OK || !items) return rc;
-#pragma omp parallel for schedule(dynamic, 64)
-  for (int64_t i = 0; i < *n_items; ++i) {
-    sg_item& it = items[i];
-    if (it.split < 0) {
-      it.e_begin = rptr[it.row_begin];
-      it.e_end = rptr[it.row_end];
-      continue;
-    }
-    const int64_t r = it.row_begin;
-    // walk the row's entries to the subgroup's first edge (it.sub * split_edges edges in)
-    int64_t edges = 0, k = rptr[r];
-    const int64_t want0 = (int64_t)it.sub * split_edges, want1 = want0 + (it.e_end - it.e_begin);
-    while (edges < want0) edges += rcnt[k++];
-    const int64_t kb = k;
-    while (edges < want1) edges += rcnt[k++];
-    it.e_begin = kb;
-    it.e_end = k;
-  }
-  return SG_OK;
-}
-
 int sg_host_plan_order(sg_item* items, int64_t n_items, const int32_t* idx) {
   SG_REQUIRE(n_items >= 0 && (n_items == 0 || (items && idx)), SG_EINVAL, "plan_order: null pointer");
   int64_t ns = 0;

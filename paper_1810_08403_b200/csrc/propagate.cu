@@ -189,9 +189,6 @@ struct PropArgs {
   int32_t accumulate;
   const int32_t* hub_rows;  // hub-row cache: idx < 0 means slot (idx & 0x7fffffff) in smem
   int32_t n_hub;
-  // run-length encoded pass (sg_propagate_rle): entry e stands for cnt[e] consecutive edges with
-  // the same (idx, w) -- multi-edges -- and ptr / items count entries, not edges
-  const uint16_t* cnt;
 };
 
 template <int MODE, int DT, int W, int VPL, int LPR, int DEPTH, bool HUB = false>
@@ -297,45 +294,24 @@ struct Prop {
       // ballot (a lane heads a run unless it repeats the previous lane's (src, w)), the run
       // heads broadcast by shuffle DEPTH at a time; the next window is prefetched while this
       // one is consumed.  A run split by a window boundary is just two runs.
-      const bool rle = a.cnt != nullptr;
       int n_next = (int)min((int64_t)32, e1 - e0);
-      int src_next = 0, cnt_next = 1;
+      int src_next = 0;
       float w_next = 0.f;
       if (tl < n_next) {
         src_next = __ldcs(a.idx + e0 + tl);
         if (M::USE_W) w_next = __ldcs(a.w + e0 + tl);
-        if (rle) cnt_next = __ldcs(a.cnt + e0 + tl);
       }
       #pragma unroll 1
       for (int64_t eb = e0; eb < e1; eb += 32) {
         const int n = n_next;
-        const int my_src = src_next, my_rc = cnt_next;
+        const int my_src = src_next;
         const float my_w = w_next;
         n_next = (int)min((int64_t)32, e1 - (eb + 32));
         if (tl < n_next) {
           src_next = __ldcs(a.idx + eb + 32 + tl);
           if (M::USE_W) w_next = __ldcs(a.w + eb + 32 + tl);
-          if (rle) cnt_next = __ldcs(a.cnt + eb + 32 + tl);
         }
-        if (rle) {
-          // host run-length encoded entries: one row load per entry, its term added cnt times
-          int d0 = 0;
-          #pragma unroll 1
-          for (; d0 < n; d0 += DEPTH) {
-            int s[DEPTH], cnt[DEPTH];
-            float wv[DEPTH];
-#pragma unroll
-            for (int d = 0; d < DEPTH; ++d) {
-              s[d] = __shfl_sync(0xffffffffu, my_src, (d0 + d) & 31);
-              wv[d] = M::USE_W ? __shfl_sync(0xffffffffu, my_w, (d0 + d) & 31) : 0.f;
-              cnt[d] = __shfl_sync(0xffffffffu, my_rc, (d0 + d) & 31);
-            }
-            if (d0 + DEPTH <= n)
-              step<true, true>(a, gl, hl, last_ok, s, wv, cnt, DEPTH, rs, acc);
-            else
-              step<false, true>(a, gl, hl, last_ok, s, wv, cnt, n - d0, rs, acc);
-          }
-        } else if constexpr (kRuns) {
+        if constexpr (kRuns) {
           const int prev_src = __shfl_up_sync(0xffffffffu, my_src, 1);
           const float prev_w = __shfl_up_sync(0xffffffffu, my_w, 1);
           const bool head = tl < n && (tl == 0 || prev_src != my_src ||
@@ -396,8 +372,7 @@ struct Prop {
       // every window slot is loaded by some team lane (a DEPTH of 6 with 4-lane teams would
       // leave slots 4-5 unloaded), and a multi-slot window is exactly one step
       static_assert(WIN % LPR == 0 && (WPL == 1 || WIN == DEPTH), "DEPTH must be a multiple of LPR");
-      const bool rle = a.cnt != nullptr;
-      int src_next[WPL], cnt_next[WPL];
+      int src_next[WPL];
       float w_next[WPL];
       int n_next = (int)min((int64_t)WIN, e1 - e0);
 #pragma unroll
@@ -405,18 +380,16 @@ struct Prop {
         const int k = q * LPR + tl;
         src_next[q] = k < n_next ? __ldcs(a.idx + e0 + k) : 0;
         w_next[q] = (M::USE_W && k < n_next) ? __ldcs(a.w + e0 + k) : 0.f;
-        cnt_next[q] = (rle && k < n_next) ? (int)__ldcs(a.cnt + e0 + k) : 1;
       }
       #pragma unroll 1
       for (int64_t eb = e0; eb < e1; eb += WIN) {
         const int n = n_next;
-        int my_src[WPL], my_rc[WPL];
+        int my_src[WPL];
         float my_w[WPL];
 #pragma unroll
         for (int q = 0; q < WPL; ++q) {
           my_src[q] = src_next[q];
           my_w[q] = w_next[q];
-          my_rc[q] = cnt_next[q];
         }
         n_next = (int)min((int64_t)WIN, e1 - (eb + WIN));
 #pragma unroll
@@ -425,32 +398,7 @@ struct Prop {
           if (k < n_next) {
             src_next[q] = __ldcs(a.idx + eb + WIN + k);
             if (M::USE_W) w_next[q] = __ldcs(a.w + eb + WIN + k);
-            if (rle) cnt_next[q] = __ldcs(a.cnt + eb + WIN + k);
           }
-        }
-        if (rle) {
-          // host run-length encoded entries (one row load per entry, term added cnt times)
-          int d0 = 0;
-          #pragma unroll 1
-          for (; d0 < n; d0 += DEPTH) {
-            int s[DEPTH], cnt[DEPTH];
-            float wv[DEPTH];
-#pragma unroll
-            for (int d = 0; d < DEPTH; ++d) {
-              // WPL > 1: WIN == DEPTH, one step per window (d0 == 0) and the slot index is a
-              // compile-time constant; WPL == 1: slot 0, lane (d0 + d) % LPR
-              const int e = WPL > 1 ? d : d0 + d;
-              const int q = WPL > 1 ? d / LPR : 0;
-              s[d] = __shfl_sync(tmask, my_src[q], e % LPR, LPR);
-              wv[d] = M::USE_W ? __shfl_sync(tmask, my_w[q], e % LPR, LPR) : 0.f;
-              cnt[d] = __shfl_sync(tmask, my_rc[q], e % LPR, LPR);
-            }
-            if (d0 + DEPTH <= n)
-              step<true, true>(a, gl, hl, last_ok, s, wv, cnt, DEPTH, rs, acc);
-            else
-              step<false, true>(a, gl, hl, last_ok, s, wv, cnt, n - d0, rs, acc);
-          }
-          continue;
         }
         if constexpr (WPL > 1) {
           // WIN == DEPTH: one step per window, edge d sits in slot d / LPR of lane d % LPR
@@ -838,14 +786,6 @@ cudaError_t dispatch_mode(int dtype, bool vec, bool half_vec, const PropArgs& a,
 
 inline bool aligned(const void* p, int bytes) { return p == nullptr || ((uintptr_t)p % bytes) == 0; }
 
-int propagate_impl(int mode, int dtype, const int64_t* ptr, const int32_t* idx, const float* w,
-                   const uint16_t* cnt, int64_t n_rows, const sg_item* items, int64_t n_items,
-                   const sg_split* splits, int64_t n_splits, int64_t n_slots, const void* G, int64_t ldg,
-                   int64_t g_off, const void* R, int64_t ldr, int64_t r_off, void* out0, int64_t ld0,
-                   void* out1, int64_t ld1, const void* mask, int64_t ldm, int64_t F, int accumulate,
-                   const int32_t* hub_rows, int64_t n_hub, void* workspace, int64_t workspace_bytes,
-                   void* stream);
-
 inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
 }  // namespace
@@ -888,13 +828,6 @@ int64_t sg_propagate_hub_capacity(int64_t F, int dtype) {
   return std::min<int64_t>(hub_smem_bytes() / row_bytes, INT32_MAX);
 }
 
-int sg_propagate_rle(int mode, int dtype, const int64_t* ptr, const int32_t* idx, const float* w,
-                     const uint16_t* cnt, int64_t n_rows, const sg_item* items, int64_t n_items,
-                     const sg_split* splits, int64_t n_splits, int64_t n_slots, const void* G, int64_t ldg,
-                     int64_t g_off, const void* R, int64_t ldr, int64_t r_off, void* out0, int64_t ld0,
-                     void* out1, int64_t ld1, const void* mask, int64_t ldm, int64_t F, int accumulate,
-                     void* workspace, int64_t workspace_bytes, void* stream);
-
 int sg_propagate_hub(int mode, int dtype, const int64_t* ptr, const int32_t* idx, const float* w,
                      int64_t n_rows, const sg_item* items, int64_t n_items, const sg_split* splits,
                      int64_t n_splits, int64_t n_slots, const void* G, int64_t ldg, int64_t g_off,
@@ -902,34 +835,6 @@ int sg_propagate_hub(int mode, int dtype, const int64_t* ptr, const int32_t* idx
                      int64_t ld1, const void* mask, int64_t ldm, int64_t F, int accumulate,
                      const int32_t* hub_rows, int64_t n_hub, void* workspace, int64_t workspace_bytes,
                      void* stream) {
-  return propagate_impl(mode, dtype, ptr, idx, w, nullptr, n_rows, items, n_items, splits, n_splits, n_slots,
-                        G, ldg, g_off, R, ldr, r_off, out0, ld0, out1, ld1, mask, ldm, F, accumulate,
-                        hub_rows, n_hub, workspace, workspace_bytes, stream);
-}
-
-int sg_propagate_rle(int mode, int dtype, const int64_t* ptr, const int32_t* idx, const float* w,
-                     const uint16_t* cnt, int64_t n_rows, const sg_item* items, int64_t n_items,
-                     const sg_split* splits, int64_t n_splits, int64_t n_slots, const void* G, int64_t ldg,
-                     int64_t g_off, const void* R, int64_t ldr, int64_t r_off, void* out0, int64_t ld0,
-                     void* out1, int64_t ld1, const void* mask, int64_t ldm, int64_t F, int accumulate,
-                     void* workspace, int64_t workspace_bytes, void* stream) {
-  SG_REQUIRE(cnt || n_rows == 0 || n_items == 0, SG_EINVAL, "propagate_rle: run counts missing");
-  return propagate_impl(mode, dtype, ptr, idx, w, cnt, n_rows, items, n_items, splits, n_splits, n_slots,
-                        G, ldg, g_off, R, ldr, r_off, out0, ld0, out1, ld1, mask, ldm, F, accumulate,
-                        nullptr, 0, workspace, workspace_bytes, stream);
-}
-
-}  // extern "C"
-
-namespace {
-
-int propagate_impl(int mode, int dtype, const int64_t* ptr, const int32_t* idx, const float* w,
-                   const uint16_t* cnt, int64_t n_rows, const sg_item* items, int64_t n_items,
-                   const sg_split* splits, int64_t n_splits, int64_t n_slots, const void* G, int64_t ldg,
-                   int64_t g_off, const void* R, int64_t ldr, int64_t r_off, void* out0, int64_t ld0,
-                   void* out1, int64_t ld1, const void* mask, int64_t ldm, int64_t F, int accumulate,
-                   const int32_t* hub_rows, int64_t n_hub, void* workspace, int64_t workspace_bytes,
-                   void* stream) {
   SG_REQUIRE(mode >= SG_PROP_PASS && mode <= SG_PROP_GGCN_FWD_S, SG_EINVAL, "bad mode %d", mode);
   SG_REQUIRE(dtype == SG_F32 || dtype == SG_BF16 || dtype == SG_BF16_F32OUT, SG_EINVAL, "bad dtype %d", dtype);
   SG_REQUIRE(dtype != SG_BF16_F32OUT || mode <= SG_PROP_GCN, SG_EINVAL,
@@ -996,7 +901,6 @@ int propagate_impl(int mode, int dtype, const int64_t* ptr, const int32_t* idx, 
     a.mask = mask ? static_cast<const char*>(mask) + c0 * esz : nullptr; a.ldm = ldm;
     a.n_items = (int32_t)n_items; a.Fv = Fv; a.Fcols = (int32_t)cols; a.accumulate = accumulate;
     a.hub_rows = hub_rows;
-    a.cnt = cnt;
     a.n_hub = 0;
     if (n_hub > 0) {
       // an index encoded for hubs must run the hub kernel (negative entries are slots)
@@ -1021,4 +925,4 @@ int propagate_impl(int mode, int dtype, const int64_t* ptr, const int32_t* idx, 
   return SG_OK;
 }
 
-}  // namespace
+}  // extern "C"

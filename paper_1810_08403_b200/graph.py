@@ -326,60 +326,8 @@ def plan(ptr, split_edges=DEFAULT_SPLIT_EDGES, pack_edges=None, max_rows=256, id
     return items, splits[: int(cnt[1])], int(cnt[2])
 
 
-# run-length encoded pass index (sg_host_rle) when multi-edges make it at least this much
-# smaller; SG_RLE=0 disables it (A/B runs)
-RLE = os.environ.get("SG_RLE", "1") == "1"
-RLE_MAX_RATIO = 0.9
-
-
-class RunIndex:
-    """Run-length encoded form of a pass index (sg_host_rle): consecutive edges of a row with the
-    same (source, weight) -- multi-edges -- are one entry with a count, so the sum passes load the
-    row once per entry (sg_propagate_rle, bitwise identical).  Entries never cross a split
-    subgroup, and the plan is the edge-level plan in entry units (sg_host_plan_rle)."""
-
-    def __init__(self, ptr, idx, w, split_edges, device, pack_edges=None, max_rows=256):
-        import torch
-
-        ptr = np.ascontiguousarray(ptr, np.int64)
-        idx = np.ascontiguousarray(idx, np.int32)
-        w = None if w is None else np.ascontiguousarray(w, np.float32)
-        n_rows = ptr.shape[0] - 1
-        rptr = np.zeros(n_rows + 1, np.int64)
-        n = np.zeros(1, np.int64)
-        check(lib.sg_host_rle(nptr(ptr), nptr(idx), nptr(w), n_rows, split_edges, nptr(rptr), None, None,
-                              None, nptr(n)))
-        self.n_entries = int(n[0])
-        ridx = np.empty(self.n_entries, np.int32)
-        rw = np.empty(self.n_entries, np.float32) if w is not None else None
-        rcnt = np.empty(self.n_entries, np.uint16)
-        check(lib.sg_host_rle(nptr(ptr), nptr(idx), nptr(w), n_rows, split_edges, nptr(rptr), nptr(ridx),
-                              nptr(rw), nptr(rcnt), nptr(n)))
-        nnz = int(ptr[-1]) if n_rows >= 0 else 0
-        if pack_edges is None:
-            pack_edges = int(min(max(32, nnz // (148 * 64)), split_edges))
-        cnt = np.zeros(3, np.int64)
-        args = (nptr(ptr), nptr(rptr), nptr(rcnt), n_rows, pack_edges, max_rows, split_edges)
-        check(lib.sg_host_plan_rle(*args, None, None, nptr(cnt[0:1]), nptr(cnt[1:2]), nptr(cnt[2:3])))
-        items = np.zeros(int(cnt[0]), _lib.ITEM_DTYPE)
-        splits = np.zeros(max(int(cnt[1]), 1), _lib.SPLIT_DTYPE)
-        check(lib.sg_host_plan_rle(*args, nptr(items), nptr(splits), nptr(cnt[0:1]), nptr(cnt[1:2]),
-                                   nptr(cnt[2:3])))
-        if PLAN_ORDER == "src" and len(items):
-            check(lib.sg_host_plan_order(nptr(items), len(items), nptr(ridx)))
-        self.n_items, self.n_splits, self.n_slots = len(items), int(cnt[1]), int(cnt[2])
-        self.ptr = torch.from_numpy(rptr).to(device)
-        self.idx = torch.from_numpy(ridx).to(device)
-        self.w = None if rw is None else torch.from_numpy(rw).to(device)
-        self.cnt = torch.from_numpy(rcnt.view(np.int16)).to(device)
-        self.items = torch.from_numpy(items.view(np.uint8)).to(device)
-        self.splits = torch.from_numpy(splits[: self.n_splits].view(np.uint8)).to(device) \
-            if self.n_splits else None
-
-
 class PassIndex:
-    """Device-resident index of one propagation pass over one chunk (CSC or CSR).  ``rle``: the
-    run-length encoded form used by the sum passes when the chunk has enough multi-edges."""
+    """Device-resident index of one propagation pass over one chunk (CSC or CSR)."""
 
     def __init__(self, ptr, idx, w, n_rows, split_edges, device):
         import torch
@@ -396,11 +344,6 @@ class PassIndex:
         self.items = torch.from_numpy(items.view(np.uint8)).to(device)
         self.splits = torch.from_numpy(splits.view(np.uint8)).to(device) if len(splits) else None
         self.max_degree = int(np.diff(ptr).max()) if n_rows > 0 else 0
-        self.rle = None
-        if RLE and self.nnz > 0:
-            r = RunIndex(ptr, idx, w, split_edges, device)
-            if r.n_entries <= RLE_MAX_RATIO * self.nnz:
-                self.rle = r
 
     @classmethod
     def from_device(cls, ptr, idx, split_edges=DEFAULT_SPLIT_EDGES):
@@ -417,7 +360,6 @@ class PassIndex:
         self.items = torch.from_numpy(items.view(np.uint8)).to(ptr.device)
         self.splits = torch.from_numpy(splits.view(np.uint8)).to(ptr.device) if len(splits) else None
         self.max_degree = int(np.diff(ptr_h).max()) if self.n_rows > 0 else 0
-        self.rle = None
         return self
 
     def workspace_bytes(self, F, mode):

@@ -80,19 +80,6 @@ def propagate(pi, mode, G, out0, F, *, g_off=0, R=None, r_off=0, out1=None, mask
     elif out0.dtype != G.dtype:
         raise TypeError(f"propagate: {G.dtype} rows into a {out0.dtype} output is not supported")
     h = _hub_for(pi, mode, dt, G, out0, mask, F, g_off) if hub and R is None and out1 is None else None
-    rl = getattr(pi, "rle", None)
-    if rl is not None and h is None:
-        # run-length encoded index: one row load per multi-edge run (bitwise identical)
-        wsb = int(lib.sg_propagate_workspace_bytes(rl.n_items, rl.n_splits, rl.n_slots, F, mode))
-        buf = ws.get(wsb) if ws is not None else torch.empty(wsb, dtype=torch.uint8, device=G.device)
-        check(lib.sg_propagate_rle(
-            mode, dt, tptr(rl.ptr), tptr(rl.idx), tptr(rl.w), tptr(rl.cnt), pi.n_rows, tptr(rl.items),
-            rl.n_items, tptr(rl.splits), rl.n_splits, rl.n_slots, tptr(G), ld(G), g_off,
-            tptr(R), ld(R) if R is not None else 0, r_off, tptr(out0), ld(out0),
-            tptr(out1), ld(out1) if out1 is not None else 0, tptr(mask),
-            ld(mask) if mask is not None else 0, F, int(bool(accumulate)), tptr(buf), buf.numel(),
-            stream_handle(stream)))
-        return
     wsb = pi.workspace_bytes(F, mode)
     buf = ws.get(wsb) if ws is not None else torch.empty(wsb, dtype=torch.uint8, device=G.device)
     idx, rows, n_hub = (h[0], h[1], h[2]) if h is not None else (pi.idx, None, 0)

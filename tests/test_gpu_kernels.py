@@ -1085,64 +1085,3 @@ def test_schedule_streaming_choice_fits_the_executor_budget(sg):
         mx, _ = S.chunk_stats(s, d, V, P)
         st_p = sg.StreamingGCN(sg.HostGrid(g, -(-V // P)), dims)
         assert st_p.working_set <= S.streaming_working_set(V, dims, P, mx)
-
-
-@pytest.mark.parametrize("F,T,mode,dt", [(602, 4096, "gcn", "f32"), (128, 256, "gcn", "f32"),
-                                         (16, 64, "pass", "f32"), (7, 64, "gcn", "f32"),
-                                         (128, 4096, "ggcn", "f32"), (602, 4096, "gcn", "bf16"),
-                                         (128, 256, "gcn", "bf16f32")])
-def test_run_length_index_bitwise(sg, F, T, mode, dt):
-    """sg_propagate_rle (one row load per multi-edge run, term added cnt times) == the edge-level
-    pass bit for bit: wide / narrow / lane-team / scalar rows, split rows, the masked CSR dual,
-    the gated G-GCN passes and the bf16 (and bf16-in / fp32-out) storage."""
-    from paper_1810_08403_b200 import _lib
-    from paper_1810_08403_b200 import kernels as K
-
-    V, E = 3000, 150000
-    s, d = _graph("rmat", V, E, 12)
-    grid = sg.ChunkGrid(sg.Graph(V, s, d), V, split_edges=T, gcn_weights=(mode == "gcn"))
-    ci, ri = grid.csc[(0, 0)], grid.csr[(0, 0)]
-    assert ci.rle is not None and ri.rle is not None
-    tdt = torch.bfloat16 if dt.startswith("bf16") else torch.float32
-    odt = torch.float32 if dt != "bf16" else torch.bfloat16
-    ld = (2 * F + 7) // 8 * 8
-
-    def mk(seed, dtype, width=F):
-        t = torch.zeros((V, ld), dtype=dtype, device="cuda")[:, :width]
-        t.copy_(torch.from_numpy(rng.features(V, width, seed=seed)))
-        return t
-
-    def both(fn):
-        outs = []
-        for use in (True, False):
-            saved = (ci.rle, ri.rle)
-            if not use:
-                ci.rle = ri.rle = None
-            try:
-                outs.append(fn())
-            finally:
-                ci.rle, ri.rle = saved
-        return outs
-
-    if mode == "ggcn":
-        HP, GQ = mk(1, tdt, 2 * F), mk(2, tdt, 2 * F)
-
-        def run():
-            A, S = (torch.zeros((V, F), dtype=odt, device="cuda") for _ in range(2))
-            dP, dH = (torch.zeros((V, F), dtype=odt, device="cuda") for _ in range(2))
-            K.propagate(ci, _lib.PROP_GGCN_FWD_S, HP, A, F, g_off=F, R=GQ[:, F:], out1=S)
-            K.propagate(ri, _lib.PROP_GGCN_BWD_SRC, GQ, dP, F, g_off=F, R=HP, r_off=F, out1=dH)
-            return [A, S, dP, dH]
-    else:
-        X, Z = mk(1, tdt), mk(8, tdt)
-        pm = _lib.PROP_GCN if mode == "gcn" else _lib.PROP_PASS
-
-        def run():
-            a = torch.zeros((V, ld), dtype=odt, device="cuda")[:, :F]
-            b = torch.zeros((V, ld), dtype=odt, device="cuda")[:, :F]
-            K.propagate(ci, pm, X, a, F)
-            K.propagate(ri, pm, X, b, F, mask=Z)
-            return [a, b]
-    got, ref = both(run)
-    for x, y in zip(got, ref):
-        assert torch.equal(x, y)

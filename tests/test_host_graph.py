@@ -138,37 +138,3 @@ def test_plan_split_items_first_and_cover_all_edges():
     kinds = [int(i["split"]) >= 0 for i in items]
     assert kinds == sorted(kinds, reverse=True)  # split items first
     assert n_slots == 3 + 8 and len(splits) == 2
-
-
-def test_run_length_index_and_plan():
-    """sg_host_rle / sg_host_plan_rle: entries = maximal runs of equal (src, w) inside a row,
-    never crossing a split-subgroup boundary or 65535 edges; expanding them gives the edge index
-    back; the entry-unit plan covers exactly the same edges per item as the edge-level plan."""
-    from paper_1810_08403_b200 import graph as G
-
-    V, E, T = 300, 20000, 64
-    s, d = rng.rmat_edges(V, E, seed=3)
-    part = og.partition_2d(s, d, V, V)
-    ch = part.chunk(0, 0)
-    ptr, idx = ch["csc_ptr"].astype(np.int64), ch["csc_idx"].astype(np.int32)
-    w = og.gcn_edge_weights(s, d, V, np.float32)[ch["csc_eid"]]
-    ri = G.RunIndex(ptr, idx, w, T, "cpu")
-    rptr, ridx, rw = ri.ptr.numpy(), ri.idx.numpy(), ri.w.numpy()
-    rcnt = ri.cnt.numpy().view(np.uint16).astype(np.int64)
-    assert ri.n_entries < 0.9 * len(idx)                      # R-MAT multi-edges
-    assert np.array_equal(np.repeat(ridx, rcnt), idx)          # expands to the edge index
-    assert np.array_equal(np.repeat(rw, rcnt), w)
-    for r in range(V):
-        c = rcnt[rptr[r]: rptr[r + 1]]
-        assert c.sum() == ptr[r + 1] - ptr[r]
-        bounds = np.cumsum(c)[:-1]                              # edge offsets of entry starts
-        assert np.all(np.isin(np.arange(T, ptr[r + 1] - ptr[r], T), bounds))
-    items_e, splits_e, slots_e = G.plan(ptr, T)
-    items_r = ri.items.numpy().view(_lib.ITEM_DTYPE)
-    assert (ri.n_items, ri.n_splits, ri.n_slots) == (len(items_e), len(splits_e), slots_e)
-    ecum = np.concatenate([[0], np.cumsum(rcnt)])              # entry index -> edge offset
-    key = lambda it: (int(it["row_begin"]), int(it["sub"]), int(it["split"] >= 0))  # noqa: E731
-    by_key = {key(it): it for it in items_e}
-    for it in items_r:
-        e = by_key[key(it)]
-        assert ecum[it["e_begin"]] == e["e_begin"] and ecum[it["e_end"]] == e["e_end"]
