@@ -118,6 +118,34 @@ int sg_host_plan(const int64_t* ptr, int64_t n_rows, int64_t pack_edges, int64_t
  * queue (results are independent of the item order). */
 int sg_host_plan_order(sg_item* items, int64_t n_items, const int32_t* idx);
 
+/* One destination row of a staged gather (or one T-edge subgroup of a row with more than T
+ * edges, SPEC.md:443 -- the same subgroups, split ids and partial slots as sg_host_plan).
+ * row < 0: an unused position of the group. */
+typedef struct sg_stage_piece {
+  int32_t row, split, slot0, sub_nsub; /* sub_nsub = sub << 16 | n_sub (split pieces) */
+} sg_stage_piece;
+
+/* Work plan of the source-staged gather (sg_propagate_staged).  Pieces (whole rows and split
+ * subgroups) are ordered by their first source and cut into groups of group_pieces; a group's
+ * pieces gather from the merged, ascending list of the sources they reference, which the
+ * kernel stages into shared memory batch_rows rows at a time, so a source row shared by
+ * several pieces of a group crosses L2 -> SM once.  Per batch: the staged source rows
+ * (batch_src), and the entries of every piece that reference them, piece-major, each a run of
+ * equal consecutive (source, weight) edges: bits 0-15 the row's slot in the batch, 16-31 the
+ * run length, 32-63 the weight (0 without w); batch_pofs[b * pofs_stride + q] is the first entry
+ * of piece q (q = 0 .. group_pieces, pofs_stride = group_pieces + 1 rounded up to 8).  Each
+ * piece's edges are visited in index order, so every row sums its terms in the same order as
+ * sg_propagate (bitwise identical).  Groups are listed by descending entry count.
+ * Requires idx non-decreasing within every row (the canonical CSC / CSR of ChunkGrid);
+ * returns SG_EINVAL otherwise or when one source's entries exceed batch_entries.
+ * Call with pieces == NULL to size: sizes = {n_groups, n_batches, n_src, n_ent, n_splits,
+ * n_slots}. */
+int sg_host_stage_plan(const int64_t* ptr, const int32_t* idx, const float* w, int64_t n_rows,
+                       int64_t split_edges, int32_t group_pieces, int32_t batch_rows,
+                       int32_t batch_entries, sg_stage_piece* pieces, int32_t* group_batch,
+                       int64_t* batch_src_off, int32_t* batch_src, int64_t* batch_ent_off,
+                       uint64_t* entries, uint16_t* batch_pofs, int64_t* sizes);
+
 /* ---------------------------------------------------------------- host: ingestion
  * load_graph's file formats.  Edge file: one "src dest
  * [edge_value]" per line, whitespace separated (blank, '#' and '%' lines skipped).
@@ -157,6 +185,26 @@ int sg_propagate(int mode, int dtype, const int64_t* ptr, const int32_t* idx, co
                  const void* R, int64_t ldr, int64_t r_off, void* out0, int64_t ld0, void* out1,
                  int64_t ld1, const void* mask, int64_t ldm, int64_t F, int accumulate,
                  void* workspace, int64_t workspace_bytes, void* stream);
+
+/* Source-staged sum pass (GCN / PASS modes, fp32, F <= 640, 16-byte aligned rows): the same
+ * function as sg_propagate -- bitwise identical outputs, same split slots / workspace
+ * (sg_propagate_workspace_bytes with the plan's n_splits, n_slots) -- driven by a
+ * sg_host_stage_plan.  Each persistent CTA takes groups of pieces from a queue and stages the
+ * group's source rows into shared memory with TMA bulk copies (cp.async.bulk, mbarrier
+ * complete_tx), batch_rows rows per batch, 2-3 stages deep; every source row a group shares
+ * is read from L2 once per group instead of once per edge.  group_pieces must be
+ * sg_stage_group_pieces(F); the dynamic shared memory is sg_stage_smem_bytes(...) (<= 227 KB).
+ * mask (optional): ReLU-backward epilogue as in sg_propagate. */
+int32_t sg_stage_group_pieces(int64_t F);
+int64_t sg_stage_smem_bytes(int32_t group_pieces, int32_t batch_rows, int32_t batch_entries, int64_t F,
+                            int32_t stages);
+int sg_propagate_staged(int mode, const sg_stage_piece* pieces, const int32_t* group_batch, int64_t n_groups,
+                        const int64_t* batch_src_off, const int32_t* batch_src, const int64_t* batch_ent_off,
+                        const uint64_t* entries, const uint16_t* batch_pofs, int32_t group_pieces,
+                        int32_t batch_rows, int32_t batch_entries, int32_t stages, int64_t n_splits,
+                        int64_t n_slots, const float* G, int64_t ldg, float* out, int64_t ldo, const float* mask,
+                        int64_t ldm, int64_t F, int accumulate, void* workspace, int64_t workspace_bytes,
+                        void* stream);
 
 /* sg_propagate with a hub-row cache (GCN / PASS modes, rows wider than 16 vectors).
  * The n_hub most referenced gathered rows (hub_rows[0..n_hub), int32 row ids of G) are

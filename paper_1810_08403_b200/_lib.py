@@ -63,6 +63,11 @@ _SIGS = {
     "sg_host_gcn_weights": (_i32, [_p, _p, _p, _p, _p, _i64, _p]),
     "sg_host_plan": (_i32, [_p, _i64, _i64, _i64, _i64, _p, _p, _p, _p, _p]),
     "sg_host_plan_order": (_i32, [_p, _i64, _p]),
+    "sg_host_stage_plan": (_i32, [_p, _p, _p, _i64, _i64, _i32, _i32, _i32] + [_p] * 8),
+    "sg_stage_group_pieces": (_i32, [_i64]),
+    "sg_stage_smem_bytes": (_i64, [_i32, _i32, _i32, _i64, _i32]),
+    "sg_propagate_staged": (_i32, [_i32, _p, _p, _i64, _p, _p, _p, _p, _p, _i32, _i32, _i32, _i32, _i64, _i64,
+                                   _p, _i64, _p, _i64, _p, _i64, _i64, _i32, _p, _i64, _p]),
     "sg_host_scan_edges": (_i32, [_s, _i64, _p, _p, _p]),
     "sg_host_read_edges": (_i32, [_s, _i64, _p, _p, _p]),
     "sg_host_scan_matrix_text": (_i32, [_s, _p, _p]),

@@ -309,6 +309,172 @@ int sg_host_plan(const int64_t* ptr, int64_t n_rows, int64_t pack_edges, int64_t
   return SG_OK;
 }
 
+int sg_host_stage_plan(const int64_t* ptr, const int32_t* idx, const float* w, int64_t n_rows,
+                       int64_t split_edges, int32_t group_pieces, int32_t batch_rows,
+                       int32_t batch_entries, sg_stage_piece* pieces, int32_t* group_batch,
+                       int64_t* batch_src_off, int32_t* batch_src, int64_t* batch_ent_off,
+                       uint64_t* entries, uint16_t* batch_pofs, int64_t* sizes) {
+  SG_REQUIRE(ptr && idx && sizes && n_rows >= 0 && n_rows <= INT32_MAX, SG_EINVAL, "stage_plan: bad args");
+  SG_REQUIRE(split_edges >= 1 && group_pieces >= 1 && group_pieces <= 1024 && batch_rows >= 1 &&
+                 batch_rows <= 65535 && batch_entries >= 1 && batch_entries <= 65535,
+             SG_EINVAL, "stage_plan: bad limits");
+  const int G = group_pieces;
+  const int pstride = (G + 1 + 7) / 8 * 8;
+  // pieces: whole rows, and split rows' T-edge subgroups numbered as sg_host_plan does
+  struct P { int64_t e0, e1; sg_stage_piece p; int32_t first; };
+  std::vector<P> ps;
+  ps.reserve(n_rows);
+  int64_t si = 0, slot = 0;
+  for (int64_t r = 0; r < n_rows; ++r) {
+    const int64_t d = ptr[r + 1] - ptr[r];
+    for (int64_t e = ptr[r] + 1; e < ptr[r + 1]; ++e)
+      SG_REQUIRE(idx[e] >= idx[e - 1], SG_EINVAL, "stage_plan: row %lld is not sorted by source", (long long)r);
+    if (d > split_edges) {
+      const int64_t k = (d + split_edges - 1) / split_edges;
+      SG_REQUIRE(k < 65536, SG_EINVAL, "stage_plan: too many subgroups in row %lld", (long long)r);
+      for (int64_t s = 0; s < k; ++s) {
+        const int64_t e0 = ptr[r] + s * split_edges, e1 = std::min(e0 + split_edges, ptr[r + 1]);
+        ps.push_back(P{e0, e1, sg_stage_piece{(int32_t)r, (int32_t)si, (int32_t)slot, (int32_t)((s << 16) | k)},
+                       idx[e0]});
+      }
+      si++;
+      slot += k;
+    } else {
+      ps.push_back(P{ptr[r], ptr[r + 1], sg_stage_piece{(int32_t)r, -1, 0, 0},
+                     d > 0 ? idx[ptr[r]] : INT32_MAX});
+    }
+  }
+  SG_REQUIRE(slot <= INT32_MAX, SG_EINVAL, "stage_plan: too many split slots");
+  // pieces that start at the same source share the most sources: adjacent, then grouped
+  std::stable_sort(ps.begin(), ps.end(), [](const P& a, const P& b) { return a.first < b.first; });
+  const int64_t n_groups = ((int64_t)ps.size() + G - 1) / G;
+
+  // per group: runs of equal (source, weight) per piece, merged source list, batches
+  struct Grp {
+    std::vector<int32_t> src;                 // staged sources, batch by batch
+    std::vector<int64_t> src_off, ent_off;    // per batch (relative)
+    std::vector<uint64_t> ent;
+    std::vector<uint16_t> pofs;
+    int64_t n_ent = 0;
+    int bad = 0;
+  };
+  std::vector<Grp> gs(n_groups);
+#pragma omp parallel for schedule(dynamic, 16)
+  for (int64_t g = 0; g < n_groups; ++g) {
+    Grp& gr = gs[g];
+    const int64_t q0 = g * G, q1 = std::min<int64_t>(q0 + G, (int64_t)ps.size());
+    // runs: (source, weight bits, count) per piece
+    struct Run { int32_t src; uint32_t wb; uint32_t cnt; };
+    std::vector<std::vector<Run>> runs(q1 - q0);
+    std::vector<int32_t> all;
+    for (int64_t q = q0; q < q1; ++q) {
+      auto& rv = runs[q - q0];
+      for (int64_t e = ps[q].e0; e < ps[q].e1; ++e) {
+        uint32_t wb = 0;
+        if (w) std::memcpy(&wb, w + e, 4);
+        if (!rv.empty() && rv.back().src == idx[e] && rv.back().wb == wb && rv.back().cnt < 65535)
+          rv.back().cnt++;
+        else
+          rv.push_back(Run{idx[e], wb, 1});
+        all.push_back(idx[e]);
+      }
+    }
+    std::sort(all.begin(), all.end());
+    all.erase(std::unique(all.begin(), all.end()), all.end());
+    // entries per source (across pieces), to close batches
+    std::vector<int32_t> cu(all.size(), 0);
+    for (auto& rv : runs)
+      for (const Run& x : rv) cu[std::lower_bound(all.begin(), all.end(), x.src) - all.begin()]++;
+    std::vector<size_t> cur(runs.size(), 0);
+    size_t u = 0;
+    gr.src_off.push_back(0);
+    gr.ent_off.push_back(0);
+    while (u < all.size()) {
+      // close the batch at batch_rows sources or batch_entries entries
+      size_t u1 = u;
+      int64_t ne = 0;
+      while (u1 < all.size() && (int64_t)(u1 - u) < batch_rows && ne + cu[u1] <= batch_entries) ne += cu[u1++];
+      if (u1 == u) { gr.bad = 1; break; }
+      const int32_t lo = all[u], hi = all[u1 - 1];
+      for (size_t k = u; k < u1; ++k) gr.src.push_back(all[k]);
+      // entries, piece-major (positions beyond the group's pieces stay empty)
+      const size_t eb = gr.ent.size();
+      for (int q = 0; q < G; ++q) {
+        gr.pofs.push_back((uint16_t)(gr.ent.size() - eb));
+        if (q >= (int)runs.size()) continue;
+        auto& rv = runs[q];
+        size_t& c = cur[q];
+        while (c < rv.size() && rv[c].src <= hi) {
+          const uint64_t sl = (uint64_t)(std::lower_bound(all.begin() + u, all.begin() + u1, rv[c].src) -
+                                         (all.begin() + u));
+          (void)lo;
+          gr.ent.push_back(sl | ((uint64_t)rv[c].cnt << 16) | ((uint64_t)rv[c].wb << 32));
+          c++;
+        }
+      }
+      const size_t n_b = gr.ent.size() - eb;
+      for (int q = G; q < pstride; ++q) gr.pofs.push_back((uint16_t)n_b);
+      if (n_b & 1) gr.ent.push_back(0);   // 16-byte aligned batches for the bulk copies
+      gr.src_off.push_back((int64_t)gr.src.size());
+      gr.ent_off.push_back((int64_t)gr.ent.size());
+      gr.n_ent += (int64_t)n_b;
+      u = u1;
+    }
+    if (gr.src_off.size() == 1 && !gr.bad) {
+      // a group of edgeless rows: one empty batch, so the kernel still writes its outputs
+      for (int q = 0; q < pstride; ++q) gr.pofs.push_back(0);
+      gr.src_off.push_back(0);
+      gr.ent_off.push_back(0);
+    }
+  }
+  for (auto& gr : gs) SG_REQUIRE(!gr.bad, SG_EINVAL, "stage_plan: a source has more than %d entries", batch_entries);
+  // groups by descending entry count (longest first on the persistent CTAs)
+  std::vector<int64_t> order(n_groups);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return gs[a].n_ent > gs[b].n_ent; });
+  int64_t nb = 0, nsrc = 0, nent = 0;
+  for (auto& gr : gs) {
+    nb += (int64_t)gr.src_off.size() - 1;
+    nsrc += (int64_t)gr.src.size();
+    nent += (int64_t)gr.ent.size();
+  }
+  sizes[0] = n_groups; sizes[1] = nb; sizes[2] = nsrc; sizes[3] = nent; sizes[4] = si; sizes[5] = slot;
+  if (!pieces) return SG_OK;
+  SG_REQUIRE(group_batch && batch_src_off && batch_src && batch_ent_off && entries && batch_pofs, SG_EINVAL,
+             "stage_plan: null output");
+  SG_REQUIRE(nb <= INT32_MAX, SG_EINVAL, "stage_plan: too many batches");
+  // output offsets in execution order
+  std::vector<int64_t> gb(n_groups + 1, 0), gsrc(n_groups + 1, 0), gent(n_groups + 1, 0);
+  for (int64_t k = 0; k < n_groups; ++k) {
+    const Grp& gr = gs[order[k]];
+    gb[k + 1] = gb[k] + (int64_t)gr.src_off.size() - 1;
+    gsrc[k + 1] = gsrc[k] + (int64_t)gr.src.size();
+    gent[k + 1] = gent[k] + (int64_t)gr.ent.size();
+  }
+  batch_src_off[nb] = nsrc;
+  batch_ent_off[nb] = nent;
+#pragma omp parallel for schedule(dynamic, 16)
+  for (int64_t k = 0; k < n_groups; ++k) {
+    const int64_t g = order[k];
+    const Grp& gr = gs[g];
+    group_batch[k] = (int32_t)gb[k];
+    for (int q = 0; q < G; ++q) {
+      const int64_t pq = g * G + q;
+      pieces[k * G + q] = pq < (int64_t)ps.size() ? ps[pq].p : sg_stage_piece{-1, -1, 0, 0};
+    }
+    const int64_t nbg = (int64_t)gr.src_off.size() - 1;
+    for (int64_t b = 0; b < nbg; ++b) {
+      batch_src_off[gb[k] + b] = gsrc[k] + gr.src_off[b];
+      batch_ent_off[gb[k] + b] = gent[k] + gr.ent_off[b];
+    }
+    std::memcpy(batch_src + gsrc[k], gr.src.data(), gr.src.size() * 4);
+    std::memcpy(entries + gent[k], gr.ent.data(), gr.ent.size() * 8);
+    std::memcpy(batch_pofs + gb[k] * pstride, gr.pofs.data(), gr.pofs.size() * 2);
+  }
+  group_batch[n_groups] = (int32_t)nb;
+  return SG_OK;
+}
+
 int sg_host_plan_order(sg_item* items, int64_t n_items, const int32_t* idx) {
   SG_REQUIRE(n_items >= 0 && (n_items == 0 || (items && idx)), SG_EINVAL, "plan_order: null pointer");
   int64_t ns = 0;

@@ -69,18 +69,7 @@ struct ModeT<SG_PROP_GCN> {
   }
 };
 
-// (a0, a1) += (t0, t1) with one packed FADD2 (add.rn.f32x2): per-lane IEEE
-// round-to-nearest, i.e. bitwise the same as two scalar adds.  (ptxas contracts a
-// packed mul.rn.f32x2 feeding this into FFMA2, so products stay scalar __fmul_rn.)
-__device__ __forceinline__ void add2_rn(float& a0, float& a1, float t0, float t1) {
-  asm("{\n\t.reg .b64 a, t;\n\t"
-      "mov.b64 a, {%0, %1};\n\t"
-      "mov.b64 t, {%2, %3};\n\t"
-      "add.rn.f32x2 a, a, t;\n\t"
-      "mov.b64 {%0, %1}, a;\n\t}"
-      : "+f"(a0), "+f"(a1)
-      : "f"(t0), "f"(t1));
-}
+using sg::add2_rn;
 
 // Gate sigmoid.  The reference computes 1.0 / (1.0 + np.exp(-x)) (tensor.py:205); device exp
 // is not bit-comparable with numpy's anyway, so the gate uses the SFU: eta = rcp(1 + 2^t)

@@ -170,4 +170,17 @@ struct VecIO<SG_BF16, 1> {
   }
 };
 
+// (a0, a1) += (t0, t1) with one packed FADD2 (add.rn.f32x2): per-lane IEEE
+// round-to-nearest, i.e. bitwise the same as two scalar adds.  (ptxas contracts a
+// packed mul.rn.f32x2 feeding this into FFMA2, so products stay scalar __fmul_rn.)
+__device__ __forceinline__ void add2_rn(float& a0, float& a1, float t0, float t1) {
+  asm("{\n\t.reg .b64 a, t;\n\t"
+      "mov.b64 a, {%0, %1};\n\t"
+      "mov.b64 t, {%2, %3};\n\t"
+      "add.rn.f32x2 a, a, t;\n\t"
+      "mov.b64 {%0, %1}, a;\n\t}"
+      : "+f"(a0), "+f"(a1)
+      : "f"(t0), "f"(t1));
+}
+
 }  // namespace sg

@@ -326,6 +326,61 @@ def plan(ptr, split_edges=DEFAULT_SPLIT_EDGES, pack_edges=None, max_rows=256, id
     return items, splits[: int(cnt[1])], int(cnt[2])
 
 
+# source-staged sum passes (sg_propagate_staged, bitwise identical to sg_propagate) for fp32 rows
+# of 64..640 columns: opt-in (SG_STAGED=1).  It halves the L2 -> SM row traffic of the Reddit
+# layer-1 pass (103 vs 190 GB) but measured 3-4x slower than the row-per-warp kernel in every
+# variant tried (profiles/r02_staged_ab.txt), so the row kernel stays the default.
+STAGED = os.environ.get("SG_STAGED", "0") == "1"
+STAGE_MIN_F, STAGE_MAX_F = 64, 640
+STAGES = int(os.environ.get("SG_STAGES", "3"))
+_STAGE_SMEM = 227 * 1024
+
+
+class StagePlan:
+    """sg_host_stage_plan of one pass for rows of F columns: pieces (rows / T-edge subgroups)
+    grouped by first source, each group's merged source list cut into shared-memory batches,
+    every piece's edges as run entries (slot in batch, run length, weight)."""
+
+    def __init__(self, ptr, idx, w, split_edges, F, device):
+        import torch
+
+        G = int(lib.sg_stage_group_pieces(F))
+        if G <= 0:
+            raise ShapeError(f"no staged gather for F = {F}")
+        emax = 1024
+        row_bytes = (F + 3) // 4 * 16
+        pofs = (G + 1 + 7) // 8 * 8 * 2
+        nst = STAGES
+        stage = (_STAGE_SMEM - 256) // nst // 128 * 128
+        S = int(min(256, (stage - emax * 8 - pofs) // row_bytes))   # <= 4 producer warps x 64 rows
+        ptr = np.ascontiguousarray(ptr, np.int64)
+        idx = np.ascontiguousarray(idx, np.int32)
+        w = None if w is None else np.ascontiguousarray(w, np.float32)
+        n_rows = ptr.shape[0] - 1
+        sz = np.zeros(6, np.int64)
+        args = (nptr(ptr), nptr(idx), nptr(w), n_rows, int(split_edges), G, S, emax)
+        check(lib.sg_host_stage_plan(*args, None, None, None, None, None, None, None, nptr(sz)))
+        ng, nb, ns, ne = (int(x) for x in sz[:4])
+        pieces = np.zeros((max(ng, 1) * G, 4), np.int32)
+        gb = np.zeros(ng + 1, np.int32)
+        bso = np.zeros(nb + 1, np.int64)
+        bs = np.zeros(max(ns, 1), np.int32)
+        beo = np.zeros(nb + 1, np.int64)
+        ent = np.zeros(max(ne, 2), np.uint64)
+        pst = (G + 1 + 7) // 8 * 8
+        pofs_a = np.zeros(max(nb, 1) * pst, np.uint16)
+        check(lib.sg_host_stage_plan(*args, nptr(pieces), nptr(gb), nptr(bso), nptr(bs), nptr(beo),
+                                     nptr(ent), nptr(pofs_a), nptr(sz)))
+        self.G, self.S, self.EMAX, self.F, self.stages = G, S, emax, F, nst
+        self.n_groups, self.n_batches, self.n_src, self.n_ent = ng, nb, ns, ne
+        self.n_splits, self.n_slots = int(sz[4]), int(sz[5])
+        t = lambda a: torch.from_numpy(a).to(device)  # noqa: E731
+        self.pieces, self.group_batch, self.batch_src_off = t(pieces), t(gb), t(bso)
+        self.batch_src, self.batch_ent_off = t(bs), t(beo)
+        self.entries = t(ent.view(np.int64))
+        self.batch_pofs = t(pofs_a.view(np.int16))
+
+
 class PassIndex:
     """Device-resident index of one propagation pass over one chunk (CSC or CSR)."""
 
@@ -344,6 +399,9 @@ class PassIndex:
         self.items = torch.from_numpy(items.view(np.uint8)).to(device)
         self.splits = torch.from_numpy(splits.view(np.uint8)).to(device) if len(splits) else None
         self.max_degree = int(np.diff(ptr).max()) if n_rows > 0 else 0
+        # host arrays kept (views of the partition) for the staged-gather plans, built lazily
+        self._host = (ptr, idx, w)
+        self._stage = {}
 
     @classmethod
     def from_device(cls, ptr, idx, split_edges=DEFAULT_SPLIT_EDGES):
@@ -364,6 +422,21 @@ class PassIndex:
 
     def workspace_bytes(self, F, mode):
         return int(lib.sg_propagate_workspace_bytes(self.n_items, self.n_splits, self.n_slots, F, mode))
+
+    def stage_plan(self, F):
+        """The staged-gather plan of this pass for rows of F columns (None if not applicable)."""
+        host = getattr(self, "_host", None)
+        if host is None or self.nnz == 0 or not (STAGE_MIN_F <= F <= STAGE_MAX_F):
+            return None
+        G = int(lib.sg_stage_group_pieces(F))
+        key = (G, (F + 3) // 4)
+        if key not in self._stage:
+            try:
+                self._stage[key] = StagePlan(host[0], host[1], host[2], self.split_edges, F,
+                                             self.ptr.device)
+            except Exception:   # e.g. a row not sorted by source: the row-per-warp kernel runs
+                self._stage[key] = None
+        return self._stage[key]
 
     def hub(self, n_cap, min_cover=HUB_MIN_COVER):
         """Hub-row cache of this pass for at most ``n_cap`` rows (sg_propagate_hub).

@@ -11,6 +11,7 @@ import os
 import torch
 
 from . import _lib
+from . import graph
 from ._lib import check, lib, stream_handle, tptr
 from .errors import ShapeError
 
@@ -80,6 +81,20 @@ def propagate(pi, mode, G, out0, F, *, g_off=0, R=None, r_off=0, out1=None, mask
     elif out0.dtype != G.dtype:
         raise TypeError(f"propagate: {G.dtype} rows into a {out0.dtype} output is not supported")
     h = _hub_for(pi, mode, dt, G, out0, mask, F, g_off) if hub and R is None and out1 is None else None
+    if (h is None and graph.STAGED and mode in (_lib.PROP_PASS, _lib.PROP_GCN) and dt == _lib.SG_F32
+            and R is None and out1 is None and g_off == 0 and hasattr(pi, "stage_plan")
+            and _vec_ok(G, 4) and _vec_ok(out0, 4) and _vec_ok(mask, 4)):
+        sp = pi.stage_plan(F)
+        if sp is not None:
+            wsb = int(lib.sg_propagate_workspace_bytes(0, sp.n_splits, sp.n_slots, F, mode))
+            buf = ws.get(wsb) if ws is not None else torch.empty(wsb, dtype=torch.uint8, device=G.device)
+            check(lib.sg_propagate_staged(
+                mode, tptr(sp.pieces), tptr(sp.group_batch), sp.n_groups, tptr(sp.batch_src_off),
+                tptr(sp.batch_src), tptr(sp.batch_ent_off), tptr(sp.entries), tptr(sp.batch_pofs), sp.G,
+                sp.S, sp.EMAX, sp.stages, sp.n_splits, sp.n_slots, tptr(G), ld(G), tptr(out0), ld(out0), tptr(mask),
+                ld(mask) if mask is not None else 0, F, int(bool(accumulate)), tptr(buf), buf.numel(),
+                stream_handle(stream)))
+            return
     wsb = pi.workspace_bytes(F, mode)
     buf = ws.get(wsb) if ws is not None else torch.empty(wsb, dtype=torch.uint8, device=G.device)
     idx, rows, n_hub = (h[0], h[1], h[2]) if h is not None else (pi.idx, None, 0)

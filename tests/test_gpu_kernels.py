@@ -1085,3 +1085,55 @@ def test_schedule_streaming_choice_fits_the_executor_budget(sg):
         mx, _ = S.chunk_stats(s, d, V, P)
         st_p = sg.StreamingGCN(sg.HostGrid(g, -(-V // P)), dims)
         assert st_p.working_set <= S.streaming_working_set(V, dims, P, mx)
+
+
+# ---------------------------------------------------------------- source-staged sum passes
+@pytest.mark.parametrize("F,T,mode,P", [(602, 4096, "gcn", 1), (128, 256, "gcn", 1), (640, 64, "pass", 2),
+                                        (200, 512, "gcn", 3), (64, 4096, "pass", 1), (96, 128, "gcn", 2)])
+def test_staged_gather_equals_row_kernel(sg, F, T, mode, P):
+    """sg_propagate_staged (source rows staged per group in shared memory by TMA bulk copies)
+    == the row-per-warp sg_propagate, bit for bit: CSC forward (accumulating chunk chains for
+    P > 1) and the CSR dual with the ReLU-mask epilogue; and == the oracle's ordered sums."""
+    from paper_1810_08403_b200 import _lib
+    from paper_1810_08403_b200 import graph as G
+    from paper_1810_08403_b200 import kernels as K
+
+    V, E = 6000, 240000
+    s, d = _graph("rmat", V, E, 11)
+    g = sg.Graph(V, s, d)
+    grid = sg.ChunkGrid(g, -(-V // P), split_edges=T)
+    m = _lib.PROP_GCN if mode == "gcn" else _lib.PROP_PASS
+    H = _padded(rng.features(V, F, seed=3))
+    Z = _padded(rng.features(V, F, seed=4))
+
+    def run(staged, csr, mask):
+        old = G.STAGED
+        G.STAGED = staged
+        try:
+            out = _padded(np.full((V, F), np.nan, np.float32))
+            idxs = grid.csr if csr else grid.csc
+            for o in range(grid.P):
+                chain = [k for k in range(grid.P) if ((o, k) if csr else (k, o)) in idxs]
+                rows = out[grid.begin(o): grid.begin(o) + grid.size(o)]
+                if not chain:
+                    rows.zero_()
+                for n, k in enumerate(chain):
+                    pi = idxs[(o, k) if csr else (k, o)]
+                    K.propagate(pi, m, H[grid.begin(k): grid.begin(k) + grid.size(k)], rows, F,
+                                accumulate=n > 0,
+                                mask=(Z[grid.begin(o): grid.begin(o) + grid.size(o)]
+                                      if mask and n == len(chain) - 1 else None))
+            torch.cuda.synchronize()
+            return out.cpu().numpy()
+        finally:
+            G.STAGED = old
+
+    for csr, mask in ((False, False), (True, True)):
+        a = run(True, csr, mask)
+        b = run(False, csr, mask)
+        assert np.array_equal(a, b), (csr, mask)
+    assert any(v is not None for pi in grid.csc.values() for v in pi._stage.values())
+    part = og.partition_2d(s, d, V, grid.part.interval_size)
+    w = og.gcn_edge_weights(s, d, V, np.float32) if mode == "gcn" else np.ones(E, np.float32)
+    want = saga.gcn_propagate_fwd(part, H.cpu().numpy(), w, T=T)
+    assert np.array_equal(run(True, False, False), want)

@@ -138,3 +138,92 @@ def test_plan_split_items_first_and_cover_all_edges():
     kinds = [int(i["split"]) >= 0 for i in items]
     assert kinds == sorted(kinds, reverse=True)  # split items first
     assert n_slots == 3 + 8 and len(splits) == 2
+
+
+def _stage_plan(ptr, idx, w, T, G_, S, EMAX):
+    from paper_1810_08403_b200._lib import nptr
+
+    args = (nptr(ptr), nptr(idx), nptr(w), len(ptr) - 1, T, G_, S, EMAX)
+    sz = np.zeros(6, np.int64)
+    _lib.check(_lib.lib.sg_host_stage_plan(*args, None, None, None, None, None, None, None, nptr(sz)))
+    ng, nb, ns, ne = (int(x) for x in sz[:4])
+    pst = (G_ + 1 + 7) // 8 * 8
+    out = dict(pieces=np.zeros((max(ng, 1) * G_, 4), np.int32), gb=np.zeros(ng + 1, np.int32),
+               bso=np.zeros(nb + 1, np.int64), bs=np.zeros(max(ns, 1), np.int32),
+               beo=np.zeros(nb + 1, np.int64), ent=np.zeros(max(ne, 2), np.uint64),
+               pofs=np.zeros(max(nb, 1) * pst, np.uint16))
+    _lib.check(_lib.lib.sg_host_stage_plan(*args, *(nptr(out[k]) for k in
+                                                    ("pieces", "gb", "bso", "bs", "beo", "ent", "pofs")),
+                                           nptr(sz)))
+    out.update(ng=ng, nb=nb, pst=pst, n_splits=int(sz[4]), n_slots=int(sz[5]))
+    return out
+
+
+def _stage_sum(ptr, idx, w, X, T, G_, S, EMAX):
+    """Run a staged-gather plan on the CPU with the kernel's rule (sg_propagate_staged): per
+    group, batch by batch, each piece adds its run entries' terms (x * w, count times) in order;
+    split subgroups into partial slots, combined in subgroup order."""
+    pl = _stage_plan(ptr, idx, w, T, G_, S, EMAX)
+    n_rows, F = len(ptr) - 1, X.shape[1]
+    out = np.full((n_rows, F), np.nan, np.float32)
+    partial = np.zeros((max(pl["n_slots"], 1), F), np.float32)
+    done = np.zeros(max(pl["n_splits"], 1), int)
+    for g in range(pl["ng"]):
+        acc = np.zeros((G_, F), np.float32)
+        for b in range(pl["gb"][g], pl["gb"][g + 1]):
+            rows = pl["bs"][pl["bso"][b]: pl["bso"][b + 1]]
+            assert len(rows) <= S and np.all(np.diff(rows) > 0)
+            ent = pl["ent"][pl["beo"][b]: pl["beo"][b + 1]]
+            po = pl["pofs"][b * pl["pst"]: b * pl["pst"] + G_ + 1]
+            assert po[G_] <= EMAX
+            for q in range(G_):
+                for x in ent[po[q]: po[q + 1]]:
+                    x = int(x)
+                    slot, cnt = x & 0xFFFF, (x >> 16) & 0xFFFF
+                    wv = np.uint32(x >> 32).view(np.float32)
+                    t = X[rows[slot]] * wv
+                    for _ in range(cnt):
+                        acc[q] = acc[q] + t
+        for q in range(G_):
+            row, split, slot0, sn = pl["pieces"][g * G_ + q]
+            if row < 0:
+                continue
+            if split < 0:
+                out[row] = acc[q]
+            else:
+                partial[slot0 + (sn >> 16)] = acc[q]
+                done[split] += 1
+                if done[split] == (sn & 0xFFFF):
+                    s4 = np.zeros(F, np.float32)
+                    for k in range(sn & 0xFFFF):
+                        s4 = s4 + partial[slot0 + k]
+                    out[row] = s4
+    return out
+
+
+@pytest.mark.parametrize("T,G_,S,EMAX", [(4096, 32, 44, 1024), (16, 8, 3, 12), (7, 4, 1, 4),
+                                         (64, 128, 161, 4096)])
+def test_stage_plan_matches_split_semantics(T, G_, S, EMAX):
+    """sg_host_stage_plan covers every edge once, keeps each row's edge order, and its pieces
+    are sg_host_plan's subgroups: simulated with the staged kernel's rule it equals the oracle's
+    seq_sum_rows of the GCN terms bit for bit (tiny batches exercise the batch boundaries)."""
+    V, E = 150, 3000
+    s, d = rng.rmat_edges(V, E, seed=4)
+    p = og.partition_2d(s, d, V, V)
+    ptr = p.csc_ptr.astype(np.int64)
+    idx = p.csc_idx.astype(np.int32)
+    w = og.gcn_edge_weights(s, d, V, np.float32)[p.csc_eid]
+    X = rng.features(V, 3, dtype=np.float32)
+    got = _stage_sum(ptr, idx, w, X, T, G_, S, EMAX)
+    want = saga.seq_sum_rows(ptr, X[idx] * w[:, None], T=T)
+    assert np.array_equal(got, want)
+    _, splits, n_slots = G.plan(ptr, T)
+    pl = _stage_plan(ptr, idx, w, T, G_, S, EMAX)
+    assert pl["n_splits"] == len(splits) and pl["n_slots"] == n_slots
+
+
+def test_stage_plan_rejects_unsorted_rows():
+    ptr = np.array([0, 3], np.int64)
+    idx = np.array([2, 1, 3], np.int32)
+    with pytest.raises(Exception):
+        _stage_plan(ptr, idx, None, 4096, 32, 8, 64)
