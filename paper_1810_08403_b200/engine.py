@@ -820,3 +820,67 @@ def run_train(config):
         m.save_checkpoint(ckpt, start + len(losses))
     return {"model": model, "V": V, "E": E, "epochs": len(losses), "start_epoch": start,
             "loss": losses}
+
+
+def run_bench(config):
+    """SPEC.md:604-612 run_bench: every scheduling strategy on the same partitioned graph.
+
+    One row per strategy of schedule.STRATEGIES ('locality', 'dest_order', 'stage_based'):
+    the scheduler's swap bytes and modelled makespan (schedule.build_schedule under the
+    config's ``budget_bytes``), and -- for the strategies the device executor runs (the resident
+    chunk orders 'locality' / 'dest_order'; 'stage_based', which materialises every stage's
+    edge tensors, is modelled only) -- the measured epoch time and the loss after ``epochs``
+    training epochs from the same seed (scheduling never changes values: SPEC.md:371).  The
+    ring / non-ring multi-device simulations of the reference's report are out of scope
+    (DESIGN.md §7).  Config keys: those of run_train plus ``budget_bytes``."""
+    import time
+
+    from . import graph as G
+    from . import schedule as S
+
+    cfg = dict(config)
+    budget = cfg.pop("budget_bytes", None)
+    known = {"model", "graph", "V", "E", "features", "hidden", "classes", "layers", "epochs", "lr",
+             "seed", "interval_size", "split_edges"}
+    bad = set(cfg) - known
+    if bad:
+        raise ConfigError(f"unknown config keys {sorted(bad)}")
+    model = cfg.get("model", "gcn")
+    if model not in ("gcn", "ggcn"):
+        raise ConfigError(f"run_bench model must be gcn or ggcn (got '{model}')")
+    V, E = int(cfg["V"]), int(cfg["E"])
+    gen = G.rmat_graph if cfg.get("graph", "uniform") == "rmat" else G.uniform_graph
+    g = gen(V, E, seed=int(cfg.get("seed", 0)))
+    F, H, C = int(cfg["features"]), int(cfg.get("hidden", 16)), int(cfg["classes"])
+    nl = int(cfg.get("layers", 2))
+    dims = [F] + [H] * (nl - 1) + [C]
+    epochs, lr = int(cfg.get("epochs", 1)), float(cfg.get("lr", 0.01))
+    X = torch.from_numpy(G.synthetic_features(V, F, seed=1))
+    labels = np.random.default_rng(3).integers(0, C, V)
+    rows = []
+    for strategy in S.STRATEGIES:
+        sch = S.build_schedule(g, dims, budget=budget, model=model, strategy=strategy)
+        row = {"strategy": strategy, "mode": sch.mode, "P": sch.P,
+               "swap_h2d_bytes": int(sch.swap_h2d_bytes), "swap_d2h_bytes": int(sch.swap_d2h_bytes),
+               "makespan_ms_model": round(sch.makespan_ms, 4), "measured_ms": None, "loss": None}
+        if sch.mode == "resident" and strategy in ("locality", "dest_order"):
+            interval = cfg.get("interval_size") or sch.interval_size
+            grid = G.ChunkGrid(g, interval, gcn_weights=model == "gcn",
+                               split_edges=cfg.get("split_edges", G.DEFAULT_SPLIT_EDGES))
+            build = gcn_model if model == "gcn" else ggcn_model
+            m = build(grid, dims, schedule=strategy)
+            m.load_features(X)
+            m.load_labels(labels)
+            losses = []
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for _ in range(epochs):
+                m.train_step(lr)
+                losses.append(float(m.loss.item()))
+            torch.cuda.synchronize()
+            m.check_status()
+            row["P"] = grid.P
+            row["measured_ms"] = round((time.perf_counter() - t0) * 1e3 / max(epochs, 1), 4)
+            row["loss"] = losses
+        rows.append(row)
+    return {"model": model, "V": V, "E": E, "dims": dims, "budget_bytes": budget, "rows": rows}

@@ -1137,3 +1137,23 @@ def test_staged_gather_equals_row_kernel(sg, F, T, mode, P):
     w = og.gcn_edge_weights(s, d, V, np.float32) if mode == "gcn" else np.ones(E, np.float32)
     want = saga.gcn_propagate_fwd(part, H.cpu().numpy(), w, T=T)
     assert np.array_equal(run(True, False, False), want)
+
+
+def test_run_bench_strategies(sg):
+    """SPEC.md:604-612 run_bench: one row per strategy; the executable resident orders give the
+    same losses (scheduling never changes values); under a streaming budget the
+    Locality row moves the fewest bytes."""
+    from paper_1810_08403_b200 import engine as E
+
+    cfg = {"model": "gcn", "graph": "rmat", "V": 3000, "E": 60000, "features": 32, "hidden": 16,
+           "classes": 4, "epochs": 3, "lr": 0.1, "interval_size": 1000}
+    rep = E.run_bench(cfg)
+    rows = {r["strategy"]: r for r in rep["rows"]}
+    assert set(rows) == {"locality", "dest_order", "stage_based"}
+    assert rows["locality"]["loss"] == rows["dest_order"]["loss"]
+    assert rows["locality"]["P"] == 3 and rows["stage_based"]["measured_ms"] is None
+    rep = E.run_bench(dict(cfg, epochs=1, budget_bytes=2_000_000))
+    rows = {r["strategy"]: r for r in rep["rows"]}
+    assert all(r["mode"] == "streaming" and r["P"] > 1 for r in rows.values())
+    tot = {k: r["swap_h2d_bytes"] + r["swap_d2h_bytes"] for k, r in rows.items()}
+    assert tot["locality"] == min(tot.values())

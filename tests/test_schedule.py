@@ -72,3 +72,18 @@ def test_infeasible_budget_and_bad_strategy(reddit_like):
 def test_ggcn_resident_bytes_exceed_gcn():
     assert S.resident_bytes(1000, 5000, [64, 32, 4], "ggcn") > S.resident_bytes(1000, 5000, [64, 32, 4])
     assert np.all(np.array(S.chunk_stats(np.array([0, 5]), np.array([9, 1]), 10, 2)) == [1, 2])
+
+
+def test_run_bench_unbounded_rows_equal_swaps():
+    """SPEC.md:610 (P = 1 -> identical rows): with no budget every strategy is resident with
+    the same swap bytes; the config is validated like run_train's."""
+    import paper_1810_08403_b200 as sg
+    import paper_1810_08403_b200.engine as E
+
+    g = sg.uniform_graph(500, 4000, seed=0)
+    rows = [S.build_schedule(g, [16, 8, 4], strategy=s) for s in S.STRATEGIES]
+    assert {(r.mode, r.swap_h2d_bytes, r.swap_d2h_bytes) for r in rows} == {("resident", 0, 0)}
+    with pytest.raises(sg.ConfigError):
+        E.run_bench({"model": "gcn", "V": 10, "E": 10, "features": 4, "classes": 2, "bogus": 1})
+    with pytest.raises(sg.ConfigError):
+        E.run_bench({"model": "mpgcn", "V": 10, "E": 10, "features": 4, "classes": 2})

@@ -1,0 +1,17 @@
+# round 2 measurement pass on the committed code: GPU suite, smoke, bench lines (all configs),
+# reference arm, ncu DRAM records of the benched kernel source, launch list, multi-GPU proxy
+set -x
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/f_smi.txt
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/f_smoke.txt 2>&1
+timeout 2400 python -m pytest tests -q -m gpu -rs 2>&1 | grep -E "passed|failed|SKIPPED|FAILED|Error" > gpurun_out/f_pytest.txt
+timeout 900 python bench.py > gpurun_out/f_bench.json 2> gpurun_out/f_bench.err
+timeout 900 python bench.py --impl reference > gpurun_out/f_ref.json 2> gpurun_out/f_ref.err
+M=dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,lts__t_sectors_srcunit_tex_op_read.sum
+timeout 600 ncu --metrics $M --clock-control none -k regex:prop_kernel --launch-skip 3 --launch-count 1 -f -o gpurun_out/f_dram_reddit python tools/profile_step.py reddit 2 > gpurun_out/f_dram_reddit.log 2>&1
+timeout 600 ncu --metrics $M --clock-control none -k regex:prop_kernel --launch-skip 2 --launch-count 1 -f -o gpurun_out/f_dram_noreuse python tools/noreuse_pass.py > gpurun_out/f_dram_noreuse.log 2>&1
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/f_launches.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --no-reorder --no-bf16 --no-noreuse > gpurun_out/f_launch_bench.log 2>&1
+timeout 1200 python tools/dist_proxy.py reddit 1 2 4 8 > gpurun_out/f_proxy.jsonl 2> gpurun_out/f_proxy.err
+for c in pubmed blogcatalog10 powerlaw_gcn powerlaw_ggcn; do
+  timeout 1200 python bench.py --config $c --no-cpu-baseline --no-noreuse --no-reorder --no-bf16 > gpurun_out/f_bench_$c.json 2> gpurun_out/f_bench_$c.err
+done
+ls -la gpurun_out | tail -40
