@@ -53,7 +53,7 @@ for N in Ns:
     shards = [D.ShardIndex(g, N, r, device=dev) for r in range(N)]
     size = shards[0].size
     blk = lambda t, i: t[i * size: i * size + shards[0].sizes[i]]  # noqa: E731
-    per_rank = []
+    per_rank, stages = [], []
     for r, s in enumerate(shards):
         n = s.rows
         a0, a1, z0, hz, z1, dz1, dz0 = mat(n, F), mat(n, H), mat(n, H), mat(n, H), mat(n, C), mat(n, C), mat(n, H)
@@ -61,20 +61,37 @@ for N in Ns:
         lab = torch.zeros(n, dtype=torch.int64, device=dev)
         loss, err = torch.zeros(1, device=dev), torch.zeros(1, dtype=torch.int32, device=dev)
 
+        marks = []
+
+        def mark(name):
+            if timing:
+                e = torch.cuda.Event(enable_timing=True)
+                e.record()
+                marks.append((name, e))
+
         def step():
+            mark("start")
             for k, i in enumerate(sorted(s.csc)):
                 K.propagate(s.csc[i], _lib.PROP_GCN, blk(X, i), a0, F, accumulate=k > 0, ws=ws)
+            mark("L0.fwd.propagate")
             K.gemm(a0, W0, z0, relu_out=hz, prec=P3, ws=ws)
+            mark("L0.fwd.gemm")
             for k, i in enumerate(sorted(s.csc)):
                 K.propagate(s.csc[i], _lib.PROP_GCN, blk(h1, i), a1, H, accumulate=k > 0, ws=ws)
+            mark("L1.fwd.propagate")
             K.gemm(a1, W1, z1, prec=P3, ws=ws)
             K.softmax_xent(z1, lab, loss, dz1, err, ws=ws)
             K.gemm(a1, dz1, dW1, trans_a=True, prec=P3, ws=ws)
+            mark("L1.gemms+loss")
             chain = sorted(s.csr)
             for k, j in enumerate(chain):
                 K.propagate(s.csr[j], _lib.PROP_GCN, blk(da1, j), dz0, H, accumulate=k > 0,
                             mask=z0 if k == len(chain) - 1 else None, ws=ws)
+            mark("L1.bwd.propagate")
             K.gemm(a0, dz0, dW0, trans_a=True, prec=P3, ws=ws)
+            mark("L0.dW.gemm")
+
+        timing = False
 
         for _ in range(3):
             step()
@@ -86,6 +103,15 @@ for N in Ns:
             e1.record()
         torch.cuda.synchronize()
         per_rank.append(float(np.mean([e0.elapsed_time(e1) for e0, e1 in ev])))
+        # one more step with a CUDA event between stages (the stage breakdown of this rank)
+        flush.zero_()
+        timing = True
+        step()
+        torch.cuda.synchronize()
+        timing = False
+        stages.append({n: round(marks[k - 1][1].elapsed_time(e), 3) for k, (n, e) in enumerate(marks) if k})
+        stages[-1]["edges"] = int(sum(pi.nnz for pi in s.csc.values()))
+        stages[-1]["chunks"] = len(s.csc)
     del shards
     torch.cuda.empty_cache()
     tmax = max(per_rank)
@@ -96,7 +122,8 @@ for N in Ns:
     out = {"config": name, "N": N, "rank_step_ms": [round(x, 3) for x in per_rank],
            "max_ms": round(tmax, 3), "mean_ms": round(float(np.mean(per_rank)), 3),
            "imbalance": round(tmax / float(np.mean(per_rank)), 3),
-           "comm_mb_per_rank": round(comm_bytes / 1e6, 1), "comm_ms_at_nvlink": round(comm_ms, 3)}
+           "comm_mb_per_rank": round(comm_bytes / 1e6, 1), "comm_ms_at_nvlink": round(comm_ms, 3),
+           "stages_slowest_rank": stages[int(np.argmax(per_rank))]}
     if t1:
         out["speedup_overlapped"] = round(t1 / tmax, 2)
         out["speedup_serial_comm"] = round(t1 / (tmax + comm_ms), 2)

@@ -43,7 +43,7 @@ def main():
         rec = {"records": {}, "launch_ms_under_ncu": {}, "kernels": {}}
     rec["kernel_source_sha256"] = sha
     rec["source"] = ("ncu --clock-control none (dram__bytes_read.sum + dram__bytes_write.sum, one "
-                     "launch per key), tools/gpu_r2_prof.sh; summarised by tools/ncu_dram.py")
+                     "launch per key), tools/gpu_r2_final.sh; summarised by tools/ncu_dram.py")
     for arg in sys.argv[1:]:
         key, rep = arg.split("=", 1)
         b, ms, name = dram_bytes(rep)
