@@ -195,7 +195,10 @@ struct Prop {
   // run-length reuse of multi-edges (see step): single-operand rows of >= 2 vectors per lane.
   // One-vector rows (F <= 128 fp32) keep one load per edge: there the run bookkeeping cost
   // more than the loads it saved (Reddit F = 128 passes 3.6 -> 4.5 ms).
-  static constexpr bool kRuns = NG == 1 && VPL >= 2;
+#ifndef SG_RUNS_MIN_VPL
+#define SG_RUNS_MIN_VPL 2
+#endif
+  static constexpr bool kRuns = NG == 1 && VPL >= SG_RUNS_MIN_VPL;
 
   // Load the lane's slice of DEPTH gathered rows (raw 16-byte vectors in flight), then add
   // their terms in edge order.  FULL: all DEPTH edges valid (no per-edge predicates).
@@ -494,15 +497,23 @@ struct Prop {
 #ifndef SG_VPL1_BLOCKS
 #define SG_VPL1_BLOCKS 2
 #endif
+// wide single-operand rows: 4 blocks/SM (64 registers, 56 B of spill) measured 4-5% faster than
+// 3 (80 registers) on the Reddit layer-1 pass (11.99 -> 11.32-11.52 ms; 5 blocks: 19.2 ms, and
+// 4 blocks without the in-register run detection: 13.8 ms; profiles/r02_occupancy_ab.txt)
 #ifndef SG_WIDE_BLOCKS
-#define SG_WIDE_BLOCKS 3
+#define SG_WIDE_BLOCKS 4
+#endif
+#ifndef SG_BF16_WIDE_BLOCKS
+#define SG_BF16_WIDE_BLOCKS 0
 #endif
 template <int MODE, int W, int VPL, int DEPTH>
 constexpr int prop_min_blocks() {
   if (VPL == 1 && ModeT<MODE>::NG == 1 && SG_VPL1_BLOCKS != 2) return SG_VPL1_BLOCKS;
-  // wide single-operand rows: one row in flight per warp at 3 blocks/SM (85 regs, no spill)
-  // beat two rows at 2 blocks/SM (F = 602 CSC pass 14.2-14.5 -> 13.1 ms)
+  // wide single-operand rows: one row in flight per warp at SG_WIDE_BLOCKS blocks/SM beat two
+  // rows at 2 blocks/SM (F = 602 CSC pass 14.2-14.5 -> 13.1 ms at 3 blocks)
   if (VPL >= 5 && ModeT<MODE>::NG == 1 && SG_WIDE_BLOCKS > 0) return SG_WIDE_BLOCKS;
+  // bf16 rows of 3-4 vectors per lane (8 bf16 per 16-B vector: F = 602 bf16 is 76 vectors)
+  if (W == 8 && VPL >= 3 && ModeT<MODE>::NG == 1 && SG_BF16_WIDE_BLOCKS > 0) return SG_BF16_WIDE_BLOCKS;
   // per in-flight edge: raw vectors + 64-bit row pointer + shuffled (src, w)
   constexpr int regs = DEPTH * (ModeT<MODE>::NG * VPL * 4 + 4) +
                        (ModeT<MODE>::NOUT + ModeT<MODE>::NR) * VPL * W + 40;

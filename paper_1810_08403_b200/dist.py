@@ -11,14 +11,19 @@ SURVEY.md §8(e), replacing the reference's ring-streaming simulator
   since layer outputs are indexed like inputs, source interval S_r = D_r of the next
   layer), the CSC chunks C_{i,r} of its column and the CSR chunks C_{r,j} of its row;
 * forward, per layer: every source-feature block (h_i for GCN, [h_i | P_i] for G-GCN)
-  is broadcast by its owner (NCCL, posted asynchronously in ascending i); the fused
-  gather over C_{i,r} waits only for block i, so it overlaps the transfer of the later
-  blocks, and accumulates into the resident A_r in ascending i -- the chunked engine's
-  Locality order, so the aggregate equals the 1-GPU chunked run with P = world bit for
-  bit -- then ApplyVertex on the local rows;
+  is broadcast by its owner (NCCL, posted asynchronously in ascending i) into one [V, F]
+  landing buffer; then ONE fused gather over the rank's whole column C_{*,r} (a pass index
+  over global ids, each row's in-edges in ascending source: the 1-GPU P = 1 pass over the
+  re-encoded graph, bit for bit) -- the default, ``ShardIndex(column=True)``: at 8 ranks the
+  per-chunk launches below ran 2.5x under one launch's per-edge rate, because every chunk
+  launch ends on its longest row (profiles/r02_dist_proxy.jsonl).  With ``column=False`` the
+  gather over C_{i,r} waits only for block i, overlapping the transfer of the later blocks,
+  and accumulates into A_r in ascending i (the 1-GPU chunked run with P = world, bitwise);
+  then ApplyVertex on the local rows;
 * loss: softmax-CE over local rows normalised by the global |V|, loss all-reduced;
 * backward: dW_r = a_r^T dz_r all-reduced; GCN streams the dA blocks and runs the CSR
-  duals over C_{r,j} (ascending j) with the ReLU mask of the layer below fused; G-GCN
+  dual over the rank's row C_{r,*} (or per chunk C_{r,j}, ascending j) with the ReLU mask of
+  the layer below fused; G-GCN
   takes dQ = dA (.) S with S summed by the forward (GGCN_FWD_S), streams the [dA | Q]
   blocks and runs pass B (CSR, dP and the take_rows part of dh) over them.
 NVSwitch gives every GPU full bandwidth to every peer, so the reference's fat-tree /
@@ -51,7 +56,7 @@ class ShardIndex:
     (select features / labels with it)."""
 
     def __init__(self, g, world, rank, split_edges="auto", device="cuda",
-                 gcn_weights=True, balance=True):
+                 gcn_weights=True, balance=True, column=True):
         size = -(-g.V // world)
         if balance and world > 1:
             g, perm = G.reencode_balance(g, world)
@@ -69,18 +74,53 @@ class ShardIndex:
         self.rows = self.sizes[rank]
         self.vertices = inv[self.begin: self.begin + self.rows]
         degs = g.degrees() if gcn_weights else None
+        self.column = bool(column)
         self.csc, self.csr = {}, {}
+        self.col_csc = self.col_csr = None
+        if self.column:
+            # the rank's whole column C_{*,r} (forward) and row C_{r,*} (backward) as ONE pass
+            # index each over global (re-encoded) ids: per local row, the chunks' edges in
+            # ascending block order -- for every row the in-edges sorted by global source, i.e.
+            # the single-GPU P = 1 pass over the re-encoded graph, bit for bit.  One launch per
+            # pass instead of world: at 8 ranks the per-chunk launches ran 2.5x below the
+            # per-edge rate of one launch (tools/dist_proxy.py, profiles/r02_dist_proxy.jsonl)
+            self.col_csc = self._column(part, g, degs, False, split_edges, device)
+            self.col_csr = self._column(part, g, degs, True, split_edges, device)
+            self.local_edges = self.col_csc.nnz if self.col_csc is not None else 0
+            return
         for i in range(world):
             ch = part.chunk(i, rank)
             if ch["nnz"]:
-                w = g.gcn_weights(ch["csc_eid"], degs) if gcn_weights else None
+                w = g.gcn_weights(ch["csc_eid"], degs) if degs is not None else None
                 self.csc[i] = G.PassIndex(ch["csc_ptr"], ch["csc_idx"], w, self.rows, split_edges, device)
         for j in range(world):
             ch = part.chunk(rank, j)
             if ch["nnz"]:
-                w = g.gcn_weights(ch["csr_eid"], degs) if gcn_weights else None
+                w = g.gcn_weights(ch["csr_eid"], degs) if degs is not None else None
                 self.csr[j] = G.PassIndex(ch["csr_ptr"], ch["csr_idx"], w, self.rows, split_edges, device)
         self.local_edges = sum(pi.nnz for pi in self.csc.values())
+
+    def _column(self, part, g, degs, csr, split_edges, device):
+        keys, idx, w = [], [], []
+        for k in range(self.world):
+            ch = part.chunk(self.rank, k) if csr else part.chunk(k, self.rank)
+            if not ch["nnz"]:
+                continue
+            ptr = ch["csr_ptr"] if csr else ch["csc_ptr"]
+            rows = np.repeat(np.arange(self.rows, dtype=np.int64), np.diff(ptr))
+            keys.append(rows * self.world + k)
+            idx.append(ch["csr_idx" if csr else "csc_idx"].astype(np.int64) + k * self.size)
+            if degs is not None:
+                w.append(g.gcn_weights(ch["csr_eid" if csr else "csc_eid"], degs))
+        if not keys:
+            return None
+        keys = np.concatenate(keys)
+        o = np.argsort(keys, kind="stable")        # by row, then block; in-chunk order kept
+        ptr = np.zeros(self.rows + 1, np.int64)
+        ptr[1:] = np.cumsum(np.bincount(keys[o] // self.world, minlength=self.rows))
+        idx = np.concatenate(idx)[o].astype(np.int32)
+        w = np.concatenate(w)[o] if w else None
+        return G.PassIndex(ptr, idx, w, self.rows, split_edges, device)
 
 
 class CudaCompute:
@@ -183,7 +223,8 @@ class DistSAGA:
             self.h[0] = self.HP[0][:, : dims[0]]
             for l in range(1, L):
                 self.h[l] = self.HP[l][:, : dims[l]]
-        self._blocks = {}  # key -> per-source-interval landing buffers
+        self._blocks = {}  # key -> per-source-interval landing buffers (views of _full[key])
+        self._full = {}
         self.labels = torch.zeros(n, dtype=torch.int64, device=dev)
         self.loss = torch.zeros(1, dtype=dtype, device=dev)
         self.err = torch.zeros(1, dtype=torch.int32, device=dev)
@@ -265,8 +306,11 @@ class DistSAGA:
         block is copied in place (its broadcast is the send)."""
         ldw = _ld(width)
         if key not in self._blocks:
-            self._blocks[key] = [torch.zeros((n, ldw), dtype=X.dtype, device=X.device)
-                                 for n in self.s.sizes]
+            # one [V, ldw] buffer, block i = rows of source interval i (a column pass reads it
+            # whole with global ids)
+            full = torch.zeros((self.s.V, ldw), dtype=X.dtype, device=X.device)
+            self._full[key] = full
+            self._blocks[key] = [full[i * self.s.size: i * self.s.size + n] for i, n in enumerate(self.s.sizes)]
         blocks = self._blocks[key]
         blocks[self.s.rank][:, :width].copy_(X[:, :width])
         works = [dist.broadcast(blocks[i], src=i, group=self.group, async_op=True)
@@ -298,18 +342,29 @@ class DistSAGA:
                 c.gemm(self.h[l], self.WC[l], self.GQ[l][:, go: go + F])  # Q = h W_C
                 self._mark(f"L{l}.fwd.hoist_gemm")
                 blocks = self._stream_blocks(("HP", l), HP, go + F)
+                if s.column:
+                    self._drain(blocks)
+                    if s.col_csc is not None:
+                        c.propagate(s.col_csc, _lib.PROP_GGCN_FWD_S, self._full[("HP", l)][:, : go + F],
+                                    self.a[l], F, g_off=go, R=self.GQ[l][:, go: go + F], out1=self.S[l])
                 for k, i in enumerate(chain):
                     blocks[i][1].wait()
                     c.propagate(s.csc[i], _lib.PROP_GGCN_FWD_S, blocks[i][0], self.a[l], F, g_off=go,
                                 R=self.GQ[l][:, go: go + F], out1=self.S[l], accumulate=k > 0)
             else:
                 blocks = self._stream_blocks(("h", F), self.h[l], F)
+                if s.column:
+                    self._drain(blocks)
+                    if s.col_csc is not None:
+                        c.propagate(s.col_csc, _lib.PROP_GCN, self._full[("h", F)][:, :F], self.a[l], F)
                 for k, i in enumerate(chain):   # source intervals ascending (Locality order)
                     blocks[i][1].wait()
                     c.propagate(s.csc[i], _lib.PROP_GCN, blocks[i][0], self.a[l], F,
                                 accumulate=k > 0)
-            if not chain:
+            if not chain and (not s.column or s.col_csc is None):
                 self.a[l].zero_()
+                if self.model == "ggcn":
+                    self.S[l].zero_()
             self._drain(blocks)
             self._mark(f"L{l}.fwd.propagate")
             c.gemm(self.a[l], self.W[l], self.z[l], relu_out=self.h[l + 1] if l + 1 < L else None)
@@ -336,7 +391,14 @@ class DistSAGA:
             self._mark(f"L{l}.bwd.apply_vertex")
             blocks = self._stream_blocks(("h", F), self.da[l], F)
             chain = [j for j in range(self.world) if j in s.csr]
-            if not chain:
+            if s.column:
+                self._drain(blocks)
+                if s.col_csr is not None:
+                    c.propagate(s.col_csr, _lib.PROP_GCN, self._full[("h", F)][:, :F], self.dz[l - 1], F,
+                                mask=self.z[l - 1])
+                else:
+                    self.dz[l - 1].zero_()
+            elif not chain:
                 self.dz[l - 1].zero_()
             for k, j in enumerate(chain):  # destination intervals ascending
                 blocks[j][1].wait()
@@ -357,7 +419,15 @@ class DistSAGA:
         # pass B over the local CSR row: dP[v], dh_take[v], with streamed [dA | Q] blocks
         blocks = self._stream_blocks(("GQ", l), GQ, go + F)
         chain = [j for j in range(self.world) if j in s.csr]
-        if not chain:
+        if s.column:
+            self._drain(blocks)
+            if s.col_csr is not None:
+                c.propagate(s.col_csr, _lib.PROP_GGCN_BWD_SRC, self._full[("GQ", l)][:, : go + F], self.dP[l], F,
+                            g_off=go, R=self.HP[l], r_off=go, out1=self.dHt[l])
+            else:
+                self.dP[l].zero_()
+                self.dHt[l].zero_()
+        elif not chain:
             self.dP[l].zero_()
             self.dHt[l].zero_()
         for k, j in enumerate(chain):

@@ -115,10 +115,11 @@ def _worker(rank, world, port, case, outdir):
     import paper_1810_08403_b200 as sg
     from paper_1810_08403_b200 import dist as D
 
-    model, V, E, F, H, C, gen, T = case
+    model, V, E, F, H, C, gen, T, column = case
     s, d = (rng.rmat_edges if gen == "rmat" else rng.uniform_edges)(V, E, seed=4)
     g = sg.Graph(V, s, d)
-    shard = D.ShardIndex(g, world, rank, split_edges=T, device="cpu", gcn_weights=model == "gcn")
+    shard = D.ShardIndex(g, world, rank, split_edges=T, device="cpu", gcn_weights=model == "gcn",
+                         column=column)
     m = D.DistSAGA(shard, [F, H, C], NumpyCompute(T), model=model,
                    weights=_case_params(model, F, H, C), dtype=torch.float64)
     X = rng.features(V, F, seed=1, dtype=np.float64)
@@ -145,13 +146,16 @@ CASES = [("gcn", 40, 300, 6, 5, 3, "uniform", 4096), ("gcn", 64, 900, 7, 4, 3, "
          ("ggcn", 48, 500, 6, 5, 3, "rmat", 7), ("ggcn", 30, 200, 5, 4, 3, "uniform", 4096)]
 
 
+@pytest.mark.parametrize("column", [True, False])
 @pytest.mark.parametrize("case", CASES)
-def test_dist_world2_matches_chunked_oracle(case):
-    """Sharded epoch (re-encoded by reencode_balance) == chunked oracle with P = world on the
-    re-encoded graph: aggregates bitwise, loss and gradients to fp64 rounding."""
+def test_dist_world2_matches_chunked_oracle(case, column):
+    """Sharded epoch (re-encoded by reencode_balance) == the chunked oracle on the re-encoded
+    graph: with column passes (the default) the P = 1 oracle (each row's in-edges in ascending
+    global source), with per-chunk passes the P = world oracle (chained in ascending block);
+    aggregates bitwise, loss and gradients to fp64 rounding."""
     world = 2
     with tempfile.TemporaryDirectory() as outdir:
-        mp.start_processes(_worker, args=(world, _free_port(), case, outdir), nprocs=world,
+        mp.start_processes(_worker, args=(world, _free_port(), case + (column,), outdir), nprocs=world,
                            join=True, start_method="spawn")
         res = [dict(np.load(os.path.join(outdir, f"r{r}.npz"))) for r in range(world)]
     model, V, E, F, H, C, gen, T = case
@@ -162,7 +166,7 @@ def test_dist_world2_matches_chunked_oracle(case):
     inv = np.argsort(perm)
     X = rng.features(V, F, seed=1, dtype=np.float64)[inv]
     y = rng.labels(V, C)[inv]
-    part = og.partition_2d(s, d, V, -(-V // world))
+    part = og.partition_2d(s, d, V, V if column else -(-V // world))
     P = _case_params(model, F, H, C)
     if model == "gcn":
         w = og.gcn_edge_weights(s, d, V, np.float32).astype(np.float64)  # the index stores fp32 w_e

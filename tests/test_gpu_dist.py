@@ -3,8 +3,9 @@
 NCCL refuses two ranks on one device, so these tests run the sharded engine of
 paper_1810_08403_b200.dist with world_size 2, 4 and 8 over gloo (which moves CUDA tensors through
 host memory) with both ranks on cuda:0 and ``CudaCompute`` doing every gather, GEMM and
-loss.  The result must equal the single-GPU chunked executor with P = world on the same
-re-encoded graph: layer-1 aggregates bitwise (same kernels, same chunk order), the rest
+loss.  The result must equal the single-GPU executor on the same re-encoded graph -- with P = 1
+for the default column passes (one pass per rank over its whole column), with P = world for
+per-chunk passes: layer-1 aggregates bitwise (same kernels, same per-row order), the rest
 within fp32 reduction-order tolerance (dW is a sum of per-rank partials).
 """
 
@@ -42,9 +43,10 @@ def _worker(rank, world, port, case, outdir):
     import paper_1810_08403_b200 as sg
     from paper_1810_08403_b200 import dist as D
 
-    model, V, E, F, H, C, gen, T = case
+    model, V, E, F, H, C, gen, T, column = case
     g = _graph(gen, V, E)
-    shard = D.ShardIndex(g, world, rank, split_edges=T, device="cuda:0", gcn_weights=model == "gcn")
+    shard = D.ShardIndex(g, world, rank, split_edges=T, device="cuda:0", gcn_weights=model == "gcn",
+                         column=column)
     m = D.DistSAGA(shard, [F, H, C], D.CudaCompute("cuda:0"), model=model, seed=2)
     X = sg.synthetic_features(V, F, seed=1)
     y = np.random.default_rng(3).integers(0, C, V)
@@ -63,10 +65,13 @@ def _worker(rank, world, port, case, outdir):
     dist.destroy_process_group()
 
 
-CASES = [("gcn", 3000, 60000, 37, 16, 5, "rmat", 4096, 2), ("gcn", 2500, 40000, 130, 24, 7, "uniform", 64, 2),
-         ("ggcn", 2000, 30000, 32, 16, 5, "rmat", 128, 2),
+# (model, V, E, F, H, C, graph, T, column passes, world)
+CASES = [("gcn", 3000, 60000, 37, 16, 5, "rmat", 4096, True, 2), ("gcn", 2500, 40000, 130, 24, 7, "uniform", 64, True, 2),
+         ("ggcn", 2000, 30000, 32, 16, 5, "rmat", 128, True, 2),
+         # per-chunk passes (column=False): the streamed, block-overlapped mode
+         ("gcn", 3000, 60000, 37, 16, 5, "rmat", 256, False, 4), ("ggcn", 2000, 30000, 32, 16, 5, "rmat", 128, False, 2),
          # the bench's rank counts: 8 (and 4) processes sharing one B200 over gloo
-         ("gcn", 4000, 80000, 40, 16, 5, "rmat", 256, 8), ("ggcn", 3000, 50000, 24, 16, 5, "rmat", 512, 4)]
+         ("gcn", 4000, 80000, 40, 16, 5, "rmat", 256, True, 8), ("ggcn", 3000, 50000, 24, 16, 5, "rmat", 512, True, 4)]
 
 
 @pytest.mark.parametrize("case", CASES)
@@ -79,12 +84,13 @@ def test_dist_cuda_matches_single_gpu_chunked(case):
         mp.start_processes(_worker, args=(world, _free_port(), case, outdir), nprocs=world,
                            join=True, start_method="spawn")
         res = [dict(np.load(os.path.join(outdir, f"r{r}.npz"))) for r in range(world)]
-    model, V, E, F, H, C, gen, T = case
+    model, V, E, F, H, C, gen, T, column = case
     g = _graph(gen, V, E)
     g2, perm = sg.reencode_balance(g, world)
     assert np.array_equal(res[0]["perm"], perm)
     inv = np.argsort(perm)
-    grid = sg.ChunkGrid(g2, -(-V // world), split_edges=T, gcn_weights=model == "gcn")
+    # column passes == the 1-GPU P = 1 run of the re-encoded graph; per-chunk passes == P = world
+    grid = sg.ChunkGrid(g2, V if column else -(-V // world), split_edges=T, gcn_weights=model == "gcn")
     build = sg.gcn_model if model == "gcn" else sg.ggcn_model
     m = build(grid, [F, H, C], seed=2)
     m.load_features(torch.from_numpy(sg.synthetic_features(V, F, seed=1)[inv]))

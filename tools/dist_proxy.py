@@ -4,7 +4,9 @@ For N = 1, 2, 4, 8: build every rank's shard (reencode_balance + P = N grid, Sha
 run rank r's whole step on this one GPU -- its CSC column C_{*,r} (forward, both layers), its
 ApplyVertex GEMMs on |D_r| rows, softmax-CE, its CSR row C_{r,*} (backward dual, ReLU mask) and
 the weight-gradient GEMMs -- with every source block already resident (what the streamed NCCL
-broadcasts deliver), CUDA-event timed, 3 warm-up + 10 timed steps each.  The N-GPU epoch is
+broadcasts deliver), captured in a CUDA graph and CUDA-event timed, 3 warm-up + 10 timed steps
+each; one more eager step with events between stages gives the slowest rank's breakdown
+(host-enqueue gaps included there).  The N-GPU epoch is
 bounded below by max_r T_r (compute) and by the per-rank broadcast volume over NVLink; the
 predicted speedup is T_1 / max(max_r T_r, comm) with comm at NVLINK_GBS (0 if fully overlapped).
 
@@ -49,8 +51,11 @@ h1 = mat(V, H).uniform_(-1, 1)      # layer-1 input of every rank (all blocks re
 da1 = mat(V, H).uniform_(-1, 1)     # layer-1 dA of every rank (backward blocks resident)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 t1 = None
+COLUMN = os.environ.get("SG_PROXY_COLUMN", "1") == "1"   # dist.ShardIndex's default
+
+
 for N in Ns:
-    shards = [D.ShardIndex(g, N, r, device=dev) for r in range(N)]
+    shards = [D.ShardIndex(g, N, r, device=dev, column=COLUMN) for r in range(N)]
     size = shards[0].size
     blk = lambda t, i: t[i * size: i * size + shards[0].sizes[i]]  # noqa: E731
     per_rank, stages = [], []
@@ -69,7 +74,26 @@ for N in Ns:
                 e.record()
                 marks.append((name, e))
 
+        colc, colr = s.col_csc, s.col_csr
+
         def step():
+            mark("start")
+            if COLUMN:
+                K.propagate(colc, _lib.PROP_GCN, X, a0, F, ws=ws)
+                mark("L0.fwd.propagate")
+                K.gemm(a0, W0, z0, relu_out=hz, prec=P3, ws=ws)
+                mark("L0.fwd.gemm")
+                K.propagate(colc, _lib.PROP_GCN, h1, a1, H, ws=ws)
+                mark("L1.fwd.propagate")
+                K.gemm(a1, W1, z1, prec=P3, ws=ws)
+                K.softmax_xent(z1, lab, loss, dz1, err, ws=ws)
+                K.gemm(a1, dz1, dW1, trans_a=True, prec=P3, ws=ws)
+                mark("L1.gemms+loss")
+                K.propagate(colr, _lib.PROP_GCN, da1, dz0, H, mask=z0, ws=ws)
+                mark("L1.bwd.propagate")
+                K.gemm(a0, dz0, dW0, trans_a=True, prec=P3, ws=ws)
+                mark("L0.dW.gemm")
+                return
             mark("start")
             for k, i in enumerate(sorted(s.csc)):
                 K.propagate(s.csc[i], _lib.PROP_GCN, blk(X, i), a0, F, accumulate=k > 0, ws=ws)
@@ -95,11 +119,18 @@ for N in Ns:
 
         for _ in range(3):
             step()
+        # the rank's step captured in a CUDA graph (as the engine's graph mode runs it): at N = 8
+        # a chunk pass is ~0.05-0.5 ms of GPU work, less than its Python enqueue
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step()
+        graph.replay()
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(10)]
         for e0, e1 in ev:
             flush.zero_()
             e0.record()
-            step()
+            graph.replay()
             e1.record()
         torch.cuda.synchronize()
         per_rank.append(float(np.mean([e0.elapsed_time(e1) for e0, e1 in ev])))
@@ -110,8 +141,8 @@ for N in Ns:
         torch.cuda.synchronize()
         timing = False
         stages.append({n: round(marks[k - 1][1].elapsed_time(e), 3) for k, (n, e) in enumerate(marks) if k})
-        stages[-1]["edges"] = int(sum(pi.nnz for pi in s.csc.values()))
-        stages[-1]["chunks"] = len(s.csc)
+        stages[-1]["edges"] = int(s.local_edges)
+        stages[-1]["launches_per_pass"] = 1 if COLUMN else len(s.csc)
     del shards
     torch.cuda.empty_cache()
     tmax = max(per_rank)
@@ -119,7 +150,7 @@ for N in Ns:
     # per rank and epoch: (N-1)/N of the layer-1 (F) and layer-2 (H) inputs and the layer-2 dA (H)
     comm_bytes = (N - 1) / N * V * 4 * ((F + 3) // 4 * 4 + 2 * ((H + 3) // 4 * 4))
     comm_ms = comm_bytes / (NVLINK_GBS * 1e9) * 1e3
-    out = {"config": name, "N": N, "rank_step_ms": [round(x, 3) for x in per_rank],
+    out = {"config": name, "N": N, "column_pass": COLUMN, "rank_step_ms": [round(x, 3) for x in per_rank],
            "max_ms": round(tmax, 3), "mean_ms": round(float(np.mean(per_rank)), 3),
            "imbalance": round(tmax / float(np.mean(per_rank)), 3),
            "comm_mb_per_rank": round(comm_bytes / 1e6, 1), "comm_ms_at_nvlink": round(comm_ms, 3),
