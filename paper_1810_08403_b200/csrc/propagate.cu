@@ -503,8 +503,10 @@ struct Prop {
 #ifndef SG_WIDE_BLOCKS
 #define SG_WIDE_BLOCKS 4
 #endif
+// bf16 rows of 3-4 vectors per lane at 3 blocks/SM (80 registers, 92 B of spill): Reddit bf16
+// layer-1 pass 11.57 -> 10.51 ms (2 blocks with 4 rows in flight: 10.88; profiles/r02_occupancy_ab.txt)
 #ifndef SG_BF16_WIDE_BLOCKS
-#define SG_BF16_WIDE_BLOCKS 0
+#define SG_BF16_WIDE_BLOCKS 3
 #endif
 template <int MODE, int W, int VPL, int DEPTH>
 constexpr int prop_min_blocks() {
