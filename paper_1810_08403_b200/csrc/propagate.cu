@@ -178,6 +178,9 @@ struct PropArgs {
   int32_t accumulate;
   const int32_t* hub_rows;  // hub-row cache: idx < 0 means slot (idx & 0x7fffffff) in smem
   int32_t n_hub;
+  // resident blocks per SM to launch for the wide single-operand kernels (0: all the kernel's
+  // occupancy allows): passes without split rows (no hubs) cap at 3, see launch_one
+  int32_t wide_blocks_cap;
 };
 
 template <int MODE, int DT, int W, int VPL, int LPR, int DEPTH, bool HUB = false>
@@ -719,6 +722,12 @@ cudaError_t launch_one(const PropArgs& a, cudaStream_t st) {
   }
   int64_t want = ((int64_t)a.n_items + kWarpsPerBlock - 1) / kWarpsPerBlock;
   int64_t cap = (int64_t)blocks_per_sm * sm_count();
+  // Wide rows: 4 blocks/SM pays on hub-heavy passes (R-MAT Reddit L0 11.5 -> 11.0 ms), but on a
+  // pass without heavy rows (uniform graph, avg degree 490 < T) the 32 warps/SM sweep a wider
+  // window of the source-sorted rows than L2 holds (DRAM 42 -> 127 GB, 16.2 -> 23.9 ms), so
+  // such passes launch 3 blocks/SM of the same kernel
+  if (VPL >= 5 && NG == 1 && a.wide_blocks_cap > 0)
+    cap = std::min<int64_t>(cap, (int64_t)std::min(blocks_per_sm, (int)a.wide_blocks_cap) * sm_count());
   int grid = (int)std::max<int64_t>(1, std::min(want, cap));
   kern<<<grid, kWarpsPerBlock * 32, 0, st>>>(a);
   sg::count_launch();
@@ -904,6 +913,7 @@ int sg_propagate_hub(int mode, int dtype, const int64_t* ptr, const int32_t* idx
     a.n_items = (int32_t)n_items; a.Fv = Fv; a.Fcols = (int32_t)cols; a.accumulate = accumulate;
     a.hub_rows = hub_rows;
     a.n_hub = 0;
+    a.wide_blocks_cap = hub_heavy ? 0 : 3;
     if (n_hub > 0) {
       // an index encoded for hubs must run the hub kernel (negative entries are slots)
       SG_REQUIRE(hub_rows && vec && mode <= SG_PROP_GCN && LPR == 32 && VPL >= kHubMinVpl &&

@@ -11,6 +11,7 @@ timeout 600 ncu --metrics $M --clock-control none -k regex:prop_kernel --launch-
 timeout 600 ncu --metrics $M --clock-control none -k regex:prop_kernel --launch-skip 2 --launch-count 1 -f -o gpurun_out/f_dram_noreuse python tools/noreuse_pass.py > gpurun_out/f_dram_noreuse.log 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/f_launches.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --no-reorder --no-bf16 --no-noreuse > gpurun_out/f_launch_bench.log 2>&1
 timeout 1200 python tools/dist_proxy.py reddit 1 2 4 8 > gpurun_out/f_proxy.jsonl 2> gpurun_out/f_proxy.err
+timeout 900 python -c "import json; from paper_1810_08403_b200 import engine as E; print(json.dumps(E.run_bench({\"model\": \"gcn\", \"graph\": \"rmat\", \"V\": 232965, \"E\": 114615892 // 8, \"features\": 602, \"hidden\": 128, \"classes\": 41, \"epochs\": 3})))" > gpurun_out/f_run_bench.json 2> gpurun_out/f_run_bench.err
 for c in pubmed blogcatalog10 powerlaw_gcn powerlaw_ggcn; do
   timeout 1200 python bench.py --config $c --no-cpu-baseline --no-noreuse --no-reorder --no-bf16 > gpurun_out/f_bench_$c.json 2> gpurun_out/f_bench_$c.err
 done
