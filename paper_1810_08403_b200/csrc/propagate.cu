@@ -511,8 +511,19 @@ struct Prop {
 #ifndef SG_BF16_WIDE_BLOCKS
 #define SG_BF16_WIDE_BLOCKS 3
 #endif
-template <int MODE, int W, int VPL, int DEPTH>
+// bf16 rows of 65-128 columns (8-byte vectors, one per lane): 4 blocks/SM with 4 rows in flight
+// (64 registers) instead of 2 blocks x 12: Reddit bf16 F = 128 passes 4.32 / 4.45 -> 3.34 / 3.44 ms
+// (the fp32 one-vector rows measured the same at 2 x 8, 3 x 4 and 4 x 3; profiles/r02_occupancy_ab.txt)
+#ifndef SG_BF16_HALF_BLOCKS
+#define SG_BF16_HALF_BLOCKS 4
+#endif
+#ifndef SG_BF16_HALF_DEPTH
+#define SG_BF16_HALF_DEPTH 4
+#endif
+template <int MODE, int DT, int W, int VPL, int DEPTH>
 constexpr int prop_min_blocks() {
+  if (DT != SG_F32 && W == 4 && VPL == 1 && ModeT<MODE>::NG == 1 && SG_BF16_HALF_BLOCKS > 0)
+    return SG_BF16_HALF_BLOCKS;
   if (VPL == 1 && ModeT<MODE>::NG == 1 && SG_VPL1_BLOCKS != 2) return SG_VPL1_BLOCKS;
   // wide single-operand rows: one row in flight per warp at SG_WIDE_BLOCKS blocks/SM beat two
   // rows at 2 blocks/SM (F = 602 CSC pass 14.2-14.5 -> 13.1 ms at 3 blocks)
@@ -529,7 +540,7 @@ constexpr int prop_min_blocks() {
 // a.hub_rows; their edges carry idx = slot | 0x80000000) into shared memory, so those
 // gathers are served on-chip instead of through L2.  One block of NWB warps per SM.
 template <int MODE, int DT, int W, int VPL, int LPR, int DEPTH, bool HUB = false, int NWB = kWarpsPerBlock>
-__global__ void __launch_bounds__(NWB * 32, (HUB ? 1 : prop_min_blocks<MODE, W, VPL, DEPTH>()))
+__global__ void __launch_bounds__(NWB * 32, (HUB ? 1 : prop_min_blocks<MODE, DT, W, VPL, DEPTH>()))
     prop_kernel(const PropArgs a) {
   using K = Prop<MODE, DT, W, VPL, LPR, DEPTH, HUB>;
   using Raw = typename K::Raw;
@@ -703,14 +714,19 @@ cudaError_t launch_one(const PropArgs& a, cudaStream_t st) {
   constexpr int MID1 = DT != SG_F32 ? SG_DEPTH_MID1_BF16 : SG_DEPTH_MID1;
   constexpr int DEPTH_MID = NG == 1 ? (MID1 / VPL > 0 ? MID1 / VPL : 1)
                                     : SG_DEPTH_MID / (VPL * NG);
-  constexpr int DEPTH1 = (DT != SG_F32 && W == 4 && NG == 1) ? SG_DEPTH1 * 3 / 2 : SG_DEPTH1;
+#ifndef SG_DEPTH1_WARP
+#define SG_DEPTH1_WARP SG_DEPTH1
+#endif
+  // one-vector rows: SG_DEPTH1 rows in flight per lane team; SG_DEPTH1_WARP for warp-wide rows
+  constexpr int D1 = LPR == 32 ? SG_DEPTH1_WARP : SG_DEPTH1;
+  constexpr int DEPTH1 = (DT != SG_F32 && W == 4 && NG == 1) ? SG_BF16_HALF_DEPTH : D1;
   constexpr int DEPTH = (VPL * NG) == 1 ? DEPTH1
                                         : ((VPL * NG) <= 4 ? DEPTH_MID : (NG > 1 ? 1 : SG_DEPTH_WIDE));
   if constexpr (LPR == 32 && NG == 1 && W > 1 && VPL >= kHubMinVpl) {
     if (a.n_hub > 0) {
       // hub-cache kernel: one block per SM holding the hub rows, as many warps as the
       // register budget allowed the default kernel (2-3 blocks of 8 warps)
-      constexpr int NWB = kWarpsPerBlock * prop_min_blocks<MODE, W, VPL, DEPTH>();
+      constexpr int NWB = kWarpsPerBlock * prop_min_blocks<MODE, DT, W, VPL, DEPTH>();
       return launch_hub<MODE, DT, W, VPL, LPR, DEPTH, NWB>(a, st);
     }
   }
