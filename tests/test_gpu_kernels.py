@@ -167,9 +167,6 @@ def test_ggcn_propagate_fwd_bwd(sg, P, T):
             K.propagate(grid.csc[(i, j)], _lib.PROP_GGCN_FWD_S, rows(HP, i), rows(A2, j), F, g_off=F,
                         R=rows(GQ, j)[:, F:], out1=rows(S, j), accumulate=k > 0)
     assert torch.equal(A2, A)
-    # elementwise floor 0.5 (not 0.1) of the 1e-5 band: the gate factor eta (1 - eta) carries the
-    # SFU's ~2-ulp error, amplified by the cancellation in 1 - eta for saturated gates, and dQ now
-    # sums it before (not after) the multiplication by dA
     # floor 0.5 of the 1e-5 band: dQ = dA (.) S re-associates the reference's
     # sum(((dA h) eta)(1 - eta)) -- the gate factor eta (1 - eta) carries the SFU's ~2-ulp error,
     # amplified by the cancellation in 1 - eta for saturated gates, and is summed before (not
