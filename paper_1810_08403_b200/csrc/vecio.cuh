@@ -11,7 +11,32 @@
 
 #include "../../include/sagann.h"
 
+#ifndef SG_ROW_LOAD
+#define SG_ROW_LOAD 3
+#endif
+
 namespace sg {
+
+// bf16 gathered rows with the same L1 policy as the fp32 ones (SG_ROW_LOAD 3: evict_last)
+__device__ __forceinline__ uint4 ld_row_u4(const uint4* p) {
+#if SG_ROW_LOAD == 3
+  uint4 r;
+  asm volatile("ld.global.nc.L1::evict_last.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+#else
+  return __ldg(p);
+#endif
+}
+__device__ __forceinline__ uint2 ld_row_u2(const uint2* p) {
+#if SG_ROW_LOAD == 3
+  uint2 r;
+  asm volatile("ld.global.nc.L1::evict_last.v2.u32 {%0, %1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
+  return r;
+#else
+  return __ldg(p);
+#endif
+}
 
 template <int DT, int W>
 struct VecIO;
@@ -20,8 +45,29 @@ template <>
 struct VecIO<SG_F32, 4> {
   using Elem = float;
   using Raw = float4;
+  // gathered-row load (SG_ROW_LOAD for A/B builds): 0 = ld.global.nc, 1 = +L1::no_allocate,
+  // 2 = +L1::evict_first, 3 = +L1::evict_last (default), 4 = ld.global.cg (L2 only).  Reddit epoch
+  // (profiles/r02_occupancy_ab.txt): evict_last 19.2-19.3 ms vs 20.1 (nc), 25.1 (no_allocate),
+  // 24.4 (evict_first), 21.2-21.4 (cg): the gathered rows are re-read by later edges, the
+  // index / weight / output streams (ld.cs / st.cs) are not
   static __device__ __forceinline__ Raw ld_raw(const Elem* p) {
+#if SG_ROW_LOAD == 0
     return __ldg(reinterpret_cast<const float4*>(p));
+#elif SG_ROW_LOAD == 4
+    return __ldcg(reinterpret_cast<const float4*>(p));
+#else
+    float4 r;
+#if SG_ROW_LOAD == 1
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+#elif SG_ROW_LOAD == 2
+    asm volatile("ld.global.nc.L1::evict_first.v4.f32 {%0, %1, %2, %3}, [%4];"
+#else
+    asm volatile("ld.global.nc.L1::evict_last.v4.f32 {%0, %1, %2, %3}, [%4];"
+#endif
+                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+                 : "l"(p));
+    return r;
+#endif
   }
   static __device__ __forceinline__ void unpack(const Raw& r, float* v) {
     v[0] = r.x; v[1] = r.y; v[2] = r.z; v[3] = r.w;
@@ -85,7 +131,7 @@ struct VecIO<SG_BF16, 8> {
   using Elem = __nv_bfloat16;
   using Raw = uint4;
   static __device__ __forceinline__ Raw ld_raw(const Elem* p) {
-    return __ldg(reinterpret_cast<const uint4*>(p));
+    return ld_row_u4(reinterpret_cast<const uint4*>(p));
   }
   static __device__ __forceinline__ void unpack(const Raw& r, float* v) {
     const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&r);
@@ -122,7 +168,7 @@ struct VecIO<SG_BF16, 4> {
   using Elem = __nv_bfloat16;
   using Raw = uint2;
   static __device__ __forceinline__ Raw ld_raw(const Elem* p) {
-    return __ldg(reinterpret_cast<const uint2*>(p));
+    return ld_row_u2(reinterpret_cast<const uint2*>(p));
   }
   static __device__ __forceinline__ void unpack(const Raw& r, float* v) {
     const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&r);
