@@ -345,9 +345,11 @@ def timed_epochs(m, a, flush):
     return ms, st
 
 
-def traffic_record(key, kernel_src="paper_1810_08403_b200/csrc/propagate.cu"):
+def traffic_record(key, kernel_srcs=("paper_1810_08403_b200/csrc/propagate.cu",
+                                     "paper_1810_08403_b200/csrc/vecio.cuh")):
     """ncu DRAM bytes per launch for `key` from profiles/ncu_dram_bytes.json, and whether the
-    record was taken on the kernel source that is benched now (sha256 of the .cu file)."""
+    record was taken on the kernel source that is benched now (sha256 over the gather kernel's
+    sources, as tools/ncu_dram.py stamps it)."""
     import hashlib
 
     path = os.path.join(ROOT, "profiles", "ncu_dram_bytes.json")
@@ -357,8 +359,12 @@ def traffic_record(key, kernel_src="paper_1810_08403_b200/csrc/propagate.cu"):
         rec = json.load(open(path))
     except Exception:
         return None, None
-    src = os.path.join(ROOT, kernel_src)
-    cur = hashlib.sha256(open(src, "rb").read()).hexdigest()[:16] if os.path.exists(src) else None
+    h = hashlib.sha256()
+    cur = None
+    if all(os.path.exists(os.path.join(ROOT, f)) for f in kernel_srcs):
+        for f in kernel_srcs:
+            h.update(open(os.path.join(ROOT, f), "rb").read())
+        cur = h.hexdigest()[:16]
     val = rec.get("records", {}).get(key)
     return val, (rec.get("kernel_source_sha256") == cur) if cur else None
 

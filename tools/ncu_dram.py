@@ -17,7 +17,15 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "profiles", "ncu_dram_bytes.json")
-SRC = os.path.join(ROOT, "paper_1810_08403_b200", "csrc", "propagate.cu")
+# the gather kernel's sources: the record is valid for the build these hash to
+SRCS = [os.path.join(ROOT, "paper_1810_08403_b200", "csrc", f) for f in ("propagate.cu", "vecio.cuh")]
+
+
+def source_sha():
+    h = hashlib.sha256()
+    for f in SRCS:
+        h.update(open(f, "rb").read())
+    return h.hexdigest()[:16]
 
 
 def dram_bytes(rep):
@@ -38,7 +46,7 @@ def dram_bytes(rep):
 
 def main():
     rec = json.load(open(OUT)) if os.path.exists(OUT) else {}
-    sha = hashlib.sha256(open(SRC, "rb").read()).hexdigest()[:16]
+    sha = source_sha()
     if rec.get("kernel_source_sha256") != sha:
         rec = {"records": {}, "launch_ms_under_ncu": {}, "kernels": {}}
     rec["kernel_source_sha256"] = sha
