@@ -16,3 +16,5 @@ for c in pubmed blogcatalog10 powerlaw_gcn powerlaw_ggcn; do
   timeout 1200 python bench.py --config $c --no-cpu-baseline --no-noreuse --no-reorder --no-bf16 > gpurun_out/f_bench_$c.json 2> gpurun_out/f_bench_$c.err
 done
 ls -la gpurun_out | tail -40
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:prop_kernel --launch-skip 3 --launch-count 2 -f -o /tmp/ffull python tools/profile_step.py reddit 2 > gpurun_out/f_full.log 2>&1
+ncu -i /tmp/ffull.ncu-rep --page details --csv > gpurun_out/f_full_details.csv 2>&1
