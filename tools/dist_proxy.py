@@ -52,10 +52,12 @@ da1 = mat(V, H).uniform_(-1, 1)     # layer-1 dA of every rank (backward blocks 
 flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 t1 = None
 COLUMN = os.environ.get("SG_PROXY_COLUMN", "1") == "1"   # dist.ShardIndex's default
+SPLIT = os.environ.get("SG_PROXY_SPLIT", "auto")          # subgroup size T of the rank passes
 
 
 for N in Ns:
-    shards = [D.ShardIndex(g, N, r, device=dev, column=COLUMN) for r in range(N)]
+    shards = [D.ShardIndex(g, N, r, device=dev, column=COLUMN,
+                           split_edges=SPLIT if SPLIT == "auto" else int(SPLIT)) for r in range(N)]
     size = shards[0].size
     blk = lambda t, i: t[i * size: i * size + shards[0].sizes[i]]  # noqa: E731
     per_rank, stages = [], []
@@ -150,7 +152,7 @@ for N in Ns:
     # per rank and epoch: (N-1)/N of the layer-1 (F) and layer-2 (H) inputs and the layer-2 dA (H)
     comm_bytes = (N - 1) / N * V * 4 * ((F + 3) // 4 * 4 + 2 * ((H + 3) // 4 * 4))
     comm_ms = comm_bytes / (NVLINK_GBS * 1e9) * 1e3
-    out = {"config": name, "N": N, "column_pass": COLUMN, "rank_step_ms": [round(x, 3) for x in per_rank],
+    out = {"config": name, "N": N, "column_pass": COLUMN, "split_edges": SPLIT, "rank_step_ms": [round(x, 3) for x in per_rank],
            "max_ms": round(tmax, 3), "mean_ms": round(float(np.mean(per_rank)), 3),
            "imbalance": round(tmax / float(np.mean(per_rank)), 3),
            "comm_mb_per_rank": round(comm_bytes / 1e6, 1), "comm_ms_at_nvlink": round(comm_ms, 3),
