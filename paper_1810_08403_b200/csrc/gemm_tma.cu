@@ -3,16 +3,16 @@
 // tensor.py:306-319).
 //
 // Per CTA (128 x BN output tile, K in blocks of 32), warp-specialised:
-//   warp 4 (one thread)  TMA producer: cp.async.bulk.tensor loads of the RAW fp32 tiles
+//   warp 8 (one thread)  TMA producer: cp.async.bulk.tensor loads of the RAW fp32 tiles
 //                        straight into the UMMA canonical layouts -- K-contiguous operands
 //                        as K-major SWIZZLE_128B, MN-contiguous operands (a^T in dW = a^T dz,
 //                        W in z = a W) as MN-major SWIZZLE_128B_BASE32B (the only MN-major
 //                        tf32 layout), 32 x 32 boxes -- so no operand is transposed anywhere;
-//   warps 0-3            converters: hi = rna_tf32(x) in place and lo = rna_tf32(x - hi)
+//   warps 0-7            converters: hi = rna_tf32(x) in place and lo = rna_tf32(x - hi)
 //                        into a lo tile of the same layout (sm100.cuh split3: round-to-nearest
 //                        split, 4x tighter than reading the raw container as truncated tf32);
 //                        then the epilogue (TMEM -> global);
-//   warp 5 (one thread)  TMEM allocator + UMMA issuer: hi*hi + hi*lo + lo*hi per k-step,
+//   warp 9 (one thread)  TMEM allocator + UMMA issuer: hi*hi + hi*lo + lo*hi per k-step,
 //                        tcgen05.commit releases the stage to the producer.
 // Stage ring: [raw A | raw B | lo A | lo B]; barriers raw-full (TMA tx bytes), full
 // (converters), empty (UMMA commit).  Split-K writes fixed-order partials like gemm_tc.cu.
@@ -31,9 +31,15 @@
 namespace {
 
 constexpr int BM = 128, BK = 32;
-constexpr int kConvThreads = 128;  // warps 0-3
-constexpr int kTmaWarp = 4, kMmaWarp = 5;
-constexpr int kThreads = 192;
+// 8 converter warps instead of 4: the five Reddit-epoch GEMMs 1.31 -> 1.14 ms (the round-to-nearest
+// split writes both planes; profiles/r02_gemm_convert_probe.txt)
+#ifndef SG_GEMM_CONV_WARPS
+#define SG_GEMM_CONV_WARPS 8
+#endif
+constexpr int kConvWarps = SG_GEMM_CONV_WARPS;   // 4 or 8 converter / epilogue warps
+constexpr int kConvThreads = kConvWarps * 32;
+constexpr int kTmaWarp = kConvWarps, kMmaWarp = kConvWarps + 1;
+constexpr int kThreads = (kConvWarps + 2) * 32;
 
 template <int BN>
 struct TCfg {
@@ -206,17 +212,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       sm100::fence_proxy_async_smem();
       sm100::mbar_arrive(full + s);
     }
-    // ---------------- epilogue: warp w drains TMEM lanes 32w..32w+31 (its rows), all BN columns
+    // ---------------- epilogue: warp w drains TMEM lanes 32(w%4)..+31 (its rows); with 8 warps
+    // warps w and w+4 take the two halves of the BN columns
     sm100::mbar_wait(done, 0);
     sm100::tc_fence_after();
-    const int64_t row = m0 + warp * 32 + lane;
+    const int lq = warp & 3;
+    const int64_t row = m0 + lq * 32 + lane;
     float* part = p.partial ? p.partial + (int64_t)blockIdx.z * p.M * p.N : nullptr;
     const bool relu = !p.partial && p.epilogue == SG_EPI_RELU_DUAL;
     bool bad = false;
+    constexpr int CW = kConvWarps == 8 ? BN / 2 : BN;
+    const int cbeg = kConvWarps == 8 ? (warp >> 2) * CW : 0;
 #pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 16) {
+    for (int c0 = cbeg; c0 < cbeg + CW; c0 += 16) {
       float v[16];
-      sm100::tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + c0, v);
+      sm100::tmem_ld16(tmem + ((uint32_t)(lq * 32) << 16) + c0, v);
       if (row < p.M) {
 #pragma unroll
         for (int j = 0; j < 16; j += 4) {
