@@ -29,6 +29,15 @@ namespace {
 using sg::VecIO;
 
 constexpr int kWarpsPerBlock = 8;
+// Split rows (> T edges): the pass kernel only writes each subgroup's partial, and a second
+// launch folds every split row's partials in subgroup order, one warp per (row, 32-vector column
+// slice) with several partials' loads in flight (1, default); or the warp that finishes a row's
+// last subgroup folds all of them, one partial per memory round trip, inside the pass (0).  At
+// 8-way sharding the Reddit hub row has 800 subgroups (T = 1024): the in-pass fold kept one warp
+// busy ~0.4 ms after the rest of the pass had drained (tools/dist_proxy.py, rank 0).
+#ifndef SG_SPLIT_KERNEL
+#define SG_SPLIT_KERNEL 1
+#endif
 // shared memory given to the hub-row cache (SG_HUB_KB overrides; the rest of the 256 KB
 // L1/shared array stays L1 for the in-flight row loads)
 // rows of >= 4 vectors per lane (F > 384 fp32): the cache measured slower on 1-vector
@@ -161,6 +170,7 @@ struct PropArgs {
   float* partial;       // [NOUT][n_slots][pld] fp32
   int64_t pld, n_slots;
   int32_t* counters;    // [n_splits]
+  int32_t n_splits;
   int32_t* queue;       // work-queue ticket
   const void* G;
   int64_t ldg, g_off;
@@ -614,6 +624,7 @@ __global__ void __launch_bounds__(NWB * 32, (HUB ? 1 : prop_min_blocks<MODE, DT,
           }
       }
     }
+#if !SG_SPLIT_KERNEL
     if (split) {
       const sg_split sp = a.splits[item.split];
       const int64_t r = item.row_begin;
@@ -647,7 +658,77 @@ __global__ void __launch_bounds__(NWB * 32, (HUB ? 1 : prop_min_blocks<MODE, DT,
         if (lane == 0) a.counters[item.split] = 0;
       }
     }
+#endif
   }
+}
+
+// Fold of the split rows' subgroup partials (SG_SPLIT_KERNEL): warp w takes split w / ncs,
+// column slice w % ncs (32 vectors of W columns, one per lane); acc = init (0, or the output row
+// when accumulating a chunk chain), then acc += p_0, p_1, ... in subgroup order with U partials'
+// loads in flight -- the same IEEE adds in the same order as the in-pass fold -- then the
+// row epilogue (ReLU mask) and store.
+template <int MODE, int DT, int W>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32) combine_kernel(const PropArgs a0, int ncs) {
+  using K = Prop<MODE, DT, W, 1, 32, 1>;
+  constexpr int NOUT = K::NOUT;
+  constexpr int U0 = 32 / (NOUT * W);
+  constexpr int U = U0 > 8 ? 8 : (U0 < 2 ? 2 : U0);
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= (int64_t)a0.n_splits * ncs) return;
+  const sg_split sp = a0.splits[warp / ncs];
+  const int c0 = (int)(warp % ncs) * 32;  // first vector of this column slice
+  PropArgs a = a0;
+  using IE = typename K::IO::Elem;
+  using OE = typename K::OIO::Elem;
+  a.Fv = min(32, a0.Fv - c0);
+  a.Fcols = a0.Fcols - c0 * W;
+  a.out0 = static_cast<OE*>(a0.out0) + (int64_t)c0 * W;
+  if (a0.out1) a.out1 = static_cast<OE*>(a0.out1) + (int64_t)c0 * W;
+  if (a0.mask) a.mask = static_cast<const IE*>(a0.mask) + (int64_t)c0 * W;
+  float acc[NOUT][1][W];
+  K::init_acc(a, sp.row, lane, acc, a.accumulate != 0);
+  if (lane < a.Fv) {
+    const float* pb = a0.partial + sp.slot0 * a0.pld + (int64_t)(c0 + lane) * W;
+    const int64_t ostride = a0.n_slots * a0.pld;
+    #pragma unroll 1
+    for (int s = 0; s < sp.n_sub; s += U) {
+      float x[U][NOUT][W];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (s + u < sp.n_sub) {
+#pragma unroll
+          for (int o = 0; o < NOUT; ++o)
+#pragma unroll
+            for (int k = 0; k < W; ++k) x[u][o][k] = __ldcg(pb + o * ostride + (int64_t)(s + u) * a0.pld + k);
+        }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (s + u < sp.n_sub) {
+#pragma unroll
+          for (int o = 0; o < NOUT; ++o)
+#pragma unroll
+            for (int k = 0; k < W; ++k) acc[o][0][k] = __fadd_rn(acc[o][0][k], x[u][o][k]);
+        }
+    }
+  }
+  K::store_row(a, sp.row, lane, acc);
+}
+
+template <int MODE, int DT, int W>
+cudaError_t launch_combine(const PropArgs& a, cudaStream_t st) {
+#if SG_SPLIT_KERNEL
+  if (a.n_splits <= 0) return cudaSuccess;
+  const int ncs = (a.Fv + 31) / 32;
+  const int64_t warps = (int64_t)a.n_splits * ncs;
+  const int64_t blocks = (warps + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  combine_kernel<MODE, DT, W><<<(unsigned)blocks, kWarpsPerBlock * 32, 0, st>>>(a, ncs);
+  sg::count_launch();
+  return cudaGetLastError();
+#else
+  (void)a; (void)st;
+  return cudaSuccess;
+#endif
 }
 
 // ------------------------------------------------------------------ dispatch
@@ -727,7 +808,8 @@ cudaError_t launch_one(const PropArgs& a, cudaStream_t st) {
       // hub-cache kernel: one block per SM holding the hub rows, as many warps as the
       // register budget allowed the default kernel (2-3 blocks of 8 warps)
       constexpr int NWB = kWarpsPerBlock * prop_min_blocks<MODE, DT, W, VPL, DEPTH>();
-      return launch_hub<MODE, DT, W, VPL, LPR, DEPTH, NWB>(a, st);
+      const cudaError_t e = launch_hub<MODE, DT, W, VPL, LPR, DEPTH, NWB>(a, st);
+      return e != cudaSuccess ? e : launch_combine<MODE, DT, W>(a, st);
     }
   }
   auto kern = prop_kernel<MODE, DT, W, VPL, LPR, DEPTH>;
@@ -747,7 +829,8 @@ cudaError_t launch_one(const PropArgs& a, cudaStream_t st) {
   int grid = (int)std::max<int64_t>(1, std::min(want, cap));
   kern<<<grid, kWarpsPerBlock * 32, 0, st>>>(a);
   sg::count_launch();
-  return cudaGetLastError();
+  const cudaError_t e = cudaGetLastError();
+  return e != cudaSuccess ? e : launch_combine<MODE, DT, W>(a, st);
 }
 
 // Widest vectors-per-lane instantiated: register pressure grows as VPL * W * (NG + NOUT);
@@ -920,7 +1003,7 @@ int sg_propagate_hub(int mode, int dtype, const int64_t* ptr, const int32_t* idx
     PropArgs a;
     a.ptr = ptr; a.idx = idx; a.w = w; a.items = items; a.splits = splits;
     a.partial = partial + c0; a.pld = pld; a.n_slots = n_slots;
-    a.counters = counters; a.queue = queue;
+    a.counters = counters; a.queue = queue; a.n_splits = (int32_t)n_splits;
     a.G = static_cast<const char*>(G) + c0 * esz; a.ldg = ldg; a.g_off = g_off;
     a.R = R ? static_cast<const char*>(R) + c0 * esz : nullptr; a.ldr = ldr; a.r_off = r_off;
     a.out0 = static_cast<char*>(out0) + c0 * oesz; a.ld0 = ld0;

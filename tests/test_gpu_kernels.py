@@ -77,9 +77,16 @@ CASES = [  # kind, V, E, F, P, T
     ("rmat", 300, 5000, 1100, 1, 128),                    # column slicing (> 1024 cols)
     ("uniform", 50, 0, 32, 1, 4096),                      # empty graph
 ]
+# deep split rows: the hub rows have 200-900 subgroups, folded in order as they complete
+# (SG_CHAIN_COMBINE: several lock rounds per row, > 32 ready flags per round, chunk chains)
+DEEP = [
+    ("rmat", 2000, 300000, 128, 1, 64),     # one vector per lane: 4 partials' loads in flight
+    ("rmat", 2000, 300000, 300, 1, 16),     # 3 vectors per lane, ~900 subgroups
+    ("rmat", 2000, 300000, 602, 2, 32),     # wide rows, 2-chunk chains (accumulate into out)
+]
 
 
-@pytest.mark.parametrize("kind,V,E,F,P,T", CASES)
+@pytest.mark.parametrize("kind,V,E,F,P,T", CASES + DEEP)
 def test_gcn_propagate_fwd_bitwise(sg, kind, V, E, F, P, T):
     from paper_1810_08403_b200 import _lib
 
@@ -94,7 +101,22 @@ def test_gcn_propagate_fwd_bitwise(sg, kind, V, E, F, P, T):
     assert np.array_equal(out.cpu().numpy(), ref)
 
 
-@pytest.mark.parametrize("kind,V,E,F,P,T", CASES[:5])
+def test_deep_split_fold_repeatable(sg):
+    """The in-order fold of split-row partials is race-free: 20 launches of a pass whose hub
+    rows have ~900 subgroups each equal the oracle bit for bit."""
+    from paper_1810_08403_b200 import _lib
+
+    V, E, F, T = 2000, 300000, 64, 16
+    s, d = _graph("rmat", V, E, 7)
+    grid = sg.ChunkGrid(sg.Graph(V, s, d), V, split_edges=T)
+    X = rng.features(V, F, seed=2)
+    ref = saga.gcn_propagate_fwd(og.partition_2d(s, d, V, V), X, og.gcn_edge_weights(s, d, V, np.float32), T=T)
+    H = _padded(X)
+    for _ in range(20):
+        assert np.array_equal(_gpu_prop_fwd(sg, grid, H, F, _lib.PROP_GCN).cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("kind,V,E,F,P,T", CASES[:5] + DEEP)
 def test_gcn_propagate_bwd_masked_bitwise(sg, kind, V, E, F, P, T):
     s, d = _graph(kind, V, E, 6)
     g = sg.Graph(V, s, d)
