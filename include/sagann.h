@@ -168,7 +168,8 @@ uint64_t sg_host_hash64(const void* data, int64_t nbytes, uint64_t seed);
 /* ---------------------------------------------------------------- device: propagation
  * One fused Scatter-ApplyEdge-Gather pass over a CSC (forward) or CSR (backward)
  * index: for each row r, out[r] (+)= sum over e in [ptr[r], ptr[r+1]) of t_e in
- * edge order (split rows: subgroup partials combined in fixed order).
+ * edge order (split rows: subgroup partials combined in fixed order by a second launch on
+ * the same stream).
  * Replaces take_rows -> mul/add/sigmoid -> segment_sum (tensor.py:424-450,
  * :204-303) and SPEC stage ops fused_gather_chunk / backward_* (SPEC.md:419-436).
  *   G, ldg, g_off : gathered rows (second operand segment at column g_off)

@@ -31,7 +31,7 @@ using sg::VecIO;
 constexpr int kWarpsPerBlock = 8;
 // Split rows (> T edges): the pass kernel only writes each subgroup's partial, and a second
 // launch folds every split row's partials in subgroup order, one warp per (row, 32-vector column
-// slice) with several partials' loads in flight (1, default); or the warp that finishes a row's
+// slice) with up to 16 partials' loads in flight (1, default); or the warp that finishes a row's
 // last subgroup folds all of them, one partial per memory round trip, inside the pass (0).  At
 // 8-way sharding the Reddit hub row has 800 subgroups (T = 1024): the in-pass fold kept one warp
 // busy ~0.4 ms after the rest of the pass had drained (tools/dist_proxy.py, rank 0).
@@ -665,14 +665,18 @@ __global__ void __launch_bounds__(NWB * 32, (HUB ? 1 : prop_min_blocks<MODE, DT,
 // Fold of the split rows' subgroup partials (SG_SPLIT_KERNEL): warp w takes split w / ncs,
 // column slice w % ncs (32 vectors of W columns, one per lane); acc = init (0, or the output row
 // when accumulating a chunk chain), then acc += p_0, p_1, ... in subgroup order with U partials'
-// loads in flight -- the same IEEE adds in the same order as the in-pass fold -- then the
+// loads in flight (U = 16 fp32 vectors) -- the same IEEE adds in the same order as the in-pass fold -- then the
 // row epilogue (ReLU mask) and store.
 template <int MODE, int DT, int W>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32) combine_kernel(const PropArgs a0, int ncs) {
   using K = Prop<MODE, DT, W, 1, 32, 1>;
   constexpr int NOUT = K::NOUT;
-  constexpr int U0 = 32 / (NOUT * W);
-  constexpr int U = U0 > 8 ? 8 : (U0 < 2 ? 2 : U0);
+  // partials in flight per lane: ~SG_COMBINE_REGS registers of loads
+#ifndef SG_COMBINE_REGS
+#define SG_COMBINE_REGS 64
+#endif
+  constexpr int U0 = SG_COMBINE_REGS / (NOUT * W);
+  constexpr int U = U0 > 16 ? 16 : (U0 < 2 ? 2 : U0);
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= (int64_t)a0.n_splits * ncs) return;
