@@ -975,9 +975,13 @@ int sg_propagate_hub(int mode, int dtype, const int64_t* ptr, const int32_t* idx
   if (R) vec = vec && (ldr % VW == 0) && (r_off % VW == 0) && aligned(R, 16);
   if (out1) vec = vec && (ld1 % OVW == 0) && aligned(out1, 16);
   if (mask) vec = vec && (ldm % VW == 0) && aligned(mask, 16);
-  // bf16 rows of 65-128 columns: 8-byte vectors (4 bf16), so all 32 lanes of a warp work on a
-  // row (16-byte vectors would leave half of them idle)
-  const bool half_vec = vec && dtype != SG_F32 && F > 64 && F <= 128 && n_hub == 0;
+  // split subgroups are half the plan's items or more (R-MAT hubs): see the lane-team note below
+  const bool hub_heavy = n_slots * 2 >= n_items;
+  // bf16 rows of 65-128 columns on hub-heavy passes: 8-byte vectors (4 bf16), so all 32 lanes
+  // of a warp work on a row (Reddit bf16 F = 128 passes 4.32 -> 3.34 ms); elsewhere 16-byte
+  // vectors with two rows per warp (uniform graphs, degree >= 32: the 8-byte rows measured up
+  // to 15% slower, profiles/r02_sweep_full_table.md)
+  const bool half_vec = vec && dtype != SG_F32 && F > 64 && F <= 128 && n_hub == 0 && hub_heavy;
   const int W = vec ? (half_vec ? 4 : VW) : 1;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
 
@@ -998,7 +1002,6 @@ int sg_propagate_hub(int mode, int dtype, const int64_t* ptr, const int32_t* idx
     // half the plan's items or more (R-MAT hubs: Reddit 56% of edges in rows > T), only
     // team 0 works on split items and heavy packed rows leave teams idle: one warp per row
     // measured 17% faster there (tools/narrow_ab.py), so teams are not used.
-    const bool hub_heavy = n_slots * 2 >= n_items;
     if (Fv <= 16 && !hub_heavy) {
       LPR = 2;
       while (LPR < Fv) LPR *= 2;

@@ -340,6 +340,17 @@ __global__ void __launch_bounds__(256) maxgather_bwd_kernel(
 //    bit (partials are combined lowest position first with strict '>');
 //  * backward: a sum, so a split row follows the subgroup rule of every propagation pass
 //    (oracle/saga.py:seq_sum_rows).
+// split rows: partials combined by a second launch (1) or by the last subgroup's warp (0).
+// MP-GCN step on the 28.6M-edge R-MAT graph (tools/mp_time.py, profiles/r02_max_split_ab.txt):
+// backward passes 1.73 / 1.97 -> 1.64 / 1.83 ms with the launch, forward passes 1.26 / 1.19 ->
+// 1.34 / 1.29 ms -- so the backward (a sum over subgroups) uses it and the forward keeps the
+// in-pass max/argmax combine
+#ifndef SG_MAX_SPLIT_FWD
+#define SG_MAX_SPLIT_FWD 0
+#endif
+#ifndef SG_MAX_SPLIT_BWD
+#define SG_MAX_SPLIT_BWD 1
+#endif
 struct MaxPlan {
   const int64_t* ptr;
   const int32_t* idx;
@@ -347,6 +358,7 @@ struct MaxPlan {
   const sg_item* items;
   const sg_split* splits;
   int32_t n_items;
+  int32_t n_splits;
   int32_t* queue;
   int32_t* counters;
   float* pval;           // [n_slots][pld]
@@ -459,6 +471,7 @@ __global__ void __launch_bounds__(256) maxgather_plan_kernel(const MaxPlan a) {
         }
       }
     }
+#if !SG_MAX_SPLIT_FWD
     if (split) {
       const sg_split sp = a.splits[item.split];
       __threadfence();
@@ -493,6 +506,7 @@ __global__ void __launch_bounds__(256) maxgather_plan_kernel(const MaxPlan a) {
         if (lane == 0) a.counters[item.split] = 0;
       }
     }
+#endif
   }
 }
 
@@ -558,6 +572,7 @@ __global__ void __launch_bounds__(256) maxgather_bwd_plan_kernel(const MaxPlan a
         }
       }
     }
+#if !SG_MAX_SPLIT_BWD
     if (split) {
       const sg_split sp = a.splits[item.split];
       __threadfence();
@@ -577,7 +592,75 @@ __global__ void __launch_bounds__(256) maxgather_bwd_plan_kernel(const MaxPlan a
         if (lane == 0) a.counters[item.split] = 0;
       }
     }
+#endif
   }
+}
+
+// Split-row combine launches (SG_MAX_SPLIT_FWD / _BWD, as sg_propagate's combine_kernel): one
+// thread per (split row, column), the row's partials read lowest subgroup first with U of them
+// in flight.  Forward: strict '>' over ascending positions keeps the first maximum (bitwise the
+// in-pass combine); backward: the subgroup sums added in subgroup order.
+#if SG_MAX_SPLIT_FWD
+__global__ void __launch_bounds__(256) maxgather_combine_kernel(const MaxPlan a, int tps) {
+  constexpr int U = 8;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t sid = t / tps;
+  const int c = (int)(t - sid * tps);
+  if (sid >= a.n_splits || c >= a.F) return;
+  const sg_split sp = a.splits[sid];
+  const int64_t r = sp.row;
+  float best = -INFINITY;
+  int32_t barg = -1;
+  if (a.accumulate) {
+    barg = a.arg[r * a.lda + c];
+    if (barg >= 0) best = a.out[r * a.ldo + c];
+  }
+  #pragma unroll 1
+  for (int q = 0; q < sp.n_sub; q += U) {
+    float v[U];
+    int32_t g[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (q + u < sp.n_sub) {
+        v[u] = __ldcg(a.pval + (sp.slot0 + q + u) * a.pld + c);
+        g[u] = __ldcg(a.parg + (sp.slot0 + q + u) * a.pld + c);
+      }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (q + u < sp.n_sub && g[u] >= 0 && v[u] > best) {
+        best = v[u];
+        barg = g[u];
+      }
+  }
+  a.out[r * a.ldo + c] = (a.finalize && barg < 0) ? a.fill : best;
+  if (a.arg64)
+    a.arg64[r * a.lda + c] = barg >= 0 ? (int64_t)__ldg(a.idx + barg) : -1;
+  else
+    a.arg[r * a.lda + c] = barg;
+}
+#endif
+
+__global__ void __launch_bounds__(256) maxgather_bwd_combine_kernel(const MaxPlan a, int tps) {
+  constexpr int U = 16;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t sid = t / tps;
+  const int c = (int)(t - sid * tps);
+  if (sid >= a.n_splits || c >= a.F) return;
+  const sg_split sp = a.splits[sid];
+  const int64_t r = sp.row;
+  float v = a.accumulate ? a.out[r * a.ldo + c] : 0.f;
+  #pragma unroll 1
+  for (int q = 0; q < sp.n_sub; q += U) {
+    float x[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (q + u < sp.n_sub) x[u] = __ldcg(a.pval + (sp.slot0 + q + u) * a.pld + c);
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (q + u < sp.n_sub) v = __fadd_rn(v, x[u]);
+  }
+  if (a.mask) v = __fmul_rn(v, __ldg(a.mask + r * a.ldm + c) > 0.f ? 1.f : 0.f);
+  a.out[r * a.ldo + c] = v;
 }
 
 int team_for(int Fv) {
@@ -685,6 +768,7 @@ static int max_plan_launch(bool bwd, const int64_t* ptr, const int32_t* idx, con
   MaxPlan a;
   a.ptr = ptr; a.idx = idx; a.pos = pos; a.items = items; a.splits = splits;
   a.n_items = (int32_t)n_items;
+  a.n_splits = (int32_t)n_splits;
   a.queue = reinterpret_cast<int32_t*>(w);
   a.counters = reinterpret_cast<int32_t*>(w + 256);
   a.pval = reinterpret_cast<float*>(w + 256 + cbytes);
@@ -711,6 +795,17 @@ static int max_plan_launch(bool bwd, const int64_t* ptr, const int32_t* idx, con
   e = cudaGetLastError();
   if (e != cudaSuccess) SG_FAIL(SG_ECUDA, "max plan launch: %s", cudaGetErrorString(e));
   sg::count_launch(1);
+  if (n_splits > 0 && (bwd ? SG_MAX_SPLIT_BWD : SG_MAX_SPLIT_FWD)) {
+    const int tps = (int)((F + 31) / 32 * 32);
+    const int64_t blocks = (n_splits * tps + 255) / 256;
+    if (bwd) maxgather_bwd_combine_kernel<<<(unsigned)blocks, 256, 0, st>>>(a, tps);
+#if SG_MAX_SPLIT_FWD
+    else maxgather_combine_kernel<<<(unsigned)blocks, 256, 0, st>>>(a, tps);
+#endif
+    e = cudaGetLastError();
+    if (e != cudaSuccess) SG_FAIL(SG_ECUDA, "max plan combine launch: %s", cudaGetErrorString(e));
+    sg::count_launch(1);
+  }
   return SG_OK;
 }
 
